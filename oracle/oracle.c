@@ -1,0 +1,406 @@
+/*
+ * oracle.c — plain CPU oracle for the Chase batched trace-replay planner.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Built with
+ *   gcc -O2 -ffp-contract=off -fopenmp -shared -fPIC
+ * Every function follows the paper (P:n) / SPEC (S:n) step by step, in fp64,
+ * one rounding per written operation, no blocking or reordering.
+ *
+ * Pins (tests/test_oracle_*.py) tie each function to something other than
+ * itself: exact rational least squares (fractions), numpy lstsq, the SPEC
+ * worked examples, closed forms, an exact-rational argmin away from ties,
+ * brute-force replay in rationals, and invariants.  See DESIGN.md §4.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---------------------------------------------------------------- Eq. 2 */
+/* sin_time(t) = sin(2*pi*t/T), cos_time(t) = cos(2*pi*t/T); the
+ * phase of step t is anchored to UTC midnight (DESIGN Q3), so the
+ * table is indexed by phi = (phase0 + t) mod T. */
+void oracle_phase_table(int32_t T, double* S, double* Cc) {
+    for (int32_t phi = 0; phi < T; ++phi) {
+        double theta = (2.0 * M_PI * (double)phi) / (double)T;
+        S[phi] = sin(theta);
+        Cc[phi] = cos(theta);
+    }
+}
+
+/* ---------------------------------------------------------------- Eq. 1 fit */
+/* Cholesky of the m x m SPD matrix G (row-major 3x3 storage) into Lc;
+ * returns 0 when some pivot d <= tol ("singularity"; DESIGN Q6). */
+static int cholesky3(int m, const double G[3][3], double tol, double Lc[3][3]) {
+    for (int j = 0; j < m; ++j) {
+        double d = G[j][j];
+        for (int k = 0; k < j; ++k) d = d - Lc[j][k] * Lc[j][k];
+        if (!(d > tol)) return 0;
+        Lc[j][j] = sqrt(d);
+        for (int i = j + 1; i < m; ++i) {
+            double v = G[i][j];
+            for (int k = 0; k < j; ++k) v = v - Lc[i][k] * Lc[j][k];
+            Lc[i][j] = v / Lc[j][j];
+        }
+    }
+    return 1;
+}
+
+/* S:131-139 fit_linear: ordinary least squares on z-scored features via the
+ * normal equations (S:196 standardisation, population sigma, DESIGN Q5),
+ * ridge lambda = 1e-8 on singularity, constant target -> intercept
+ * only, zero-variance columns dropped (DESIGN Q7). */
+int32_t oracle_fit(const double* hist, int32_t L, int32_t T, int32_t phi0,
+                   const double* S, const double* Cc,
+                   double ridge_lambda, double singular_tol, oracle_model_t* m) {
+    memset(m, 0, sizeof(*m));
+    const int32_t n = L - 1;           /* L points give L-1 lagged rows (Q2) */
+    const double dn = (double)n;
+
+    /* F2: constant target */
+    int constant = 1;
+    for (int32_t i = 2; i <= n; ++i)
+        if (hist[i] != hist[1]) { constant = 0; break; }
+    if (constant) {
+        m->kind = 1;
+        m->c0 = hist[1];
+        m->mu[3] = hist[1];
+        return 0;
+    }
+
+    /* Row i (1..n): x = (S[phi], Cc[phi], hist[i-1]), y = hist[i]. */
+    #define XS(i) S[((phi0) + (i)) % T]
+    #define XC(i) Cc[((phi0) + (i)) % T]
+    #define XL(i) hist[(i) - 1]
+    #define Y(i)  hist[(i)]
+
+    /* F3: sequential means ... */
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int32_t i = 1; i <= n; ++i) {
+        sum[0] = sum[0] + XS(i);
+        sum[1] = sum[1] + XC(i);
+        sum[2] = sum[2] + XL(i);
+        sum[3] = sum[3] + Y(i);
+    }
+    double mu[4];
+    for (int j = 0; j < 4; ++j) mu[j] = sum[j] / dn;
+    /* ... and two-pass population standard deviations */
+    double ss[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int32_t i = 1; i <= n; ++i) {
+        double d0 = XS(i) - mu[0];
+        double d1 = XC(i) - mu[1];
+        double d2 = XL(i) - mu[2];
+        double d3 = Y(i) - mu[3];
+        ss[0] = ss[0] + d0 * d0;
+        ss[1] = ss[1] + d1 * d1;
+        ss[2] = ss[2] + d2 * d2;
+        ss[3] = ss[3] + d3 * d3;
+    }
+    double sg[4];
+    for (int j = 0; j < 4; ++j) sg[j] = sqrt(ss[j] / dn);
+    for (int j = 0; j < 4; ++j) { m->mu[j] = mu[j]; m->sigma[j] = sg[j]; }
+    if (!(sg[3] > 0.0)) {              /* numerically constant target */
+        m->kind = 1;
+        m->c0 = mu[3];
+        return 0;
+    }
+
+    int cols[3], mcols = 0;
+    for (int j = 0; j < 3; ++j)
+        if (sg[j] > 0.0) cols[mcols++] = j;
+    m->n_cols = mcols;
+
+    /* F4: G = Z^T Z, h = Z^T u, sequential over rows */
+    double G[3][3] = {{0}}, h[3] = {0};
+    for (int32_t i = 1; i <= n; ++i) {
+        double x[3] = {XS(i), XC(i), XL(i)};
+        double z[3];
+        for (int a = 0; a < mcols; ++a) z[a] = (x[cols[a]] - mu[cols[a]]) / sg[cols[a]];
+        double u = (Y(i) - mu[3]) / sg[3];
+        for (int a = 0; a < mcols; ++a) {
+            for (int b = 0; b <= a; ++b) G[a][b] = G[a][b] + z[a] * z[b];
+            h[a] = h[a] + z[a] * u;
+        }
+    }
+    for (int a = 0; a < mcols; ++a)
+        for (int b = 0; b < a; ++b) G[b][a] = G[a][b];
+    #undef XS
+    #undef XC
+    #undef XL
+    #undef Y
+
+    /* F5: Cholesky, ridge fallback */
+    double Lc[3][3] = {{0}};
+    const double tol = singular_tol * dn;
+    if (mcols > 0 && !cholesky3(mcols, G, tol, Lc)) {
+        for (int a = 0; a < mcols; ++a) G[a][a] = G[a][a] + ridge_lambda;
+        m->ridge = 1;
+        memset(Lc, 0, sizeof(Lc));
+        if (!cholesky3(mcols, G, tol, Lc)) { m->status = 6; return 6; }
+    }
+
+    /* F6: beta = G^-1 h  (L z = h, then L^T beta = z) */
+    double zt[3] = {0}, beta[3] = {0};
+    for (int a = 0; a < mcols; ++a) {
+        double v = h[a];
+        for (int b = 0; b < a; ++b) v = v - Lc[a][b] * zt[b];
+        zt[a] = v / Lc[a][a];
+    }
+    for (int a = mcols - 1; a >= 0; --a) {
+        double v = zt[a];
+        for (int b = a + 1; b < mcols; ++b) v = v - Lc[b][a] * beta[b];
+        beta[a] = v / Lc[a][a];
+    }
+
+    /* Un-standardise: w_j = (sigma_y*beta_j)/sigma_j,
+     * c0 = ((mu_y - w_s*mu_s) - w_c*mu_c) - w_l*mu_l (kept columns only). */
+    double w[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < mcols; ++a) w[cols[a]] = (sg[3] * beta[a]) / sg[cols[a]];
+    double c0 = mu[3];
+    for (int a = 0; a < mcols; ++a) c0 = c0 - w[cols[a]] * mu[cols[a]];
+    m->c0 = c0;
+    m->ws = w[0];
+    m->wc = w[1];
+    m->wl = w[2];
+    m->kind = 0;
+    return 0;
+}
+
+/* Eq. 1 predict_one, clamp below at 0 (Q8). */
+double oracle_predict(const oracle_model_t* m, double s, double c, double lag) {
+    double A = (m->c0 + m->ws * s) + m->wc * c;
+    double p = A + m->wl * lag;
+    return p > 0.0 ? p : 0.0;
+}
+
+/* ---------------------------------------------------------------- Eq. 6 */
+double oracle_cost(double eta, double avg_power, double thr, double pmax,
+                   double maxci, double chat) {
+    double a = eta * avg_power;
+    double Kc = ((1.0 - eta) * pmax) * maxci;
+    return ((a * chat) + Kc) / thr;
+}
+
+/* P:120-124 min over p in P; ties -> lowest limit. */
+int32_t oracle_choose(int32_t K, const double* avg_power, const double* thr,
+                      double eta, double pmax, double maxci, double chat) {
+    int32_t best = 0;
+    double best_cost = oracle_cost(eta, avg_power[0], thr[0], pmax, maxci, chat);
+    for (int32_t k = 1; k < K; ++k) {
+        double ck = oracle_cost(eta, avg_power[k], thr[k], pmax, maxci, chat);
+        if (ck < best_cost) { best_cost = ck; best = k; }
+    }
+    return best;
+}
+
+/* S:300-308 cta = tta*avg_power*avg_ci / 3.6e6 (W*s*(g/kWh) -> g). */
+double oracle_cta(double tta_s, double avg_power_w, double avg_ci) {
+    return ((tta_s * avg_power_w) * avg_ci) / 3.6e6;
+}
+
+/* S:309-317 / Eq. 5. */
+double oracle_total_cost(double tta_s, double avg_power_w, double avg_ci,
+                         double eta, double pmax, double maxci) {
+    double inner = (eta * (avg_power_w * avg_ci)) + ((1.0 - eta) * (pmax * maxci));
+    return (tta_s * inner) / 3.6e6;
+}
+
+/* ---------------------------------------------------------------- replay */
+/* DESIGN R1-R2: fixed work ("does not change the number of samples"),
+ * stepwise carbon (Q14), pro-rata last window, trace
+ * exhaustion is an error. */
+int32_t oracle_replay(const double* c, int32_t N, int32_t s0,
+                      const uint8_t* choice, const double* avg_power,
+                      const double* thr, double delta, double J,
+                      double* out4, int32_t* completion_window) {
+    double S = 0.0, E = 0.0, C = 0.0;
+    for (int32_t w = s0; w < N; ++w) {
+        int k = choice[w - s0];
+        double sk = thr[k] * delta;
+        double prevS = S;
+        S = S + sk;
+        if (J > 0.0 && S >= J) {
+            double f = (J - prevS) / sk;
+            out4[0] = ((double)(w - s0) + f) * delta;
+            out4[1] = (E + f * avg_power[k]) * delta;
+            out4[2] = ((C + f * (avg_power[k] * c[w])) * delta) / 3.6e6;
+            out4[3] = J;
+            *completion_window = w;
+            return 0;
+        }
+        E = E + avg_power[k];
+        C = C + avg_power[k] * c[w];
+    }
+    out4[0] = (double)(N - s0) * delta;
+    out4[1] = E * delta;
+    out4[2] = (C * delta) / 3.6e6;
+    out4[3] = S;
+    *completion_window = -1;
+    return J > 0.0 ? 3 : 0;
+}
+
+/* ---------------------------------------------------------------- planner */
+int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
+                          int32_t phase0, int32_t refit_stride,
+                          double ridge_lambda, double singular_tol,
+                          const double* S, const double* Cc,
+                          int32_t K, const double* avg_power, const double* thr,
+                          int32_t n_eta, const double* eta,
+                          double pmax, double max_ci_cfg,
+                          double delta, double J,
+                          double* forecast, uint8_t* choice,
+                          oracle_totals_t* totals) {
+    const int32_t s0 = L, W = N - L;
+    memset(totals, 0, sizeof(oracle_totals_t) * (size_t)n_eta);
+    for (int e = 0; e < n_eta; ++e) totals[e].completion_window = -1;
+
+    int32_t status = 0;
+    for (int32_t t = 0; t < N; ++t)          /* values >= 0, finite */
+        if (!(c[t] >= 0.0) || !isfinite(c[t])) { status = 4; break; }
+    double maxci = max_ci_cfg;
+    if (status == 0 && !(max_ci_cfg > 0.0)) {  /* P:184, S:73 window_max */
+        maxci = c[0];
+        for (int32_t t = 1; t < L; ++t) if (c[t] > maxci) maxci = c[t];
+        if (!(maxci > 0.0)) status = 5;
+    }
+
+    uint8_t* own = NULL;
+    if (!choice) { own = (uint8_t*)malloc((size_t)n_eta * (size_t)W); choice = own; }
+
+    oracle_model_t m;
+    int32_t origin = -1;
+    for (int32_t w = s0; status == 0 && w < N; ++w) {
+        int32_t r = refit_stride > 0 ? s0 + refit_stride * ((w - s0) / refit_stride) : s0;
+        if (r != origin) {
+            origin = r;
+            int32_t phi0 = (int32_t)(((int64_t)phase0 + r - L) % T);
+            if (oracle_fit(c + (r - L), L, T, phi0, S, Cc, ridge_lambda,
+                           singular_tol, &m) != 0) { status = 6; break; }
+        }
+        int32_t phi = (int32_t)(((int64_t)phase0 + w) % T);
+        double chat = oracle_predict(&m, S[phi], Cc[phi], c[w - 1]);
+        if (forecast) forecast[w - s0] = chat;
+        for (int e = 0; e < n_eta; ++e)
+            choice[(size_t)e * W + (w - s0)] =
+                (uint8_t)oracle_choose(K, avg_power, thr, eta[e], pmax, maxci, chat);
+    }
+
+    if (status != 0) {
+        if (forecast) for (int32_t j = 0; j < W; ++j) forecast[j] = NAN;
+        memset(choice, 0xFF, (size_t)n_eta * W);
+        for (int e = 0; e < n_eta; ++e) totals[e].status = status;
+        free(own);
+        return status;
+    }
+
+    /* baseline: constant max limit */
+    uint8_t* base = (uint8_t*)malloc((size_t)W);
+    memset(base, K - 1, (size_t)W);
+    double b4[4];
+    int32_t bw;
+    int32_t bst = oracle_replay(c, N, s0, base, avg_power, thr, delta, J, b4, &bw);
+    free(base);
+
+    int32_t worst = bst;
+    for (int e = 0; e < n_eta; ++e) {
+        double a4[4];
+        int32_t aw;
+        int32_t ast = oracle_replay(c, N, s0, choice + (size_t)e * W, avg_power,
+                                    thr, delta, J, a4, &aw);
+        totals[e].time_s = a4[0];
+        totals[e].energy_j = a4[1];
+        totals[e].carbon_g = a4[2];
+        totals[e].samples = a4[3];
+        totals[e].base_time_s = b4[0];
+        totals[e].base_energy_j = b4[1];
+        totals[e].base_carbon_g = b4[2];
+        totals[e].completion_window = aw;
+        totals[e].status = ast ? ast : bst;
+        if (totals[e].status > worst) worst = totals[e].status;
+    }
+    free(own);
+    return worst;
+}
+
+int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
+                              int64_t ld, int32_t L, int32_t T, int32_t phase0,
+                              int32_t refit_stride, double ridge_lambda,
+                              double singular_tol, int32_t n_profiles,
+                              const int32_t* prof_K, const int32_t* prof_off,
+                              const double* avg_power, const double* thr,
+                              const double* prof_pmax,
+                              const uint8_t* profile_id, int32_t n_eta,
+                              const double* eta, double pmax_cfg,
+                              double max_ci_cfg, double delta,
+                              const double* job_samples, double* forecast,
+                              uint8_t* choice, oracle_totals_t* totals,
+                              double* sums, int32_t threads) {
+    const int64_t W = N - L;
+    double* S = (double*)malloc(sizeof(double) * (size_t)T);
+    double* Cc = (double*)malloc(sizeof(double) * (size_t)T);
+    oracle_phase_table(T, S, Cc);
+    (void)n_profiles;
+    int32_t used = 1;
+#ifdef _OPENMP
+    if (threads <= 0) threads = omp_get_max_threads();
+    #pragma omp parallel num_threads(threads)
+    {
+        #pragma omp single
+        used = omp_get_num_threads();
+    }
+#else
+    threads = 1;
+#endif
+
+    #pragma omp parallel num_threads(threads)
+    {
+        double* c = (double*)malloc(sizeof(double) * (size_t)N);
+        uint8_t* ch = (uint8_t*)malloc((size_t)n_eta * (size_t)W);
+        oracle_totals_t* tt = (oracle_totals_t*)malloc(sizeof(oracle_totals_t) * (size_t)n_eta);
+        #pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < n_traces; ++i) {
+            for (int64_t t = 0; t < N; ++t) c[t] = (double)traces[i * ld + t];
+            int p = profile_id ? profile_id[i] : 0;
+            int K = prof_K[p];
+            const double* P = avg_power + prof_off[p];
+            const double* Th = thr + prof_off[p];
+            /* MaxPower defaults to the highest power limit */
+            double pmax = pmax_cfg > 0.0 ? pmax_cfg : prof_pmax[p];
+            double J = job_samples ? job_samples[i] : 0.0;
+            oracle_plan_trace(c, (int32_t)N, L, T, phase0, refit_stride,
+                              ridge_lambda, singular_tol, S, Cc, K, P, Th,
+                              n_eta, eta, pmax, max_ci_cfg, delta, J,
+                              forecast ? forecast + i * W : NULL, ch, tt);
+            for (int e = 0; e < n_eta; ++e) {
+                if (choice) memcpy(choice + ((size_t)e * n_traces + i) * W, ch + (size_t)e * W, (size_t)W);
+                totals[(size_t)e * n_traces + i] = tt[e];
+            }
+        }
+        free(c); free(ch); free(tt);
+    }
+
+    if (sums) {
+        memset(sums, 0, sizeof(double) * 8 * (size_t)n_eta);
+        for (int e = 0; e < n_eta; ++e) {
+            double* s = sums + 8 * e;
+            for (int64_t i = 0; i < n_traces; ++i) {
+                const oracle_totals_t* t = &totals[(size_t)e * n_traces + i];
+                if (t->status != 0) continue;
+                s[0] = s[0] + t->time_s;
+                s[1] = s[1] + t->energy_j;
+                s[2] = s[2] + t->carbon_g;
+                s[3] = s[3] + t->samples;
+                s[4] = s[4] + t->base_time_s;
+                s[5] = s[5] + t->base_energy_j;
+                s[6] = s[6] + t->base_carbon_g;
+                s[7] = s[7] + 1.0;
+            }
+        }
+    }
+    free(S); free(Cc);
+    return used;
+}
