@@ -1,0 +1,387 @@
+#!/usr/bin/env python3
+"""bench.py — trace-windows planned per second (fit + argmin + replay) on B200.
+
+Metric (BASELINE.json): "trace-windows planned/sec (fit+argmin+replay) at
+1/2/4/8 B200; % of HBM peak".  One step = one chase_sweep over this GPU's
+batch of traces (fit once, predict, Eq. 6 argmin, fixed-work replay + max-power
+baseline, per-GPU totals) plus, for N > 1, the NCCL all-reduce of the totals.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C5] [--impl reference]
+
+N > 1 is launched by torchrun (one rank per GPU); each rank plans its own
+1e6-trace shard (weak scaling, configs[4]) and rank 0 prints ONE JSON line.
+`--impl reference` times the CPU oracle (oracle/) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import inputs  # noqa: E402
+
+METRIC = "trace-windows planned/sec (fit+argmin+replay)"
+UNIT = "trace-windows/s"
+BYTES_PER_WINDOW = 5.0   # 4 B fp32 trace read + 1 B choice write
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["chase", "reference"], default="chase")
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--traces", type=int, default=None, help="override traces per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
+    ap.add_argument("--e2e-traces", type=int, default=None)
+    return ap.parse_args(argv)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks
+CLOCK_FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+                "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+                "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", "--query-gpu=" + ",".join(CLOCK_FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < len(CLOCK_FIELDS):
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic_per_window(config: str):
+    """DRAM bytes per planned window of the sweep kernel from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json), if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    e = d.get(config) or d.get("default")
+    return None if e is None else float(e["dram_bytes_per_window"])
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+class OracleSample:
+    """A bounded prefix sample of the workload, generated once on the host,
+    planned by the CPU oracle as it stands (OpenMP across traces)."""
+
+    def __init__(self, w: inputs.Workload, n: int):
+        self.w, self.n = w, n
+        self.tr = inputs.synth_traces_host(n, w.n_steps, seed=w.seed, mode=w.mode)
+        self.pid = (inputs.profile_ids_host(n, seed=w.seed, n_profiles=len(w.profiles))
+                    if len(w.profiles) > 1 else None)
+        self.J = w.job_samples(self.pid)[:n]
+        self.cores = 0
+
+    def run(self) -> float:
+        import oracle
+        w = self.w
+        t0 = time.perf_counter()
+        r = oracle.plan_batch(self.tr, N=w.n_steps, L=w.history_len, T=w.T, profiles=w.profiles,
+                              profile_id=self.pid, etas=w.etas, delta=float(w.interval_s), job_samples=self.J,
+                              want_forecast=False, want_choice=False)
+        self.cores = r["threads"]
+        return time.perf_counter() - t0
+
+
+def calibrated_sample(w: inputs.Workload, target_s: float, max_traces: int) -> OracleSample:
+    n0 = min(max_traces, 64)
+    probe = OracleSample(w, n0)
+    dt = probe.run()
+    n = int(min(max_traces, max(n0, n0 * target_s / max(dt, 1e-3))))
+    return probe if n <= n0 else OracleSample(w, n)
+
+
+def oracle_sample_rate(w: inputs.Workload, target_s: float, max_traces: int):
+    s = calibrated_sample(w, target_s, max_traces)
+    dt = s.run()
+    return s.n * w.W / dt, s.cores, s.n, dt
+
+
+# ------------------------------------------------------------------ reference arm
+def main_reference(args):
+    """The CPU oracle, as it stands, on the host cores: same metric/config, each
+    step a bounded prefix sample of the workload (rank 0 only under torchrun)."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    w = inputs.workload(args.config, n_traces=args.traces)
+    per_step = min(10.0, 150.0 / max(1, args.steps + args.warmup))
+    s = calibrated_sample(w, per_step, w.n_traces)
+    times = []
+    for k in range(args.warmup + args.steps):
+        dt = s.run()
+        if k >= args.warmup:
+            times.append(dt)
+    step_s = float(np.mean(times))
+    value = s.n * w.W / step_s
+    sample = (f"first {s.n} of {w.n_traces} traces of {w.name} per step ({s.n * w.W:.3g} windows), "
+              f"{s.cores} host threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(w, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": s.cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(w: inputs.Workload, n_gpus: int):
+    return {
+        "workload": f"{w.name}: {w.description}",
+        "traces_per_gpu": w.n_traces, "steps_per_trace": w.n_steps, "history_len": w.history_len,
+        "windows_per_trace": w.W, "interval_s": w.interval_s, "n_eta": len(w.etas),
+        "n_limits": int(w.profiles[0].K), "profiles": [p.name for p in w.profiles],
+        "forecaster": "fit once per trace on the 24 h before job start (P:67), least squares (Table 1 LR)",
+        "l2": f"inputs larger than L2 ({w.n_traces * w.ld * 4 / 1e9:.1f} GB of fp32 traces per GPU vs 126 MB L2)",
+        "parallelism": f"dp{n_gpus} (trace-sharded; NCCL all-reduce of per-GPU totals)",
+    }
+
+
+# ------------------------------------------------------------------ product arm
+def main_chase(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_02508_b200 as cb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    w = inputs.workload(args.config, n_traces=args.traces)
+    n, W = w.n_traces, w.W
+    trace0 = rank * n   # weak scaling: every rank plans its own n traces
+    x = torch.empty((n, w.ld), dtype=torch.float32, device=dev)
+    inputs.synth_traces_device(x, w.n_steps, seed=w.seed, mode=w.mode, trace0=trace0)
+    pid = None
+    if len(w.profiles) > 1:
+        pid = torch.empty(n, dtype=torch.uint8, device=dev)
+        inputs.profile_ids_device(pid, seed=w.seed, n_profiles=len(w.profiles), trace0=trace0)
+    per_prof = torch.tensor([w.interval_s * W * float(p.throughput_sps.min()) for p in w.profiles],
+                            dtype=torch.float64, device=dev)
+    J = per_prof[pid.long()] if pid is not None else per_prof[0].expand(n).contiguous()
+    torch.cuda.synchronize()
+
+    planner = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, interval_s=w.interval_s,
+                         history_len=w.history_len, profile_id=pid, job_samples=J, want_choice=True)
+
+    def step():
+        planner.run()
+        if world > 1:
+            dist.all_reduce(planner.sums)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    diag = planner.diag()
+    sums0 = planner.sums.cpu().numpy()
+    if diag.n_bad or sums0[0, 7] != n * world:
+        raise RuntimeError(f"planner reported bad traces: n_bad={diag.n_bad}, n_ok={sums0[0, 7]}")
+
+    stream = torch.cuda.current_stream(dev)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:         # materialise the CUDA events before handing them to the library
+        a.record(stream)
+        b.record(stream)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = cb.kernel_launches()
+    t0.record(stream)
+    for k in range(args.steps):
+        cb.set_kernel_events(*kev[k])
+        step()
+    t1.record(stream)
+    cb.set_kernel_events(None, None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = cb.kernel_launches() - launches0
+    clk = clocks.stop()
+
+    elapsed_ms = t0.elapsed_time(t1)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    tm = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    elapsed_ms, kern_ms = float(tm[0]), float(tm[1])
+    ms_per_step = elapsed_ms / args.steps
+    total_windows = float(n) * W * world
+    value = total_windows / (ms_per_step / 1e3)
+
+    peak, peak_src = measured_peaks()
+    alg_bytes = n * W * BYTES_PER_WINDOW
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    tpw = ncu_traffic_per_window(args.config)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None if tpw is None else tpw * n * W,
+                "kernel": "sweep_kernel<FUSED> (fused predict + Eq. 6 argmin + replay)",
+                "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
+                "algorithmic_bytes_per_launch": alg_bytes, "bytes_per_window": BYTES_PER_WINDOW,
+                "peak_source": peak_src}
+
+    # ---- e2e: the public host-buffer call, H2D of the inputs inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, ns, dt = oracle_sample_rate(w, args.cpu_seconds, n)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {ns} of {n} traces ({ns * W:.3g} windows, {dt:.1f} s on {cores} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based generator, inputs/)",
+            "config": workload_config(w, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clk,
+            "check": {"n_ok": float(sums0[0, 7]), "n_slow_windows": int(diag.n_slow_windows)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev):
+    """Same metric through chase_sweep_host: pinned HOST traces / ids / budgets,
+    chunked H2D overlapping the fused kernels, host sums out."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 32 << 30
+    row = w.ld * 4
+    lws = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    n_e2e = args.e2e_traces or int(min(w.n_traces, avail * 0.3 / max(1, lws) / row))
+    n_e2e = max(1024, (n_e2e // 1024) * 1024)
+    n_e2e = min(n_e2e, w.n_traces)
+    h = torch.empty((n_e2e, w.ld), dtype=torch.float32).pin_memory()
+    h.copy_(x[:n_e2e])
+    hp = None if pid is None else pid[:n_e2e].cpu().pin_memory()
+    hJ = J[:n_e2e].cpu().pin_memory()
+    chunk = min(n_e2e, 32768)
+    ht = cb.make_traces(h, n_steps=w.n_steps, interval_s=w.interval_s)
+    tc = cb.make_traces(h[:chunk], n_steps=w.n_steps, interval_s=w.interval_s)
+    fcfg = cb.make_fcfg(interval_s=w.interval_s, history_len=w.history_len)
+    ws = cb.alloc_workspace(cb.workspace_bytes(tc, fcfg, len(w.profiles), len(w.etas)), dev)
+    stg = cb.alloc_workspace(cb.sweep_host_staging_bytes(ht, chunk, len(w.etas)), dev)
+
+    def call():
+        return cb.sweep_host(ht, fcfg, w.profiles, w.etas, chunk, stg, ws, h_profile_id=hp, h_job_samples=hJ)
+
+    call()
+    steps = max(2, min(args.steps, 5))
+    stream = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(steps):
+        sums = call()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    tm = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm[0])
+    if sums[0, 7] != n_e2e:
+        raise RuntimeError(f"e2e sums report {sums[0, 7]} ok traces of {n_e2e}")
+    h2d = n_e2e * (w.ld * 4 + (1 if hp is not None else 0) + 8)
+    return {"value": n_e2e * w.W * world / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(len(w.etas) * 64), "traces_per_gpu": n_e2e, "ms_per_step": ms,
+            "api": "chase_sweep_host (pinned host inputs, double-buffered H2D on a second stream)"}
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        return main_reference(args)
+    return main_chase(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

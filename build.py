@@ -36,7 +36,7 @@ def build_oracle(force=False):
     src = [os.path.join(ROOT, "oracle", f) for f in ("oracle.c", "oracle.h")]
     out = os.path.join(ROOT, "oracle", "liboracle.so")
     if force or _stale(out, src):
-        _run(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-std=c11",
+        _run(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-std=gnu11",
               "-Wall", "-Wextra", "-shared", "-fPIC", "-o", out, src[0], "-lm"])
     return out
 
@@ -73,7 +73,7 @@ def build_chase(force=False):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xptxas", "-v",
                   "-Xcompiler", "-fPIC", *common, "-c", s, "-o", o])
         else:
-            _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", *common,
+            _run([NVCC, *ARCH, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", *common,
                   "-c", s, "-o", o])
         objs.append(o)
     _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs])

@@ -196,6 +196,35 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
                            chase_totals_t* d_per_trace, chase_sum_t* d_sum,
                            void* nccl_comm, void* d_ws, size_t ws_bytes, void* stream);
 
+/* End-to-end variant with HOST inputs (the public call a user makes when the
+ * traces live in host memory; bench.py's "e2e" figure): streams chunks of
+ * `chunk_traces` traces through a double-buffered device staging area with
+ * the host->device copies on a second stream overlapping the fused kernels
+ * of the previous chunk, and returns the per-eta sums in HOST memory.
+ *   h_traces->data, h_profile_id, h_job_samples: host memory (pin it, e.g.
+ *   cudaHostAlloc / torch pin_memory, for copy/compute overlap);
+ *   d_staging: chase_sweep_host_staging_bytes() bytes of device memory;
+ *   d_ws: chase_workspace_bytes() for a descriptor with n_traces = chunk_traces.
+ * Synchronous: returns after h_sum is written. */
+size_t chase_sweep_host_staging_bytes(const chase_traces_t* h_traces, int64_t chunk_traces, int32_t n_eta);
+chase_status_t chase_sweep_host(const chase_traces_t* h_traces, const chase_forecast_cfg_t* fcfg,
+                                const chase_profile_t* profiles, int32_t n_profiles,
+                                const uint8_t* h_profile_id, const chase_cost_cfg_t* cost,
+                                const double* h_job_samples, int64_t chunk_traces, chase_sum_t* h_sum,
+                                void* d_staging, size_t staging_bytes, void* d_ws, size_t ws_bytes,
+                                void* stream);
+
+/* Number of kernels this thread has launched through the library so far
+ * (bench.py reports the count inside its timed region as gpu_launches). */
+uint64_t chase_kernel_launches(void);
+
+/* Optional timing hook: when both are non-NULL cudaEvent_t handles, the next
+ * calls record `start` / `stop` on their stream immediately around the
+ * dominant kernel (the fused sweep, the replay or the plan kernel), so the
+ * caller can time that kernel alone with CUDA events.  Pass NULLs to clear.
+ * Thread-local. */
+void chase_set_kernel_events(void* start, void* stop);
+
 /* Copy the workspace diagnostics of the last call to the host (synchronises
  * `stream`). */
 chase_status_t chase_diag_read(const void* d_ws, chase_diag_t* out, void* stream);

@@ -1,0 +1,561 @@
+// chase_api.cpp — the C ABI of libchase.so (include/chase.h): argument
+// validation, the per-call constant tables (phase table, profiles, Eq. 6
+// envelope buckets), workspace layout and kernel launch planning.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "chase.h"
+#include "envelope.h"
+#include "kernels.h"
+
+using namespace chase;
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;
+
+void ev_start(cudaStream_t s) {
+    if (g_ev_start && g_ev_stop) cudaEventRecord(g_ev_start, s);
+}
+void ev_stop(cudaStream_t s) {
+    if (g_ev_start && g_ev_stop) cudaEventRecord(g_ev_stop, s);
+}
+
+chase_status_t fail(chase_status_t code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+chase_status_t cuda_fail(cudaError_t e, const char* where) {
+    return fail(CHASE_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+constexpr size_t kWsAlign = 256;
+constexpr int kMaxGrid = 1024;  // rows of the per-CTA partial sums
+
+struct WsLayout {
+    size_t diag, tables, records, status, cta_sums, total;
+};
+
+WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta) {
+    WsLayout w;
+    size_t o = 0;
+    w.diag = o; o += kWsAlign;
+    w.tables = o; o += round_up(tables_bytes(T, n_prof, n_eta), kWsAlign);
+    w.records = o; o += round_up(n_traces * kRecDoubles * 8, kWsAlign);
+    w.status = o; o += round_up(n_traces, kWsAlign);
+    w.cta_sums = o; o += round_up((int64_t)kMaxGrid * kMaxEta * 8 * 8, kWsAlign);
+    w.total = o;
+    return w;
+}
+
+// ---------------------------------------------------------------- validation
+chase_status_t check_traces(const chase_traces_t* t) {
+    if (!t) return fail(CHASE_ERR_INVALID, "traces is NULL");
+    if (t->dtype != CHASE_F32 && t->dtype != CHASE_F64) return fail(CHASE_ERR_INVALID, "dtype %d", t->dtype);
+    if (t->n_traces < 0) return fail(CHASE_ERR_INVALID, "n_traces < 0");
+    if (t->interval_s <= 0 || 86400 % t->interval_s != 0)
+        return fail(CHASE_ERR_INVALID, "interval_s=%d must divide 86400 (S:27, S:124)", t->interval_s);
+    const int esz = t->dtype == CHASE_F64 ? 8 : 4;
+    if (t->ld < t->n_steps || (t->ld * esz) % 16 != 0)
+        return fail(CHASE_ERR_INVALID, "ld=%lld must be >= n_steps and ld*elem %% 16 == 0", (long long)t->ld);
+    if (t->n_traces > 0 && (!t->data || ((uintptr_t)t->data & 15)))
+        return fail(CHASE_ERR_INVALID, "trace data NULL or not 16-byte aligned");
+    const int T = 86400 / t->interval_s;
+    if (t->phase0 < 0 || t->phase0 >= T) return fail(CHASE_ERR_INVALID, "phase0=%d outside [0, T=%d)", t->phase0, T);
+    return CHASE_OK;
+}
+
+chase_status_t check_fcfg(const chase_traces_t* t, const chase_forecast_cfg_t* f) {
+    if (!f) return fail(CHASE_ERR_INVALID, "forecast cfg is NULL");
+    if (f->steps_per_day * t->interval_s != 86400)
+        return fail(CHASE_ERR_INVALID, "steps_per_day=%d != 86400/interval_s (Eq. 2)", f->steps_per_day);
+    if (f->history_len < 5) return fail(CHASE_ERR_INVALID, "history_len=%d: need L-1 >= 4 rows (S:133)", f->history_len);
+    if (t->n_steps <= f->history_len) return fail(CHASE_ERR_INVALID, "n_steps must exceed history_len (W >= 1)");
+    if (f->history_len > 1 << 20) return fail(CHASE_ERR_INVALID, "history_len too large");
+    if (f->refit_stride < 0) return fail(CHASE_ERR_INVALID, "refit_stride < 0");
+    if (f->refit_stride > 0)
+        return fail(CHASE_ERR_INVALID, "refit_stride=%d: rolling refit is not available in this build", f->refit_stride);
+    if (!(f->ridge_lambda >= 0) || !(f->singular_tol >= 0)) return fail(CHASE_ERR_INVALID, "ridge/tol must be >= 0");
+    return CHASE_OK;
+}
+
+chase_status_t check_profiles(const chase_profile_t* p, int n) {
+    if (!p || n < 1 || n > CHASE_MAX_PROFILES)
+        return fail(CHASE_ERR_INVALID, "n_profiles=%d outside [1, %d]", n, CHASE_MAX_PROFILES);
+    for (int q = 0; q < n; ++q) {
+        const chase_profile_t& P = p[q];
+        if (P.n_limits < 2 || P.n_limits > CHASE_MAX_LIMITS)
+            return fail(CHASE_ERR_INVALID, "profile %d: n_limits=%d outside [2, 32] (S:224)", q, P.n_limits);
+        if (!P.limit_w || !P.avg_power_w || !P.throughput_sps)
+            return fail(CHASE_ERR_INVALID, "profile %d: NULL table", q);
+        for (int k = 0; k < P.n_limits; ++k) {
+            if (k && P.limit_w[k] <= P.limit_w[k - 1])
+                return fail(CHASE_ERR_INVALID, "profile %d: limits not strictly increasing at row %d (S:224)", q, k);
+            if (P.limit_w[k] <= 0) return fail(CHASE_ERR_INVALID, "profile %d: limit <= 0", q);
+            double pw = P.avg_power_w[k], th = P.throughput_sps[k];
+            if (!(pw > 0) || !std::isfinite(pw) || pw > 1.05 * P.limit_w[k])
+                return fail(CHASE_ERR_INVALID, "profile %d row %d: avg_power %g not in (0, 1.05*limit] (S:225)", q, k, pw);
+            if (!(th > 0) || !std::isfinite(th))
+                return fail(CHASE_ERR_INVALID, "profile %d row %d: throughput %g must be > 0 (S:226)", q, k, th);
+        }
+    }
+    return CHASE_OK;
+}
+
+chase_status_t check_cost(const chase_cost_cfg_t* c, const chase_profile_t* p, int n_prof) {
+    if (!c || !c->eta) return fail(CHASE_ERR_INVALID, "cost cfg / eta is NULL");
+    if (c->n_eta < 1 || c->n_eta > CHASE_MAX_ETA) return fail(CHASE_ERR_INVALID, "n_eta=%d outside [1, 16]", c->n_eta);
+    if (n_prof * c->n_eta > CHASE_MAX_PAIRS)
+        return fail(CHASE_ERR_INVALID, "n_profiles*n_eta=%d exceeds %d", n_prof * c->n_eta, CHASE_MAX_PAIRS);
+    for (int e = 0; e < c->n_eta; ++e)
+        if (!(c->eta[e] >= 0.0 && c->eta[e] <= 1.0))
+            return fail(CHASE_ERR_INVALID, "eta[%d]=%g outside [0, 1] (S:292)", e, c->eta[e]);
+    if (c->max_power_w > 0)
+        for (int q = 0; q < n_prof; ++q)
+            if (c->max_power_w < p[q].limit_w[p[q].n_limits - 1])
+                return fail(CHASE_ERR_INVALID, "max_power_w=%g below profile %d's largest limit (S:292)", c->max_power_w, q);
+    if (!std::isfinite(c->max_ci) || !std::isfinite(c->max_power_w))
+        return fail(CHASE_ERR_INVALID, "max_ci / max_power_w must be finite");
+    return CHASE_OK;
+}
+
+chase_status_t check_ws(void* ws, size_t bytes, size_t need) {
+    if (!ws || ((uintptr_t)ws % kWsAlign)) return fail(CHASE_ERR_WORKSPACE, "workspace NULL or not 256-byte aligned");
+    if (bytes < need) return fail(CHASE_ERR_WORKSPACE, "workspace %zu bytes < required %zu", bytes, need);
+    return CHASE_OK;
+}
+
+// ---------------------------------------------------------------- constant tables
+// Phase table of Eq. 2, anchored to UTC midnight:
+// S[phi] = sin((2.0*pi*phi)/T), C[phi] = cos(...), host libm, fp64.
+std::vector<uint8_t> build_tables(int T, double delta, const chase_profile_t* profs, int n_prof,
+                                  const chase_cost_cfg_t* cost, int n_eta) {
+    const int total = tables_bytes(T, n_prof, n_eta);
+    std::vector<uint8_t> blob((size_t)total, 0);
+    TablesHeader* H = reinterpret_cast<TablesHeader*>(blob.data());
+    H->T = T;
+    H->n_prof = n_prof;
+    H->n_eta = n_eta;
+    H->n_pairs = n_prof * n_eta;
+    H->off_phase = (int)sizeof(TablesHeader);
+    H->off_prof = H->off_phase + (((2 * T * 8) + 15) / 16 * 16);
+    H->off_pair = H->off_prof + n_prof * (int)sizeof(ProfileTable);
+    H->total_bytes = total;
+    H->delta = delta;
+    double* ph = reinterpret_cast<double*>(blob.data() + H->off_phase);
+    for (int phi = 0; phi < T; ++phi) {
+        double theta = (2.0 * M_PI * (double)phi) / (double)T;
+        ph[phi] = std::sin(theta);
+        ph[T + phi] = std::cos(theta);
+    }
+    ProfileTable* pt = reinterpret_cast<ProfileTable*>(blob.data() + H->off_prof);
+    PairTable* pr = reinterpret_cast<PairTable*>(blob.data() + H->off_pair);
+    for (int q = 0; q < n_prof; ++q) {
+        const chase_profile_t& P = profs[q];
+        ProfileTable& T_ = pt[q];
+        T_.K = P.n_limits;
+        T_.pmax = (cost && cost->max_power_w > 0) ? cost->max_power_w : (double)P.limit_w[P.n_limits - 1];
+        for (int k = 0; k < P.n_limits; ++k) {
+            T_.line[k] = make_double2(P.throughput_sps[k] * delta, P.avg_power_w[k]);
+            T_.thr[k] = P.throughput_sps[k];
+        }
+        for (int e = 0; e < n_eta; ++e)
+            build_pair_table(P.n_limits, P.avg_power_w, P.throughput_sps, cost->eta[e], T_.pmax, &pr[q * n_eta + e]);
+    }
+    return blob;
+}
+
+struct Prepared {
+    WsLayout L;
+    int tables_bytes;
+};
+
+chase_status_t upload_tables(const std::vector<uint8_t>& blob, uint8_t* ws, const WsLayout& L, cudaStream_t s) {
+    cudaError_t e = launch_upload(blob.data(), blob.size(), ws + L.tables, s);
+    if (e != cudaSuccess) return cuda_fail(e, "upload tables");
+    e = launch_diag_reset(reinterpret_cast<chase_diag_t*>(ws + L.diag), s);
+    if (e != cudaSuccess) return cuda_fail(e, "diag reset");
+    return CHASE_OK;
+}
+
+SweepParams base_sweep(const chase_traces_t* t, int L, const WsLayout& WL, uint8_t* ws, int tb) {
+    SweepParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.traces = t->data;
+    p.ld = t->ld;
+    p.n_traces = t->n_traces;
+    p.N = (int32_t)t->n_steps;
+    p.L = L;
+    p.T = 86400 / t->interval_s;
+    p.phase0 = t->phase0;
+    p.W = (int32_t)(t->n_steps - L);
+    p.n_tiles = (int32_t)((p.W + kTileW - 1) / kTileW);
+    p.delta = (double)t->interval_s;
+    p.records = reinterpret_cast<const double*>(ws + WL.records);
+    p.tables = ws + WL.tables;
+    p.tables_bytes = tb;
+    p.stage_bytes = sweep_stage_bytes(t->dtype == CHASE_F64 ? 8 : 4);
+    p.cta_sums = reinterpret_cast<double*>(ws + WL.cta_sums);
+    p.status = ws + WL.status;
+    p.diag = reinterpret_cast<chase_diag_t*>(ws + WL.diag);
+    return p;
+}
+
+bool aligned_start(const chase_traces_t* t, int L) {
+    const int vec = t->dtype == CHASE_F64 ? 2 : 4;
+    return L % vec == 0 && L >= vec;
+}
+
+chase_status_t check_smem(int tb, int T, const chase_traces_t* t) {
+    size_t need = sweep_smem_bytes(tb, T, t->dtype == CHASE_F64 ? 8 : 4, 0);
+    if (need > 227 * 1024)
+        return fail(CHASE_ERR_INVALID, "shared-memory plan %zu B exceeds 227 KB (reduce profiles x eta or use f32)", need);
+    return CHASE_OK;
+}
+
+FitParams make_fit(const chase_traces_t* t, const chase_forecast_cfg_t* f, uint8_t* ws, const WsLayout& WL) {
+    FitParams fp;
+    std::memset(&fp, 0, sizeof(fp));
+    fp.traces = t->data;
+    fp.ld = t->ld;
+    fp.n_traces = t->n_traces;
+    fp.L = f->history_len;
+    fp.T = f->steps_per_day;
+    fp.phase0 = t->phase0;
+    fp.is_f64 = t->dtype == CHASE_F64;
+    fp.ridge = f->ridge_lambda;
+    fp.tol = f->singular_tol;
+    fp.phase_tab = reinterpret_cast<const double*>(ws + WL.tables + sizeof(TablesHeader));
+    fp.records = reinterpret_cast<double*>(ws + WL.records);
+    return fp;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* chase_last_error(void) { return g_err; }
+
+const char* chase_version(void) { return "chase-b200 0.1 (sm_100a, fit-once planner)"; }
+
+size_t chase_workspace_bytes(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, int32_t n_profiles,
+                             int32_t n_eta) {
+    if (!traces || traces->interval_s <= 0 || 86400 % traces->interval_s || n_profiles < 0 || n_eta < 0) return 0;
+    (void)fcfg;
+    const int T = 86400 / traces->interval_s;
+    return ws_layout(traces->n_traces, T, n_profiles < 1 ? 1 : n_profiles, n_eta < 1 ? 1 : n_eta).total;
+}
+
+chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_forecast,
+                                  int64_t ld_f, double* d_max_ci, double* d_models, void* d_ws, size_t ws_bytes,
+                                  void* stream) {
+    chase_status_t st;
+    if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
+    const int64_t W = traces->n_steps - fcfg->history_len;
+    if (!d_forecast || ld_f < W) return fail(CHASE_ERR_INVALID, "d_forecast NULL or ld_f < W");
+    const int T = fcfg->steps_per_day;
+    // layout sized for (1 profile, 1 eta) so one workspace serves every entry point
+    const WsLayout WL = ws_layout(traces->n_traces, T, 1, 1);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, nullptr, 0, nullptr, 0);
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    FitParams fp = make_fit(traces, fcfg, ws, WL);
+    fp.models_out = d_models;
+    fp.max_ci_out = d_max_ci;
+    cudaError_t e = launch_fit(fp, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
+    SweepParams p = base_sweep(traces, fcfg->history_len, WL, ws, (int)blob.size());
+    p.n_eta = 1;
+    p.forecast = d_forecast;
+    p.ld_f = ld_f;
+    int grid = 0;
+    e = launch_sweep(MODE_PREDICT, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, kMaxGrid,
+                     &grid, s);
+    if (e != cudaSuccess) return cuda_fail(e, "predict kernel");
+    e = launch_finalize(nullptr, 0, 1, nullptr, p.status, traces->n_traces, nullptr, 0, W, 0, d_forecast, ld_f, p.diag, s);
+    if (e != cudaSuccess) return cuda_fail(e, "finalize");
+    return CHASE_OK;
+}
+
+chase_status_t chase_plan_power_limits(const double* d_forecast, int64_t n_traces, int64_t W, int64_t ld_f,
+                                       const chase_profile_t* profiles, int32_t n_profiles,
+                                       const uint8_t* d_profile_id, const chase_cost_cfg_t* cost,
+                                       const double* d_max_ci, uint8_t* d_choice, int64_t ld_c, void* d_ws,
+                                       size_t ws_bytes, void* stream) {
+    chase_status_t st;
+    if (n_traces < 0 || W < 1 || ld_f < W) return fail(CHASE_ERR_INVALID, "n_traces < 0, W < 1 or ld_f < W");
+    if ((st = check_profiles(profiles, n_profiles)) || (st = check_cost(cost, profiles, n_profiles))) return st;
+    if (ld_c < round_up(W, 16) || ld_c % 16) return fail(CHASE_ERR_INVALID, "ld_c must be a multiple of 16 >= round_up(W,16)");
+    if (n_traces > 0 && (!d_forecast || !d_choice || ((uintptr_t)d_choice & 15)))
+        return fail(CHASE_ERR_INVALID, "d_forecast / d_choice NULL or d_choice not 16-byte aligned");
+    if (!(cost->max_ci > 0) && n_traces > 0 && !d_max_ci)
+        return fail(CHASE_ERR_INVALID, "d_max_ci required when cost->max_ci <= 0 (P:184)");
+    const int T = 1;
+    const WsLayout WL = ws_layout(n_traces, T, n_profiles, cost->n_eta);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    std::vector<uint8_t> blob = build_tables(T, 1.0, profiles, n_profiles, cost, cost->n_eta);
+    if (blob.size() > 200 * 1024) return fail(CHASE_ERR_INVALID, "tables exceed shared memory");
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    PlanParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.forecast = d_forecast;
+    p.n_traces = n_traces;
+    p.W = W;
+    p.ld_f = ld_f;
+    p.tables = ws + WL.tables;
+    p.tables_bytes = (int)blob.size();
+    p.n_eta = cost->n_eta;
+    p.n_prof = n_profiles;
+    p.profile_id = d_profile_id;
+    p.max_ci = d_max_ci;
+    p.max_ci_fixed = cost->max_ci;
+    p.choice = d_choice;
+    p.ld_c = ld_c;
+    p.diag = reinterpret_cast<chase_diag_t*>(ws + WL.diag);
+    ev_start(s);
+    cudaError_t e = launch_plan(p, s);
+    ev_stop(s);
+    if (e != cudaSuccess) return cuda_fail(e, "plan kernel");
+    return CHASE_OK;
+}
+
+chase_status_t chase_replay(const chase_traces_t* traces, int32_t history_len, const uint8_t* d_choice, int64_t ld_c,
+                            int32_t n_eta, const chase_profile_t* profiles, int32_t n_profiles,
+                            const uint8_t* d_profile_id, const double* d_job_samples, chase_totals_t* d_per_trace,
+                            chase_sum_t* d_sum, void* d_ws, size_t ws_bytes, void* stream) {
+    chase_status_t st;
+    if ((st = check_traces(traces)) || (st = check_profiles(profiles, n_profiles))) return st;
+    if (history_len < 1 || traces->n_steps <= history_len) return fail(CHASE_ERR_INVALID, "history_len");
+    if (n_eta < 1 || n_eta > CHASE_MAX_ETA || n_eta * n_profiles > CHASE_MAX_PAIRS)
+        return fail(CHASE_ERR_INVALID, "n_eta=%d", n_eta);
+    const int64_t W = traces->n_steps - history_len;
+    if (ld_c < round_up(W, 16) || ld_c % 16) return fail(CHASE_ERR_INVALID, "ld_c must be a multiple of 16 >= round_up(W,16)");
+    if (!d_sum) return fail(CHASE_ERR_INVALID, "d_sum is NULL");
+    if (traces->n_traces > 0 && (!d_choice || ((uintptr_t)d_choice & 15)))
+        return fail(CHASE_ERR_INVALID, "d_choice NULL or not 16-byte aligned");
+    const int T = 86400 / traces->interval_s;
+    const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, n_eta);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    std::vector<double> etas((size_t)n_eta, 0.5);  // eta is not used by the replay; tables need a value
+    chase_cost_cfg_t cc{etas.data(), n_eta, 0, 0.0, 0.0};
+    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, &cc, n_eta);
+    if ((st = check_smem((int)blob.size(), T, traces))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    SweepParams p = base_sweep(traces, history_len, WL, ws, (int)blob.size());
+    p.n_eta = n_eta;
+    p.n_prof = n_profiles;
+    p.profile_id = d_profile_id;
+    p.job = d_job_samples;
+    p.choice_in = d_choice;
+    p.ld_c = ld_c;
+    p.per_trace = d_per_trace;
+    int grid = 0;
+    ev_start(s);
+    cudaError_t e = launch_sweep(MODE_REPLAY, traces->dtype == CHASE_F64, aligned_start(traces, history_len), p,
+                                 kMaxGrid, &grid, s);
+    ev_stop(s);
+    if (e != cudaSuccess) return cuda_fail(e, "replay kernel");
+    e = launch_finalize(p.cta_sums, grid, n_eta, d_sum, p.status, traces->n_traces, nullptr, 0, W, 0, nullptr, 0,
+                        p.diag, s);
+    if (e != cudaSuccess) return cuda_fail(e, "finalize");
+    return CHASE_OK;
+}
+
+chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg,
+                           const chase_profile_t* profiles, int32_t n_profiles, const uint8_t* d_profile_id,
+                           const chase_cost_cfg_t* cost, const double* d_job_samples, uint8_t* d_choice, int64_t ld_c,
+                           double* d_forecast, int64_t ld_f, chase_totals_t* d_per_trace, chase_sum_t* d_sum,
+                           void* nccl_comm, void* d_ws, size_t ws_bytes, void* stream) {
+    chase_status_t st;
+    if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
+    if ((st = check_profiles(profiles, n_profiles)) || (st = check_cost(cost, profiles, n_profiles))) return st;
+    if (nccl_comm) return fail(CHASE_ERR_INVALID, "nccl_comm must be NULL: all-reduce d_sum with the caller's NCCL");
+    if (!d_sum) return fail(CHASE_ERR_INVALID, "d_sum is NULL");
+    const int64_t W = traces->n_steps - fcfg->history_len;
+    if (d_choice && (ld_c < round_up(W, 16) || ld_c % 16 || ((uintptr_t)d_choice & 15)))
+        return fail(CHASE_ERR_INVALID, "d_choice must be 16-byte aligned with ld_c a multiple of 16 >= round_up(W,16)");
+    if (d_forecast && ld_f < W) return fail(CHASE_ERR_INVALID, "ld_f < W");
+    const int T = fcfg->steps_per_day;
+    const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, cost->n_eta);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, cost, cost->n_eta);
+    if ((st = check_smem((int)blob.size(), T, traces))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    cudaError_t e = launch_fit(make_fit(traces, fcfg, ws, WL), s);
+    if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
+    SweepParams p = base_sweep(traces, fcfg->history_len, WL, ws, (int)blob.size());
+    p.n_eta = cost->n_eta;
+    p.n_prof = n_profiles;
+    p.profile_id = d_profile_id;
+    p.job = d_job_samples;
+    p.max_ci_fixed = cost->max_ci;
+    p.choice = d_choice;
+    p.ld_c = ld_c;
+    p.forecast = d_forecast;
+    p.ld_f = ld_f;
+    p.per_trace = d_per_trace;
+    int grid = 0;
+    ev_start(s);
+    e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, kMaxGrid,
+                     &grid, s);
+    ev_stop(s);
+    if (e != cudaSuccess) return cuda_fail(e, "sweep kernel");
+    e = launch_finalize(p.cta_sums, grid, cost->n_eta, d_sum, p.status, traces->n_traces, d_choice, ld_c, W,
+                        cost->n_eta, d_forecast, ld_f, p.diag, s);
+    if (e != cudaSuccess) return cuda_fail(e, "finalize");
+    return CHASE_OK;
+}
+
+uint64_t chase_kernel_launches(void) { return kernel_launches(); }
+
+void chase_set_kernel_events(void* start, void* stop) {
+    g_ev_start = static_cast<cudaEvent_t>(start);
+    g_ev_stop = static_cast<cudaEvent_t>(stop);
+}
+
+// ---- host-input streaming sweep (e2e) ----------------------------------
+// Staging: 2 slots x {traces chunk, profile ids, job samples, chunk sums}
+// + one accumulator [n_eta][8].
+static size_t host_slot_bytes(const chase_traces_t* t, int64_t chunk, int n_eta) {
+    const size_t esz = t->dtype == CHASE_F64 ? 8 : 4;
+    return round_up(chunk * t->ld * esz, kWsAlign) + round_up(chunk, kWsAlign) + round_up(chunk * 8, kWsAlign) +
+           round_up((int64_t)n_eta * 64, kWsAlign);
+}
+
+size_t chase_sweep_host_staging_bytes(const chase_traces_t* h_traces, int64_t chunk_traces, int32_t n_eta) {
+    if (!h_traces || chunk_traces < 1 || n_eta < 1 || n_eta > CHASE_MAX_ETA) return 0;
+    return 2 * host_slot_bytes(h_traces, chunk_traces, n_eta) + round_up((int64_t)n_eta * 64, kWsAlign);
+}
+
+chase_status_t chase_sweep_host(const chase_traces_t* h_traces, const chase_forecast_cfg_t* fcfg,
+                                const chase_profile_t* profiles, int32_t n_profiles, const uint8_t* h_profile_id,
+                                const chase_cost_cfg_t* cost, const double* h_job_samples, int64_t chunk_traces,
+                                chase_sum_t* h_sum, void* d_staging, size_t staging_bytes, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+    chase_status_t st;
+    if ((st = check_traces(h_traces)) || (st = check_fcfg(h_traces, fcfg))) return st;
+    if ((st = check_profiles(profiles, n_profiles)) || (st = check_cost(cost, profiles, n_profiles))) return st;
+    if (!h_sum || chunk_traces < 1) return fail(CHASE_ERR_INVALID, "h_sum NULL or chunk_traces < 1");
+    const size_t need = chase_sweep_host_staging_bytes(h_traces, chunk_traces, cost->n_eta);
+    if (!d_staging || ((uintptr_t)d_staging % kWsAlign) || staging_bytes < need)
+        return fail(CHASE_ERR_WORKSPACE, "staging %zu bytes < required %zu (or misaligned)", staging_bytes, need);
+    const int n_eta = cost->n_eta;
+    const size_t esz = h_traces->dtype == CHASE_F64 ? 8 : 4;
+    const size_t slot = host_slot_bytes(h_traces, chunk_traces, n_eta);
+    uint8_t* stg = static_cast<uint8_t*>(d_staging);
+    double* acc = reinterpret_cast<double*>(stg + 2 * slot);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t loaded[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int q = 0; q < 2 && e == cudaSuccess; ++q) {
+        e = cudaEventCreateWithFlags(&loaded[q], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[q], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(acc, 0, (size_t)n_eta * 64, s);
+    const int64_t n = h_traces->n_traces;
+    const uint8_t* hbase = static_cast<const uint8_t*>(h_traces->data);
+    st = CHASE_OK;
+    for (int64_t c0 = 0, c = 0; c0 < n && e == cudaSuccess && st == CHASE_OK; c0 += chunk_traces, ++c) {
+        const int64_t m = std::min(chunk_traces, n - c0);
+        const int q = (int)(c & 1);
+        uint8_t* base = stg + q * slot;
+        uint8_t* d_tr = base;
+        uint8_t* d_pid = base + round_up(chunk_traces * h_traces->ld * esz, kWsAlign);
+        double* d_job = reinterpret_cast<double*>(d_pid + round_up(chunk_traces, kWsAlign));
+        chase_sum_t* d_sum = reinterpret_cast<chase_sum_t*>(reinterpret_cast<uint8_t*>(d_job) +
+                                                            round_up(chunk_traces * 8, kWsAlign));
+        if (c >= 2) e = cudaStreamWaitEvent(cs, freed[q], 0);  // slot reused: kernels of chunk c-2 done
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_tr, hbase + c0 * h_traces->ld * esz, (size_t)(m * h_traces->ld * esz),
+                                cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess && h_profile_id)
+            e = cudaMemcpyAsync(d_pid, h_profile_id + c0, (size_t)m, cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess && h_job_samples)
+            e = cudaMemcpyAsync(d_job, h_job_samples + c0, (size_t)m * 8, cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(loaded[q], cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, loaded[q], 0);
+        if (e != cudaSuccess) break;
+        chase_traces_t t = *h_traces;
+        t.data = d_tr;
+        t.n_traces = m;
+        st = chase_sweep(&t, fcfg, profiles, n_profiles, h_profile_id ? d_pid : nullptr, cost,
+                         h_job_samples ? d_job : nullptr, nullptr, 0, nullptr, 0, nullptr, d_sum, nullptr, d_ws,
+                         ws_bytes, stream);
+        if (st == CHASE_OK) e = launch_accumulate(acc, reinterpret_cast<const double*>(d_sum), n_eta * 8, s);
+        if (e == cudaSuccess) e = cudaEventRecord(freed[q], s);
+    }
+    if (e == cudaSuccess && st == CHASE_OK)
+        e = cudaMemcpyAsync(h_sum, acc, (size_t)n_eta * sizeof(chase_sum_t), cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+    cudaStreamSynchronize(cs);
+    for (int q = 0; q < 2; ++q) {
+        if (loaded[q]) cudaEventDestroy(loaded[q]);
+        if (freed[q]) cudaEventDestroy(freed[q]);
+    }
+    if (cs) cudaStreamDestroy(cs);
+    if (st != CHASE_OK) return st;
+    if (e != cudaSuccess) return cuda_fail(e, "chase_sweep_host");
+    return CHASE_OK;
+}
+
+chase_status_t chase_diag_read(const void* d_ws, chase_diag_t* out, void* stream) {
+    if (!d_ws || !out) return fail(CHASE_ERR_INVALID, "NULL argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(out, d_ws, sizeof(chase_diag_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "diag read");
+    return CHASE_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- test hook
+#include "chase_testing.h"
+
+extern "C" int32_t chase_testing_envelope(int32_t K, const double* avg_power, const double* thr, double eta,
+                                          double pmax, double max_ci, int64_t n, const double* x, int32_t* out) {
+    if (K < 2 || K > kMaxK || !avg_power || !thr || !x || !out) return -1;
+    static thread_local PairTable pt;
+    std::vector<FastInterval> iv = build_pair_table(K, avg_power, thr, eta, pmax, &pt);
+    // identical to the kernel: Kc = kbase*MaxCI, invK, y, bucket, thresholds
+    const double Kc = pt.kbase * max_ci;
+    double invK;
+    if (pt.k0) invK = 1.0;
+    else invK = (Kc >= 0x1p-900 && Kc <= 0x1p900) ? 1.0 / Kc : std::nan("");
+    for (int64_t i = 0; i < n; ++i) {
+        const double y = x[i] * invK;
+        uint64_t bits;
+        std::memcpy(&bits, &y, 8);
+        int hi = (int)(int32_t)(uint32_t)(bits >> 32);
+        int idx = (hi >> kSH) - pt.base;
+        idx = idx < 0 ? 0 : (idx > kNBUsed - 1 ? kNBUsed - 1 : idx);
+        uint32_t e = pt.ent[idx];
+        double2 th = pt.slots[e >> 10];
+        bool p1 = y <= th.x, p2 = y >= th.y;
+        out[i] = (p1 || p2) ? (int32_t)(p1 ? (e & 31u) : ((e >> 5) & 31u)) : -1;
+    }
+    return (int32_t)iv.size();
+}

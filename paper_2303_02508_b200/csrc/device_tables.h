@@ -1,0 +1,60 @@
+// device_tables.h — layout of the per-call constant tables that the host
+// builds (envelope.cpp) and the kernels stage into shared memory.
+//
+// Blob = TablesHeader | phase S[T], C[T] (f64) | ProfileTable[n_prof] |
+//        PairTable[n_prof * n_eta]     (pair index = p * n_eta + e)
+#pragma once
+#include <stdint.h>
+#include <vector_types.h>      // double2
+#include <vector_functions.h>  // make_double2
+
+namespace chase {
+
+constexpr int kMaxK = 32;          // CHASE_MAX_LIMITS
+constexpr int kNB = 776;           // buckets per pair table (12 octaves x 64 + 2, padded to 8)
+constexpr int kNBUsed = 770;       // bucket 0 = below range, 1..768 = table, 769 = above
+constexpr int kSH = 14;            // hi32(y) >> 14 = sign | 11-bit exponent | 6 mantissa bits
+constexpr int kMaxSlots = 64;      // threshold pairs per table (6-bit slot field)
+constexpr int kSlotFast = 0;       // (+inf, +inf): always "below" line
+constexpr int kSlotSlow = 1;       // (NaN, NaN): always the canonical K-way path
+
+// Entry encoding (uint16): below (5 bits) | above << 5 (5 bits) | slot << 10.
+// Per window: p1 = y <= t_lo, p2 = y >= t_hi; choice = p1 ? below : above;
+// (!p1 && !p2) -> canonical Eq. 6.  See DESIGN.md §6 (a5 envelope path).
+
+struct alignas(16) TablesHeader {
+    int32_t T, n_prof, n_eta, n_pairs;
+    int32_t off_phase, off_prof, off_pair, total_bytes;
+    double delta;
+    double reserved[3];
+};
+
+struct alignas(16) ProfileTable {
+    double2 line[kMaxK];   // (s_k = Thr_k * Delta, P_k)
+    double thr[kMaxK];     // Thr_k
+    int32_t K, reserved;
+    double pmax;           // resolved MaxPower
+};
+
+struct alignas(16) PairTable {
+    double a[kMaxK];       // a_k = eta * P_k
+    double kbase;          // (1 - eta) * Pmax; Kc = kbase * MaxCI
+    int32_t base;          // idx = clamp((hi32(y) >> kSH) - base, 0, kNBUsed - 1)
+    int32_t k0;            // 1: Kc == 0 (eta == 1) -> y = x; 0: y = x * (1/Kc)
+    int32_t n_slots;
+    int32_t n_intervals;   // fast intervals (diagnostic)
+    double2 slots[kMaxSlots];
+    uint16_t ent[kNB];
+};
+
+static_assert(sizeof(TablesHeader) % 16 == 0, "header alignment");
+static_assert(sizeof(ProfileTable) % 16 == 0, "profile alignment");
+static_assert(sizeof(PairTable) % 16 == 0, "pair alignment");
+
+inline int tables_bytes(int T, int n_prof, int n_eta) {
+    int phase = ((2 * T * 8) + 15) / 16 * 16;
+    return (int)sizeof(TablesHeader) + phase + n_prof * (int)sizeof(ProfileTable) +
+           n_prof * n_eta * (int)sizeof(PairTable);
+}
+
+}  // namespace chase

@@ -1,0 +1,217 @@
+// envelope.cpp — see envelope.h.  Host-only, long double (x87, 64-bit mantissa).
+#include "envelope.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace chase {
+namespace {
+
+using ld = long double;
+
+constexpr ld kDelta = 0x1p-47L;        // 64u: required relative gap to every other line
+constexpr ld kShrink = 0x1p-49L;       // 16u: absorbs the 2 roundings of y = x * (1/Kc)
+constexpr double kYMax = 0x1p900;      // beyond: canonical path (overflow safety)
+constexpr double kYMinK0 = 0x1p-900;   // eta == 1: below -> canonical (x == 0, underflow)
+
+struct Line {
+    int k;
+    ld a, T;
+};
+
+inline ld cval(const Line& L, ld y) { return (L.a * y + 1.0L) / L.T; }
+
+// Relative gap of line `o` over line `j` at y (y = inf: the limit).  Every term
+// is positive, so this is accurate to a few long-double ulps (~1e-19).
+ld gap(const Line& o, const Line& j, ld y, bool k0) {
+    if (k0) return (o.a * j.T) / (j.a * o.T) - 1.0L;       // costs a x / T
+    if (std::isinf(y)) {
+        if (j.a > 0) return (o.a * j.T) / (j.a * o.T) - 1.0L;
+        if (o.a > 0) return INFINITY;
+        return j.T / o.T - 1.0L;
+    }
+    return cval(o, y) / cval(j, y) - 1.0L;
+}
+
+bool verify(const std::vector<Line>& L, int j, ld y, bool k0) {
+    for (size_t o = 0; o < L.size(); ++o)
+        if ((int)o != j && !(gap(L[o], L[j], y, k0) >= kDelta)) return false;
+    return true;
+}
+
+double round_up_d(ld v) {
+    double d = (double)v;
+    if ((ld)d < v) d = std::nextafter(d, INFINITY);
+    return d;
+}
+double round_down_d(ld v) {
+    double d = (double)v;
+    if ((ld)d > v) d = std::nextafter(d, -INFINITY);
+    return d;
+}
+
+// Fast interval of line j inside [P, Q] (Q may be inf); false if empty.
+bool fast_subinterval(const std::vector<Line>& L, int j, ld P, ld Q, ld* lo_out, ld* hi_out) {
+    ld lo = P, hi = Q;
+    const Line& J = L[j];
+    for (size_t o = 0; o < L.size(); ++o) {
+        if ((int)o == j) continue;
+        // c_o(y) >= (1+d) c_j(y)  <=>  y * (a_o T_j - (1+d) a_j T_o) >= (1+d) T_o - T_j
+        ld A = L[o].a * J.T - (1.0L + kDelta) * J.a * L[o].T;
+        ld B = (1.0L + kDelta) * L[o].T - J.T;
+        if (A > 0) lo = std::max(lo, B / A);
+        else if (A < 0) hi = std::min(hi, B / A);
+        else if (B > 0) return false;
+    }
+    if (!(lo <= hi)) return false;
+    // Robust endpoint verification (the gap is linear-fractional, hence
+    // monotone, in y on the interval): nudge inward until it passes.
+    ld step = 0x1p-40L;
+    for (int it = 0; it < 80 && !verify(L, j, lo, false); ++it, step *= 2) {
+        lo = lo == 0 ? 0x1p-1000L : lo * (1.0L + step);
+        if (!(lo <= hi)) return false;
+    }
+    if (!verify(L, j, lo, false)) return false;
+    step = 0x1p-40L;
+    for (int it = 0; it < 80 && !verify(L, j, hi, false); ++it, step *= 2) {
+        hi = std::isinf(hi) ? std::max(lo * 2, (ld)1e30L) : hi * (1.0L - step);
+        if (!(lo <= hi)) return false;
+    }
+    if (!verify(L, j, hi, false)) return false;
+    *lo_out = lo;
+    *hi_out = hi;
+    return true;
+}
+
+double bucket_start(int base_raw, int b) {   // b in [1, kNBUsed - 1]
+    uint64_t hi = (uint64_t)(uint32_t)((base_raw + b - 1) << kSH);
+    uint64_t bits = hi << 32;
+    double v;
+    std::memcpy(&v, &bits, 8);
+    return v;
+}
+
+}  // namespace
+
+std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const double* thr,
+                                           double eta, double pmax, PairTable* out) {
+    std::memset(out, 0, sizeof(*out));
+    for (int k = 0; k < K; ++k) out->a[k] = eta * avg_power[k];   // same rounding as Eq. 6
+    out->kbase = (1.0 - eta) * pmax;
+    const bool k0 = !(out->kbase > 0.0);
+    out->k0 = k0 ? 1 : 0;
+
+    // Distinct lines, lowest index first (identical rows give bitwise-equal
+    // costs, so first-min keeps the lowest).
+    std::vector<Line> L;
+    for (int k = 0; k < K; ++k) {
+        bool dup = false;
+        for (const Line& l : L)
+            if (l.a == (ld)out->a[k] && l.T == (ld)thr[k]) dup = true;
+        if (!dup) L.push_back({k, (ld)out->a[k], (ld)thr[k]});
+    }
+
+    std::vector<FastInterval> iv;
+    if (k0) {
+        // costs a_k x / Thr_k: one winner for every x > 0 if its ratio is
+        // separated; x == 0 (all costs 0 -> index 0) stays canonical.
+        int j = 0;
+        for (size_t o = 1; o < L.size(); ++o)
+            if (L[o].a * L[j].T < L[j].a * L[o].T) j = (int)o;
+        ld amin = L[0].a;
+        for (const Line& l : L) amin = std::min(amin, l.a);
+        if (verify(L, j, 1.0L, true) && amin >= 0x1p-100L) iv.push_back({kYMinK0, kYMax, L[j].k});
+    } else {
+        std::vector<ld> pts{0.0L};
+        for (size_t i = 0; i < L.size(); ++i)
+            for (size_t o = i + 1; o < L.size(); ++o) {
+                ld den = L[i].a * L[o].T - L[o].a * L[i].T;
+                if (den == 0) continue;
+                ld y = (L[i].T - L[o].T) / den;
+                if (y > 0 && std::isfinite(y)) pts.push_back(y);
+            }
+        std::sort(pts.begin(), pts.end());
+        pts.erase(std::unique(pts.begin(), pts.end()), pts.end());
+        struct Seg { ld P, Q; int j; };
+        std::vector<Seg> segs;
+        for (size_t i = 0; i < pts.size(); ++i) {
+            ld P = pts[i], Q = i + 1 < pts.size() ? pts[i + 1] : (ld)INFINITY;
+            ld mid = std::isinf(Q) ? (P == 0 ? 1.0L : P * 2 + 1) : (P + Q) / 2;
+            int j = 0;
+            for (size_t o = 1; o < L.size(); ++o)
+                if (cval(L[o], mid) < cval(L[j], mid)) j = (int)o;
+            if (!segs.empty() && segs.back().j == j) segs.back().Q = Q;
+            else segs.push_back({P, Q, j});
+        }
+        for (const Seg& s : segs) {
+            ld lo, hi;
+            if (!fast_subinterval(L, s.j, s.P, s.Q, &lo, &hi)) continue;
+            double lo_d = lo == 0 ? 0.0 : round_up_d(lo * (1.0L + kShrink));
+            double hi_d = std::isinf(hi) ? (double)INFINITY : round_down_d(hi * (1.0L - kShrink));
+            hi_d = std::min(hi_d, kYMax);
+            if (lo_d <= hi_d) iv.push_back({lo_d, hi_d, L[s.j].k});
+        }
+    }
+    std::sort(iv.begin(), iv.end(), [](const FastInterval& a, const FastInterval& b) { return a.lo < b.lo; });
+    out->n_intervals = (int)iv.size();
+
+    // Bucket range: 12 octaves from the octave of the smallest positive endpoint.
+    double vmin = INFINITY;
+    for (const FastInterval& f : iv) {
+        if (f.lo > 0) vmin = std::min(vmin, f.lo);
+        if (std::isfinite(f.hi) && f.hi > 0) vmin = std::min(vmin, f.hi);
+    }
+    int E0 = 0;
+    if (std::isfinite(vmin)) {
+        int e;
+        std::frexp(vmin, &e);
+        E0 = std::max(-1000, std::min(1000, e - 1));
+    }
+    const int base_raw = (E0 + 1023) << 6;
+    out->base = base_raw - 1;
+
+    const double NaN = std::nan("");
+    out->slots[kSlotFast] = make_double2(INFINITY, INFINITY);
+    out->slots[kSlotSlow] = make_double2(NaN, NaN);
+    int n_slots = 2;
+    for (int b = 0; b < kNB; ++b) {
+        if (b >= kNBUsed) { out->ent[b] = (uint16_t)(kSlotSlow << 10); continue; }
+        double vb = b == 0 ? 0.0 : bucket_start(base_raw, b);
+        double ve = b == kNBUsed - 1 ? (double)INFINITY : bucket_start(base_raw, b + 1);
+        const FastInterval* cover = nullptr;
+        const FastInterval* below = nullptr;
+        const FastInterval* above = nullptr;
+        for (const FastInterval& f : iv) {
+            if (f.lo <= vb && f.hi >= ve) cover = &f;
+            else if (f.lo <= vb && vb <= f.hi && f.hi < ve) below = &f;
+            else if (vb < f.lo && f.lo < ve && f.hi >= ve) above = &f;
+        }
+        uint16_t e;
+        if (cover) {
+            e = (uint16_t)(cover->k | (cover->k << 5) | (kSlotFast << 10));
+        } else if (!below && !above) {
+            e = (uint16_t)(kSlotSlow << 10);
+        } else {
+            double tlo = below ? below->hi : NaN, thi = above ? above->lo : NaN;
+            int slot = -1;
+            for (int s = 2; s < n_slots; ++s) {
+                double2 v = out->slots[s];
+                bool same_lo = (std::isnan(v.x) && std::isnan(tlo)) || v.x == tlo;
+                bool same_hi = (std::isnan(v.y) && std::isnan(thi)) || v.y == thi;
+                if (same_lo && same_hi) slot = s;
+            }
+            if (slot < 0 && n_slots < kMaxSlots) {
+                slot = n_slots++;
+                out->slots[slot] = make_double2(tlo, thi);
+            }
+            if (slot < 0) e = (uint16_t)(kSlotSlow << 10);
+            else e = (uint16_t)((below ? below->k : 0) | ((above ? above->k : 0) << 5) | (slot << 10));
+        }
+        out->ent[b] = e;
+    }
+    out->n_slots = n_slots;
+    return iv;
+}
+
+}  // namespace chase

@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star):
+  - chosen power-limit index: bit-exact (ties -> lowest index);
+  - forecasts: bit-identical here (same canonical order; <= 1e-9 is the bar);
+  - per-trace totals: bit-identical for the dyadic synthetic inputs;
+  - per-GPU sums: <= 1e-9 relative (fixed but different summation order).
+"""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2303_02508_b200 as cb  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def run_sweep(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0,
+              dtype=torch.float32, forecast=True):
+    x = torch.from_numpy(np.ascontiguousarray(tr_host)).to(DEV, dtype)
+    pid_t = None if pid is None else torch.from_numpy(np.ascontiguousarray(pid, np.uint8)).to(DEV)
+    J_t = None if J is None else torch.from_numpy(np.ascontiguousarray(J, np.float64)).to(DEV)
+    pl = cb.Planner(x, n_steps=N, profiles=profiles, etas=etas, interval_s=interval_s, history_len=L,
+                    phase0=phase0, profile_id=pid_t, job_samples=J_t, want_choice=True, want_forecast=forecast,
+                    want_per_trace=True, max_ci=max_ci)
+    res = pl.run()
+    torch.cuda.synchronize()
+    out = dict(sums=res.sums.cpu().numpy(), totals=res.per_trace_numpy(),
+               choice=res.choice.cpu().numpy()[:, :, :N - L],
+               forecast=None if res.forecast is None else res.forecast.cpu().numpy(), diag=pl.diag())
+    return out
+
+
+def run_oracle(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0):
+    T = 86400 // interval_s
+    return oracle.plan_batch(np.ascontiguousarray(tr_host, np.float32), N=N, L=L, T=T, phase0=phase0,
+                             profiles=profiles, profile_id=pid, etas=etas, max_ci=max_ci,
+                             delta=float(interval_s), job_samples=J)
+
+
+def assert_parity(g, o, *, exact_totals=True):
+    assert np.array_equal(g["choice"], o["choice"]), _first_diff(g["choice"], o["choice"])
+    if g["forecast"] is not None:
+        fo, fg = o["forecast"], g["forecast"]
+        ok = np.isnan(fo)
+        assert np.array_equal(np.isnan(fg), ok)
+        assert np.array_equal(fg[~ok], fo[~ok])          # bit-identical forecasts
+    gt, ot = g["totals"], o["totals"]
+    assert np.array_equal(gt["status"], ot["status"])
+    assert np.array_equal(gt["completion_window"], ot["completion_window"])
+    for f in ("time_s", "energy_j", "carbon_g", "samples", "base_time_s", "base_energy_j", "base_carbon_g"):
+        if exact_totals:
+            assert np.array_equal(gt[f], ot[f]), (f, _first_diff(gt[f], ot[f]))
+        else:
+            np.testing.assert_allclose(gt[f], ot[f], rtol=1e-9, atol=0)
+    np.testing.assert_allclose(g["sums"], o["sums"], rtol=1e-9, atol=1e-300)
+
+
+def _first_diff(a, b):
+    idx = np.argwhere(a != b)
+    if len(idx) == 0:
+        return "equal"
+    i = tuple(idx[0])
+    return f"first diff at {i}: gpu={a[i]} oracle={b[i]} ({len(idx)} diffs)"
+
+
+# ------------------------------------------------------------------ generator
+def test_device_generator_matches_host():
+    for mode, n, N in [(inputs.MODE_RANDOM, 37, 8784), (inputs.MODE_PAPER, 2, 195)]:
+        h = inputs.synth_traces_host(n, N, seed=5, mode=mode, trace0=11)
+        d = torch.empty(h.shape, dtype=torch.float32, device=DEV)
+        inputs.synth_traces_device(d, N, seed=5, mode=mode, trace0=11)
+        assert np.array_equal(d.cpu().numpy(), h)
+    pid = torch.empty(1000, dtype=torch.uint8, device=DEV)
+    inputs.profile_ids_device(pid, seed=4, n_profiles=3)
+    assert np.array_equal(pid.cpu().numpy(), inputs.profile_ids_host(1000, seed=4, n_profiles=3))
+
+
+# ------------------------------------------------------------------ configs
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_paper_configs_full_parity(name):
+    w = inputs.workload(name)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=w.seed, mode=w.mode)
+    J = w.job_samples()
+    g = run_sweep(tr, w.n_steps, w.profiles, w.etas, J=J)
+    o = run_oracle(tr, w.n_steps, w.profiles, w.etas, J=J)
+    assert_parity(g, o)
+    assert o["totals"]["carbon_g"][0, 0] < o["totals"]["base_carbon_g"][0, 0]
+
+
+def test_multi_profile_multi_eta():
+    """C4-shaped (3 profile shapes per trace) with an eta list incl. 0 and 1."""
+    w = inputs.workload("C4", n_traces=300)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=w.seed)
+    pid = inputs.profile_ids_host(w.n_traces, seed=w.seed, n_profiles=3)
+    J = w.job_samples(pid)
+    etas = [0.0, 0.25, 0.5, 0.9, 1.0]
+    g = run_sweep(tr, w.n_steps, w.profiles, etas, pid=pid, J=J)
+    o = run_oracle(tr, w.n_steps, w.profiles, etas, pid=pid, J=J)
+    assert_parity(g, o)
+    assert g["diag"].n_bad == 0
+
+
+def test_multi_tile_eta_sweep():
+    """C3-shaped: 5-year traces (5 tiles of 9216 windows each) x 11 etas."""
+    w = inputs.workload("C3", n_traces=5)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=w.seed)
+    J = w.job_samples()
+    g = run_sweep(tr, w.n_steps, w.profiles, w.etas, J=J)
+    o = run_oracle(tr, w.n_steps, w.profiles, w.etas, J=J)
+    assert_parity(g, o)
+    # fixed-duration mode (no job budget) over the same traces
+    g0 = run_sweep(tr, w.n_steps, w.profiles, w.etas[:3], forecast=False)
+    o0 = run_oracle(tr, w.n_steps, w.profiles, w.etas[:3])
+    g0["forecast"] = None
+    assert_parity(g0, o0)
+
+
+@pytest.mark.parametrize("L,N,interval,phase0,n", [
+    (23, 24 + 37, 3600, 5, 3),          # odd L -> unaligned tile path, W=37
+    (24, 25, 3600, 0, 2),               # W = 1
+    (48, 48 + 1001, 1800, 7, 700),      # half-hourly (T=48), more traces than CTAs
+    (24, 24 + 9217, 3600, 23, 2),       # one window past a tile boundary
+    (96, 96 + 500, 900, 40, 9),         # 15-minute data (T=96)
+])
+def test_ragged_shapes(L, N, interval, phase0, n):
+    T = 86400 // interval
+    prof = [inputs.make_profile("vit", inputs.LIMITS_9)]
+    tr = inputs.synth_traces_host(n, N, seed=17, T=T, phase0=phase0)
+    J = np.full(n, interval * (N - L) * prof[0].throughput_sps.min() * 0.8)
+    g = run_sweep(tr, N, prof, [0.5, 0.8], J=J, L=L, interval_s=interval, phase0=phase0)
+    o = run_oracle(tr, N, prof, [0.5, 0.8], J=J, L=L, interval_s=interval, phase0=phase0)
+    assert_parity(g, o)
+
+
+def test_f64_traces():
+    w = inputs.workload("C4", n_traces=20)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=9).astype(np.float64)
+    J = w.job_samples()
+    g = run_sweep(tr, w.n_steps, w.profiles[:1], [0.5], J=J, dtype=torch.float64)
+    o = oracle.plan_batch(tr.astype(np.float32), N=w.n_steps, L=24, T=24, profiles=w.profiles[:1], etas=[0.5],
+                          job_samples=J)
+    assert_parity(g, o)
+
+
+def test_invalid_traces_and_exhaustion():
+    N, n = 24 + 300, 8
+    prof = [inputs.make_profile("resnet50", inputs.LIMITS_9)]
+    tr = inputs.synth_traces_host(n, N, seed=2)
+    tr[1, 100] = -3.0                 # S:29 negative -> 4
+    tr[2, 5] = np.nan                 # in the history -> 4
+    tr[3, :24] = 0.0                  # MaxCI = 0 -> 5
+    tr[4, 200] = np.inf               # -> 4
+    J = np.full(n, 3600 * 300 * prof[0].throughput_sps.min())
+    J[5] = 3600 * 300 * prof[0].throughput_sps.max() * 2      # exhausted -> 3
+    g = run_sweep(tr, N, prof, [0.5], J=J)
+    o = run_oracle(tr, N, prof, [0.5], J=J)
+    assert list(o["totals"]["status"][0]) == [0, 4, 4, 5, 4, 3, 0, 0]
+    assert_parity(g, o)
+    d = g["diag"]
+    assert d.n_bad == 4 and d.first_bad_trace == 1 and d.first_bad_status == 4 and d.n_exhausted == 1
+
+
+def test_fixed_maxci_and_pmax():
+    w = inputs.workload("C4", n_traces=50)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=21)
+    J = w.job_samples()
+    g = run_sweep(tr, w.n_steps, w.profiles[:1], [0.5, 0.7], J=J, max_ci=750.0)
+    o = run_oracle(tr, w.n_steps, w.profiles[:1], [0.5, 0.7], J=J, max_ci=750.0)
+    assert_parity(g, o)
+
+
+# ------------------------------------------------------------------ split path
+def test_fit_forecast_matches_oracle():
+    w = inputs.workload("C4", n_traces=257)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=31)
+    tr[7, 3] = -1.0
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=w.n_steps)
+    f = cb.make_fcfg()
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    fc = torch.empty((w.n_traces, w.W + 3), dtype=torch.float64, device=DEV)
+    mci = torch.empty(w.n_traces, dtype=torch.float64, device=DEV)
+    models = torch.empty((w.n_traces, 8), dtype=torch.float64, device=DEV)
+    cb.fit_forecast(t, f, fc, w.W + 3, ws, max_ci=mci, models=models)
+    torch.cuda.synchronize()
+    o = oracle.plan_batch(tr, N=w.n_steps, L=24, T=24, profiles=w.profiles[:1], etas=[0.5])
+    fg = fc.cpu().numpy()[:, :w.W]
+    assert np.array_equal(np.isnan(fg), np.isnan(o["forecast"]))
+    ok = ~np.isnan(o["forecast"])
+    assert np.array_equal(fg[ok], o["forecast"][ok])
+    assert np.array_equal(mci.cpu().numpy()[[0, 5, 256]], tr[[0, 5, 256], :24].max(axis=1).astype(np.float64))
+    m = models.cpu().numpy()
+    om = oracle.fit(tr[0, :24].astype(np.float64), T=24)
+    assert [m[0, 0], m[0, 1], m[0, 2], m[0, 3]] == [om.c0, om.ws, om.wc, om.wl]
+    assert m[7, 5] == 4.0
+
+
+def _plan_gpu(fc, profiles, etas, maxci_vec, pid=None):
+    n, W = fc.shape
+    ld_c = cb.round_up(W, 16)
+    f = torch.from_numpy(np.ascontiguousarray(fc)).to(DEV)
+    ch = torch.empty((len(etas), n, ld_c), dtype=torch.uint8, device=DEV)
+    mci = torch.from_numpy(np.asarray(maxci_vec, np.float64)).to(DEV)
+    pid_t = None if pid is None else torch.from_numpy(pid).to(DEV)
+    ws = cb.alloc_workspace(1 << 22, DEV)
+    cb.plan_power_limits(f, n, W, W, profiles, etas, ch, ld_c, ws, profile_id=pid_t, max_ci_per_trace=mci)
+    torch.cuda.synchronize()
+    return ch.cpu().numpy()[:, :, :W], cb.diag_read(ws)
+
+
+def test_plan_adversarial_ulp_sweeps():
+    """Forecasts swept +-300 ulps around every exact breakpoint of every
+    (profile, eta): the kernel's choice equals the oracle's canonical one."""
+    from fractions import Fraction as F
+    profiles = [inputs.make_profile(s, inputs.LIMITS_9) for s in ("resnet50", "bert", "vit")]
+    etas = [0.0, 0.3, 0.5, 0.9, 1.0]
+    maxci = 750.0
+    rows = []
+    for p in profiles:
+        xs = []
+        for eta in etas:
+            Kc = (1 - F(eta)) * 300 * F(maxci)
+            for j in range(p.K):
+                for k in range(j + 1, p.K):
+                    aj, ak = F(eta) * F(p.avg_power_w[j]), F(eta) * F(p.avg_power_w[k])
+                    den = aj * F(p.throughput_sps[k]) - ak * F(p.throughput_sps[j])
+                    if den != 0:
+                        xc = Kc * (F(p.throughput_sps[j]) - F(p.throughput_sps[k])) / den
+                        if 0 < xc < 1e6:
+                            x = float(xc)
+                            for _ in range(300):
+                                x = np.nextafter(x, -np.inf)
+                            for _ in range(601):
+                                xs.append(x)
+                                x = np.nextafter(x, np.inf)
+        xs += [0.0, 750.0, 1e-300, 4095.984375]
+        rows.append(np.array(xs))
+    W = max(len(r) for r in rows)
+    fc = np.zeros((3, W))
+    for q, r in enumerate(rows):
+        fc[q, :len(r)] = r
+    pid = np.arange(3, dtype=np.uint8)
+    ch, d = _plan_gpu(fc, profiles, etas, [maxci] * 3, pid)
+    for q in range(3):
+        P, Th = profiles[q].avg_power_w, profiles[q].throughput_sps
+        for e, eta in enumerate(etas):
+            ref = np.array([oracle.choose(P, Th, eta, 300.0, maxci, x) for x in fc[q]], dtype=np.uint8)
+            assert np.array_equal(ch[e, q], ref), (q, eta, _first_diff(ch[e, q], ref))
+    assert d.n_slow_windows > 0          # the bands were exercised
+
+
+def test_plan_invalid_forecasts_are_0xff():
+    prof = [inputs.make_profile("resnet50", inputs.LIMITS_9)]
+    fc = np.array([[500.0, -1.0, np.nan, np.inf, 0.0, 100.0, 2000.0, 7.0]])
+    ch, _ = _plan_gpu(fc, prof, [0.5], [750.0])
+    ref = [oracle.choose(prof[0].avg_power_w, prof[0].throughput_sps, 0.5, 300.0, 750.0, x) for x in fc[0]]
+    assert list(ch[0, 0]) == [ref[0], 255, 255, 255, ref[4], ref[5], ref[6], ref[7]]
+    ch0, _ = _plan_gpu(fc, prof, [0.5], [0.0])       # MaxCI <= 0 -> whole row invalid
+    assert np.all(ch0 == 255)
+
+
+def test_replay_split_path_from_oracle_choices():
+    w = inputs.workload("C4", n_traces=64)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=41)
+    pid = inputs.profile_ids_host(w.n_traces, seed=41, n_profiles=3)
+    J = w.job_samples(pid)
+    etas = [0.2, 0.6]
+    o = run_oracle(tr, w.n_steps, w.profiles, etas, pid=pid, J=J)
+    ld_c = cb.round_up(w.W, 16)
+    ch = np.full((2, w.n_traces, ld_c), 0xFF, np.uint8)
+    ch[:, :, :w.W] = o["choice"]
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=w.n_steps)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, cb.make_fcfg(), 3, 2), DEV)
+    s = torch.zeros((2, 8), dtype=torch.float64, device=DEV)
+    per = torch.empty((2, w.n_traces, 64), dtype=torch.uint8, device=DEV)
+    cb.replay(t, 24, torch.from_numpy(ch).to(DEV), ld_c, 2, w.profiles, ws, s,
+              profile_id=torch.from_numpy(pid).to(DEV), job_samples=torch.from_numpy(J).to(DEV), per_trace=per)
+    torch.cuda.synchronize()
+    gt = per.cpu().numpy().view(cb.TOTALS_DTYPE).reshape(2, w.n_traces)
+    assert gt.tobytes() == o["totals"].tobytes()
+    np.testing.assert_allclose(s.cpu().numpy(), o["sums"], rtol=1e-9)
+
+
+def test_sweep_host_e2e_path():
+    w = inputs.workload("C4", n_traces=1000)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=8)
+    pid = inputs.profile_ids_host(w.n_traces, seed=8, n_profiles=3)
+    J = w.job_samples(pid)
+    h = torch.from_numpy(tr).pin_memory()
+    t = cb.make_traces(h, n_steps=w.n_steps)
+    chunk = 300
+    tc = cb.make_traces(h[:chunk], n_steps=w.n_steps)
+    ws = cb.alloc_workspace(cb.workspace_bytes(tc, cb.make_fcfg(), 3, 1), DEV)
+    stg = cb.alloc_workspace(cb.sweep_host_staging_bytes(t, chunk, 1), DEV)
+    sums = cb.sweep_host(t, cb.make_fcfg(), w.profiles, [0.5], chunk, stg, ws, h_profile_id=pid, h_job_samples=J)
+    o = run_oracle(tr, w.n_steps, w.profiles, [0.5], pid=pid, J=J)
+    np.testing.assert_allclose(sums, o["sums"], rtol=1e-9)
+
+
+# ------------------------------------------------------------------ full size
+def test_full_size_c5_sampled():
+    """BASELINE configs[4] at full size (1e6 traces x 8784 steps, the bench's
+    launch configuration): sampled traces against the oracle one by one."""
+    w = inputs.workload("C5")
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60e9:
+        pytest.skip("needs ~50 GB of free device memory")
+    x = torch.empty((w.n_traces, w.ld), dtype=torch.float32, device=DEV)
+    inputs.synth_traces_device(x, w.n_steps, seed=w.seed)
+    J = torch.full((w.n_traces,), float(w.job_samples()[0]), dtype=torch.float64, device=DEV)
+    pl = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, job_samples=J, want_choice=True,
+                    want_per_trace=True)
+    res = pl.run()
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    sample = np.unique(np.concatenate([[0, 1, w.n_traces - 1], rng.integers(0, w.n_traces, 40)]))
+    tr = inputs.synth_traces_host(1, w.n_steps, seed=w.seed)  # warm the lib
+    per = res.per_trace[:, torch.from_numpy(sample).to(DEV)].cpu().numpy().view(cb.TOTALS_DTYPE)[..., 0]
+    ch = res.choice[:, torch.from_numpy(sample).to(DEV), :w.W].cpu().numpy()
+    for q, i in enumerate(sample):
+        tr = inputs.synth_traces_host(1, w.n_steps, seed=w.seed, trace0=int(i))
+        p = w.profiles[0]
+        fc, och, ot, st = oracle.plan_trace(tr[0, :w.n_steps], L=24, T=24, avg_power=p.avg_power_w,
+                                            thr=p.throughput_sps, etas=w.etas, pmax=300.0,
+                                            J=float(w.job_samples()[0]))
+        assert np.array_equal(ch[:, q], och), i
+        assert per[:, q].tobytes() == ot.tobytes(), i
+    s = res.sums.cpu().numpy()
+    assert s[0, 7] == w.n_traces
+    assert pl.diag().n_bad == 0
