@@ -43,10 +43,12 @@ chase_status_t cuda_fail(cudaError_t e, const char* where) {
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 constexpr size_t kWsAlign = 256;
-constexpr int kMaxGrid = 1024;  // rows of the per-CTA partial sums
 
+// Workspace: diagnostics | constant tables | per-trace records [n][16] |
+// per-(eta, trace) raw replay results [n_eta][n][8] | status [n] |
+// finalize block sums [ceil(n/256)][n_eta][8].
 struct WsLayout {
-    size_t diag, tables, records, status, cta_sums, total;
+    size_t diag, tables, records, raw, status, block_sums, total;
 };
 
 WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta) {
@@ -55,8 +57,9 @@ WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta) {
     w.diag = o; o += kWsAlign;
     w.tables = o; o += round_up(tables_bytes(T, n_prof, n_eta), kWsAlign);
     w.records = o; o += round_up(n_traces * kRecDoubles * 8, kWsAlign);
+    w.raw = o; o += round_up((int64_t)n_eta * n_traces * kRawDoubles * 8, kWsAlign);
     w.status = o; o += round_up(n_traces, kWsAlign);
-    w.cta_sums = o; o += round_up((int64_t)kMaxGrid * kMaxEta * 8 * 8, kWsAlign);
+    w.block_sums = o; o += round_up((finalize_grid(n_traces) + 1) * n_eta * 8 * 8, kWsAlign);
     w.total = o;
     return w;
 }
@@ -204,11 +207,11 @@ SweepParams base_sweep(const chase_traces_t* t, int L, const WsLayout& WL, uint8
     p.W = (int32_t)(t->n_steps - L);
     p.n_tiles = (int32_t)((p.W + kTileW - 1) / kTileW);
     p.delta = (double)t->interval_s;
-    p.records = reinterpret_cast<const double*>(ws + WL.records);
+    p.records = reinterpret_cast<double*>(ws + WL.records);
+    p.raw = reinterpret_cast<double*>(ws + WL.raw);
     p.tables = ws + WL.tables;
     p.tables_bytes = tb;
     p.stage_bytes = sweep_stage_bytes(t->dtype == CHASE_F64 ? 8 : 4);
-    p.cta_sums = reinterpret_cast<double*>(ws + WL.cta_sums);
     p.status = ws + WL.status;
     p.diag = reinterpret_cast<chase_diag_t*>(ws + WL.diag);
     return p;
@@ -226,21 +229,51 @@ chase_status_t check_smem(int tb, int T, const chase_traces_t* t) {
     return CHASE_OK;
 }
 
-FitParams make_fit(const chase_traces_t* t, const chase_forecast_cfg_t* f, uint8_t* ws, const WsLayout& WL) {
+FitParams make_fit(const chase_traces_t* t, int L, const chase_forecast_cfg_t* f, uint8_t* ws, const WsLayout& WL,
+                   int n_prof, const uint8_t* pid, const double* job) {
     FitParams fp;
     std::memset(&fp, 0, sizeof(fp));
     fp.traces = t->data;
     fp.ld = t->ld;
     fp.n_traces = t->n_traces;
-    fp.L = f->history_len;
-    fp.T = f->steps_per_day;
+    fp.L = L;
+    fp.T = 86400 / t->interval_s;
     fp.phase0 = t->phase0;
     fp.is_f64 = t->dtype == CHASE_F64;
-    fp.ridge = f->ridge_lambda;
-    fp.tol = f->singular_tol;
-    fp.phase_tab = reinterpret_cast<const double*>(ws + WL.tables + sizeof(TablesHeader));
+    fp.W = (int32_t)(t->n_steps - L);
+    fp.n_prof = n_prof;
+    fp.baseline_only = f ? 0 : 1;
+    fp.ridge = f ? f->ridge_lambda : 0.0;
+    fp.tol = f ? f->singular_tol : 0.0;
+    fp.tables = ws + WL.tables;
+    fp.profile_id = pid;
+    fp.job = job;
     fp.records = reinterpret_cast<double*>(ws + WL.records);
     return fp;
+}
+
+FinalizeParams make_finalize(const chase_traces_t* t, int L, int n_eta, int n_prof, uint8_t* ws, const WsLayout& WL,
+                             const uint8_t* pid, const double* job, chase_totals_t* per_trace) {
+    FinalizeParams f;
+    std::memset(&f, 0, sizeof(f));
+    f.traces = t->data;
+    f.ld = t->ld;
+    f.n_traces = t->n_traces;
+    f.L = L;
+    f.W = (int32_t)(t->n_steps - L);
+    f.n_eta = n_eta;
+    f.n_prof = n_prof;
+    f.is_f64 = t->dtype == CHASE_F64;
+    f.delta = (double)t->interval_s;
+    f.records = reinterpret_cast<const double*>(ws + WL.records);
+    f.raw = reinterpret_cast<const double*>(ws + WL.raw);
+    f.tables = ws + WL.tables;
+    f.profile_id = pid;
+    f.job = job;
+    f.status = ws + WL.status;
+    f.per_trace = per_trace;
+    f.block_sums = reinterpret_cast<double*>(ws + WL.block_sums);
+    return f;
 }
 
 }  // namespace
@@ -274,7 +307,7 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     std::vector<uint8_t> blob = build_tables(T, traces->interval_s, nullptr, 0, nullptr, 0);
     if ((st = upload_tables(blob, ws, WL, s))) return st;
-    FitParams fp = make_fit(traces, fcfg, ws, WL);
+    FitParams fp = make_fit(traces, fcfg->history_len, fcfg, ws, WL, 0, nullptr, nullptr);
     fp.models_out = d_models;
     fp.max_ci_out = d_max_ci;
     cudaError_t e = launch_fit(fp, s);
@@ -283,12 +316,10 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     p.n_eta = 1;
     p.forecast = d_forecast;
     p.ld_f = ld_f;
-    int grid = 0;
-    e = launch_sweep(MODE_PREDICT, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, kMaxGrid,
-                     &grid, s);
+    e = launch_sweep(MODE_PREDICT, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, s);
     if (e != cudaSuccess) return cuda_fail(e, "predict kernel");
-    e = launch_finalize(nullptr, 0, 1, nullptr, p.status, traces->n_traces, nullptr, 0, W, 0, d_forecast, ld_f, p.diag, s);
-    if (e != cudaSuccess) return cuda_fail(e, "finalize");
+    e = launch_fixup(p.status, traces->n_traces, nullptr, 0, W, 0, d_forecast, ld_f, p.diag, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fixup");
     return CHASE_OK;
 }
 
@@ -360,6 +391,8 @@ chase_status_t chase_replay(const chase_traces_t* traces, int32_t history_len, c
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     if ((st = upload_tables(blob, ws, WL, s))) return st;
+    cudaError_t e = launch_fit(make_fit(traces, history_len, nullptr, ws, WL, n_profiles, d_profile_id, d_job_samples), s);
+    if (e != cudaSuccess) return cuda_fail(e, "baseline prep kernel");
     SweepParams p = base_sweep(traces, history_len, WL, ws, (int)blob.size());
     p.n_eta = n_eta;
     p.n_prof = n_profiles;
@@ -367,15 +400,13 @@ chase_status_t chase_replay(const chase_traces_t* traces, int32_t history_len, c
     p.job = d_job_samples;
     p.choice_in = d_choice;
     p.ld_c = ld_c;
-    p.per_trace = d_per_trace;
-    int grid = 0;
     ev_start(s);
-    cudaError_t e = launch_sweep(MODE_REPLAY, traces->dtype == CHASE_F64, aligned_start(traces, history_len), p,
-                                 kMaxGrid, &grid, s);
+    e = launch_sweep(MODE_REPLAY, traces->dtype == CHASE_F64, aligned_start(traces, history_len), p, s);
     ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "replay kernel");
-    e = launch_finalize(p.cta_sums, grid, n_eta, d_sum, p.status, traces->n_traces, nullptr, 0, W, 0, nullptr, 0,
-                        p.diag, s);
+    FinalizeParams fz = make_finalize(traces, history_len, n_eta, n_profiles, ws, WL, d_profile_id, d_job_samples,
+                                      d_per_trace);
+    e = launch_finalize(fz, d_sum, nullptr, 0, 0, nullptr, 0, p.diag, s);
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
     return CHASE_OK;
 }
@@ -402,7 +433,8 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     if ((st = upload_tables(blob, ws, WL, s))) return st;
-    cudaError_t e = launch_fit(make_fit(traces, fcfg, ws, WL), s);
+    cudaError_t e = launch_fit(make_fit(traces, fcfg->history_len, fcfg, ws, WL, n_profiles, d_profile_id,
+                                        d_job_samples), s);
     if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
     SweepParams p = base_sweep(traces, fcfg->history_len, WL, ws, (int)blob.size());
     p.n_eta = cost->n_eta;
@@ -414,15 +446,13 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     p.ld_c = ld_c;
     p.forecast = d_forecast;
     p.ld_f = ld_f;
-    p.per_trace = d_per_trace;
-    int grid = 0;
     ev_start(s);
-    e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, kMaxGrid,
-                     &grid, s);
+    e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, s);
     ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "sweep kernel");
-    e = launch_finalize(p.cta_sums, grid, cost->n_eta, d_sum, p.status, traces->n_traces, d_choice, ld_c, W,
-                        cost->n_eta, d_forecast, ld_f, p.diag, s);
+    FinalizeParams fz = make_finalize(traces, fcfg->history_len, cost->n_eta, n_profiles, ws, WL, d_profile_id,
+                                      d_job_samples, d_per_trace);
+    e = launch_finalize(fz, d_sum, d_choice, ld_c, cost->n_eta, d_forecast, ld_f, p.diag, s);
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
     return CHASE_OK;
 }
@@ -553,9 +583,11 @@ extern "C" int32_t chase_testing_envelope(int32_t K, const double* avg_power, co
         int idx = (hi >> kSH) - pt.base;
         idx = idx < 0 ? 0 : (idx > kNBUsed - 1 ? kNBUsed - 1 : idx);
         uint32_t e = pt.ent[idx];
-        double2 th = pt.slots[e >> 10];
+        double2 th;
+        std::memcpy(&th, reinterpret_cast<const uint8_t*>(&pt) + (e >> 16), sizeof(th));
         bool p1 = y <= th.x, p2 = y >= th.y;
-        out[i] = (p1 || p2) ? (int32_t)(p1 ? (e & 31u) : ((e >> 5) & 31u)) : -1;
+        uint32_t k = p1 ? (e & 0xffu) : (p2 ? ((e >> 8) & 0xffu) : (uint32_t)kZeroLine);
+        out[i] = k == (uint32_t)kZeroLine ? -1 : (int32_t)k;
     }
     return (int32_t)iv.size();
 }

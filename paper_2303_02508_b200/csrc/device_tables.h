@@ -18,9 +18,12 @@ constexpr int kMaxSlots = 64;      // threshold pairs per table (6-bit slot fiel
 constexpr int kSlotFast = 0;       // (+inf, +inf): always "below" line
 constexpr int kSlotSlow = 1;       // (NaN, NaN): always the canonical K-way path
 
-// Entry encoding (uint16): below (5 bits) | above << 5 (5 bits) | slot << 10.
-// Per window: p1 = y <= t_lo, p2 = y >= t_hi; choice = p1 ? below : above;
-// (!p1 && !p2) -> canonical Eq. 6.  See DESIGN.md §6 (a5 envelope path).
+constexpr int kZeroLine = 32;      // ProfileTable.line[32] = (0, 0): marks a deferred canonical window
+
+// Entry encoding (uint32): below (bits 0-7) | above (8-15) | byte offset of the
+// (t_lo, t_hi) slot inside the PairTable (16-31).  Per window:
+//   p1 = y <= t_lo, p2 = y >= t_hi; k = p1 ? below : (p2 ? above : kZeroLine);
+// kZeroLine -> the canonical K-way Eq. 6 (deferred).  See DESIGN.md §6.
 
 struct alignas(16) TablesHeader {
     int32_t T, n_prof, n_eta, n_pairs;
@@ -30,7 +33,7 @@ struct alignas(16) TablesHeader {
 };
 
 struct alignas(16) ProfileTable {
-    double2 line[kMaxK];   // (s_k = Thr_k * Delta, P_k)
+    double2 line[kMaxK + 1];  // (s_k = Thr_k * Delta, P_k); line[kZeroLine] = (0, 0)
     double thr[kMaxK];     // Thr_k
     int32_t K, reserved;
     double pmax;           // resolved MaxPower
@@ -44,7 +47,7 @@ struct alignas(16) PairTable {
     int32_t n_slots;
     int32_t n_intervals;   // fast intervals (diagnostic)
     double2 slots[kMaxSlots];
-    uint16_t ent[kNB];
+    uint32_t ent[kNB];
 };
 
 static_assert(sizeof(TablesHeader) % 16 == 0, "header alignment");

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 
 namespace chase {
@@ -175,8 +176,12 @@ std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const
     out->slots[kSlotFast] = make_double2(INFINITY, INFINITY);
     out->slots[kSlotSlow] = make_double2(NaN, NaN);
     int n_slots = 2;
+    auto enc = [](int below, int above, int slot) -> uint32_t {
+        return (uint32_t)below | ((uint32_t)above << 8) |
+               ((uint32_t)(offsetof(PairTable, slots) + 16 * slot) << 16);
+    };
     for (int b = 0; b < kNB; ++b) {
-        if (b >= kNBUsed) { out->ent[b] = (uint16_t)(kSlotSlow << 10); continue; }
+        if (b >= kNBUsed) { out->ent[b] = enc(0, 0, kSlotSlow); continue; }
         double vb = b == 0 ? 0.0 : bucket_start(base_raw, b);
         double ve = b == kNBUsed - 1 ? (double)INFINITY : bucket_start(base_raw, b + 1);
         const FastInterval* cover = nullptr;
@@ -187,11 +192,11 @@ std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const
             else if (f.lo <= vb && vb <= f.hi && f.hi < ve) below = &f;
             else if (vb < f.lo && f.lo < ve && f.hi >= ve) above = &f;
         }
-        uint16_t e;
+        uint32_t e;
         if (cover) {
-            e = (uint16_t)(cover->k | (cover->k << 5) | (kSlotFast << 10));
+            e = enc(cover->k, cover->k, kSlotFast);
         } else if (!below && !above) {
-            e = (uint16_t)(kSlotSlow << 10);
+            e = enc(0, 0, kSlotSlow);
         } else {
             double tlo = below ? below->hi : NaN, thi = above ? above->lo : NaN;
             int slot = -1;
@@ -205,8 +210,8 @@ std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const
                 slot = n_slots++;
                 out->slots[slot] = make_double2(tlo, thi);
             }
-            if (slot < 0) e = (uint16_t)(kSlotSlow << 10);
-            else e = (uint16_t)((below ? below->k : 0) | ((above ? above->k : 0) << 5) | (slot << 10));
+            if (slot < 0) e = enc(0, 0, kSlotSlow);
+            else e = enc(below ? below->k : 0, above ? above->k : 0, slot);
         }
         out->ent[b] = e;
     }

@@ -12,9 +12,18 @@ namespace chase {
 constexpr int kThreads = 256;              // sweep CTA size
 constexpr int kChunk = 36;                 // windows per thread per tile (4 x odd -> conflict-free LDS.128)
 constexpr int kTileW = kThreads * kChunk;  // 9216 windows per tile
-constexpr int kRecDoubles = 8;             // fit record: c0, ws, wc, wl, max_ci, status, ridge, kind
+constexpr int kRecDoubles = 16;            // workspace record per trace (see below)
+constexpr int kModelDoubles = 8;           // d_models row of chase_fit_forecast
+constexpr int kRawDoubles = 8;             // per (eta, trace) replay raw result
 constexpr int kMaxEta = CHASE_MAX_ETA;
+constexpr int kFinThreads = 256;           // finalize CTA size
 
+// Workspace record of trace i (written by fit_kernel, read by sweep/finalize):
+//  [0] c0 [1] w_sin [2] w_cos [3] w_lag [4] max_ci(history) [5] status
+//  [6] ridge [7] kind [8] m_base (baseline completion count, 0: J <= 0)
+//  [9] Cb (baseline sum of c over the windows before w*_b; sweep writes)
+// Raw per (eta, trace) (sweep writes, finalize reads):
+//  [0] E [1] C [2] S [3] f [4] w* [5] P_k* [6] c[w*] [7] done
 enum SweepMode { MODE_FUSED = 0, MODE_PREDICT = 1, MODE_REPLAY = 2 };
 
 struct SweepParams {
@@ -22,11 +31,12 @@ struct SweepParams {
     int64_t ld, n_traces;
     int32_t N, L, T, phase0, W, n_tiles;
     double delta;
-    const double* records;        // [n][8] (FUSED / PREDICT)
+    double* records;              // [n][16]
+    double* raw;                  // [n_eta][n][8]
     const uint8_t* tables;        // blob in the workspace
     int32_t tables_bytes;
     int32_t n_eta, n_prof;
-    int32_t stage_bytes;          // per pipeline stage (trace tile + 64 B record slot)
+    int32_t stage_bytes;          // per pipeline stage (trace tile + record slot)
     const uint8_t* profile_id;    // may be null
     const double* job;            // may be null
     double max_ci_fixed;          // > 0: fixed MaxCI
@@ -35,8 +45,6 @@ struct SweepParams {
     int64_t ld_c;
     double* forecast;             // may be null (PREDICT: required)
     int64_t ld_f;
-    chase_totals_t* per_trace;    // may be null
-    double* cta_sums;             // [grid][n_eta][8]
     uint8_t* status;              // [n]
     chase_diag_t* diag;
 };
@@ -44,12 +52,30 @@ struct SweepParams {
 struct FitParams {
     const void* traces;
     int64_t ld, n_traces;
-    int32_t L, T, phase0, is_f64;
+    int32_t L, T, phase0, is_f64, W, n_prof;
+    int32_t baseline_only;        // 1: only the baseline count m (chase_replay)
     double ridge, tol;
-    const double* phase_tab;      // S[T], C[T] in the workspace blob
-    double* records;              // [n][8]
+    const uint8_t* tables;        // blob (phase table, profiles)
+    const uint8_t* profile_id;
+    const double* job;
+    double* records;              // [n][16]
     double* models_out;           // optional user copy [n][8]
     double* max_ci_out;           // optional [n]
+};
+
+struct FinalizeParams {
+    const void* traces;
+    int64_t ld, n_traces;
+    int32_t L, W, n_eta, n_prof, is_f64;
+    double delta;
+    const double* records;
+    const double* raw;
+    const uint8_t* tables;
+    const uint8_t* profile_id;
+    const double* job;
+    uint8_t* status;              // in: sweep status; out: final (incl. exhausted)
+    chase_totals_t* per_trace;    // may be null
+    double* block_sums;           // [grid][n_eta][8]
 };
 
 struct PlanParams {
@@ -65,22 +91,21 @@ struct PlanParams {
     chase_diag_t* diag;
 };
 
-// Shared-memory bytes of one sweep CTA for these shapes.
 size_t sweep_smem_bytes(int tables_bytes, int T, int elem_size, int mode);
 int sweep_stage_bytes(int elem_size);
+int64_t finalize_grid(int64_t n_traces);
 
 cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_t s);
 cudaError_t launch_fit(const FitParams& p, cudaStream_t s);
-// grid_out receives the number of CTAs used (rows of cta_sums).
-cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, int max_grid,
-                         int* grid_out, cudaStream_t s);
+cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s);
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
-cudaError_t launch_finalize(const double* cta_sums, int grid, int n_eta, chase_sum_t* sum,
-                            const uint8_t* status, int64_t n_traces, uint8_t* choice, int64_t ld_c,
-                            int64_t W, int n_eta_choice, double* forecast, int64_t ld_f,
-                            chase_diag_t* diag, cudaStream_t s);
+// per-trace totals + fixed-order per-GPU sums (+ invalid-trace fix-up)
+cudaError_t launch_finalize(const FinalizeParams& p, chase_sum_t* sum, uint8_t* choice, int64_t ld_c,
+                            int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag, cudaStream_t s);
+cudaError_t launch_fixup(const uint8_t* status, int64_t n_traces, uint8_t* choice, int64_t ld_c, int64_t W,
+                         int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag, cudaStream_t s);
 cudaError_t launch_diag_reset(chase_diag_t* diag, cudaStream_t s);
-uint64_t kernel_launches();
 cudaError_t launch_accumulate(double* acc, const double* add, int n, cudaStream_t s);
+uint64_t kernel_launches();
 
 }  // namespace chase
