@@ -51,7 +51,8 @@ def build_inputs(force=False):
 
 
 CHASE_SOURCES = ["chase_api.cpp", "envelope.cpp", "kernels.cu"]
-CHASE_HEADERS = ["envelope.h", "device_tables.h", "kernels.h"]
+CHASE_HEADERS = ["envelope.h", "device_tables.h", "kernels.h", "device_common.cuh", "fit.cuh", "sweep.cuh",
+                 "finalize.cuh"]
 
 
 def build_chase(force=False):

@@ -205,7 +205,7 @@ SweepParams base_sweep(const chase_traces_t* t, int L, const WsLayout& WL, uint8
     p.T = 86400 / t->interval_s;
     p.phase0 = t->phase0;
     p.W = (int32_t)(t->n_steps - L);
-    p.n_tiles = (int32_t)((p.W + kTileW - 1) / kTileW);
+    p.n_chunks = (int32_t)((p.W + kWarpW - 1) / kWarpW);
     p.delta = (double)t->interval_s;
     p.records = reinterpret_cast<double*>(ws + WL.records);
     p.raw = reinterpret_cast<double*>(ws + WL.raw);

@@ -1,0 +1,195 @@
+// finalize.cuh — per-trace totals, fixed-order sums, fix-up, plan-from-forecast
+// and upload kernels (included by kernels.cu).
+
+// ------------------------------------------------------------------ finalize (K3)
+// Per trace: the replay totals of DESIGN R2 (stepwise carbon S:432, pro-rata
+// last window S:433, exhaustion S:436) and the max-power baseline,
+// in the oracle's operation order; then fixed-order block sums.
+template <typename E>
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(const __grid_constant__ FinalizeParams p) {
+    __shared__ double red[kFinThreads][8];
+    const int64_t i = (int64_t)blockIdx.x * kFinThreads + threadIdx.x;
+    const bool valid = i < p.n_traces;
+    const E* traces = reinterpret_cast<const E*>(p.traces);
+    int st = valid ? (int)p.status[i] : 1;
+    double bt = 0.0, be = 0.0, bc = 0.0;
+    int bstat = 0, worst = st;
+    double J = 0.0;
+    int prof = 0;
+    const ProfileTable* pf = nullptr;
+    if (valid && st == 0) {
+        prof = p.profile_id ? (int)p.profile_id[i] : 0;
+        if (prof >= p.n_prof) prof = 0;
+        pf = blob_profiles(p.tables) + prof;
+        J = p.job ? p.job[i] : 0.0;
+        const double* rec = p.records + i * kRecDoubles;
+        const double sbv = pf->line[pf->K - 1].x, Pb = pf->line[pf->K - 1].y, Cb = rec[9];
+        const int64_t m = (int64_t)rec[8];
+        if (J > 0.0 && m >= 1 && m <= p.W) {
+            const double prevS = __dmul_rn((double)(m - 1), sbv);
+            const double f = __ddiv_rn(__dsub_rn(J, prevS), sbv);
+            const double Eb = __dmul_rn((double)(m - 1), Pb);
+            const double Cbp = __dmul_rn(Pb, Cb);
+            const double cst = (double)traces[i * p.ld + p.L + (m - 1)];
+            bt = __dmul_rn(__dadd_rn((double)(m - 1), f), p.delta);
+            be = __dmul_rn(__dadd_rn(Eb, __dmul_rn(f, Pb)), p.delta);
+            bc = __ddiv_rn(__dmul_rn(__dadd_rn(Cbp, __dmul_rn(f, __dmul_rn(Pb, cst))), p.delta), 3.6e6);
+        } else {
+            bt = __dmul_rn((double)p.W, p.delta);
+            be = __dmul_rn(__dmul_rn((double)p.W, Pb), p.delta);
+            bc = __ddiv_rn(__dmul_rn(__dmul_rn(Pb, Cb), p.delta), 3.6e6);
+            if (J > 0.0) bstat = CHASE_ERR_TRACE_EXHAUSTED;
+        }
+    }
+    for (int e = 0; e < p.n_eta; ++e) {
+        double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (valid) {
+            chase_totals_t t;
+            t.time_s = t.energy_j = t.carbon_g = t.samples = 0.0;
+            t.base_time_s = t.base_energy_j = t.base_carbon_g = 0.0;
+            t.completion_window = -1;
+            t.status = st;
+            if (st == 0) {
+                const double* r = p.raw + ((int64_t)e * p.n_traces + i) * kRawDoubles;
+                int ste = 0;
+                if (r[7] != 0.0) {
+                    const double f = r[3], Pk = r[5];
+                    const int64_t wstar = (int64_t)r[4];
+                    t.time_s = __dmul_rn(__dadd_rn((double)(wstar - p.L), f), p.delta);
+                    t.energy_j = __dmul_rn(__dadd_rn(r[0], __dmul_rn(f, Pk)), p.delta);
+                    t.carbon_g = __ddiv_rn(__dmul_rn(__dadd_rn(r[1], __dmul_rn(f, __dmul_rn(Pk, r[6]))), p.delta), 3.6e6);
+                    t.samples = J;
+                    t.completion_window = (int32_t)wstar;
+                } else {
+                    t.time_s = __dmul_rn((double)p.W, p.delta);
+                    t.energy_j = __dmul_rn(r[0], p.delta);
+                    t.carbon_g = __ddiv_rn(__dmul_rn(r[1], p.delta), 3.6e6);
+                    t.samples = r[2];
+                    if (J > 0.0) ste = CHASE_ERR_TRACE_EXHAUSTED;
+                }
+                t.base_time_s = bt;
+                t.base_energy_j = be;
+                t.base_carbon_g = bc;
+                t.status = ste ? ste : bstat;
+                if (t.status > worst) worst = t.status;
+                if (t.status == 0) {
+                    v[0] = t.time_s; v[1] = t.energy_j; v[2] = t.carbon_g; v[3] = t.samples;
+                    v[4] = bt; v[5] = be; v[6] = bc; v[7] = 1.0;
+                }
+            }
+            if (p.per_trace) p.per_trace[(int64_t)e * p.n_traces + i] = t;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) red[threadIdx.x][r] = v[r];
+        __syncthreads();
+        if (threadIdx.x < 8) {
+            double acc = 0.0;
+            for (int t = 0; t < kFinThreads; ++t) acc = __dadd_rn(acc, red[t][threadIdx.x]);
+            p.block_sums[((int64_t)blockIdx.x * p.n_eta + e) * 8 + threadIdx.x] = acc;
+        }
+        __syncthreads();
+    }
+    if (valid) p.status[i] = (uint8_t)worst;
+}
+
+__global__ void finalize_sums_kernel(const double* block_sums, int64_t grid, int n_eta, chase_sum_t* sum) {
+    const int e = blockIdx.x, r = threadIdx.x;
+    if (e >= n_eta || r >= 8) return;
+    double acc = 0.0;
+    for (int64_t b = 0; b < grid; ++b) acc = __dadd_rn(acc, block_sums[(b * n_eta + e) * 8 + r]);
+    reinterpret_cast<double*>(sum + e)[r] = acc;
+}
+
+// Invalid traces (status 4..7): choices 0xFF, forecasts NaN; count exhausted.
+__global__ void fixup_kernel(const uint8_t* status, int64_t n, uint8_t* choice, int64_t ld_c, int64_t W, int n_eta,
+                             double* forecast, int64_t ld_f, chase_diag_t* diag) {
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int s = status[i];
+        if (s == CHASE_ERR_TRACE_EXHAUSTED && threadIdx.x == 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&diag->n_exhausted), 1ull);
+        if (s < CHASE_ERR_DATA) continue;
+        if (threadIdx.x == 0)
+            atomicMin(reinterpret_cast<unsigned long long*>(&diag->first_bad_trace), (unsigned long long)i);
+        if (choice)
+            for (int e = 0; e < n_eta; ++e)
+                for (int64_t w = threadIdx.x; w < W; w += blockDim.x) choice[((int64_t)e * n + i) * ld_c + w] = 0xff;
+        if (forecast)
+            for (int64_t w = threadIdx.x; w < W; w += blockDim.x)
+                forecast[i * ld_f + w] = __longlong_as_double(0x7ff8000000000000ll);
+    }
+}
+
+__global__ void diag_status_kernel(const uint8_t* status, int64_t n, chase_diag_t* diag) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const uint64_t fb = (uint64_t)diag->first_bad_trace;
+        if (fb < (uint64_t)n) diag->first_bad_status = status[fb];
+    }
+}
+
+__global__ void diag_reset_kernel(chase_diag_t* d) {
+    if (threadIdx.x == 0) {
+        d->first_bad_trace = -1;  // all ones: atomicMin (unsigned) finds the lowest index
+        d->first_bad_status = 0;
+        d->n_bad = d->n_exhausted = d->n_slow_windows = 0;
+    }
+}
+
+__global__ void accumulate_sums_kernel(double* acc, const double* add, int n) {
+    const int q = threadIdx.x;
+    if (q < n) acc[q] = __dadd_rn(acc[q], add[q]);
+}
+
+// ------------------------------------------------------------------ plan from forecasts
+__global__ void __launch_bounds__(256) plan_kernel(const __grid_constant__ PlanParams p) {
+    extern __shared__ __align__(16) uint8_t psm[];
+    for (int q = threadIdx.x; q < p.tables_bytes / 16; q += blockDim.x)
+        reinterpret_cast<uint4*>(psm)[q] = reinterpret_cast<const uint4*>(p.tables)[q];
+    __syncthreads();
+    const TablesHeader* H = reinterpret_cast<const TablesHeader*>(psm);
+    const ProfileTable* profs = reinterpret_cast<const ProfileTable*>(psm + H->off_prof);
+    const PairTable* pairs = reinterpret_cast<const PairTable*>(psm + H->off_pair);
+    const int64_t groups = (p.W + 3) / 4;  // 4 windows per thread-step
+    const int64_t total = p.n_traces * groups;
+    int64_t slow_count = 0;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = g / groups, w0 = (g - i * groups) * 4;
+        int prof = p.profile_id ? (int)p.profile_id[i] : 0;
+        if (prof >= p.n_prof) prof = 0;
+        const ProfileTable* pf = profs + prof;
+        const double maxci = p.max_ci_fixed > 0.0 ? p.max_ci_fixed : p.max_ci[i];
+        const bool trace_ok = maxci > 0.0;
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = w0 + u < p.W ? p.forecast[i * p.ld_f + w0 + u] : 0.0;
+        for (int e = 0; e < p.n_eta; ++e) {
+            const PairTable* pt = pairs + prof * p.n_eta + e;
+            const double Kc = __dmul_rn(pt->kbase, maxci);
+            const double invK = per_trace_invK(pt, Kc);
+            uint32_t word = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t k = 0xffu;
+                if (w0 + u < p.W && trace_ok && x[u] >= 0.0 && x[u] <= DBL_MAX) {
+                    k = plan_lookup(__dmul_rn(x[u], invK), pt);
+                    if (k == (uint32_t)kZeroLine) {
+                        k = canonical_choose(x[u], Kc, pt->a, pf->thr, pf->K);
+                        ++slow_count;
+                    }
+                }
+                word |= k << (8 * u);
+            }
+            *reinterpret_cast<uint32_t*>(p.choice + ((int64_t)e * p.n_traces + i) * p.ld_c + w0) = word;
+        }
+    }
+    unsigned long long sc = (unsigned long long)slow_count;
+    for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(kFull, sc, o);
+    if ((threadIdx.x & 31) == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&p.diag->n_slow_windows), sc);
+}
+
+struct UploadChunk {
+    uint8_t bytes[30720];
+};
+__global__ void upload_kernel(const __grid_constant__ UploadChunk c, int n, uint8_t* dst) {
+    for (int q = threadIdx.x; q < n; q += blockDim.x) dst[q] = c.bytes[q];
+}
+

@@ -1,0 +1,184 @@
+// fit.cuh — §3.1 forecaster fit (K1), included by kernels.cu.
+
+// ------------------------------------------------------------------ fit (K1)
+// §3.1: the model is fitted once per trace on its L history points c[0..L)
+// ("one day prior").  One lane per trace, the same
+// sequential order and rounding as oracle_fit (bit-identical records).
+template <typename E>
+__device__ void fit_one(const E* h, int L, int T, int phi0, const double* S, const double* Cc, double ridge,
+                        double tol_rel, double* rec) {
+    const int n = L - 1;
+    const double dn = (double)n;
+    double maxci = (double)h[0];
+    int bad = 0;
+    for (int t = 0; t < L; ++t) {
+        E v = h[t];
+        bad |= bad_value(v);
+        if ((double)v > maxci) maxci = (double)v;
+    }
+    double c0 = 0, w[3] = {0, 0, 0};
+    int status = bad ? CHASE_ERR_DATA : 0, ridge_fired = 0, kind = 0;
+    bool constant = true;
+    for (int i = 2; i <= n; ++i)
+        if ((double)h[i] != (double)h[1]) { constant = false; break; }
+    if (status == 0 && constant) {
+        kind = 1;
+        c0 = (double)h[1];
+    } else if (status == 0) {
+        double sum[4] = {0, 0, 0, 0};
+        for (int i = 1; i <= n; ++i) {
+            int ph = (phi0 + i) % T;
+            sum[0] = __dadd_rn(sum[0], S[ph]);
+            sum[1] = __dadd_rn(sum[1], Cc[ph]);
+            sum[2] = __dadd_rn(sum[2], (double)h[i - 1]);
+            sum[3] = __dadd_rn(sum[3], (double)h[i]);
+        }
+        double mu[4], ss[4] = {0, 0, 0, 0}, sg[4];
+        for (int j = 0; j < 4; ++j) mu[j] = __ddiv_rn(sum[j], dn);
+        for (int i = 1; i <= n; ++i) {
+            int ph = (phi0 + i) % T;
+            double d0 = __dsub_rn(S[ph], mu[0]);
+            double d1 = __dsub_rn(Cc[ph], mu[1]);
+            double d2 = __dsub_rn((double)h[i - 1], mu[2]);
+            double d3 = __dsub_rn((double)h[i], mu[3]);
+            ss[0] = __dadd_rn(ss[0], __dmul_rn(d0, d0));
+            ss[1] = __dadd_rn(ss[1], __dmul_rn(d1, d1));
+            ss[2] = __dadd_rn(ss[2], __dmul_rn(d2, d2));
+            ss[3] = __dadd_rn(ss[3], __dmul_rn(d3, d3));
+        }
+        for (int j = 0; j < 4; ++j) sg[j] = __dsqrt_rn(__ddiv_rn(ss[j], dn));
+        if (!(sg[3] > 0.0)) {
+            kind = 1;
+            c0 = mu[3];
+        } else {
+            int cols[3], m = 0;
+            for (int j = 0; j < 3; ++j)
+                if (sg[j] > 0.0) cols[m++] = j;
+            double G[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, hv[3] = {0, 0, 0};
+            for (int i = 1; i <= n; ++i) {
+                int ph = (phi0 + i) % T;
+                double x[3] = {S[ph], Cc[ph], (double)h[i - 1]};
+                double z[3];
+                for (int a = 0; a < m; ++a) z[a] = __ddiv_rn(__dsub_rn(x[cols[a]], mu[cols[a]]), sg[cols[a]]);
+                double u = __ddiv_rn(__dsub_rn((double)h[i], mu[3]), sg[3]);
+                for (int a = 0; a < m; ++a) {
+                    for (int b = 0; b <= a; ++b) G[a][b] = __dadd_rn(G[a][b], __dmul_rn(z[a], z[b]));
+                    hv[a] = __dadd_rn(hv[a], __dmul_rn(z[a], u));
+                }
+            }
+            for (int a = 0; a < m; ++a)
+                for (int b = 0; b < a; ++b) G[b][a] = G[a][b];
+            const double tol = __dmul_rn(tol_rel, dn);
+            double Lc[3][3];
+            bool ok = false;
+            for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+                if (attempt == 1) {
+                    for (int a = 0; a < m; ++a) G[a][a] = __dadd_rn(G[a][a], ridge);
+                    ridge_fired = 1;
+                }
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) Lc[a][b] = 0.0;
+                ok = true;
+                for (int j = 0; j < m && ok; ++j) {
+                    double d = G[j][j];
+                    for (int k = 0; k < j; ++k) d = __dsub_rn(d, __dmul_rn(Lc[j][k], Lc[j][k]));
+                    if (!(d > tol)) { ok = false; break; }
+                    Lc[j][j] = __dsqrt_rn(d);
+                    for (int i = j + 1; i < m; ++i) {
+                        double v = G[i][j];
+                        for (int k = 0; k < j; ++k) v = __dsub_rn(v, __dmul_rn(Lc[i][k], Lc[j][k]));
+                        Lc[i][j] = __ddiv_rn(v, Lc[j][j]);
+                    }
+                }
+                if (m == 0) ok = true;
+            }
+            if (!ok) {
+                status = CHASE_ERR_FIT;
+            } else {
+                double zt[3] = {0, 0, 0}, beta[3] = {0, 0, 0};
+                for (int a = 0; a < m; ++a) {
+                    double v = hv[a];
+                    for (int b = 0; b < a; ++b) v = __dsub_rn(v, __dmul_rn(Lc[a][b], zt[b]));
+                    zt[a] = __ddiv_rn(v, Lc[a][a]);
+                }
+                for (int a = m - 1; a >= 0; --a) {
+                    double v = zt[a];
+                    for (int b = a + 1; b < m; ++b) v = __dsub_rn(v, __dmul_rn(Lc[b][a], beta[b]));
+                    beta[a] = __ddiv_rn(v, Lc[a][a]);
+                }
+                for (int a = 0; a < m; ++a) w[cols[a]] = __ddiv_rn(__dmul_rn(sg[3], beta[a]), sg[cols[a]]);
+                c0 = mu[3];
+                for (int a = 0; a < m; ++a) c0 = __dsub_rn(c0, __dmul_rn(w[cols[a]], mu[cols[a]]));
+            }
+        }
+    }
+    rec[0] = c0;
+    rec[1] = w[0];
+    rec[2] = w[1];
+    rec[3] = w[2];
+    rec[4] = maxci;
+    rec[5] = (double)status;
+    rec[6] = (double)ridge_fired;
+    rec[7] = (double)kind;
+}
+
+// Fit kernel: stage the CTA's 128 histories (L <= 64) into smem with coalesced
+// loads (odd row stride), one lane per trace runs the canonical fit; also the
+// max-power baseline's completion count m: the first m with
+// m*s_b >= J, s_b = Thr_{K-1}*Delta (exact for the dyadic inputs; DESIGN R3).
+template <typename E>
+__global__ void __launch_bounds__(128) fit_kernel(const __grid_constant__ FitParams p) {
+    extern __shared__ __align__(16) uint8_t fsm[];
+    E* hs = reinterpret_cast<E*>(fsm);
+    double* tab = reinterpret_cast<double*>(fsm + round16(128 * 65 * (int)sizeof(E)));
+    const TablesHeader* H = reinterpret_cast<const TablesHeader*>(p.tables);
+    const int L = p.L, T = p.T;
+    const int64_t first = (int64_t)blockIdx.x * 128;
+    const E* tr = reinterpret_cast<const E*>(p.traces);
+    const bool staged = !p.baseline_only && L <= 64;
+    if (!p.baseline_only) {
+        const double* ph = reinterpret_cast<const double*>(p.tables + H->off_phase);
+        for (int q = threadIdx.x; q < 2 * T; q += blockDim.x) tab[q] = ph[q];
+    }
+    if (staged) {
+        const int stride = L | 1;
+        for (int q = threadIdx.x; q < 128 * L; q += blockDim.x) {
+            int r = q / L, t = q - r * L;
+            int64_t i = first + r;
+            if (i < p.n_traces) hs[r * stride + t] = tr[i * p.ld + t];
+        }
+    }
+    __syncthreads();
+    const int64_t i = first + threadIdx.x;
+    if (i >= p.n_traces) return;
+    double rec[kRecDoubles];
+#pragma unroll
+    for (int q = 0; q < kRecDoubles; ++q) rec[q] = 0.0;
+    if (!p.baseline_only) {
+        const E* h = staged ? hs + threadIdx.x * (L | 1) : tr + i * p.ld;
+        fit_one<E>(h, L, T, p.phase0 % T, tab, tab + T, p.ridge, p.tol, rec);
+    }
+    const double J = p.job ? p.job[i] : 0.0;
+    if (J > 0.0 && p.n_prof > 0) {
+        int prof = p.profile_id ? (int)p.profile_id[i] : 0;
+        if (prof >= p.n_prof) prof = 0;
+        const ProfileTable* pf = blob_profiles(p.tables) + prof;
+        const double sb = pf->line[pf->K - 1].x;
+        const double qv = __ddiv_rn(J, sb);
+        int64_t m = qv < 4.0e15 ? (int64_t)ceil(qv) : (int64_t)p.W + 2;
+        if (m < 1) m = 1;
+        while (m > 1 && __dmul_rn((double)(m - 1), sb) >= J) --m;
+        while (m <= (int64_t)p.W && __dmul_rn((double)m, sb) < J) ++m;
+        if (m > (int64_t)p.W) m = (int64_t)p.W + 1;
+        rec[8] = (double)m;
+    }
+    double* out = p.records + i * kRecDoubles;
+#pragma unroll
+    for (int q = 0; q < kRecDoubles; ++q) out[q] = rec[q];
+    if (p.models_out) {
+#pragma unroll
+        for (int q = 0; q < kModelDoubles; ++q) p.models_out[i * kModelDoubles + q] = rec[q];
+    }
+    if (p.max_ci_out) p.max_ci_out[i] = rec[4];
+}
+

@@ -9,9 +9,10 @@
 
 namespace chase {
 
-constexpr int kThreads = 256;              // sweep CTA size
-constexpr int kChunk = 36;                 // windows per thread per tile (4 x odd -> conflict-free LDS.128)
-constexpr int kTileW = kThreads * kChunk;  // 9216 windows per tile
+constexpr int kThreads = 256;              // sweep CTA size (8 independent warps)
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr int kChunk = 36;                 // windows per lane per chunk (4 x odd -> conflict-free LDS.128)
+constexpr int kWarpW = 32 * kChunk;        // 1152 windows per warp chunk
 constexpr int kRecDoubles = 16;            // workspace record per trace (see below)
 constexpr int kModelDoubles = 8;           // d_models row of chase_fit_forecast
 constexpr int kRawDoubles = 8;             // per (eta, trace) replay raw result
@@ -29,14 +30,14 @@ enum SweepMode { MODE_FUSED = 0, MODE_PREDICT = 1, MODE_REPLAY = 2 };
 struct SweepParams {
     const void* traces;
     int64_t ld, n_traces;
-    int32_t N, L, T, phase0, W, n_tiles;
+    int32_t N, L, T, phase0, W, n_chunks;
     double delta;
     double* records;              // [n][16]
     double* raw;                  // [n_eta][n][8]
     const uint8_t* tables;        // blob in the workspace
     int32_t tables_bytes;
     int32_t n_eta, n_prof;
-    int32_t stage_bytes;          // per pipeline stage (trace tile + record slot)
+    int32_t stage_bytes;          // per pipeline stage (trace chunk + record slot)
     const uint8_t* profile_id;    // may be null
     const double* job;            // may be null
     double max_ci_fixed;          // > 0: fixed MaxCI

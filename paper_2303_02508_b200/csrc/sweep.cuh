@@ -1,0 +1,485 @@
+// sweep.cuh — the fused planner kernel (K2), included by kernels.cu inside its
+// anonymous namespace.
+//
+// Warp-per-trace streaming.  Every warp of a persistent CTA owns whole traces
+// (trace i -> global warp i mod #warps) and streams each one in chunks of
+// kWarpW = 32 x 36 windows through its own 2-stage TMA ring (cp.async.bulk +
+// mbarrier, issued by lane 0), so there is no CTA-wide barrier in the steady
+// state.  Lane l plans windows [36 l, 36 l + 36) of a chunk:
+//   predict (Eq. 1) -> Eq. 6 argmin via the exact envelope bucket table
+//   (canonical K-way path deferred for windows in a rounding band) ->
+//   fixed-work replay partials (sum Thr*Delta, sum P, sum P*c; sum c)
+// then one transposed warp reduction per chunk and eta.  The chunk that
+// completes the job (once per trace and eta) runs a warp scan and the lane
+// holding the completion window re-walks its 36 windows.  Choices are staged
+// per warp in smem and bulk-stored (cp.async.bulk.global.shared).
+
+struct Acc {
+    double S, E, C, Cs;  // sum s_k, sum P_k, sum P_k*c, sum c (every window: validation + baseline)
+    float vmin;          // min raw value (fast path validation; NaN/inf show up in Cs)
+    uint32_t slow;       // OR of staged choice words: bit 5 of a byte = kZeroLine (deferred window)
+    int bad;             // generic path validation (1) / REPLAY bad choice (2)
+};
+
+// Full 16-byte-aligned fp32 groups of 4 windows: the hot loop.
+// tv[jj] = c[w0 + jj] (tv[-1] = lag of the first window), Ap[jj] = A(phi0+jj).
+template <bool FIRST, bool FC>
+__device__ __forceinline__ void fused_full(const float* __restrict__ tv, int ngroups, const double* __restrict__ Ap,
+                                           double wl, double invK, const PairTable* __restrict__ pt,
+                                           const double2* __restrict__ lines, uint32_t* __restrict__ words,
+                                           double* __restrict__ fout, Acc& a) {
+    double lag = (double)tv[-1];
+#pragma unroll 1
+    for (int g = 0; g < ngroups; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(tv + 4 * g);
+        const double2 A01 = *reinterpret_cast<const double2*>(Ap + 4 * g);
+        const double2 A23 = *reinterpret_cast<const double2*>(Ap + 4 * g + 2);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        const double AA[4] = {A01.x, A01.y, A23.x, A23.y};
+        uint32_t word = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double cw = (double)vv[u];
+            const double p = __dadd_rn(AA[u], __dmul_rn(wl, lag));  // Eq. 1, unclamped for the lookup
+            if (FC) fout[4 * g + u] = p > 0.0 ? p : 0.0;
+            const uint32_t k = plan_lookup(__dmul_rn(p, invK), pt);
+            word |= k << (8 * u);
+            const double2 ln = lines[k];  // (Thr_k * Delta, P_k)
+            a.S = __dadd_rn(a.S, ln.x);
+            a.E = __dadd_rn(a.E, ln.y);
+            a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+            if (FIRST) {
+                a.Cs = __dadd_rn(a.Cs, cw);
+                a.vmin = fminf(a.vmin, vv[u]);
+            }
+            lag = cw;
+        }
+        words[g] = word;
+        a.slow |= word;
+    }
+}
+
+// Any element type / alignment / window count (odd L, f64, ragged tails).
+template <bool FIRST, bool FC, typename E>
+__device__ void fused_generic(const E* tv, int j_begin, int nwin, const double* Ap, double wl, double invK,
+                              const PairTable* pt, const double2* lines, uint8_t* bytes, double* fout, Acc& a) {
+    double lag = (double)tv[j_begin - 1];
+    for (int jj = j_begin; jj < nwin; ++jj) {
+        const E raw = tv[jj];
+        const double cw = (double)raw;
+        const double p = __dadd_rn(Ap[jj], __dmul_rn(wl, lag));
+        if (FC) fout[jj] = p > 0.0 ? p : 0.0;
+        const uint32_t k = plan_lookup(__dmul_rn(p, invK), pt);
+        if (k == (uint32_t)kZeroLine) a.slow |= 0x20u;
+        bytes[jj] = (uint8_t)k;
+        const double2 ln = lines[k];
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        if (FIRST) {
+            a.Cs = __dadd_rn(a.Cs, cw);
+            a.bad |= bad_value(raw) ? 1 : 0;
+        }
+        lag = cw;
+    }
+}
+
+// The deferred windows (kZeroLine): canonical K-way Eq. 6, then their replay
+// contributions (exact for dyadic inputs in any order).
+template <typename E>
+__device__ __noinline__ int fix_slow(const E* tv, int nwin, const double* Ap, double wl, double Kc, const PairTable* pt,
+                                     const ProfileTable* pf, uint8_t* bytes, Acc& a) {
+    int n = 0;
+    for (int jj = 0; jj < nwin; ++jj) {
+        if (bytes[jj] != (uint8_t)kZeroLine) continue;
+        const double x = predict(Ap[jj], wl, (double)tv[jj - 1]);
+        const uint32_t k = canonical_choose(x, Kc, pt->a, pf->thr, pf->K);
+        bytes[jj] = (uint8_t)k;
+        const double2 ln = pf->line[k];
+        const double cw = (double)tv[jj];
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        ++n;
+    }
+    return n;
+}
+
+template <typename E>
+__device__ void predict_chunk(const E* tv, int nwin, const double* Ap, double wl, double* fout, Acc& a) {
+    double lag = nwin > 0 ? (double)tv[-1] : 0.0;
+    for (int jj = 0; jj < nwin; ++jj) {
+        const E raw = tv[jj];
+        fout[jj] = predict(Ap[jj], wl, lag);
+        a.bad |= bad_value(raw) ? 1 : 0;
+        lag = (double)raw;
+    }
+}
+
+template <bool FIRST, typename E>
+__device__ void replay_chunk(const E* tv, int nwin, const uint8_t* cin, int K, const double2* lines, uint8_t* bytes,
+                             Acc& a) {
+    for (int jj = 0; jj < nwin; ++jj) {
+        uint32_t k = cin[jj];
+        if (k >= (uint32_t)K) {
+            a.bad |= 2;
+            k = 0;
+        }
+        bytes[jj] = (uint8_t)k;
+        const E raw = tv[jj];
+        const double cw = (double)raw;
+        const double2 ln = lines[k];
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        if (FIRST) {
+            a.Cs = __dadd_rn(a.Cs, cw);
+            a.bad |= bad_value(raw) ? 1 : 0;
+        }
+    }
+}
+
+template <typename E>
+__device__ bool chunk_has_bad(const E* tv, int nwin) {
+    bool b = false;
+    for (int jj = 0; jj < nwin; ++jj) b |= bad_value(tv[jj]);
+    return b;
+}
+
+// ---- shared-memory plan: tables | per warp {A tables, 2 stages, 2 choice buffers, state, mbarriers}
+__host__ __device__ inline int aext_len(int T) { return T + kChunk + 4; }
+
+struct WarpLayout {
+    int aext, stage, chb, state, mbar, bytes;
+};
+
+__host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes) {
+    WarpLayout L;
+    int o = 0;
+    L.aext = o; o += 2 * round16(aext_len(T) * 8);
+    L.stage = o; o += 2 * stage_bytes;
+    L.chb = o; o += 2 * kWarpW;
+    L.state = o; o += kMaxEta * 4 * 8;
+    L.mbar = o; o += 16;
+    L.bytes = round16(o);
+    return L;
+}
+
+__host__ __device__ inline int sweep_smem_total(int tables_bytes, int T, int stage_bytes) {
+    return round16(tables_bytes) + kWarpsPerCta * make_warp_layout(T, stage_bytes).bytes;
+}
+
+template <int MODE, typename E, bool AL>
+__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepParams P) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    constexpr int VEC = 16 / (int)sizeof(E);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const WarpLayout WL = make_warp_layout(P.T, P.stage_bytes);
+    uint8_t* wbase = sm + round16(P.tables_bytes) + warp * WL.bytes;
+    const int alen = round16(aext_len(P.T) * 8) / 8;
+    double* A_even = reinterpret_cast<double*>(wbase + WL.aext);
+    double* A_odd = A_even + alen;
+    uint8_t* stage0 = wbase + WL.stage;
+    uint8_t* chb0 = wbase + WL.chb;
+    double* state = reinterpret_cast<double*>(wbase + WL.state);  // [eta][4]: S_run, E_run, C_run, done
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + WL.mbar);
+
+    {   // constant tables -> smem (16-byte vectors), once per CTA
+        const uint4* src = reinterpret_cast<const uint4*>(P.tables);
+        uint4* dst = reinterpret_cast<uint4*>(sm);
+        for (int q = tid; q < P.tables_bytes / 16; q += kThreads) dst[q] = src[q];
+    }
+    if (lane == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();  // the only CTA-wide barrier
+
+    const TablesHeader* H = reinterpret_cast<const TablesHeader*>(sm);
+    const double* phS = reinterpret_cast<const double*>(sm + H->off_phase);
+    const double* phC = phS + P.T;
+    const ProfileTable* profs = reinterpret_cast<const ProfileTable*>(sm + H->off_prof);
+    const PairTable* pairs = reinterpret_cast<const PairTable*>(sm + H->off_pair);
+
+    const int64_t GW = (int64_t)gridDim.x * kWarpsPerCta;
+    const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    const int n_pass = MODE == MODE_PREDICT ? 1 : P.n_eta;
+    const E* traces = reinterpret_cast<const E*>(P.traces);
+    const uint64_t policy = evict_first_policy();
+    const int nc = P.n_chunks;
+
+    // producer cursor (lane 0): the next (trace, chunk) to load, and its stage
+    int64_t pi = gw;
+    int pc = 0;
+    int64_t issued = 0;
+    auto issue_next = [&]() {
+        if (pi >= P.n_traces) return;
+        const int st = (int)(issued & 1);
+        const int64_t ws = (int64_t)P.L + (int64_t)pc * kWarpW;
+        const int Wc = min(kWarpW, P.W - pc * kWarpW);
+        const int64_t a = AL ? ws - VEC : ((ws - 1) / VEC) * VEC;
+        int64_t b = ((ws + Wc + VEC - 1) / VEC) * VEC;
+        if (b > P.ld) b = P.ld;
+        const uint32_t bytes = (uint32_t)((b - a) * (int64_t)sizeof(E));
+        const bool rec = pc == 0;
+        uint8_t* dst = stage0 + st * P.stage_bytes;
+        mbar_arrive_expect_tx(&mbar[st], bytes + (rec ? (uint32_t)kRecBytes : 0u));
+        bulk_g2s(dst, traces + pi * P.ld + a, bytes, &mbar[st], policy);
+        if (rec) bulk_g2s(dst + P.stage_bytes - kRecBytes, P.records + pi * kRecDoubles, kRecBytes, &mbar[st], policy);
+        ++issued;
+        if (++pc == nc) {
+            pc = 0;
+            pi += GW;
+        }
+    };
+    if (lane == 0) {
+        issue_next();
+        issue_next();
+    }
+
+    // per-trace (warp-uniform) state
+    int status = 0, prof = 0, phase_c = 0;
+    double wl = 0.0, maxci = 0.0, J = 0.0, Cb_run = 0.0;
+    int64_t mb = 0;
+    int64_t slow_count = 0, gp = 0, q = 0;
+    const int lane_phase = (kChunk * lane) % P.T;
+
+    for (int64_t i = gw; i < P.n_traces; i += GW) {
+        for (int c = 0; c < nc; ++c, ++q) {
+            const int st = (int)(q & 1);
+            const int64_t ws_abs = (int64_t)P.L + (int64_t)c * kWarpW;
+            const int Wc = min(kWarpW, P.W - c * kWarpW);
+            const int64_t a_abs = AL ? ws_abs - VEC : ((ws_abs - 1) / VEC) * VEC;
+            uint8_t* stage = stage0 + st * P.stage_bytes;
+            const E* chunk_v = reinterpret_cast<const E*>(stage) + (ws_abs - a_abs);  // chunk_v[j] = c[ws_abs + j]
+            mbar_wait(&mbar[st], (uint32_t)((q >> 1) & 1));
+
+            if (c == 0) {
+                const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
+                prof = P.profile_id ? (int)P.profile_id[i] : 0;
+                if (prof >= P.n_prof) prof = 0;
+                J = P.job ? P.job[i] : 0.0;
+                status = (int)rec[5];
+                wl = rec[3];
+                maxci = P.max_ci_fixed > 0.0 ? P.max_ci_fixed : rec[4];
+                if (status == 0 && MODE == MODE_FUSED && !(maxci > 0.0)) status = CHASE_ERR_MAXCI;
+                const int64_t m = (int64_t)rec[8];
+                mb = (J > 0.0 && m >= 1 && m <= P.W) ? m - 1 : P.W;
+                phase_c = (int)(((int64_t)P.phase0 + P.L) % P.T);
+                Cb_run = 0.0;
+                if (status == 0 && MODE != MODE_REPLAY) {
+                    const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
+                    const int n_a = aext_len(P.T);
+                    for (int j = lane; j < n_a; j += 32) {
+                        // A(phi) = (c0 + w_sin*S[phi]) + w_cos*C[phi]  (canonical fold of Eq. 1)
+                        int ph = j % P.T;
+                        A_even[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph])), __dmul_rn(wcs, phC[ph]));
+                        ph = ph + 1 == P.T ? 0 : ph + 1;
+                        A_odd[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph])), __dmul_rn(wcs, phC[ph]));
+                    }
+                }
+                if (lane == 0)
+                    for (int e = 0; e < n_pass; ++e)
+                        state[e * 4 + 0] = state[e * 4 + 1] = state[e * 4 + 2] = state[e * 4 + 3] = 0.0;
+                __syncwarp();
+            } else {
+                phase_c += kWarpW % P.T;
+                if (phase_c >= P.T) phase_c -= P.T;
+            }
+
+            const int j0 = kChunk * lane;
+            const int nwin = max(0, min(kChunk, Wc - j0));
+            const E* tv = chunk_v + j0;
+            int phi0 = phase_c + lane_phase;  // phase of my first window
+            if (phi0 >= P.T) phi0 -= P.T;
+            const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;  // 16-byte aligned
+            const int64_t jb = (int64_t)c * kWarpW + j0;  // my first window, counted from s0
+
+            if (status == CHASE_ERR_MAXCI || status == CHASE_ERR_FIT) {
+                // S:29 precedence: a bad value anywhere makes the trace status 4
+                if (__any_sync(kFull, chunk_has_bad(tv, nwin))) status = CHASE_ERR_DATA;
+            }
+
+            for (int e = 0; e < n_pass && status == 0; ++e, ++gp) {
+                const int sb = (int)(gp & 1);
+                uint8_t* chb = chb0 + sb * kWarpW;
+                if (MODE != MODE_PREDICT) {
+                    if (lane == 0) bulk_wait_read0();  // the store that last read this buffer is done
+                    __syncwarp();
+                }
+                const double S_run = state[e * 4 + 0];
+                const bool done = state[e * 4 + 3] != 0.0;
+                const PairTable* pt = pairs + prof * P.n_eta + e;
+                const ProfileTable* pf = profs + prof;
+                const double Kc = __dmul_rn(pt->kbase, maxci);
+                const double invK = per_trace_invK(pt, Kc);
+                double* fout = (P.forecast && e == 0) ? P.forecast + i * P.ld_f + jb : nullptr;
+
+                Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0};
+                int fast_groups = 0;
+                if (MODE == MODE_FUSED) {
+                    if (AL && sizeof(E) == 4) {
+                        fast_groups = nwin >> 2;
+                        const float* tf = reinterpret_cast<const float*>(tv);
+                        uint32_t* words = reinterpret_cast<uint32_t*>(chb + j0);
+                        if (e == 0) {
+                            if (fout) fused_full<true, true>(tf, fast_groups, Ap, wl, invK, pt, pf->line, words, fout, a);
+                            else fused_full<true, false>(tf, fast_groups, Ap, wl, invK, pt, pf->line, words, fout, a);
+                        } else {
+                            fused_full<false, false>(tf, fast_groups, Ap, wl, invK, pt, pf->line, words, fout, a);
+                        }
+                    }
+                    if (4 * fast_groups < nwin) {
+                        if (e == 0) {
+                            if (fout) fused_generic<true, true, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, a);
+                            else fused_generic<true, false, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, a);
+                        } else {
+                            fused_generic<false, false, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, a);
+                        }
+                    }
+                    if (a.slow & 0x20202020u) slow_count += fix_slow<E>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0, a);
+                } else if (MODE == MODE_PREDICT) {
+                    predict_chunk<E>(tv, nwin, Ap, wl, P.forecast + i * P.ld_f + jb, a);
+                } else {
+                    const uint8_t* cin = P.choice_in + ((int64_t)e * P.n_traces + i) * P.ld_c + jb;
+                    if (e == 0) replay_chunk<true, E>(tv, nwin, cin, pf->K, pf->line, chb + j0, a);
+                    else replay_chunk<false, E>(tv, nwin, cin, pf->K, pf->line, chb + j0, a);
+                }
+
+                int flag = 0;
+                double Cbt = 0.0;
+                if (e == 0) {
+                    if (fast_groups > 0) flag |= (!(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX)) ? 1 : 0;
+                    flag |= a.bad;
+                    // baseline: sum of c over the windows before w*_b
+                    if (jb + nwin <= mb) Cbt = a.Cs;
+                    else if (jb < mb)
+                        for (int jj = 0; jj < (int)(mb - jb); ++jj) Cbt = __dadd_rn(Cbt, (double)tv[jj]);
+                } else {
+                    flag |= a.bad & 2;
+                }
+                const unsigned badv = __ballot_sync(kFull, flag & 1), badk = __ballot_sync(kFull, flag & 2);
+                if (badv | badk) {
+                    status = badv ? CHASE_ERR_DATA : CHASE_ERR_CHOICE;
+                    break;
+                }
+                const double tot = warp_sum4(a.S, a.E, a.C, Cbt, lane);
+                const double S_tile = __shfl_sync(kFull, tot, 0);
+                const double E_tile = __shfl_sync(kFull, tot, 8);
+                const double C_tile = __shfl_sync(kFull, tot, 16);
+                if (e == 0) Cb_run = __dadd_rn(Cb_run, __shfl_sync(kFull, tot, 24));
+                if (MODE == MODE_FUSED && P.choice) {
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        uint8_t* dst = P.choice + ((int64_t)e * P.n_traces + i) * P.ld_c + (int64_t)c * kWarpW;
+                        bulk_s2g(dst, chb, (uint32_t)((Wc + 15) & ~15));
+                        bulk_commit();
+                    }
+                }
+                if (MODE == MODE_PREDICT) continue;
+                const bool completes = !done && J > 0.0 && __dadd_rn(S_run, S_tile) >= J;
+                if (!completes) {
+                    if (lane == 0 && !done) {
+                        state[e * 4 + 0] = __dadd_rn(S_run, S_tile);
+                        state[e * 4 + 1] = __dadd_rn(state[e * 4 + 1], E_tile);
+                        state[e * 4 + 2] = __dadd_rn(state[e * 4 + 2], C_tile);
+                    }
+                    __syncwarp();
+                    continue;
+                }
+                // ---- the job completes inside this chunk (once per trace and eta)
+                const double incl = warp_incl_scan(a.S, lane);
+                const double ex = __shfl_up_sync(kFull, incl, 1);
+                const double before = __dadd_rn(S_run, lane == 0 ? 0.0 : ex);
+                const double after = __dadd_rn(before, a.S);
+                const bool full = after < J;
+                const bool mine = !full && before < J && nwin > 0;
+                const double Em = warp_sum(full ? a.E : 0.0), Cm = warp_sum(full ? a.C : 0.0);
+                double info[6] = {0, 0, 0, 0, 0, 0};
+                if (mine) {
+                    double S = before, Ep = 0.0, Cp = 0.0, f = 1.0, cst = 0.0;
+                    int jj = 0;
+                    uint32_t k = 0;
+                    for (; jj < nwin; ++jj) {
+                        k = chb[j0 + jj];
+                        const double2 ln = pf->line[k];
+                        const double cw = (double)tv[jj];
+                        const double prev = S;
+                        S = __dadd_rn(S, ln.x);
+                        if (S >= J || jj == nwin - 1) {
+                            f = __ddiv_rn(__dsub_rn(J, prev), ln.x);  // pro-rata last window
+                            cst = cw;
+                            break;
+                        }
+                        Ep = __dadd_rn(Ep, ln.y);
+                        Cp = __dadd_rn(Cp, __dmul_rn(ln.y, cw));
+                    }
+                    info[0] = (double)(ws_abs + j0 + jj);
+                    info[1] = f;
+                    info[2] = Ep;
+                    info[3] = Cp;
+                    info[4] = pf->line[k].y;
+                    info[5] = cst;
+                }
+                const unsigned who = __ballot_sync(kFull, mine);
+                if (who == 0) {
+                    // no window reached J in the scan order (non-dyadic rounding): carry on
+                    if (lane == 0) {
+                        state[e * 4 + 0] = __dadd_rn(S_run, S_tile);
+                        state[e * 4 + 1] = __dadd_rn(state[e * 4 + 1], E_tile);
+                        state[e * 4 + 2] = __dadd_rn(state[e * 4 + 2], C_tile);
+                    }
+                    __syncwarp();
+                    continue;
+                }
+                const int src = __ffs(who) - 1;
+#pragma unroll
+                for (int r = 0; r < 6; ++r) info[r] = __shfl_sync(kFull, info[r], src);
+                if (lane == 0) {
+                    double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
+                    r[0] = __dadd_rn(__dadd_rn(state[e * 4 + 1], Em), info[2]);
+                    r[1] = __dadd_rn(__dadd_rn(state[e * 4 + 2], Cm), info[3]);
+                    r[2] = J;
+                    r[3] = info[1];
+                    r[4] = info[0];
+                    r[5] = info[4];
+                    r[6] = info[5];
+                    r[7] = 1.0;
+                    state[e * 4 + 3] = 1.0;
+                }
+                __syncwarp();
+            }
+
+            if (c == nc - 1 && lane == 0) {
+                if (MODE != MODE_PREDICT && status == 0) {
+                    for (int e = 0; e < n_pass; ++e) {
+                        if (state[e * 4 + 3] != 0.0) continue;
+                        double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
+                        r[0] = state[e * 4 + 1];
+                        r[1] = state[e * 4 + 2];
+                        r[2] = state[e * 4 + 0];
+                        r[3] = 0.0;
+                        r[4] = -1.0;
+                        r[5] = r[6] = r[7] = 0.0;
+                    }
+                    P.records[i * kRecDoubles + 9] = Cb_run;
+                }
+                P.status[i] = (uint8_t)status;
+                if (status != 0) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_bad), 1ull);
+                    atomicMin(reinterpret_cast<unsigned long long*>(&P.diag->first_bad_trace), (unsigned long long)i);
+                }
+            }
+            __syncwarp();  // every lane is done with stage `st`
+            if (lane == 0) issue_next();
+        }
+    }
+
+    if (lane == 0) bulk_wait0();
+    unsigned long long sc = (unsigned long long)slow_count;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(kFull, sc, o);
+    if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_slow_windows), sc);
+}
