@@ -146,8 +146,11 @@ __device__ bool chunk_has_bad(const E* tv, int nwin) {
     return b;
 }
 
+
 // ---- shared-memory plan: tables | per warp {A tables, 2 stages, 2 choice buffers, state, mbarriers}
 __host__ __device__ inline int aext_len(int T) { return T + kChunk + 4; }
+
+constexpr int kStateDoubles = 8;  // per eta: S_run, E_run, C_run, done, Kc, invK, Cb_run, -
 
 struct WarpLayout {
     int aext, stage, chb, state, mbar, bytes;
@@ -159,7 +162,7 @@ __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes) {
     L.aext = o; o += 2 * round16(aext_len(T) * 8);
     L.stage = o; o += 2 * stage_bytes;
     L.chb = o; o += 2 * kWarpW;
-    L.state = o; o += kMaxEta * 4 * 8;
+    L.state = o; o += kMaxEta * kStateDoubles * 8;
     L.mbar = o; o += 16;
     L.bytes = round16(o);
     return L;
@@ -167,6 +170,52 @@ __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes) {
 
 __host__ __device__ inline int sweep_smem_total(int tables_bytes, int T, int stage_bytes) {
     return round16(tables_bytes) + kWarpsPerCta * make_warp_layout(T, stage_bytes).bytes;
+}
+
+// Warp-parallel search for the completion window inside lane `src`'s
+// windows: 32 windows per round, inclusive scan of s_k = Thr_k*Delta from
+// `before` (the samples done before them).  Returns w (chunk-relative to the
+// lane's first window) and f, plus E/C of the windows before it.
+template <typename E>
+__device__ void find_completion(const E* tv_src, const uint8_t* bytes_src, int nwin_src, double before, double J,
+                                const double2* lines, int lane, int& w_out, double& f_out, double& Ep, double& Cp,
+                                double& Pk, double& cw_out) {
+    double carry = before;
+    Ep = 0.0;
+    Cp = 0.0;
+    w_out = nwin_src - 1;
+    f_out = 1.0;
+    Pk = 0.0;
+    cw_out = 0.0;
+    for (int r0 = 0; r0 < nwin_src; r0 += 32) {
+        const int jj = r0 + lane;
+        const bool valid = jj < nwin_src;
+        const uint32_t k = valid ? bytes_src[jj] : 0u;
+        const double2 ln = valid ? lines[k] : make_double2(0.0, 0.0);
+        const double cw = valid ? (double)tv_src[jj] : 0.0;
+        const double incl = __dadd_rn(carry, warp_incl_scan(ln.x, lane));
+        const double prev = __shfl_up_sync(kFull, incl, 1);
+        const double before_w = lane == 0 ? carry : prev;
+        const bool hit = valid && incl >= J;
+        const unsigned hits = __ballot_sync(kFull, hit);
+        const int last_valid = min(31, nwin_src - 1 - r0);
+        const bool is_last = r0 + 32 >= nwin_src;
+        const int wl_ = hits ? __ffs(hits) - 1 : (is_last ? last_valid : 32);
+        // windows strictly before the completion window contribute fully
+        const bool pre = valid && lane < wl_;
+        Ep = __dadd_rn(Ep, warp_sum(pre ? ln.y : 0.0));
+        Cp = __dadd_rn(Cp, warp_sum(pre ? __dmul_rn(ln.y, cw) : 0.0));
+        if (wl_ < 32) {
+            const double bw = __shfl_sync(kFull, before_w, wl_);
+            const double sk = __shfl_sync(kFull, ln.x, wl_);
+            w_out = r0 + wl_;
+            f_out = __ddiv_rn(__dsub_rn(J, bw), sk);  // pro-rata last window
+            Pk = __shfl_sync(kFull, ln.y, wl_);
+            cw_out = __shfl_sync(kFull, cw, wl_);
+            return;
+        }
+        carry = __shfl_sync(kFull, incl, 31);
+    }
 }
 
 template <int MODE, typename E, bool AL>
@@ -181,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     double* A_odd = A_even + alen;
     uint8_t* stage0 = wbase + WL.stage;
     uint8_t* chb0 = wbase + WL.chb;
-    double* state = reinterpret_cast<double*>(wbase + WL.state);  // [eta][4]: S_run, E_run, C_run, done
+    double* state = reinterpret_cast<double*>(wbase + WL.state);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + WL.mbar);
 
     {   // constant tables -> smem (16-byte vectors), once per CTA
@@ -206,31 +255,41 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
     const int n_pass = MODE == MODE_PREDICT ? 1 : P.n_eta;
     const E* traces = reinterpret_cast<const E*>(P.traces);
-    const uint64_t policy = evict_first_policy();
     const int nc = P.n_chunks;
+    const int T = P.T;
+    const int W_last = P.W - (nc - 1) * kWarpW;              // windows of the last chunk
+    // loaded element range of chunk c: [a0 + c*kWarpW, ...), a0 16-byte aligned
+    const int a0 = AL ? P.L - VEC : ((P.L - 1) / VEC) * VEC;
+    const int off0 = P.L - a0;                                // chunk_v = stage + off0 elements
+    const uint32_t bytes_full = (uint32_t)((((P.L + kWarpW + VEC - 1) / VEC) * VEC - a0) * (int)sizeof(E));
+    const uint32_t bytes_last = (uint32_t)((min((int64_t)((P.L + (int64_t)(nc - 1) * kWarpW + W_last + VEC - 1) / VEC) * VEC, P.ld) -
+                                           (a0 + (int64_t)(nc - 1) * kWarpW)) * (int)sizeof(E));
 
-    // producer cursor (lane 0): the next (trace, chunk) to load, and its stage
+    // producer cursor (lane 0): next (trace, chunk) to load
     int64_t pi = gw;
     int pc = 0;
-    int64_t issued = 0;
+    const E* psrc = traces + pi * P.ld + a0;
+    uint32_t issued = 0;
+    const uint64_t policy = evict_first_policy();
     auto issue_next = [&]() {
         if (pi >= P.n_traces) return;
         const int st = (int)(issued & 1);
-        const int64_t ws = (int64_t)P.L + (int64_t)pc * kWarpW;
-        const int Wc = min(kWarpW, P.W - pc * kWarpW);
-        const int64_t a = AL ? ws - VEC : ((ws - 1) / VEC) * VEC;
-        int64_t b = ((ws + Wc + VEC - 1) / VEC) * VEC;
-        if (b > P.ld) b = P.ld;
-        const uint32_t bytes = (uint32_t)((b - a) * (int64_t)sizeof(E));
-        const bool rec = pc == 0;
         uint8_t* dst = stage0 + st * P.stage_bytes;
-        mbar_arrive_expect_tx(&mbar[st], bytes + (rec ? (uint32_t)kRecBytes : 0u));
-        bulk_g2s(dst, traces + pi * P.ld + a, bytes, &mbar[st], policy);
-        if (rec) bulk_g2s(dst + P.stage_bytes - kRecBytes, P.records + pi * kRecDoubles, kRecBytes, &mbar[st], policy);
+        const uint32_t bytes = pc == nc - 1 ? bytes_last : bytes_full;
+        if (pc == 0) {
+            mbar_arrive_expect_tx(&mbar[st], bytes + (uint32_t)kRecBytes);
+            bulk_g2s(dst + P.stage_bytes - kRecBytes, P.records + pi * kRecDoubles, kRecBytes, &mbar[st], policy);
+        } else {
+            mbar_arrive_expect_tx(&mbar[st], bytes);
+        }
+        bulk_g2s(dst, psrc, bytes, &mbar[st], policy);
         ++issued;
         if (++pc == nc) {
             pc = 0;
             pi += GW;
+            psrc = traces + pi * P.ld + a0;
+        } else {
+            psrc += kWarpW;
         }
     };
     if (lane == 0) {
@@ -238,23 +297,23 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         issue_next();
     }
 
-    // per-trace (warp-uniform) state
-    int status = 0, prof = 0, phase_c = 0;
-    double wl = 0.0, maxci = 0.0, J = 0.0, Cb_run = 0.0;
-    int64_t mb = 0;
-    int64_t slow_count = 0, gp = 0, q = 0;
-    const int lane_phase = (kChunk * lane) % P.T;
+    const int lane_phase = (kChunk * lane) % T;
+    const int phase_step = kWarpW % T;
+    const int phase_start = (int)(((int64_t)P.phase0 + P.L) % T);
+    const int j0 = kChunk * lane;
+    int64_t slow_count = 0;
+    uint32_t q = 0, gp = 0;
 
     for (int64_t i = gw; i < P.n_traces; i += GW) {
+        // ---- per-trace setup (warp-uniform)
+        int status = 0, prof = 0;
+        double wl = 0.0, J = 0.0;
+        int64_t mb = P.W;
+        int phase_c = phase_start;
         for (int c = 0; c < nc; ++c, ++q) {
             const int st = (int)(q & 1);
-            const int64_t ws_abs = (int64_t)P.L + (int64_t)c * kWarpW;
-            const int Wc = min(kWarpW, P.W - c * kWarpW);
-            const int64_t a_abs = AL ? ws_abs - VEC : ((ws_abs - 1) / VEC) * VEC;
             uint8_t* stage = stage0 + st * P.stage_bytes;
-            const E* chunk_v = reinterpret_cast<const E*>(stage) + (ws_abs - a_abs);  // chunk_v[j] = c[ws_abs + j]
-            mbar_wait(&mbar[st], (uint32_t)((q >> 1) & 1));
-
+            mbar_wait(&mbar[st], (q >> 1) & 1);
             if (c == 0) {
                 const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
                 prof = P.profile_id ? (int)P.profile_id[i] : 0;
@@ -262,39 +321,43 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 J = P.job ? P.job[i] : 0.0;
                 status = (int)rec[5];
                 wl = rec[3];
-                maxci = P.max_ci_fixed > 0.0 ? P.max_ci_fixed : rec[4];
+                const double maxci = P.max_ci_fixed > 0.0 ? P.max_ci_fixed : rec[4];
                 if (status == 0 && MODE == MODE_FUSED && !(maxci > 0.0)) status = CHASE_ERR_MAXCI;
                 const int64_t m = (int64_t)rec[8];
                 mb = (J > 0.0 && m >= 1 && m <= P.W) ? m - 1 : P.W;
-                phase_c = (int)(((int64_t)P.phase0 + P.L) % P.T);
-                Cb_run = 0.0;
                 if (status == 0 && MODE != MODE_REPLAY) {
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
-                    const int n_a = aext_len(P.T);
+                    const int n_a = aext_len(T);
+                    int ph = lane % T;
                     for (int j = lane; j < n_a; j += 32) {
                         // A(phi) = (c0 + w_sin*S[phi]) + w_cos*C[phi]  (canonical fold of Eq. 1)
-                        int ph = j % P.T;
+                        const int ph1 = ph + 1 == T ? 0 : ph + 1;
                         A_even[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph])), __dmul_rn(wcs, phC[ph]));
-                        ph = ph + 1 == P.T ? 0 : ph + 1;
-                        A_odd[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph])), __dmul_rn(wcs, phC[ph]));
+                        A_odd[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph1])), __dmul_rn(wcs, phC[ph1]));
+                        ph += 32;
+                        while (ph >= T) ph -= T;
                     }
                 }
-                if (lane == 0)
-                    for (int e = 0; e < n_pass; ++e)
-                        state[e * 4 + 0] = state[e * 4 + 1] = state[e * 4 + 2] = state[e * 4 + 3] = 0.0;
+                if (lane < n_pass) {  // per-eta state; Kc and 1/Kc once per trace
+                    const PairTable* pt = pairs + prof * P.n_eta + lane;
+                    const double Kc = __dmul_rn(pt->kbase, maxci);
+                    double* s = state + lane * kStateDoubles;
+                    s[0] = s[1] = s[2] = s[3] = s[6] = 0.0;
+                    s[4] = Kc;
+                    s[5] = per_trace_invK(pt, Kc);
+                }
                 __syncwarp();
             } else {
-                phase_c += kWarpW % P.T;
-                if (phase_c >= P.T) phase_c -= P.T;
+                phase_c += phase_step;
+                if (phase_c >= T) phase_c -= T;
             }
 
-            const int j0 = kChunk * lane;
-            const int nwin = max(0, min(kChunk, Wc - j0));
-            const E* tv = chunk_v + j0;
-            int phi0 = phase_c + lane_phase;  // phase of my first window
-            if (phi0 >= P.T) phi0 -= P.T;
+            const int nwin = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - j0));
+            const E* tv = reinterpret_cast<const E*>(stage) + off0 + j0;  // tv[jj] = c[w0 + jj]
+            int phi0 = phase_c + lane_phase;                              // phase of my first window
+            if (phi0 >= T) phi0 -= T;
             const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;  // 16-byte aligned
-            const int64_t jb = (int64_t)c * kWarpW + j0;  // my first window, counted from s0
+            const int64_t jb = (int64_t)c * kWarpW + j0;                  // my first window, from s0
 
             if (status == CHASE_ERR_MAXCI || status == CHASE_ERR_FIT) {
                 // S:29 precedence: a bad value anywhere makes the trace status 4
@@ -308,17 +371,17 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     if (lane == 0) bulk_wait_read0();  // the store that last read this buffer is done
                     __syncwarp();
                 }
-                const double S_run = state[e * 4 + 0];
-                const bool done = state[e * 4 + 3] != 0.0;
+                double* s = state + e * kStateDoubles;
+                const double S_run = s[0];
+                const bool done = s[3] != 0.0;
+                const double Kc = s[4], invK = s[5];
                 const PairTable* pt = pairs + prof * P.n_eta + e;
                 const ProfileTable* pf = profs + prof;
-                const double Kc = __dmul_rn(pt->kbase, maxci);
-                const double invK = per_trace_invK(pt, Kc);
-                double* fout = (P.forecast && e == 0) ? P.forecast + i * P.ld_f + jb : nullptr;
 
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0};
                 int fast_groups = 0;
                 if (MODE == MODE_FUSED) {
+                    double* fout = (P.forecast && e == 0) ? P.forecast + i * P.ld_f + jb : nullptr;
                     if (AL && sizeof(E) == 4) {
                         fast_groups = nwin >> 2;
                         const float* tf = reinterpret_cast<const float*>(tv);
@@ -347,44 +410,40 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     else replay_chunk<false, E>(tv, nwin, cin, pf->K, pf->line, chb + j0, a);
                 }
 
-                int flag = 0;
+                int flag = a.bad;
                 double Cbt = 0.0;
                 if (e == 0) {
-                    if (fast_groups > 0) flag |= (!(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX)) ? 1 : 0;
-                    flag |= a.bad;
+                    if (fast_groups > 0 && (!(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX))) flag |= 1;
                     // baseline: sum of c over the windows before w*_b
                     if (jb + nwin <= mb) Cbt = a.Cs;
                     else if (jb < mb)
                         for (int jj = 0; jj < (int)(mb - jb); ++jj) Cbt = __dadd_rn(Cbt, (double)tv[jj]);
-                } else {
-                    flag |= a.bad & 2;
                 }
-                const unsigned badv = __ballot_sync(kFull, flag & 1), badk = __ballot_sync(kFull, flag & 2);
-                if (badv | badk) {
-                    status = badv ? CHASE_ERR_DATA : CHASE_ERR_CHOICE;
+                flag = (int)__reduce_or_sync(kFull, (unsigned)flag);
+                if (flag) {
+                    status = (flag & 1) ? CHASE_ERR_DATA : CHASE_ERR_CHOICE;
                     break;
                 }
+                // lanes 0, 8, 16, 24 receive the warp totals of S, E, C, Cb
                 const double tot = warp_sum4(a.S, a.E, a.C, Cbt, lane);
                 const double S_tile = __shfl_sync(kFull, tot, 0);
-                const double E_tile = __shfl_sync(kFull, tot, 8);
-                const double C_tile = __shfl_sync(kFull, tot, 16);
-                if (e == 0) Cb_run = __dadd_rn(Cb_run, __shfl_sync(kFull, tot, 24));
+                if (e == 0 && lane == 24) s[6] = __dadd_rn(s[6], tot);
                 if (MODE == MODE_FUSED && P.choice) {
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) {
                         uint8_t* dst = P.choice + ((int64_t)e * P.n_traces + i) * P.ld_c + (int64_t)c * kWarpW;
-                        bulk_s2g(dst, chb, (uint32_t)((Wc + 15) & ~15));
+                        bulk_s2g(dst, chb, (uint32_t)((c < nc - 1 ? kWarpW : W_last + 15) & ~15));
                         bulk_commit();
                     }
                 }
                 if (MODE == MODE_PREDICT) continue;
                 const bool completes = !done && J > 0.0 && __dadd_rn(S_run, S_tile) >= J;
                 if (!completes) {
-                    if (lane == 0 && !done) {
-                        state[e * 4 + 0] = __dadd_rn(S_run, S_tile);
-                        state[e * 4 + 1] = __dadd_rn(state[e * 4 + 1], E_tile);
-                        state[e * 4 + 2] = __dadd_rn(state[e * 4 + 2], C_tile);
+                    if (!done) {
+                        if (lane == 0) s[0] = __dadd_rn(S_run, S_tile);
+                        if (lane == 8) s[1] = __dadd_rn(s[1], tot);
+                        if (lane == 16) s[2] = __dadd_rn(s[2], tot);
                     }
                     __syncwarp();
                     continue;
@@ -395,59 +454,34 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 const double before = __dadd_rn(S_run, lane == 0 ? 0.0 : ex);
                 const double after = __dadd_rn(before, a.S);
                 const bool full = after < J;
-                const bool mine = !full && before < J && nwin > 0;
+                const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
                 const double Em = warp_sum(full ? a.E : 0.0), Cm = warp_sum(full ? a.C : 0.0);
-                double info[6] = {0, 0, 0, 0, 0, 0};
-                if (mine) {
-                    double S = before, Ep = 0.0, Cp = 0.0, f = 1.0, cst = 0.0;
-                    int jj = 0;
-                    uint32_t k = 0;
-                    for (; jj < nwin; ++jj) {
-                        k = chb[j0 + jj];
-                        const double2 ln = pf->line[k];
-                        const double cw = (double)tv[jj];
-                        const double prev = S;
-                        S = __dadd_rn(S, ln.x);
-                        if (S >= J || jj == nwin - 1) {
-                            f = __ddiv_rn(__dsub_rn(J, prev), ln.x);  // pro-rata last window
-                            cst = cw;
-                            break;
-                        }
-                        Ep = __dadd_rn(Ep, ln.y);
-                        Cp = __dadd_rn(Cp, __dmul_rn(ln.y, cw));
-                    }
-                    info[0] = (double)(ws_abs + j0 + jj);
-                    info[1] = f;
-                    info[2] = Ep;
-                    info[3] = Cp;
-                    info[4] = pf->line[k].y;
-                    info[5] = cst;
-                }
-                const unsigned who = __ballot_sync(kFull, mine);
+                __syncwarp();
                 if (who == 0) {
                     // no window reached J in the scan order (non-dyadic rounding): carry on
-                    if (lane == 0) {
-                        state[e * 4 + 0] = __dadd_rn(S_run, S_tile);
-                        state[e * 4 + 1] = __dadd_rn(state[e * 4 + 1], E_tile);
-                        state[e * 4 + 2] = __dadd_rn(state[e * 4 + 2], C_tile);
-                    }
+                    if (lane == 0) s[0] = __dadd_rn(S_run, S_tile);
+                    if (lane == 8) s[1] = __dadd_rn(s[1], tot);
+                    if (lane == 16) s[2] = __dadd_rn(s[2], tot);
                     __syncwarp();
                     continue;
                 }
                 const int src = __ffs(who) - 1;
-#pragma unroll
-                for (int r = 0; r < 6; ++r) info[r] = __shfl_sync(kFull, info[r], src);
+                const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
+                int wrel;
+                double f, Ep, Cp, Pk, cst;
+                find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
+                                   __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep, Cp, Pk, cst);
                 if (lane == 0) {
                     double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
-                    r[0] = __dadd_rn(__dadd_rn(state[e * 4 + 1], Em), info[2]);
-                    r[1] = __dadd_rn(__dadd_rn(state[e * 4 + 2], Cm), info[3]);
+                    r[0] = __dadd_rn(__dadd_rn(s[1], Em), Ep);
+                    r[1] = __dadd_rn(__dadd_rn(s[2], Cm), Cp);
                     r[2] = J;
-                    r[3] = info[1];
-                    r[4] = info[0];
-                    r[5] = info[4];
-                    r[6] = info[5];
+                    r[3] = f;
+                    r[4] = (double)((int64_t)P.L + (int64_t)c * kWarpW + kChunk * src + wrel);
+                    r[5] = Pk;
+                    r[6] = cst;
                     r[7] = 1.0;
-                    state[e * 4 + 3] = 1.0;
+                    s[3] = 1.0;
                 }
                 __syncwarp();
             }
@@ -455,16 +489,17 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
             if (c == nc - 1 && lane == 0) {
                 if (MODE != MODE_PREDICT && status == 0) {
                     for (int e = 0; e < n_pass; ++e) {
-                        if (state[e * 4 + 3] != 0.0) continue;
+                        const double* s = state + e * kStateDoubles;
+                        if (s[3] != 0.0) continue;
                         double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
-                        r[0] = state[e * 4 + 1];
-                        r[1] = state[e * 4 + 2];
-                        r[2] = state[e * 4 + 0];
+                        r[0] = s[1];
+                        r[1] = s[2];
+                        r[2] = s[0];
                         r[3] = 0.0;
                         r[4] = -1.0;
                         r[5] = r[6] = r[7] = 0.0;
                     }
-                    P.records[i * kRecDoubles + 9] = Cb_run;
+                    P.records[i * kRecDoubles + 9] = state[6];
                 }
                 P.status[i] = (uint8_t)status;
                 if (status != 0) {
