@@ -222,8 +222,8 @@ bool aligned_start(const chase_traces_t* t, int L) {
     return L % vec == 0 && L >= vec;
 }
 
-chase_status_t check_smem(int tb, int T, const chase_traces_t* t) {
-    size_t need = sweep_smem_bytes(tb, T, t->dtype == CHASE_F64 ? 8 : 4, 0);
+chase_status_t check_smem(int tb, int T, const chase_traces_t* t, int n_eta) {
+    size_t need = sweep_smem_bytes(tb, T, t->dtype == CHASE_F64 ? 8 : 4, n_eta);
     if (need > 227 * 1024)
         return fail(CHASE_ERR_INVALID, "shared-memory plan %zu B exceeds 227 KB (reduce profiles x eta or use f32)", need);
     return CHASE_OK;
@@ -387,7 +387,7 @@ chase_status_t chase_replay(const chase_traces_t* traces, int32_t history_len, c
     std::vector<double> etas((size_t)n_eta, 0.5);  // eta is not used by the replay; tables need a value
     chase_cost_cfg_t cc{etas.data(), n_eta, 0, 0.0, 0.0};
     std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, &cc, n_eta);
-    if ((st = check_smem((int)blob.size(), T, traces))) return st;
+    if ((st = check_smem((int)blob.size(), T, traces, n_eta))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     if ((st = upload_tables(blob, ws, WL, s))) return st;
@@ -429,7 +429,7 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, cost->n_eta);
     if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
     std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, cost, cost->n_eta);
-    if ((st = check_smem((int)blob.size(), T, traces))) return st;
+    if ((st = check_smem((int)blob.size(), T, traces, cost->n_eta))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     if ((st = upload_tables(blob, ws, WL, s))) return st;

@@ -40,7 +40,7 @@ int num_sms() {
 
 template <int MODE, typename E, bool AL>
 cudaError_t launch_sweep_t(const SweepParams& p, cudaStream_t s) {
-    const int smem = sweep_smem_total(p.tables_bytes, p.T, p.stage_bytes);
+    const int smem = sweep_smem_total(p.tables_bytes, p.T, p.stage_bytes, p.n_eta);
     auto kern = sweep_kernel<MODE, E, AL>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
@@ -63,9 +63,8 @@ uint64_t kernel_launches() { return g_launches; }
 
 int sweep_stage_bytes(int elem_size) { return round16((kWarpW + 8) * elem_size) + kRecBytes; }
 
-size_t sweep_smem_bytes(int tables_bytes, int T, int elem_size, int mode) {
-    (void)mode;
-    return (size_t)sweep_smem_total(tables_bytes, T, sweep_stage_bytes(elem_size));
+size_t sweep_smem_bytes(int tables_bytes, int T, int elem_size, int mode) {  // mode: n_eta
+    return (size_t)sweep_smem_total(tables_bytes, T, sweep_stage_bytes(elem_size), mode);
 }
 
 int64_t finalize_grid(int64_t n_traces) { return (n_traces + kFinThreads - 1) / kFinThreads; }

@@ -85,11 +85,16 @@ __device__ void fused_generic(const E* tv, int j_begin, int nwin, const double* 
 }
 
 // The deferred windows (kZeroLine): canonical K-way Eq. 6, then their replay
-// contributions (exact for dyadic inputs in any order).
+// contributions (exact for dyadic inputs in any order).  Returns
+// the corrections by value so the accumulators stay in registers.
+struct SlowFix {
+    double S, E, C;
+    int n;
+};
 template <typename E>
-__device__ __noinline__ int fix_slow(const E* tv, int nwin, const double* Ap, double wl, double Kc, const PairTable* pt,
-                                     const ProfileTable* pf, uint8_t* bytes, Acc& a) {
-    int n = 0;
+__device__ __noinline__ SlowFix fix_slow(const E* tv, int nwin, const double* Ap, double wl, double Kc,
+                                         const PairTable* pt, const ProfileTable* pf, uint8_t* bytes) {
+    SlowFix r{0.0, 0.0, 0.0, 0};
     for (int jj = 0; jj < nwin; ++jj) {
         if (bytes[jj] != (uint8_t)kZeroLine) continue;
         const double x = predict(Ap[jj], wl, (double)tv[jj - 1]);
@@ -97,12 +102,12 @@ __device__ __noinline__ int fix_slow(const E* tv, int nwin, const double* Ap, do
         bytes[jj] = (uint8_t)k;
         const double2 ln = pf->line[k];
         const double cw = (double)tv[jj];
-        a.S = __dadd_rn(a.S, ln.x);
-        a.E = __dadd_rn(a.E, ln.y);
-        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
-        ++n;
+        r.S = __dadd_rn(r.S, ln.x);
+        r.E = __dadd_rn(r.E, ln.y);
+        r.C = __dadd_rn(r.C, __dmul_rn(ln.y, cw));
+        ++r.n;
     }
-    return n;
+    return r;
 }
 
 template <typename E>
@@ -156,20 +161,20 @@ struct WarpLayout {
     int aext, stage, chb, state, mbar, bytes;
 };
 
-__host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes) {
+__host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, int n_eta) {
     WarpLayout L;
     int o = 0;
     L.aext = o; o += 2 * round16(aext_len(T) * 8);
     L.stage = o; o += 2 * stage_bytes;
     L.chb = o; o += 2 * kWarpW;
-    L.state = o; o += kMaxEta * kStateDoubles * 8;
+    L.state = o; o += n_eta * kStateDoubles * 8;
     L.mbar = o; o += 16;
     L.bytes = round16(o);
     return L;
 }
 
-__host__ __device__ inline int sweep_smem_total(int tables_bytes, int T, int stage_bytes) {
-    return round16(tables_bytes) + kWarpsPerCta * make_warp_layout(T, stage_bytes).bytes;
+__host__ __device__ inline int sweep_smem_total(int tables_bytes, int T, int stage_bytes, int n_eta) {
+    return round16(tables_bytes) + kWarpsPerCta * make_warp_layout(T, stage_bytes, n_eta).bytes;
 }
 
 // Warp-parallel search for the completion window inside lane `src`'s
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     extern __shared__ __align__(128) uint8_t sm[];
     constexpr int VEC = 16 / (int)sizeof(E);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const WarpLayout WL = make_warp_layout(P.T, P.stage_bytes);
+    const WarpLayout WL = make_warp_layout(P.T, P.stage_bytes, P.n_eta);
     uint8_t* wbase = sm + round16(P.tables_bytes) + warp * WL.bytes;
     const int alen = round16(aext_len(P.T) * 8) / 8;
     double* A_even = reinterpret_cast<double*>(wbase + WL.aext);
@@ -401,7 +406,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                             fused_generic<false, false, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, a);
                         }
                     }
-                    if (a.slow & 0x20202020u) slow_count += fix_slow<E>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0, a);
+                    if (a.slow & 0x20202020u) {
+                        const SlowFix fx = fix_slow<E>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0);
+                        a.S = __dadd_rn(a.S, fx.S);
+                        a.E = __dadd_rn(a.E, fx.E);
+                        a.C = __dadd_rn(a.C, fx.C);
+                        slow_count += fx.n;
+                    }
                 } else if (MODE == MODE_PREDICT) {
                     predict_chunk<E>(tv, nwin, Ap, wl, P.forecast + i * P.ld_f + jb, a);
                 } else {
