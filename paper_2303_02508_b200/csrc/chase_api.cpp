@@ -171,9 +171,11 @@ std::vector<uint8_t> build_tables(int T, double delta, const chase_profile_t* pr
         ProfileTable& T_ = pt[q];
         T_.K = P.n_limits;
         T_.pmax = (cost && cost->max_power_w > 0) ? cost->max_power_w : (double)P.limit_w[P.n_limits - 1];
+        T_.smax = 0.0;
         for (int k = 0; k < P.n_limits; ++k) {
             T_.line[k] = make_double2(P.throughput_sps[k] * delta, P.avg_power_w[k]);
             T_.thr[k] = P.throughput_sps[k];
+            if (T_.line[k].x > T_.smax) T_.smax = T_.line[k].x;
         }
         for (int e = 0; e < n_eta; ++e)
             build_pair_table(P.n_limits, P.avg_power_w, P.throughput_sps, cost->eta[e], T_.pmax, &pr[q * n_eta + e]);

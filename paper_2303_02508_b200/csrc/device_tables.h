@@ -37,6 +37,8 @@ struct alignas(16) ProfileTable {
     double thr[kMaxK];     // Thr_k
     int32_t K, reserved;
     double pmax;           // resolved MaxPower
+    double smax;           // max_k s_k (bounds the samples done after n windows)
+    double reserved2;
 };
 
 struct alignas(16) PairTable {

@@ -151,14 +151,15 @@ __device__ bool chunk_has_bad(const E* tv, int nwin) {
     return b;
 }
 
-
 // ---- shared-memory plan: tables | per warp {A tables, 2 stages, 2 choice buffers, state, mbarriers}
 __host__ __device__ inline int aext_len(int T) { return T + kChunk + 4; }
 
-constexpr int kStateDoubles = 8;  // per eta: S_run, E_run, C_run, done, Kc, invK, Cb_run, -
+// per eta (warp-uniform): Kc, 1/Kc, done, -; per (eta, lane): running S, E, C, Cb
+constexpr int kEtaState = 4;
+constexpr int kLaneState = 4;
 
 struct WarpLayout {
-    int aext, stage, chb, state, mbar, bytes;
+    int aext, stage, chb, eta, lanes, mbar, bytes;
 };
 
 __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, int n_eta) {
@@ -167,7 +168,8 @@ __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, i
     L.aext = o; o += 2 * round16(aext_len(T) * 8);
     L.stage = o; o += 2 * stage_bytes;
     L.chb = o; o += 2 * kWarpW;
-    L.state = o; o += n_eta * kStateDoubles * 8;
+    L.eta = o; o += n_eta * kEtaState * 8;
+    L.lanes = o; o += n_eta * 32 * kLaneState * 8;
     L.mbar = o; o += 16;
     L.bytes = round16(o);
     return L;
@@ -179,8 +181,8 @@ __host__ __device__ inline int sweep_smem_total(int tables_bytes, int T, int sta
 
 // Warp-parallel search for the completion window inside lane `src`'s
 // windows: 32 windows per round, inclusive scan of s_k = Thr_k*Delta from
-// `before` (the samples done before them).  Returns w (chunk-relative to the
-// lane's first window) and f, plus E/C of the windows before it.
+// `before` (the samples done before them).  Returns the window (relative to
+// the lane's first), f, and E/C of the windows before it.
 template <typename E>
 __device__ void find_completion(const E* tv_src, const uint8_t* bytes_src, int nwin_src, double before, double J,
                                 const double2* lines, int lane, int& w_out, double& f_out, double& Ep, double& Cp,
@@ -201,13 +203,10 @@ __device__ void find_completion(const E* tv_src, const uint8_t* bytes_src, int n
         const double incl = __dadd_rn(carry, warp_incl_scan(ln.x, lane));
         const double prev = __shfl_up_sync(kFull, incl, 1);
         const double before_w = lane == 0 ? carry : prev;
-        const bool hit = valid && incl >= J;
-        const unsigned hits = __ballot_sync(kFull, hit);
-        const int last_valid = min(31, nwin_src - 1 - r0);
+        const unsigned hits = __ballot_sync(kFull, valid && incl >= J);
         const bool is_last = r0 + 32 >= nwin_src;
-        const int wl_ = hits ? __ffs(hits) - 1 : (is_last ? last_valid : 32);
-        // windows strictly before the completion window contribute fully
-        const bool pre = valid && lane < wl_;
+        const int wl_ = hits ? __ffs(hits) - 1 : (is_last ? min(31, nwin_src - 1 - r0) : 32);
+        const bool pre = valid && lane < wl_;  // windows strictly before the completion window
         Ep = __dadd_rn(Ep, warp_sum(pre ? ln.y : 0.0));
         Cp = __dadd_rn(Cp, warp_sum(pre ? __dmul_rn(ln.y, cw) : 0.0));
         if (wl_ < 32) {
@@ -235,7 +234,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     double* A_odd = A_even + alen;
     uint8_t* stage0 = wbase + WL.stage;
     uint8_t* chb0 = wbase + WL.chb;
-    double* state = reinterpret_cast<double*>(wbase + WL.state);
+    double* eta_st = reinterpret_cast<double*>(wbase + WL.eta);
+    double* lane_st = reinterpret_cast<double*>(wbase + WL.lanes) + lane * kLaneState;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + WL.mbar);
 
     {   // constant tables -> smem (16-byte vectors), once per CTA
@@ -262,13 +262,15 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     const E* traces = reinterpret_cast<const E*>(P.traces);
     const int nc = P.n_chunks;
     const int T = P.T;
-    const int W_last = P.W - (nc - 1) * kWarpW;              // windows of the last chunk
+    const int W_last = P.W - (nc - 1) * kWarpW;  // windows of the last chunk
     // loaded element range of chunk c: [a0 + c*kWarpW, ...), a0 16-byte aligned
     const int a0 = AL ? P.L - VEC : ((P.L - 1) / VEC) * VEC;
-    const int off0 = P.L - a0;                                // chunk_v = stage + off0 elements
+    const int off0 = P.L - a0;  // tv = stage + off0 elements
     const uint32_t bytes_full = (uint32_t)((((P.L + kWarpW + VEC - 1) / VEC) * VEC - a0) * (int)sizeof(E));
-    const uint32_t bytes_last = (uint32_t)((min((int64_t)((P.L + (int64_t)(nc - 1) * kWarpW + W_last + VEC - 1) / VEC) * VEC, P.ld) -
-                                           (a0 + (int64_t)(nc - 1) * kWarpW)) * (int)sizeof(E));
+    const uint32_t bytes_last =
+        (uint32_t)((min((int64_t)((P.L + (int64_t)(nc - 1) * kWarpW + W_last + VEC - 1) / VEC) * VEC, P.ld) -
+                    (a0 + (int64_t)(nc - 1) * kWarpW)) *
+                   (int)sizeof(E));
 
     // producer cursor (lane 0): next (trace, chunk) to load
     int64_t pi = gw;
@@ -310,19 +312,19 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     uint32_t q = 0, gp = 0;
 
     for (int64_t i = gw; i < P.n_traces; i += GW) {
-        // ---- per-trace setup (warp-uniform)
         int status = 0, prof = 0;
-        double wl = 0.0, J = 0.0;
+        double wl = 0.0, J = 0.0, smax = 0.0;
         int64_t mb = P.W;
         int phase_c = phase_start;
         for (int c = 0; c < nc; ++c, ++q) {
             const int st = (int)(q & 1);
             uint8_t* stage = stage0 + st * P.stage_bytes;
             mbar_wait(&mbar[st], (q >> 1) & 1);
-            if (c == 0) {
+            if (c == 0) {  // ---- per-trace setup (warp-uniform)
                 const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
                 prof = P.profile_id ? (int)P.profile_id[i] : 0;
                 if (prof >= P.n_prof) prof = 0;
+                smax = profs[prof].smax;
                 J = P.job ? P.job[i] : 0.0;
                 status = (int)rec[5];
                 wl = rec[3];
@@ -343,13 +345,17 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                         while (ph >= T) ph -= T;
                     }
                 }
-                if (lane < n_pass) {  // per-eta state; Kc and 1/Kc once per trace
+                if (lane < n_pass) {  // Kc and 1/Kc once per trace and eta
                     const PairTable* pt = pairs + prof * P.n_eta + lane;
                     const double Kc = __dmul_rn(pt->kbase, maxci);
-                    double* s = state + lane * kStateDoubles;
-                    s[0] = s[1] = s[2] = s[3] = s[6] = 0.0;
-                    s[4] = Kc;
-                    s[5] = per_trace_invK(pt, Kc);
+                    double* es = eta_st + lane * kEtaState;
+                    es[0] = Kc;
+                    es[1] = per_trace_invK(pt, Kc);
+                    es[2] = 0.0;
+                }
+                for (int e = 0; e < n_pass; ++e) {
+                    double* ls = lane_st + e * 32 * kLaneState;
+                    ls[0] = ls[1] = ls[2] = ls[3] = 0.0;
                 }
                 __syncwarp();
             } else {
@@ -363,6 +369,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
             if (phi0 >= T) phi0 -= T;
             const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;  // 16-byte aligned
             const int64_t jb = (int64_t)c * kWarpW + j0;                  // my first window, from s0
+            // samples cannot reach J before this many windows: skip the completion test until then
+            const int64_t w_through = min((int64_t)P.W, (int64_t)(c + 1) * kWarpW);
+            const bool may_complete = J > 0.0 && __dmul_rn(__dmul_rn((double)w_through, smax), 1.000001) >= J;
 
             if (status == CHASE_ERR_MAXCI || status == CHASE_ERR_FIT) {
                 // S:29 precedence: a bad value anywhere makes the trace status 4
@@ -376,10 +385,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     if (lane == 0) bulk_wait_read0();  // the store that last read this buffer is done
                     __syncwarp();
                 }
-                double* s = state + e * kStateDoubles;
-                const double S_run = s[0];
-                const bool done = s[3] != 0.0;
-                const double Kc = s[4], invK = s[5];
+                double* es = eta_st + e * kEtaState;
+                const double Kc = es[0], invK = es[1];
+                const bool done = es[2] != 0.0;
                 const PairTable* pt = pairs + prof * P.n_eta + e;
                 const ProfileTable* pf = profs + prof;
 
@@ -422,23 +430,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 }
 
                 int flag = a.bad;
-                double Cbt = 0.0;
-                if (e == 0) {
-                    if (fast_groups > 0 && (!(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX))) flag |= 1;
-                    // baseline (S:386-389): sum of c over the windows before w*_b
-                    if (jb + nwin <= mb) Cbt = a.Cs;
-                    else if (jb < mb)
-                        for (int jj = 0; jj < (int)(mb - jb); ++jj) Cbt = __dadd_rn(Cbt, (double)tv[jj]);
-                }
+                if (e == 0 && fast_groups > 0 && (!(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX))) flag |= 1;
                 flag = (int)__reduce_or_sync(kFull, (unsigned)flag);
                 if (flag) {
                     status = (flag & 1) ? CHASE_ERR_DATA : CHASE_ERR_CHOICE;
                     break;
                 }
-                // lanes 0, 8, 16, 24 receive the warp totals of S, E, C, Cb
-                const double tot = warp_sum4(a.S, a.E, a.C, Cbt, lane);
-                const double S_tile = __shfl_sync(kFull, tot, 0);
-                if (e == 0 && lane == 24) s[6] = __dadd_rn(s[6], tot);
                 if (MODE == MODE_FUSED && P.choice) {
                     fence_proxy_async();
                     __syncwarp();
@@ -449,73 +446,96 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     }
                 }
                 if (MODE == MODE_PREDICT) continue;
-                const bool completes = !done && J > 0.0 && __dadd_rn(S_run, S_tile) >= J;
-                if (!completes) {
-                    if (!done) {
-                        if (lane == 0) s[0] = __dadd_rn(S_run, S_tile);
-                        if (lane == 8) s[1] = __dadd_rn(s[1], tot);
-                        if (lane == 16) s[2] = __dadd_rn(s[2], tot);
+
+                // ---- replay bookkeeping: per-lane running sums, warp sums only when needed
+                double* ls = lane_st + e * 32 * kLaneState;
+                double2 se = *reinterpret_cast<double2*>(ls);      // (S_l, E_l)
+                double2 cc = *reinterpret_cast<double2*>(ls + 2);  // (C_l, Cb_l)
+                if (e == 0) {
+                    // baseline (S:386-389): sum of c over the windows before w*_b
+                    if (jb + nwin <= mb) cc.y = __dadd_rn(cc.y, a.Cs);
+                    else if (jb < mb)
+                        for (int jj = 0; jj < (int)(mb - jb); ++jj) cc.y = __dadd_rn(cc.y, (double)tv[jj]);
+                }
+                bool completes = false;
+                double S_prev = 0.0;
+                if (!done && may_complete) {
+                    S_prev = warp_sum(se.x);
+                    completes = __dadd_rn(S_prev, warp_sum(a.S)) >= J;
+                }
+                if (!done && completes) {
+                    // ---- the job completes inside this chunk (once per trace and eta)
+                    const double incl = warp_incl_scan(a.S, lane);
+                    const double ex = __shfl_up_sync(kFull, incl, 1);
+                    const double before = __dadd_rn(S_prev, lane == 0 ? 0.0 : ex);
+                    const bool full = __dadd_rn(before, a.S) < J;
+                    const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
+                    if (who != 0) {
+                        const double Eb = warp_sum(full ? __dadd_rn(se.y, a.E) : se.y);
+                        const double Cb = warp_sum(full ? __dadd_rn(cc.x, a.C) : cc.x);
+                        const int src = __ffs(who) - 1;
+                        const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
+                        int wrel;
+                        double f, Ep, Cp, Pk, cst;
+                        find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
+                                           __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep, Cp, Pk,
+                                           cst);
+                        if (lane == 0) {
+                            double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
+                            r[0] = __dadd_rn(Eb, Ep);
+                            r[1] = __dadd_rn(Cb, Cp);
+                            r[2] = J;
+                            r[3] = f;
+                            r[4] = (double)((int64_t)P.L + (int64_t)c * kWarpW + kChunk * src + wrel);
+                            r[5] = Pk;
+                            r[6] = cst;
+                            r[7] = 1.0;
+                            es[2] = 1.0;
+                        }
+                        *reinterpret_cast<double2*>(ls + 2) = cc;
+                        __syncwarp();
+                        continue;
                     }
-                    __syncwarp();
-                    continue;
-                }
-                // ---- the job completes inside this chunk (once per trace and eta)
-                const double incl = warp_incl_scan(a.S, lane);
-                const double ex = __shfl_up_sync(kFull, incl, 1);
-                const double before = __dadd_rn(S_run, lane == 0 ? 0.0 : ex);
-                const double after = __dadd_rn(before, a.S);
-                const bool full = after < J;
-                const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
-                const double Em = warp_sum(full ? a.E : 0.0), Cm = warp_sum(full ? a.C : 0.0);
-                __syncwarp();
-                if (who == 0) {
                     // no window reached J in the scan order (non-dyadic rounding): carry on
-                    if (lane == 0) s[0] = __dadd_rn(S_run, S_tile);
-                    if (lane == 8) s[1] = __dadd_rn(s[1], tot);
-                    if (lane == 16) s[2] = __dadd_rn(s[2], tot);
-                    __syncwarp();
-                    continue;
                 }
-                const int src = __ffs(who) - 1;
-                const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
-                int wrel;
-                double f, Ep, Cp, Pk, cst;
-                find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
-                                   __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep, Cp, Pk, cst);
-                if (lane == 0) {
-                    double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
-                    r[0] = __dadd_rn(__dadd_rn(s[1], Em), Ep);
-                    r[1] = __dadd_rn(__dadd_rn(s[2], Cm), Cp);
-                    r[2] = J;
-                    r[3] = f;
-                    r[4] = (double)((int64_t)P.L + (int64_t)c * kWarpW + kChunk * src + wrel);
-                    r[5] = Pk;
-                    r[6] = cst;
-                    r[7] = 1.0;
-                    s[3] = 1.0;
+                if (!done) {
+                    se.x = __dadd_rn(se.x, a.S);
+                    se.y = __dadd_rn(se.y, a.E);
+                    cc.x = __dadd_rn(cc.x, a.C);
+                    *reinterpret_cast<double2*>(ls) = se;
                 }
-                __syncwarp();
+                *reinterpret_cast<double2*>(ls + 2) = cc;
             }
 
-            if (c == nc - 1 && lane == 0) {
+            if (c == nc - 1) {  // ---- end of trace: totals of the jobs that did not complete
                 if (MODE != MODE_PREDICT && status == 0) {
                     for (int e = 0; e < n_pass; ++e) {
-                        const double* s = state + e * kStateDoubles;
-                        if (s[3] != 0.0) continue;
-                        double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
-                        r[0] = s[1];
-                        r[1] = s[2];
-                        r[2] = s[0];
-                        r[3] = 0.0;
-                        r[4] = -1.0;
-                        r[5] = r[6] = r[7] = 0.0;
+                        const double* ls = lane_st + e * 32 * kLaneState;
+                        const bool done = eta_st[e * kEtaState + 2] != 0.0;
+                        if (e == 0) {
+                            const double Cb = warp_sum(ls[3]);
+                            if (lane == 0) P.records[i * kRecDoubles + 9] = Cb;
+                        }
+                        if (done) continue;
+                        const double Sx = warp_sum(ls[0]), Ex = warp_sum(ls[1]), Cx = warp_sum(ls[2]);
+                        if (lane == 0) {
+                            double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
+                            r[0] = Ex;
+                            r[1] = Cx;
+                            r[2] = Sx;
+                            r[3] = 0.0;
+                            r[4] = -1.0;
+                            r[5] = r[6] = r[7] = 0.0;
+                        }
                     }
-                    P.records[i * kRecDoubles + 9] = state[6];
                 }
-                P.status[i] = (uint8_t)status;
-                if (status != 0) {
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_bad), 1ull);
-                    atomicMin(reinterpret_cast<unsigned long long*>(&P.diag->first_bad_trace), (unsigned long long)i);
+                if (lane == 0) {
+                    P.status[i] = (uint8_t)status;
+                    if (status != 0) {
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_bad), 1ull);
+                        atomicMin(reinterpret_cast<unsigned long long*>(&P.diag->first_bad_trace),
+                                  (unsigned long long)i);
+                    }
                 }
             }
             __syncwarp();  // every lane is done with stage `st`
