@@ -38,10 +38,10 @@ int num_sms() {
     return sms > 0 ? sms : 148;
 }
 
-template <int MODE, typename E, bool AL>
+template <int MODE, typename E, bool AL, bool MULTI>
 cudaError_t launch_sweep_t(const SweepParams& p, cudaStream_t s) {
     const int smem = sweep_smem_total(p.tables_bytes, p.T, p.stage_bytes, p.n_eta);
-    auto kern = sweep_kernel<MODE, E, AL>;
+    auto kern = sweep_kernel<MODE, E, AL, MULTI>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;
@@ -101,14 +101,17 @@ cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
 
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
-#define CHASE_SWEEP_CASE(M)                                                                                 \
-    if (mode == M) {                                                                                        \
-        if (f64) return aligned ? launch_sweep_t<M, double, true>(p, s) : launch_sweep_t<M, double, false>(p, s); \
-        return aligned ? launch_sweep_t<M, float, true>(p, s) : launch_sweep_t<M, float, false>(p, s);    \
+#define CHASE_SWEEP_CASE(M, MU)                                                                        \
+    if (mode == M && multi == MU) {                                                                    \
+        if (f64) return aligned ? launch_sweep_t<M, double, true, MU>(p, s) : launch_sweep_t<M, double, false, MU>(p, s); \
+        return aligned ? launch_sweep_t<M, float, true, MU>(p, s) : launch_sweep_t<M, float, false, MU>(p, s); \
     }
-    CHASE_SWEEP_CASE(MODE_FUSED)
-    CHASE_SWEEP_CASE(MODE_PREDICT)
-    CHASE_SWEEP_CASE(MODE_REPLAY)
+    const bool multi = mode != MODE_PREDICT && p.n_eta > 1;
+    CHASE_SWEEP_CASE(MODE_FUSED, false)
+    CHASE_SWEEP_CASE(MODE_FUSED, true)
+    CHASE_SWEEP_CASE(MODE_PREDICT, false)
+    CHASE_SWEEP_CASE(MODE_REPLAY, false)
+    CHASE_SWEEP_CASE(MODE_REPLAY, true)
 #undef CHASE_SWEEP_CASE
     return cudaErrorInvalidValue;
 }

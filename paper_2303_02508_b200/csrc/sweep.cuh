@@ -154,12 +154,13 @@ __device__ bool chunk_has_bad(const E* tv, int nwin) {
 // ---- shared-memory plan: tables | per warp {A tables, 2 stages, 2 choice buffers, state, mbarriers}
 __host__ __device__ inline int aext_len(int T) { return T + kChunk + 4; }
 
-// per eta (warp-uniform): Kc, 1/Kc, done, -; per (eta, lane): running S, E, C, Cb
-constexpr int kEtaState = 4;
-constexpr int kLaneState = 4;
+// per eta (warp-uniform): Kc, 1/Kc, done, S_run, E_run, C_run, Cb_run, -
+// (the running sums are used by the multi-eta path; the single-eta path keeps
+// per-lane running sums in registers and reduces only when it must)
+constexpr int kEtaState = 8;
 
 struct WarpLayout {
-    int aext, stage, chb, eta, lanes, mbar, bytes;
+    int aext, stage, chb, eta, mbar, bytes;
 };
 
 __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, int n_eta) {
@@ -169,7 +170,6 @@ __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, i
     L.stage = o; o += 2 * stage_bytes;
     L.chb = o; o += 2 * kWarpW;
     L.eta = o; o += n_eta * kEtaState * 8;
-    L.lanes = o; o += n_eta * 32 * kLaneState * 8;
     L.mbar = o; o += 16;
     L.bytes = round16(o);
     return L;
@@ -222,7 +222,7 @@ __device__ void find_completion(const E* tv_src, const uint8_t* bytes_src, int n
     }
 }
 
-template <int MODE, typename E, bool AL>
+template <int MODE, typename E, bool AL, bool MULTI>
 __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     constexpr int VEC = 16 / (int)sizeof(E);
@@ -235,7 +235,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     uint8_t* stage0 = wbase + WL.stage;
     uint8_t* chb0 = wbase + WL.chb;
     double* eta_st = reinterpret_cast<double*>(wbase + WL.eta);
-    double* lane_st = reinterpret_cast<double*>(wbase + WL.lanes) + lane * kLaneState;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + WL.mbar);
 
     {   // constant tables -> smem (16-byte vectors), once per CTA
@@ -311,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     int64_t slow_count = 0;
     uint32_t q = 0, gp = 0;
 
+    double Sl = 0.0, El = 0.0, Cl = 0.0, Cbl = 0.0;  // single-eta path: per-lane running sums
     for (int64_t i = gw; i < P.n_traces; i += GW) {
         int status = 0, prof = 0;
         double wl = 0.0, J = 0.0, smax = 0.0;
@@ -351,12 +351,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     double* es = eta_st + lane * kEtaState;
                     es[0] = Kc;
                     es[1] = per_trace_invK(pt, Kc);
-                    es[2] = 0.0;
+                    es[2] = es[3] = es[4] = es[5] = es[6] = 0.0;
                 }
-                for (int e = 0; e < n_pass; ++e) {
-                    double* ls = lane_st + e * 32 * kLaneState;
-                    ls[0] = ls[1] = ls[2] = ls[3] = 0.0;
-                }
+                Sl = El = Cl = Cbl = 0.0;
                 __syncwarp();
             } else {
                 phase_c += phase_step;
@@ -447,82 +444,129 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 }
                 if (MODE == MODE_PREDICT) continue;
 
-                // ---- replay bookkeeping: per-lane running sums, warp sums only when needed
-                double* ls = lane_st + e * 32 * kLaneState;
-                double2 se = *reinterpret_cast<double2*>(ls);      // (S_l, E_l)
-                double2 cc = *reinterpret_cast<double2*>(ls + 2);  // (C_l, Cb_l)
+                double Cbt = 0.0;  // baseline: sum of c over the windows before w*_b
                 if (e == 0) {
-                    // baseline: sum of c over the windows before w*_b
-                    if (jb + nwin <= mb) cc.y = __dadd_rn(cc.y, a.Cs);
+                    if (jb + nwin <= mb) Cbt = a.Cs;
                     else if (jb < mb)
-                        for (int jj = 0; jj < (int)(mb - jb); ++jj) cc.y = __dadd_rn(cc.y, (double)tv[jj]);
+                        for (int jj = 0; jj < (int)(mb - jb); ++jj) Cbt = __dadd_rn(Cbt, (double)tv[jj]);
                 }
-                bool completes = false;
-                double S_prev = 0.0;
-                if (!done && may_complete) {
-                    S_prev = warp_sum(se.x);
-                    completes = __dadd_rn(S_prev, warp_sum(a.S)) >= J;
-                }
-                if (!done && completes) {
-                    // ---- the job completes inside this chunk (once per trace and eta)
-                    const double incl = warp_incl_scan(a.S, lane);
-                    const double ex = __shfl_up_sync(kFull, incl, 1);
-                    const double before = __dadd_rn(S_prev, lane == 0 ? 0.0 : ex);
-                    const bool full = __dadd_rn(before, a.S) < J;
-                    const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
-                    if (who != 0) {
-                        const double Eb = warp_sum(full ? __dadd_rn(se.y, a.E) : se.y);
-                        const double Cb = warp_sum(full ? __dadd_rn(cc.x, a.C) : cc.x);
-                        const int src = __ffs(who) - 1;
-                        const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
-                        int wrel;
-                        double f, Ep, Cp, Pk, cst;
-                        find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
-                                           __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep, Cp, Pk,
-                                           cst);
-                        if (lane == 0) {
-                            double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
-                            r[0] = __dadd_rn(Eb, Ep);
-                            r[1] = __dadd_rn(Cb, Cp);
-                            r[2] = J;
-                            r[3] = f;
-                            r[4] = (double)((int64_t)P.L + (int64_t)c * kWarpW + kChunk * src + wrel);
-                            r[5] = Pk;
-                            r[6] = cst;
-                            r[7] = 1.0;
-                            es[2] = 1.0;
+                if constexpr (!MULTI) {
+                    // ---- one eta: per-lane running sums; warp sums only where the job can complete
+                    Cbl = __dadd_rn(Cbl, Cbt);
+                    if (!done && may_complete) {
+                        const double S_prev = warp_sum(Sl);
+                        if (__dadd_rn(S_prev, warp_sum(a.S)) >= J) {
+                            const double incl = warp_incl_scan(a.S, lane);
+                            const double ex = __shfl_up_sync(kFull, incl, 1);
+                            const double before = __dadd_rn(S_prev, lane == 0 ? 0.0 : ex);
+                            const bool full = __dadd_rn(before, a.S) < J;
+                            const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
+                            if (who != 0) {
+                                const double Eb = warp_sum(full ? __dadd_rn(El, a.E) : El);
+                                const double Cb = warp_sum(full ? __dadd_rn(Cl, a.C) : Cl);
+                                const int src = __ffs(who) - 1;
+                                const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
+                                int wrel;
+                                double f, Ep, Cp, Pk, cst;
+                                find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
+                                                   __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep,
+                                                   Cp, Pk, cst);
+                                if (lane == 0) {
+                                    double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
+                                    r[0] = __dadd_rn(Eb, Ep);
+                                    r[1] = __dadd_rn(Cb, Cp);
+                                    r[2] = J;
+                                    r[3] = f;
+                                    r[4] = (double)((int64_t)P.L + (int64_t)c * kWarpW + kChunk * src + wrel);
+                                    r[5] = Pk;
+                                    r[6] = cst;
+                                    r[7] = 1.0;
+                                    es[2] = 1.0;
+                                }
+                                __syncwarp();
+                                continue;
+                            }
+                            // no window reached J in the scan order (non-dyadic rounding): carry on
                         }
-                        *reinterpret_cast<double2*>(ls + 2) = cc;
-                        __syncwarp();
-                        continue;
                     }
-                    // no window reached J in the scan order (non-dyadic rounding): carry on
+                    if (!done) {
+                        Sl = __dadd_rn(Sl, a.S);
+                        El = __dadd_rn(El, a.E);
+                        Cl = __dadd_rn(Cl, a.C);
+                    }
+                } else {
+                    // ---- several etas: per-chunk warp totals into the warp-uniform state
+                    const double tot = warp_sum4(a.S, a.E, a.C, Cbt, lane);  // lanes 0, 8, 16, 24
+                    const double S_tile = __shfl_sync(kFull, tot, 0);
+                    const double S_run = es[3];
+                    if (e == 0 && lane == 24) es[6] = __dadd_rn(es[6], tot);
+                    bool carried = false;
+                    if (!done && J > 0.0 && __dadd_rn(S_run, S_tile) >= J) {
+                        const double incl = warp_incl_scan(a.S, lane);
+                        const double ex = __shfl_up_sync(kFull, incl, 1);
+                        const double before = __dadd_rn(S_run, lane == 0 ? 0.0 : ex);
+                        const bool full = __dadd_rn(before, a.S) < J;
+                        const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
+                        if (who != 0) {
+                            const double Em = warp_sum(full ? a.E : 0.0), Cm = warp_sum(full ? a.C : 0.0);
+                            const int src = __ffs(who) - 1;
+                            const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
+                            int wrel;
+                            double f, Ep, Cp, Pk, cst;
+                            find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
+                                               __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep, Cp,
+                                               Pk, cst);
+                            if (lane == 0) {
+                                double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
+                                r[0] = __dadd_rn(__dadd_rn(es[4], Em), Ep);
+                                r[1] = __dadd_rn(__dadd_rn(es[5], Cm), Cp);
+                                r[2] = J;
+                                r[3] = f;
+                                r[4] = (double)((int64_t)P.L + (int64_t)c * kWarpW + kChunk * src + wrel);
+                                r[5] = Pk;
+                                r[6] = cst;
+                                r[7] = 1.0;
+                                es[2] = 1.0;
+                            }
+                            carried = true;
+                        }
+                    }
+                    if (!done && !carried) {
+                        if (lane == 0) es[3] = __dadd_rn(S_run, S_tile);
+                        if (lane == 8) es[4] = __dadd_rn(es[4], tot);
+                        if (lane == 16) es[5] = __dadd_rn(es[5], tot);
+                    }
+                    __syncwarp();
                 }
-                if (!done) {
-                    se.x = __dadd_rn(se.x, a.S);
-                    se.y = __dadd_rn(se.y, a.E);
-                    cc.x = __dadd_rn(cc.x, a.C);
-                    *reinterpret_cast<double2*>(ls) = se;
-                }
-                *reinterpret_cast<double2*>(ls + 2) = cc;
             }
 
             if (c == nc - 1) {  // ---- end of trace: totals of the jobs that did not complete
                 if (MODE != MODE_PREDICT && status == 0) {
-                    for (int e = 0; e < n_pass; ++e) {
-                        const double* ls = lane_st + e * 32 * kLaneState;
-                        const bool done = eta_st[e * kEtaState + 2] != 0.0;
-                        if (e == 0) {
-                            const double Cb = warp_sum(ls[3]);
-                            if (lane == 0) P.records[i * kRecDoubles + 9] = Cb;
-                        }
-                        if (done) continue;
-                        const double Sx = warp_sum(ls[0]), Ex = warp_sum(ls[1]), Cx = warp_sum(ls[2]);
+                    if constexpr (!MULTI) {
+                        const double Cb = warp_sum(Cbl);
+                        const bool done = eta_st[2] != 0.0;
+                        const double Sx = warp_sum(Sl), Ex = warp_sum(El), Cx = warp_sum(Cl);
                         if (lane == 0) {
+                            P.records[i * kRecDoubles + 9] = Cb;
+                            if (!done) {
+                                double* r = P.raw + i * kRawDoubles;
+                                r[0] = Ex;
+                                r[1] = Cx;
+                                r[2] = Sx;
+                                r[3] = 0.0;
+                                r[4] = -1.0;
+                                r[5] = r[6] = r[7] = 0.0;
+                            }
+                        }
+                    } else if (lane == 0) {
+                        P.records[i * kRecDoubles + 9] = eta_st[6];
+                        for (int e = 0; e < n_pass; ++e) {
+                            const double* es = eta_st + e * kEtaState;
+                            if (es[2] != 0.0) continue;
                             double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
-                            r[0] = Ex;
-                            r[1] = Cx;
-                            r[2] = Sx;
+                            r[0] = es[4];
+                            r[1] = es[5];
+                            r[2] = es[3];
                             r[3] = 0.0;
                             r[4] = -1.0;
                             r[5] = r[6] = r[7] = 0.0;
