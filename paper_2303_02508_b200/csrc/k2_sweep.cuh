@@ -61,7 +61,7 @@ __device__ __forceinline__ void fused_full(const float* __restrict__ tv, int ngr
 
 // Any element type / alignment / window count (odd L, f64, ragged tails).
 template <bool FIRST, bool FC, typename E>
-__device__ void fused_generic(const E* tv, int j_begin, int nwin, const double* Ap, double wl, double invK,
+__device__ __noinline__ void fused_generic(const E* tv, int j_begin, int nwin, const double* Ap, double wl, double invK,
                               const PairTable* pt, const double2* lines, uint8_t* bytes, double* fout, Acc& a) {
     double lag = (double)tv[j_begin - 1];
     for (int jj = j_begin; jj < nwin; ++jj) {
@@ -160,7 +160,18 @@ __host__ __device__ inline int aext_len(int T) { return T + kChunk + 4; }
 constexpr int kEtaState = 8;
 
 struct WarpLayout {
-    int aext, stage, chb, eta, mbar, bytes;
+    int aext, stage, chb, eta, ctx, mbar, bytes;
+};
+
+// Producer cursor and counters, kept in smem (lane 0 reads/writes them once
+// per chunk) so they do not occupy registers across the hot loop.
+struct WarpCtx {
+    const void* psrc;       // next chunk's first element
+    int64_t pi;             // next trace to load
+    int32_t pc;             // next chunk index
+    uint32_t issued;        // loads issued so far (stage parity)
+    unsigned long long slow;  // deferred-window count
+    int64_t reserved;
 };
 
 __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, int n_eta) {
@@ -170,6 +181,7 @@ __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, i
     L.stage = o; o += 2 * stage_bytes;
     L.chb = o; o += 2 * kWarpW;
     L.eta = o; o += n_eta * kEtaState * 8;
+    L.ctx = o; o += (int)sizeof(WarpCtx);
     L.mbar = o; o += 16;
     L.bytes = round16(o);
     return L;
@@ -184,7 +196,7 @@ __host__ __device__ inline int sweep_smem_total(int tables_bytes, int T, int sta
 // `before` (the samples done before them).  Returns the window (relative to
 // the lane's first), f, and E/C of the windows before it.
 template <typename E>
-__device__ void find_completion(const E* tv_src, const uint8_t* bytes_src, int nwin_src, double before, double J,
+__device__ __noinline__ void find_completion(const E* tv_src, const uint8_t* bytes_src, int nwin_src, double before, double J,
                                 const double2* lines, int lane, int& w_out, double& f_out, double& Ep, double& Cp,
                                 double& Pk, double& cw_out) {
     double carry = before;
@@ -235,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     uint8_t* stage0 = wbase + WL.stage;
     uint8_t* chb0 = wbase + WL.chb;
     double* eta_st = reinterpret_cast<double*>(wbase + WL.eta);
+    WarpCtx* ctx = reinterpret_cast<WarpCtx*>(wbase + WL.ctx);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + WL.mbar);
 
     {   // constant tables -> smem (16-byte vectors), once per CTA
@@ -271,14 +284,14 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     (a0 + (int64_t)(nc - 1) * kWarpW)) *
                    (int)sizeof(E));
 
-    // producer cursor (lane 0): next (trace, chunk) to load
-    int64_t pi = gw;
-    int pc = 0;
-    const E* psrc = traces + pi * P.ld + a0;
-    uint32_t issued = 0;
-    const uint64_t policy = evict_first_policy();
+    // producer (lane 0): next (trace, chunk) to load; cursor lives in smem
     auto issue_next = [&]() {
+        const int64_t pi = ctx->pi;
         if (pi >= P.n_traces) return;
+        const int pc = ctx->pc;
+        const uint32_t issued = ctx->issued;
+        const E* psrc = reinterpret_cast<const E*>(ctx->psrc);
+        const uint64_t policy = evict_first_policy();
         const int st = (int)(issued & 1);
         uint8_t* dst = stage0 + st * P.stage_bytes;
         const uint32_t bytes = pc == nc - 1 ? bytes_last : bytes_full;
@@ -289,16 +302,22 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
             mbar_arrive_expect_tx(&mbar[st], bytes);
         }
         bulk_g2s(dst, psrc, bytes, &mbar[st], policy);
-        ++issued;
-        if (++pc == nc) {
-            pc = 0;
-            pi += GW;
-            psrc = traces + pi * P.ld + a0;
+        ctx->issued = issued + 1;
+        if (pc + 1 == nc) {
+            ctx->pc = 0;
+            ctx->pi = pi + GW;
+            ctx->psrc = traces + (pi + GW) * P.ld + a0;
         } else {
-            psrc += kWarpW;
+            ctx->pc = pc + 1;
+            ctx->psrc = psrc + kWarpW;
         }
     };
     if (lane == 0) {
+        ctx->pi = gw;
+        ctx->pc = 0;
+        ctx->issued = 0;
+        ctx->psrc = traces + gw * P.ld + a0;
+        ctx->slow = 0ull;
         issue_next();
         issue_next();
     }
@@ -307,7 +326,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     const int phase_step = kWarpW % T;
     const int phase_start = (int)(((int64_t)P.phase0 + P.L) % T);
     const int j0 = kChunk * lane;
-    int64_t slow_count = 0;
     uint32_t q = 0, gp = 0;
 
     double Sl = 0.0, El = 0.0, Cl = 0.0, Cbl = 0.0;  // single-eta path: per-lane running sums
@@ -416,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                         a.S = __dadd_rn(a.S, fx.S);
                         a.E = __dadd_rn(a.E, fx.E);
                         a.C = __dadd_rn(a.C, fx.C);
-                        slow_count += fx.n;
+                        atomicAdd(&ctx->slow, (unsigned long long)fx.n);
                     }
                 } else if (MODE == MODE_PREDICT) {
                     predict_chunk<E>(tv, nwin, Ap, wl, P.forecast + i * P.ld_f + jb, a);
@@ -587,9 +605,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         }
     }
 
-    if (lane == 0) bulk_wait0();
-    unsigned long long sc = (unsigned long long)slow_count;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(kFull, sc, o);
-    if (lane == 0 && sc) atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_slow_windows), sc);
+    if (lane == 0) {
+        bulk_wait0();
+        if (ctx->slow) atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_slow_windows), ctx->slow);
+    }
 }

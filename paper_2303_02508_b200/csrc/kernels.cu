@@ -28,7 +28,7 @@ namespace {
 
 #include "device_common.cuh"
 #include "fit.cuh"
-#include "sweep.cuh"
+#include "k2_sweep.cuh"
 #include "finalize.cuh"
 
 int num_sms() {
