@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchase.so")
+LIB_PATH = os.environ.get("CHASE_LIB_OVERRIDE") or os.path.join(_HERE, "libchase.so")  # override: A/B builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python build.py` (no CPU fallback exists)")

@@ -32,6 +32,7 @@ __device__ __forceinline__ void fused_full(const float* __restrict__ tv, int ngr
 #pragma unroll 1
     for (int g = 0; g < ngroups; ++g) {
         const float4 v = *reinterpret_cast<const float4*>(tv + 4 * g);
+        if (FIRST) a.vmin = fminf(fminf(fminf(a.vmin, v.x), v.y), fminf(v.z, v.w));  // FMNMX3 x2
         const double2 A01 = *reinterpret_cast<const double2*>(Ap + 4 * g);
         const double2 A23 = *reinterpret_cast<const double2*>(Ap + 4 * g + 2);
         const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -48,10 +49,7 @@ __device__ __forceinline__ void fused_full(const float* __restrict__ tv, int ngr
             a.S = __dadd_rn(a.S, ln.x);
             a.E = __dadd_rn(a.E, ln.y);
             a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
-            if (FIRST) {
-                a.Cs = __dadd_rn(a.Cs, cw);
-                a.vmin = fminf(a.vmin, vv[u]);
-            }
+            if (FIRST) a.Cs = __dadd_rn(a.Cs, cw);
             lag = cw;
         }
         words[g] = word;
@@ -60,9 +58,12 @@ __device__ __forceinline__ void fused_full(const float* __restrict__ tv, int ngr
 }
 
 // Any element type / alignment / window count (odd L, f64, ragged tails).
+// Out of line (cold); returns its partial sums by value so the caller's
+// accumulators stay in registers.
 template <bool FIRST, bool FC, typename E>
-__device__ __noinline__ void fused_generic(const E* tv, int j_begin, int nwin, const double* Ap, double wl, double invK,
-                              const PairTable* pt, const double2* lines, uint8_t* bytes, double* fout, Acc& a) {
+__device__ __noinline__ Acc fused_generic(const E* tv, int j_begin, int nwin, const double* Ap, double wl, double invK,
+                                          const PairTable* pt, const double2* lines, uint8_t* bytes, double* fout) {
+    Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0};
     double lag = (double)tv[j_begin - 1];
     for (int jj = j_begin; jj < nwin; ++jj) {
         const E raw = tv[jj];
@@ -82,6 +83,16 @@ __device__ __noinline__ void fused_generic(const E* tv, int j_begin, int nwin, c
         }
         lag = cw;
     }
+    return a;
+}
+
+__device__ __forceinline__ void acc_merge(Acc& a, const Acc& b) {
+    a.S = __dadd_rn(a.S, b.S);
+    a.E = __dadd_rn(a.E, b.E);
+    a.C = __dadd_rn(a.C, b.C);
+    a.Cs = __dadd_rn(a.Cs, b.Cs);
+    a.slow |= b.slow;
+    a.bad |= b.bad;
 }
 
 // The deferred windows (kZeroLine): canonical K-way Eq. 6, then their replay
@@ -158,6 +169,10 @@ __host__ __device__ inline int aext_len(int T) { return T + kChunk + 4; }
 // (the running sums are used by the multi-eta path; the single-eta path keeps
 // per-lane running sums in registers and reduces only when it must)
 constexpr int kEtaState = 8;
+#ifndef CHASE_STAGES
+#define CHASE_STAGES 3
+#endif
+constexpr int kStages = CHASE_STAGES;  // per-warp TMA ring depth
 
 struct WarpLayout {
     int aext, stage, chb, eta, ctx, mbar, bytes;
@@ -178,11 +193,11 @@ __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, i
     WarpLayout L;
     int o = 0;
     L.aext = o; o += 2 * round16(aext_len(T) * 8);
-    L.stage = o; o += 2 * stage_bytes;
+    L.stage = o; o += kStages * stage_bytes;
     L.chb = o; o += 2 * kWarpW;
     L.eta = o; o += n_eta * kEtaState * 8;
     L.ctx = o; o += (int)sizeof(WarpCtx);
-    L.mbar = o; o += 16;
+    L.mbar = o; o += 8 * kStages;
     L.bytes = round16(o);
     return L;
 }
@@ -256,8 +271,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         for (int q = tid; q < P.tables_bytes / 16; q += kThreads) dst[q] = src[q];
     }
     if (lane == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        for (int q0 = 0; q0 < kStages; ++q0) mbar_init(&mbar[q0], 1);
         fence_mbar_init();
     }
     __syncthreads();  // the only CTA-wide barrier
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         const uint32_t issued = ctx->issued;
         const E* psrc = reinterpret_cast<const E*>(ctx->psrc);
         const uint64_t policy = evict_first_policy();
-        const int st = (int)(issued & 1);
+        const int st = (int)(issued % kStages);
         uint8_t* dst = stage0 + st * P.stage_bytes;
         const uint32_t bytes = pc == nc - 1 ? bytes_last : bytes_full;
         if (pc == 0) {
@@ -318,8 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         ctx->issued = 0;
         ctx->psrc = traces + gw * P.ld + a0;
         ctx->slow = 0ull;
-        issue_next();
-        issue_next();
+        for (int q0 = 0; q0 < kStages; ++q0) issue_next();
     }
 
     const int lane_phase = (kChunk * lane) % T;
@@ -335,9 +348,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         int64_t mb = P.W;
         int phase_c = phase_start;
         for (int c = 0; c < nc; ++c, ++q) {
-            const int st = (int)(q & 1);
+            const int st = (int)(q % kStages);
             uint8_t* stage = stage0 + st * P.stage_bytes;
-            mbar_wait(&mbar[st], (q >> 1) & 1);
+            mbar_wait(&mbar[st], (q / kStages) & 1);
             if (c == 0) {  // ---- per-trace setup (warp-uniform)
                 const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
                 prof = P.profile_id ? (int)P.profile_id[i] : 0;
@@ -422,12 +435,14 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                         }
                     }
                     if (4 * fast_groups < nwin) {
+                        Acc b;
                         if (e == 0) {
-                            if (fout) fused_generic<true, true, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, a);
-                            else fused_generic<true, false, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, a);
+                            if (fout) b = fused_generic<true, true, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout);
+                            else b = fused_generic<true, false, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout);
                         } else {
-                            fused_generic<false, false, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, a);
+                            b = fused_generic<false, false, E>(tv, 4 * fast_groups, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout);
                         }
+                        acc_merge(a, b);
                     }
                     if (a.slow & 0x20202020u) {
                         const SlowFix fx = fix_slow<E>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0);

@@ -9,7 +9,7 @@
 
 namespace chase {
 
-constexpr int kThreads = 256;              // sweep CTA size (8 independent warps)
+constexpr int kThreads = 192;              // sweep CTA size (6 independent warps; 12 per SM at <= 168 registers)
 constexpr int kWarpsPerCta = kThreads / 32;
 constexpr int kChunk = 36;                 // windows per lane per chunk (4 x odd -> conflict-free LDS.128)
 constexpr int kWarpW = 32 * kChunk;        // 1152 windows per warp chunk
