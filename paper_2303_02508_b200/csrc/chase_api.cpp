@@ -208,6 +208,20 @@ SweepParams base_sweep(const chase_traces_t* t, int L, const WsLayout& WL, uint8
     p.phase0 = t->phase0;
     p.W = (int32_t)(t->n_steps - L);
     p.n_chunks = (int32_t)((p.W + kWarpW - 1) / kWarpW);
+    {   // chunk geometry (see k2_sweep.cuh): loaded range of chunk c is [a0 + c*kWarpW, ...)
+        const int esz = t->dtype == CHASE_F64 ? 8 : 4, vec = 16 / esz;
+        const bool al = L % vec == 0 && L >= vec;
+        p.a0 = al ? L - vec : ((L - 1) / vec) * vec;
+        p.off0 = L - p.a0;
+        p.W_last = p.W - (p.n_chunks - 1) * kWarpW;
+        p.bytes_full = (uint32_t)((((int64_t)L + kWarpW + vec - 1) / vec * vec - p.a0) * esz);
+        const int64_t last_end = std::min(((int64_t)L + (int64_t)(p.n_chunks - 1) * kWarpW + p.W_last + vec - 1) / vec * vec,
+                                          t->ld);
+        p.bytes_last = (uint32_t)((last_end - (p.a0 + (int64_t)(p.n_chunks - 1) * kWarpW)) * esz);
+        const int T = 86400 / t->interval_s;
+        p.phase_step = kWarpW % T;
+        p.phase_start = (int32_t)(((int64_t)t->phase0 + L) % T);
+    }
     p.delta = (double)t->interval_s;
     p.records = reinterpret_cast<double*>(ws + WL.records);
     p.raw = reinterpret_cast<double*>(ws + WL.raw);
@@ -576,19 +590,19 @@ extern "C" int32_t chase_testing_envelope(int32_t K, const double* avg_power, co
     const double Kc = pt.kbase * max_ci;
     double invK;
     if (pt.k0) invK = 1.0;
-    else invK = (Kc >= 0x1p-900 && Kc <= 0x1p900) ? 1.0 / Kc : std::nan("");
+    else invK = (Kc >= 0x1p-900 && Kc <= 0x1p900) ? 1.0 / Kc : 0.0;
     for (int64_t i = 0; i < n; ++i) {
+        if (invK == 0.0) { out[i] = -1; continue; }  // whole trace canonical
         const double y = x[i] * invK;
         uint64_t bits;
         std::memcpy(&bits, &y, 8);
-        int hi = (int)(int32_t)(uint32_t)(bits >> 32);
-        int idx = (hi >> kSH) - pt.base;
+        const int h = (int)(int32_t)(uint32_t)(bits >> 32);
+        int idx = (h >> kSH) - pt.base;
         idx = idx < 0 ? 0 : (idx > kNBUsed - 1 ? kNBUsed - 1 : idx);
-        uint32_t e = pt.ent[idx];
-        double2 th;
-        std::memcpy(&th, reinterpret_cast<const uint8_t*>(&pt) + (e >> 16), sizeof(th));
-        bool p1 = y <= th.x, p2 = y >= th.y;
-        uint32_t k = p1 ? (e & 0xffu) : (p2 ? ((e >> 8) & 0xffu) : (uint32_t)kZeroLine);
+        const uint2 e = pt.ent[idx];
+        const int T1 = (int)e.x;
+        const bool p1 = h < T1, p2 = h > T1 + (int)(e.y >> 16);
+        const uint32_t k = p1 ? (e.y & 0xffu) : (p2 ? ((e.y >> 8) & 0xffu) : (uint32_t)kZeroLine);
         out[i] = k == (uint32_t)kZeroLine ? -1 : (int32_t)k;
     }
     return (int32_t)iv.size();

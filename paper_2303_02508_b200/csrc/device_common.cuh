@@ -59,6 +59,11 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ void st_na_v4(uint4* p, uint4 v) {  // streaming store, no L1 allocation
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
 __device__ __forceinline__ uint32_t ldg_nc_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -85,22 +90,24 @@ __device__ __noinline__ uint32_t canonical_choose(double x, double Kc, const dou
 }
 
 // Envelope fast path: bucket of y = x * (1/Kc) by the high bits of
-// its fp64 encoding, then at most one threshold pair.  Returns kZeroLine when
-// y lies in a band where only the canonical rule is trusted.  Negative y (an
-// unclamped forecast) lands in bucket 0 and decides exactly like x = 0.
+// its fp64 encoding, then at most one integer threshold test on hi32(y).
+// Returns kZeroLine when y lies where only the canonical rule is trusted.
+// Negative y (an unclamped forecast) lands in bucket 0 and decides like x = 0.
 __device__ __forceinline__ uint32_t plan_lookup(double y, const PairTable* pt) {
-    const int hs = __double2hiint(y) >> kSH;
-    const int idx = max(min(hs - pt->base, kNBUsed - 1), 0);
-    const uint32_t e = pt->ent[idx];
-    const double2 th = *reinterpret_cast<const double2*>(reinterpret_cast<const uint8_t*>(pt) + (e >> 16));
-    const bool p1 = y <= th.x, p2 = y >= th.y;
-    return p1 ? (e & 0xffu) : (p2 ? ((e >> 8) & 0xffu) : (uint32_t)kZeroLine);
+    const int h = __double2hiint(y);
+    const int idx = max(min((h >> kSH) - pt->base, kNBUsed - 1), 0);
+    const uint2 e = pt->ent[idx];
+    const int T1 = (int)e.x;
+    const bool p1 = h < T1;
+    const bool p2 = h > T1 + (int)(e.y >> 16);
+    return p1 ? (e.y & 0xffu) : (p2 ? ((e.y >> 8) & 0xffu) : (uint32_t)kZeroLine);
 }
 
+// 1/Kc for the lookup; 0 when Kc is outside [2^-900, 2^900] (or 0 with
+// eta < 1): the trace then takes the canonical path for every window.
 __device__ __forceinline__ double per_trace_invK(const PairTable* pt, double Kc) {
     if (pt->k0) return 1.0;
-    // Kc outside [2^-900, 2^900]: every window takes the canonical path (y = NaN).
-    return (Kc >= 0x1p-900 && Kc <= 0x1p900) ? __ddiv_rn(1.0, Kc) : __longlong_as_double(0x7ff8000000000000ll);
+    return (Kc >= 0x1p-900 && Kc <= 0x1p900) ? __ddiv_rn(1.0, Kc) : 0.0;
 }
 
 template <typename E>

@@ -5,7 +5,7 @@
 //        PairTable[n_prof * n_eta]     (pair index = p * n_eta + e)
 #pragma once
 #include <stdint.h>
-#include <vector_types.h>      // double2
+#include <vector_types.h>      // double2, uint2
 #include <vector_functions.h>  // make_double2
 
 namespace chase {
@@ -14,15 +14,15 @@ constexpr int kMaxK = 32;          // CHASE_MAX_LIMITS
 constexpr int kNB = 776;           // buckets per pair table (12 octaves x 64 + 2, padded to 8)
 constexpr int kNBUsed = 770;       // bucket 0 = below range, 1..768 = table, 769 = above
 constexpr int kSH = 14;            // hi32(y) >> 14 = sign | 11-bit exponent | 6 mantissa bits
-constexpr int kMaxSlots = 64;      // threshold pairs per table (6-bit slot field)
-constexpr int kSlotFast = 0;       // (+inf, +inf): always "below" line
-constexpr int kSlotSlow = 1;       // (NaN, NaN): always the canonical K-way path
-
 constexpr int kZeroLine = 32;      // ProfileTable.line[32] = (0, 0): marks a deferred canonical window
 
-// Entry encoding (uint32): below (bits 0-7) | above (8-15) | byte offset of the
-// (t_lo, t_hi) slot inside the PairTable (16-31).  Per window:
-//   p1 = y <= t_lo, p2 = y >= t_hi; k = p1 ? below : (p2 ? above : kZeroLine);
+// Bucket entry (uint2), compared on h = hi32(y) as a signed int (monotone in
+// y for y >= 0; negative y has h < 0):
+//   x = T1                          (hi32 of the "below" threshold)
+//   y = below | above << 8 | delta << 16,  T2 = T1 + delta
+//   p1 = h < T1  (=> y < t_lo),  p2 = h > T2  (=> y > t_hi)
+//   k = p1 ? below : (p2 ? above : kZeroLine)
+// FAST: T1 = INT32_MAX.  All-slow: T1 = INT32_MIN, above = kZeroLine.
 // kZeroLine -> the canonical K-way Eq. 6 (deferred).  See DESIGN.md §6.
 
 struct alignas(16) TablesHeader {
@@ -46,10 +46,9 @@ struct alignas(16) PairTable {
     double kbase;          // (1 - eta) * Pmax; Kc = kbase * MaxCI
     int32_t base;          // idx = clamp((hi32(y) >> kSH) - base, 0, kNBUsed - 1)
     int32_t k0;            // 1: Kc == 0 (eta == 1) -> y = x; 0: y = x * (1/Kc)
-    int32_t n_slots;
+    int32_t n_test;        // entries with a threshold test (diagnostic)
     int32_t n_intervals;   // fast intervals (diagnostic)
-    double2 slots[kMaxSlots];
-    uint32_t ent[kNB];
+    uint2 ent[kNB];
 };
 
 static_assert(sizeof(TablesHeader) % 16 == 0, "header alignment");

@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstddef>
+#include <climits>
+#include <cstdint>
 #include <cstring>
 
 namespace chase {
@@ -157,31 +159,46 @@ std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const
     std::sort(iv.begin(), iv.end(), [](const FastInterval& a, const FastInterval& b) { return a.lo < b.lo; });
     out->n_intervals = (int)iv.size();
 
-    // Bucket range: 12 octaves from the octave of the smallest positive endpoint.
-    double vmin = INFINITY;
+    // Bucket range: the 12-octave window [2^E0, 2^(E0+12)) holding the most
+    // interval endpoints (endpoints outside it fall in the clamped end buckets,
+    // which still take one exact threshold test, else the canonical path).
+    std::vector<int> ex;
     for (const FastInterval& f : iv) {
-        if (f.lo > 0) vmin = std::min(vmin, f.lo);
-        if (std::isfinite(f.hi) && f.hi > 0) vmin = std::min(vmin, f.hi);
+        for (double v : {f.lo, f.hi}) {
+            if (v > 0 && std::isfinite(v)) {
+                int e;
+                std::frexp(v, &e);
+                ex.push_back(e - 1);  // floor(log2(v))
+            }
+        }
     }
     int E0 = 0;
-    if (std::isfinite(vmin)) {
-        int e;
-        std::frexp(vmin, &e);
-        E0 = std::max(-1000, std::min(1000, e - 1));
+    if (!ex.empty()) {
+        int best = -1;
+        for (int cand : ex) {
+            const int e0 = cand - 1;
+            int n = 0;
+            for (int e : ex) n += (e >= e0 && e < e0 + 12) ? 1 : 0;
+            if (n > best || (n == best && e0 < E0)) { best = n; E0 = e0; }
+        }
+        E0 = std::max(-1000, std::min(1000, E0));
     }
     const int base_raw = (E0 + 1023) << 6;
     out->base = base_raw - 1;
 
-    const double NaN = std::nan("");
-    out->slots[kSlotFast] = make_double2(INFINITY, INFINITY);
-    out->slots[kSlotSlow] = make_double2(NaN, NaN);
-    int n_slots = 2;
-    auto enc = [](int below, int above, int slot) -> uint32_t {
-        return (uint32_t)below | ((uint32_t)above << 8) |
-               ((uint32_t)(offsetof(PairTable, slots) + 16 * slot) << 16);
+    auto hi32 = [](double v) -> int32_t {
+        uint64_t b;
+        std::memcpy(&b, &v, 8);
+        return (int32_t)(uint32_t)(b >> 32);
     };
+    auto enc = [](int32_t T1, int below, int above, int32_t delta) -> uint2 {
+        if (delta < 0 || delta > 0xFFFF) { above = kZeroLine; delta = 0; }
+        return make_uint2((uint32_t)T1, (uint32_t)below | ((uint32_t)above << 8) | ((uint32_t)delta << 16));
+    };
+    const uint2 all_slow = enc(INT32_MIN, kZeroLine, kZeroLine, 0);
+    int n_test = 0;
     for (int b = 0; b < kNB; ++b) {
-        if (b >= kNBUsed) { out->ent[b] = enc(0, 0, kSlotSlow); continue; }
+        if (b >= kNBUsed) { out->ent[b] = all_slow; continue; }
         double vb = b == 0 ? 0.0 : bucket_start(base_raw, b);
         double ve = b == kNBUsed - 1 ? (double)INFINITY : bucket_start(base_raw, b + 1);
         const FastInterval* cover = nullptr;
@@ -192,30 +209,26 @@ std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const
             else if (f.lo <= vb && vb <= f.hi && f.hi < ve) below = &f;
             else if (vb < f.lo && f.lo < ve && f.hi >= ve) above = &f;
         }
-        uint32_t e;
+        uint2 e;
         if (cover) {
-            e = enc(cover->k, cover->k, kSlotFast);
+            e = enc(INT32_MAX, cover->k, cover->k, 0);
         } else if (!below && !above) {
-            e = enc(0, 0, kSlotSlow);
+            e = all_slow;
+        } else if (below && above) {
+            // h < hi32(t_lo) => y < t_lo;  h > hi32(t_hi) => y > t_hi
+            const int32_t T1 = hi32(below->hi), T2 = hi32(above->lo);
+            e = enc(T1, below->k, above->k, T2 - T1);
+            ++n_test;
+        } else if (below) {
+            e = enc(hi32(below->hi), below->k, kZeroLine, 0);
+            ++n_test;
         } else {
-            double tlo = below ? below->hi : NaN, thi = above ? above->lo : NaN;
-            int slot = -1;
-            for (int s = 2; s < n_slots; ++s) {
-                double2 v = out->slots[s];
-                bool same_lo = (std::isnan(v.x) && std::isnan(tlo)) || v.x == tlo;
-                bool same_hi = (std::isnan(v.y) && std::isnan(thi)) || v.y == thi;
-                if (same_lo && same_hi) slot = s;
-            }
-            if (slot < 0 && n_slots < kMaxSlots) {
-                slot = n_slots++;
-                out->slots[slot] = make_double2(tlo, thi);
-            }
-            if (slot < 0) e = enc(0, 0, kSlotSlow);
-            else e = enc(below ? below->k : 0, above ? above->k : 0, slot);
+            e = enc(hi32(above->lo), kZeroLine, above->k, 0);
+            ++n_test;
         }
         out->ent[b] = e;
     }
-    out->n_slots = n_slots;
+    out->n_test = n_test;
     return iv;
 }
 

@@ -19,6 +19,7 @@ struct Acc {
     float vmin;          // min raw value (fast path validation; NaN/inf show up in Cs)
     uint32_t slow;       // OR of staged choice words: bit 5 of a byte = kZeroLine (deferred window)
     int bad;             // generic path validation (1) / REPLAY bad choice (2)
+    int bad_pad;         // canonical-path window count (diagnostic)
 };
 
 // Full 16-byte-aligned fp32 groups of 4 windows: the hot loop.
@@ -60,18 +61,25 @@ __device__ __forceinline__ void fused_full(const float* __restrict__ tv, int ngr
 // Any element type / alignment / window count (odd L, f64, ragged tails).
 // Out of line (cold); returns its partial sums by value so the caller's
 // accumulators stay in registers.
-template <bool FIRST, bool FC, typename E>
+template <bool FIRST, bool FC, typename E, bool CANON = false>
 __device__ __noinline__ Acc fused_generic(const E* tv, int j_begin, int nwin, const double* Ap, double wl, double invK,
-                                          const PairTable* pt, const double2* lines, uint8_t* bytes, double* fout) {
-    Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0};
+                                          const PairTable* pt, const double2* lines, uint8_t* bytes, double* fout,
+                                          double Kc = 0.0, const ProfileTable* pf = nullptr) {
+    Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
     double lag = (double)tv[j_begin - 1];
     for (int jj = j_begin; jj < nwin; ++jj) {
         const E raw = tv[jj];
         const double cw = (double)raw;
         const double p = __dadd_rn(Ap[jj], __dmul_rn(wl, lag));
         if (FC) fout[jj] = p > 0.0 ? p : 0.0;
-        const uint32_t k = plan_lookup(__dmul_rn(p, invK), pt);
-        if (k == (uint32_t)kZeroLine) a.slow |= 0x20u;
+        uint32_t k;
+        if (CANON) {
+            k = canonical_choose(p > 0.0 ? p : 0.0, Kc, pt->a, pf->thr, pf->K);
+            ++a.bad_pad;
+        } else {
+            k = plan_lookup(__dmul_rn(p, invK), pt);
+            if (k == (uint32_t)kZeroLine) a.slow |= 0x20u;
+        }
         bytes[jj] = (uint8_t)k;
         const double2 ln = lines[k];
         a.S = __dadd_rn(a.S, ln.x);
@@ -93,6 +101,7 @@ __device__ __forceinline__ void acc_merge(Acc& a, const Acc& b) {
     a.Cs = __dadd_rn(a.Cs, b.Cs);
     a.slow |= b.slow;
     a.bad |= b.bad;
+    a.bad_pad += b.bad_pad;
 }
 
 // The deferred windows (kZeroLine): canonical K-way Eq. 6, then their replay
@@ -194,7 +203,7 @@ __host__ __device__ inline WarpLayout make_warp_layout(int T, int stage_bytes, i
     int o = 0;
     L.aext = o; o += 2 * round16(aext_len(T) * 8);
     L.stage = o; o += kStages * stage_bytes;
-    L.chb = o; o += 2 * kWarpW;
+    L.chb = o; o += kWarpW;
     L.eta = o; o += n_eta * kEtaState * 8;
     L.ctx = o; o += (int)sizeof(WarpCtx);
     L.mbar = o; o += 8 * kStages;
@@ -210,17 +219,15 @@ __host__ __device__ inline int sweep_smem_total(int tables_bytes, int T, int sta
 // windows: 32 windows per round, inclusive scan of s_k = Thr_k*Delta from
 // `before` (the samples done before them).  Returns the window (relative to
 // the lane's first), f, and E/C of the windows before it.
+struct Completion {
+    double f, Ep, Cp, Pk, cw;
+    int w;
+};
 template <typename E>
-__device__ __noinline__ void find_completion(const E* tv_src, const uint8_t* bytes_src, int nwin_src, double before, double J,
-                                const double2* lines, int lane, int& w_out, double& f_out, double& Ep, double& Cp,
-                                double& Pk, double& cw_out) {
+__device__ __noinline__ Completion find_completion(const E* tv_src, const uint8_t* bytes_src, int nwin_src,
+                                                   double before, double J, const double2* lines, int lane) {
+    Completion r{1.0, 0.0, 0.0, 0.0, 0.0, nwin_src - 1};
     double carry = before;
-    Ep = 0.0;
-    Cp = 0.0;
-    w_out = nwin_src - 1;
-    f_out = 1.0;
-    Pk = 0.0;
-    cw_out = 0.0;
     for (int r0 = 0; r0 < nwin_src; r0 += 32) {
         const int jj = r0 + lane;
         const bool valid = jj < nwin_src;
@@ -234,19 +241,20 @@ __device__ __noinline__ void find_completion(const E* tv_src, const uint8_t* byt
         const bool is_last = r0 + 32 >= nwin_src;
         const int wl_ = hits ? __ffs(hits) - 1 : (is_last ? min(31, nwin_src - 1 - r0) : 32);
         const bool pre = valid && lane < wl_;  // windows strictly before the completion window
-        Ep = __dadd_rn(Ep, warp_sum(pre ? ln.y : 0.0));
-        Cp = __dadd_rn(Cp, warp_sum(pre ? __dmul_rn(ln.y, cw) : 0.0));
+        r.Ep = __dadd_rn(r.Ep, warp_sum(pre ? ln.y : 0.0));
+        r.Cp = __dadd_rn(r.Cp, warp_sum(pre ? __dmul_rn(ln.y, cw) : 0.0));
         if (wl_ < 32) {
             const double bw = __shfl_sync(kFull, before_w, wl_);
             const double sk = __shfl_sync(kFull, ln.x, wl_);
-            w_out = r0 + wl_;
-            f_out = __ddiv_rn(__dsub_rn(J, bw), sk);  // pro-rata last window
-            Pk = __shfl_sync(kFull, ln.y, wl_);
-            cw_out = __shfl_sync(kFull, cw, wl_);
-            return;
+            r.w = r0 + wl_;
+            r.f = __ddiv_rn(__dsub_rn(J, bw), sk);  // pro-rata last window
+            r.Pk = __shfl_sync(kFull, ln.y, wl_);
+            r.cw = __shfl_sync(kFull, cw, wl_);
+            return r;
         }
         carry = __shfl_sync(kFull, incl, 31);
     }
+    return r;
 }
 
 template <int MODE, typename E, bool AL, bool MULTI>
@@ -288,15 +296,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     const E* traces = reinterpret_cast<const E*>(P.traces);
     const int nc = P.n_chunks;
     const int T = P.T;
-    const int W_last = P.W - (nc - 1) * kWarpW;  // windows of the last chunk
-    // loaded element range of chunk c: [a0 + c*kWarpW, ...), a0 16-byte aligned
-    const int a0 = AL ? P.L - VEC : ((P.L - 1) / VEC) * VEC;
-    const int off0 = P.L - a0;  // tv = stage + off0 elements
-    const uint32_t bytes_full = (uint32_t)((((P.L + kWarpW + VEC - 1) / VEC) * VEC - a0) * (int)sizeof(E));
-    const uint32_t bytes_last =
-        (uint32_t)((min((int64_t)((P.L + (int64_t)(nc - 1) * kWarpW + W_last + VEC - 1) / VEC) * VEC, P.ld) -
-                    (a0 + (int64_t)(nc - 1) * kWarpW)) *
-                   (int)sizeof(E));
+    const int W_last = P.W_last;  // windows of the last chunk
+    const int a0 = P.a0;          // chunk c loads elements [a0 + c*kWarpW, ...), 16-byte aligned
+    const int off0 = P.off0;      // tv = stage + off0 elements
 
     // producer (lane 0): next (trace, chunk) to load; cursor lives in smem
     auto issue_next = [&]() {
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
         const uint64_t policy = evict_first_policy();
         const int st = (int)(issued % kStages);
         uint8_t* dst = stage0 + st * P.stage_bytes;
-        const uint32_t bytes = pc == nc - 1 ? bytes_last : bytes_full;
+        const uint32_t bytes = pc == nc - 1 ? P.bytes_last : P.bytes_full;
         if (pc == 0) {
             mbar_arrive_expect_tx(&mbar[st], bytes + (uint32_t)kRecBytes);
             bulk_g2s(dst + P.stage_bytes - kRecBytes, P.records + pi * kRecDoubles, kRecBytes, &mbar[st], policy);
@@ -336,17 +338,15 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     }
 
     const int lane_phase = (kChunk * lane) % T;
-    const int phase_step = kWarpW % T;
-    const int phase_start = (int)(((int64_t)P.phase0 + P.L) % T);
     const int j0 = kChunk * lane;
-    uint32_t q = 0, gp = 0;
+    uint32_t q = 0;
 
     double Sl = 0.0, El = 0.0, Cl = 0.0, Cbl = 0.0;  // single-eta path: per-lane running sums
     for (int64_t i = gw; i < P.n_traces; i += GW) {
         int status = 0, prof = 0;
         double wl = 0.0, J = 0.0, smax = 0.0;
         int64_t mb = P.W;
-        int phase_c = phase_start;
+        int phase_c = P.phase_start;
         for (int c = 0; c < nc; ++c, ++q) {
             const int st = (int)(q % kStages);
             uint8_t* stage = stage0 + st * P.stage_bytes;
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 Sl = El = Cl = Cbl = 0.0;
                 __syncwarp();
             } else {
-                phase_c += phase_step;
+                phase_c += P.phase_step;
                 if (phase_c >= T) phase_c -= T;
             }
 
@@ -406,23 +406,28 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 if (__any_sync(kFull, chunk_has_bad(tv, nwin))) status = CHASE_ERR_DATA;
             }
 
-            for (int e = 0; e < n_pass && status == 0; ++e, ++gp) {
-                const int sb = (int)(gp & 1);
-                uint8_t* chb = chb0 + sb * kWarpW;
-                if (MODE != MODE_PREDICT) {
-                    if (lane == 0) bulk_wait_read0();  // the store that last read this buffer is done
-                    __syncwarp();
-                }
+            for (int e = 0; e < n_pass && status == 0; ++e) {
+                uint8_t* chb = chb0;
+                if (MODE != MODE_PREDICT) __syncwarp();  // every lane finished reading the choice buffer
                 double* es = eta_st + e * kEtaState;
                 const double Kc = es[0], invK = es[1];
                 const bool done = es[2] != 0.0;
                 const PairTable* pt = pairs + prof * P.n_eta + e;
                 const ProfileTable* pf = profs + prof;
 
-                Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0};
+                Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
                 int fast_groups = 0;
                 if (MODE == MODE_FUSED) {
                     double* fout = (P.forecast && e == 0) ? P.forecast + i * P.ld_f + jb : nullptr;
+                    if (invK == 0.0) {
+                        // Kc outside [2^-900, 2^900]: every window on the canonical rule (cold)
+                        Acc b;
+                        if (e == 0 && fout) b = fused_generic<true, true, E, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, Kc, pf);
+                        else if (e == 0) b = fused_generic<true, false, E, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, Kc, pf);
+                        else b = fused_generic<false, false, E, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line, chb + j0, fout, Kc, pf);
+                        acc_merge(a, b);
+                        if (b.bad_pad) atomicAdd(&ctx->slow, (unsigned long long)b.bad_pad);
+                    } else {
                     if (AL && sizeof(E) == 4) {
                         fast_groups = nwin >> 2;
                         const float* tf = reinterpret_cast<const float*>(tv);
@@ -451,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                         a.C = __dadd_rn(a.C, fx.C);
                         atomicAdd(&ctx->slow, (unsigned long long)fx.n);
                     }
+                    }
                 } else if (MODE == MODE_PREDICT) {
                     predict_chunk<E>(tv, nwin, Ap, wl, P.forecast + i * P.ld_f + jb, a);
                 } else {
@@ -467,13 +473,13 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     break;
                 }
                 if (MODE == MODE_FUSED && P.choice) {
-                    fence_proxy_async();
+                    // coalesced 16-byte copies of the staged choices (bytes [W, round16(W)) are scratch)
                     __syncwarp();
-                    if (lane == 0) {
-                        uint8_t* dst = P.choice + ((int64_t)e * P.n_traces + i) * P.ld_c + (int64_t)c * kWarpW;
-                        bulk_s2g(dst, chb, (uint32_t)((c < nc - 1 ? kWarpW : W_last + 15) & ~15));
-                        bulk_commit();
-                    }
+                    uint4* dst = reinterpret_cast<uint4*>(P.choice + ((int64_t)e * P.n_traces + i) * P.ld_c +
+                                                          (int64_t)c * kWarpW);
+                    const uint4* srcv = reinterpret_cast<const uint4*>(chb);
+                    const int n16 = (c < nc - 1 ? kWarpW : W_last + 15) >> 4;
+                    for (int q16 = lane; q16 < n16; q16 += 32) st_na_v4(dst + q16, srcv[q16]);
                 }
                 if (MODE == MODE_PREDICT) continue;
 
@@ -499,11 +505,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                                 const double Cb = warp_sum(full ? __dadd_rn(Cl, a.C) : Cl);
                                 const int src = __ffs(who) - 1;
                                 const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
-                                int wrel;
-                                double f, Ep, Cp, Pk, cst;
-                                find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
-                                                   __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep,
-                                                   Cp, Pk, cst);
+                                const Completion cp = find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src,
+                                                                         nw_src, __shfl_sync(kFull, before, src), J,
+                                                                         pf->line, lane);
+                                const int wrel = cp.w;
+                                const double f = cp.f, Ep = cp.Ep, Cp = cp.Cp, Pk = cp.Pk, cst = cp.cw;
                                 if (lane == 0) {
                                     double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
                                     r[0] = __dadd_rn(Eb, Ep);
@@ -544,11 +550,11 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                             const double Em = warp_sum(full ? a.E : 0.0), Cm = warp_sum(full ? a.C : 0.0);
                             const int src = __ffs(who) - 1;
                             const int nw_src = c < nc - 1 ? kChunk : max(0, min(kChunk, W_last - kChunk * src));
-                            int wrel;
-                            double f, Ep, Cp, Pk, cst;
-                            find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
-                                               __shfl_sync(kFull, before, src), J, pf->line, lane, wrel, f, Ep, Cp,
-                                               Pk, cst);
+                            const Completion cp = find_completion<E>(tv + kChunk * (src - lane), chb + kChunk * src,
+                                                                     nw_src, __shfl_sync(kFull, before, src), J,
+                                                                     pf->line, lane);
+                            const int wrel = cp.w;
+                            const double f = cp.f, Ep = cp.Ep, Cp = cp.Cp, Pk = cp.Pk, cst = cp.cw;
                             if (lane == 0) {
                                 double* r = P.raw + ((int64_t)e * P.n_traces + i) * kRawDoubles;
                                 r[0] = __dadd_rn(__dadd_rn(es[4], Em), Ep);
@@ -621,7 +627,6 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
     }
 
     if (lane == 0) {
-        bulk_wait0();
         if (ctx->slow) atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_slow_windows), ctx->slow);
     }
 }

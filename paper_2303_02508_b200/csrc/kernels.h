@@ -38,6 +38,9 @@ struct SweepParams {
     int32_t tables_bytes;
     int32_t n_eta, n_prof;
     int32_t stage_bytes;          // per pipeline stage (trace chunk + record slot)
+    // host-precomputed chunk geometry (kept in the constant bank, not registers)
+    int32_t a0, off0, W_last, phase_step, phase_start;
+    uint32_t bytes_full, bytes_last;
     const uint8_t* profile_id;    // may be null
     const double* job;            // may be null
     double max_ci_fixed;          // > 0: fixed MaxCI
