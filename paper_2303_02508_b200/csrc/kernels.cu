@@ -19,6 +19,7 @@
 // in the same order as the oracle (DESIGN.md §3 Q9), so forecasts and choices
 // are bit-identical and dyadic replay totals are exact.
 #include <cfloat>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
@@ -29,6 +30,7 @@ namespace {
 #include "device_common.cuh"
 #include "fit.cuh"
 #include "k2_sweep.cuh"
+#include "k2_fast.cuh"
 #include "finalize.cuh"
 
 int num_sms() {
@@ -101,6 +103,22 @@ cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
 
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
+    if (mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !getenv("CHASE_FORCE_GENERAL")) {
+        // the headline shape: lean specialised kernel (k2_fast.cuh)
+        const int smem = fast_smem_total(p.tables_bytes, p.T, p.stage_bytes);
+        cudaError_t err = cudaFuncSetAttribute(sweep_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (err != cudaSuccess) return err;
+        int per_sm = 0;
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_fast_kernel, kThreads, smem);
+        if (err != cudaSuccess) return err;
+        if (per_sm < 1) return cudaErrorInvalidConfiguration;
+        int64_t grid = (int64_t)num_sms() * per_sm;
+        const int64_t need = (p.n_traces + kWarpsPerCta - 1) / kWarpsPerCta;
+        if (grid > need) grid = need;
+        sweep_fast_kernel<<<(unsigned)grid, kThreads, smem, s>>>(p);
+        ++g_launches;
+        return cudaGetLastError();
+    }
 #define CHASE_SWEEP_CASE(M, MU)                                                                        \
     if (mode == M && multi == MU) {                                                                    \
         if (f64) return aligned ? launch_sweep_t<M, double, true, MU>(p, s) : launch_sweep_t<M, double, false, MU>(p, s); \

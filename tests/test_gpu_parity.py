@@ -123,6 +123,7 @@ def test_multi_tile_eta_sweep():
     assert_parity(g0, o0)
 
 
+@pytest.mark.parametrize("etas", [[0.5, 0.8], [0.6]])
 @pytest.mark.parametrize("L,N,interval,phase0,n", [
     (23, 24 + 37, 3600, 5, 3),          # odd L -> unaligned tile path, W=37
     (24, 25, 3600, 0, 2),               # W = 1
@@ -130,14 +131,51 @@ def test_multi_tile_eta_sweep():
     (24, 24 + 9217, 3600, 23, 2),       # one window past a tile boundary
     (96, 96 + 500, 900, 40, 9),         # 15-minute data (T=96)
 ])
-def test_ragged_shapes(L, N, interval, phase0, n):
+def test_ragged_shapes(L, N, interval, phase0, n, etas):
+    """Odd L (unaligned tile path), tiny W, sub-hourly data, chunk edges; one
+    eta exercises the specialised headline kernel, two etas the general one."""
     T = 86400 // interval
     prof = [inputs.make_profile("vit", inputs.LIMITS_9)]
     tr = inputs.synth_traces_host(n, N, seed=17, T=T, phase0=phase0)
     J = np.full(n, interval * (N - L) * prof[0].throughput_sps.min() * 0.8)
-    g = run_sweep(tr, N, prof, [0.5, 0.8], J=J, L=L, interval_s=interval, phase0=phase0)
-    o = run_oracle(tr, N, prof, [0.5, 0.8], J=J, L=L, interval_s=interval, phase0=phase0)
+    g = run_sweep(tr, N, prof, etas, J=J, L=L, interval_s=interval, phase0=phase0, forecast=False)
+    o = run_oracle(tr, N, prof, etas, J=J, L=L, interval_s=interval, phase0=phase0)
+    g["forecast"] = None
     assert_parity(g, o)
+
+
+@pytest.mark.parametrize("force_general", [False, True])
+def test_headline_kernel_matches_general_kernel(force_general, monkeypatch):
+    """The specialised kernel (fp32, aligned, one eta, no forecast output) and
+    the general kernel give identical results on the C4 shape, incl. invalid
+    traces, exhaustion and a fixed-duration trace."""
+    if force_general:
+        monkeypatch.setenv("CHASE_FORCE_GENERAL", "1")
+    w = inputs.workload("C4", n_traces=257)
+    tr = inputs.synth_traces_host(w.n_traces, w.n_steps, seed=77)
+    tr[3, 500] = -2.0
+    tr[9, 30] = np.inf
+    tr[11, :24] = 0.0
+    J = w.job_samples()
+    J[5] = 0.0
+    J[6] = J[6] * 3.0
+    g = run_sweep(tr, w.n_steps, w.profiles[:1], [0.4], J=J, forecast=False)
+    o = run_oracle(tr, w.n_steps, w.profiles[:1], [0.4], J=J)
+    g["forecast"] = None
+    assert_parity(g, o)
+
+
+def test_extreme_kc_takes_canonical_path():
+    """MaxCI so small that Kc < 2^-900: every window on the canonical rule."""
+    w = inputs.workload("C2")
+    tr = inputs.synth_traces_host(2, w.n_steps, seed=0, mode=inputs.MODE_PAPER)
+    J = np.full(2, float(w.job_samples()[0]))
+    for etas in ([0.5], [0.5, 0.7]):
+        g = run_sweep(tr, w.n_steps, w.profiles, etas, J=J, max_ci=1e-300, forecast=False)
+        o = run_oracle(tr, w.n_steps, w.profiles, etas, J=J, max_ci=1e-300)
+        g["forecast"] = None
+        assert_parity(g, o)
+        assert g["diag"].n_slow_windows >= 2 * w.W
 
 
 def test_f64_traces():
