@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
         const int64_t pi = ctx->pi;
         if (pi >= P.n_traces) return;
         const int pc = ctx->pc;
-        const uint32_t issued = ctx->issued;
-        const int st = (int)(issued % kStages);
+        const uint32_t st = ctx->issued;  // stage index (wraps at kStages)
+        const float* psrc = reinterpret_cast<const float*>(ctx->psrc);
         uint8_t* dst = stage0 + st * P.stage_bytes;
         const uint32_t bytes = pc == nc - 1 ? P.bytes_last : P.bytes_full;
         const uint64_t policy = evict_first_policy();
@@ -115,26 +115,30 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
         } else {
             mbar_arrive_expect_tx(&mbar[st], bytes);
         }
-        bulk_g2s(dst, traces + pi * P.ld + P.a0 + (int64_t)pc * kWarpW, bytes, &mbar[st], policy);
-        ctx->issued = issued + 1;
+        bulk_g2s(dst, psrc, bytes, &mbar[st], policy);
+        ctx->issued = st + 1 == kStages ? 0 : st + 1;
         if (pc + 1 == nc) {
             ctx->pc = 0;
             ctx->pi = pi + GW;
+            ctx->psrc = traces + (pi + GW) * P.ld + P.a0;
         } else {
             ctx->pc = pc + 1;
+            ctx->psrc = psrc + kWarpW;
         }
     };
     if (lane == 0) {
         ctx->pi = gw;
         ctx->pc = 0;
         ctx->issued = 0;
+        ctx->psrc = traces + gw * P.ld + P.a0;
         ctx->slow = 0ull;
         for (int q0 = 0; q0 < kStages; ++q0) issue_next();
     }
 
     const int j0 = kChunk * lane;
     const int lane_phase = j0 % T;
-    uint32_t q = 0;
+    int st = 0;          // stage of the next chunk
+    uint32_t par = 0;    // its mbarrier phase parity
 
     for (int64_t i = gw; i < P.n_traces; i += GW) {
         int status = 0, prof = 0;
@@ -144,10 +148,10 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
         bool done = false;
         int phase_c = P.phase_start;
         uint32_t* crow = P.choice ? reinterpret_cast<uint32_t*>(P.choice + i * P.ld_c) + (j0 >> 2) : nullptr;
-        for (int c = 0, jb = j0; c < nc; ++c, ++q, jb += kWarpW) {
-            const int st = (int)(q % kStages);
+        int c_may = 0;   // first chunk in which S can reach J (S <= windows * max_k s_k)
+        for (int c = 0, jb = j0; c < nc; ++c, jb += kWarpW) {
             uint8_t* stage = stage0 + st * P.stage_bytes;
-            mbar_wait(&mbar[st], (q / kStages) & 1);
+            mbar_wait(&mbar[st], par);
             if (c == 0) {  // ---- per-trace setup
                 const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
                 prof = P.profile_id ? (int)P.profile_id[i] : 0;
@@ -163,6 +167,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
                 const PairTable* pt0 = pairs + prof;
                 Kc = __dmul_rn(pt0->kbase, maxci);
                 invK = per_trace_invK(pt0, Kc);
+                if (J > 0.0) {
+                    const double wmin = __ddiv_rn(J, __dmul_rn(smax, 1.000001));  // windows needed, rounded down
+                    c_may = wmin >= (double)P.W ? nc - 1 : max(0, (int)(wmin / kWarpW) - 1);
+                } else {
+                    c_may = nc;  // fixed duration: never completes
+                }
                 if (status == 0) {
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
                     const int n_a = aext_len(T);
@@ -227,8 +237,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
                         for (int jj = 0; jj < mb - jb; ++jj) Cbt = __dadd_rn(Cbt, (double)tv[jj]);
                     Cbl = __dadd_rn(Cbl, Cbt);
                     bool completed = false;
-                    if (!done && J > 0.0 &&
-                        __dmul_rn(__dmul_rn((double)min(P.W, jb - j0 + kWarpW), smax), 1.000001) >= J) {
+                    if (!done && c >= c_may) {
                         const double S_prev = warp_sum(Sl);
                         if (__dadd_rn(S_prev, warp_sum(a.S)) >= J) {
                             const double incl = warp_incl_scan(a.S, lane);
@@ -301,6 +310,10 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
             }
             __syncwarp();  // every lane is done with stage `st` and the choice buffer
             if (lane == 0) issue_next();
+            if (++st == kStages) {
+                st = 0;
+                par ^= 1u;
+            }
         }
     }
     if (lane == 0 && ctx->slow)

@@ -30,7 +30,7 @@ namespace {
 #include "device_common.cuh"
 #include "fit.cuh"
 #include "k2_sweep.cuh"
-#include "k2_fast.cuh"
+#include "k2_headline.cuh"
 #include "finalize.cuh"
 
 int num_sms() {
