@@ -11,6 +11,19 @@
 //   k = bucket(p / Kc)                   (Eq. 6 envelope; rare windows -> canonical)
 //   S += Thr_k*Delta; E += P_k; C += P_k*c[w]; Cs += c[w]
 
+#ifndef CHASE_H_WARPS
+#define CHASE_H_WARPS 6
+#endif
+#ifndef CHASE_H_STAGES
+#define CHASE_H_STAGES 2
+#endif
+#ifndef CHASE_H_MINB
+#define CHASE_H_MINB 2
+#endif
+constexpr int kHWarps = CHASE_H_WARPS;    // independent warps per CTA
+constexpr int kHThreads = 32 * kHWarps;
+constexpr int kHStages = CHASE_H_STAGES;  // per-warp TMA ring depth
+
 struct FastLayout {
     int aext, stage, chb, ctx, mbar, bytes;
 };
@@ -19,23 +32,37 @@ __host__ __device__ inline FastLayout make_fast_layout(int T, int stage_bytes) {
     FastLayout L;
     int o = 0;
     L.aext = o; o += 2 * round16(aext_len(T) * 8);
-    L.stage = o; o += kStages * stage_bytes;
+    L.stage = o; o += kHStages * stage_bytes;
     L.chb = o; o += kWarpW;
     L.ctx = o; o += (int)sizeof(WarpCtx);
-    L.mbar = o; o += 8 * kStages;
+    L.mbar = o; o += 8 * kHStages;
     L.bytes = round16(o);
     return L;
 }
 
-__host__ __device__ inline int fast_smem_total(int tables_bytes, int T, int stage_bytes) {
-    return round16(tables_bytes) + kWarpsPerCta * make_fast_layout(T, stage_bytes).bytes;
+__host__ __device__ inline int fast_ent4_bytes(int n_prof) { return n_prof * kNB * (int)sizeof(int4); }
+__host__ __device__ inline int fast_smem_total(int tables_bytes, int T, int stage_bytes, int n_prof) {
+    return round16(tables_bytes) + fast_ent4_bytes(n_prof) + kHWarps * make_fast_layout(T, stage_bytes).bytes;
+}
+
+// Headline lookup: 16-byte entries {T1, T2, below, above} expanded in smem at
+// kernel start from the blob's 8-byte entries (one LDS.128, 2 ISETP, 2 SEL).
+struct Ent4 {
+    int T1, T2;
+    uint32_t below, above;
+};
+__device__ __forceinline__ uint32_t plan_lookup4(double y, const Ent4* __restrict__ ent, int base) {
+    const int h = __double2hiint(y);
+    const int idx = max(min((h >> kSH) - base, kNBUsed - 1), 0);
+    const int4 e = *reinterpret_cast<const int4*>(ent + idx);
+    return h < e.x ? (uint32_t)e.z : (h > e.y ? (uint32_t)e.w : (uint32_t)kZeroLine);
 }
 
 // One full-aligned chunk of ngroups x 4 windows; choice words go to smem
 // (for the completion search) and, when `cdst` is set, straight to global.
 template <bool FIRST_STORE>
 __device__ __forceinline__ void fast_groups(const float* __restrict__ tv, int ngroups, const double* __restrict__ Ap,
-                                            double wl, double invK, const PairTable* __restrict__ pt,
+                                            double wl, double invK, const Ent4* __restrict__ ent4, int ebase,
                                             const double2* __restrict__ lines, uint32_t* __restrict__ words,
                                             uint32_t* __restrict__ cdst, Acc& a) {
     double lag = (double)tv[-1];
@@ -52,7 +79,7 @@ __device__ __forceinline__ void fast_groups(const float* __restrict__ tv, int ng
         for (int u = 0; u < 4; ++u) {
             const double cw = (double)vv[u];
             const double p = __dadd_rn(AA[u], __dmul_rn(wl, lag));  // Eq. 1, unclamped for the lookup
-            const uint32_t k = plan_lookup(__dmul_rn(p, invK), pt);
+            const uint32_t k = plan_lookup4(__dmul_rn(p, invK), ent4, ebase);
             word |= k << (8 * u);
             const double2 ln = lines[k];  // (Thr_k * Delta, P_k)
             a.S = __dadd_rn(a.S, ln.x);
@@ -67,11 +94,12 @@ __device__ __forceinline__ void fast_groups(const float* __restrict__ tv, int ng
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_constant__ SweepParams P) {
+__global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(const __grid_constant__ SweepParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const FastLayout FL = make_fast_layout(P.T, P.stage_bytes);
-    uint8_t* wbase = sm + round16(P.tables_bytes) + warp * FL.bytes;
+    Ent4* ent4_all = reinterpret_cast<Ent4*>(sm + round16(P.tables_bytes));
+    uint8_t* wbase = sm + round16(P.tables_bytes) + fast_ent4_bytes(P.n_prof) + warp * FL.bytes;
     const int alen = round16(aext_len(P.T) * 8) / 8;
     double* A_even = reinterpret_cast<double*>(wbase + FL.aext);
     double* A_odd = A_even + alen;
@@ -83,10 +111,24 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
     {   // constant tables -> smem, once per CTA
         const uint4* src = reinterpret_cast<const uint4*>(P.tables);
         uint4* dst = reinterpret_cast<uint4*>(sm);
-        for (int q = tid; q < P.tables_bytes / 16; q += kThreads) dst[q] = src[q];
+        for (int q = tid; q < P.tables_bytes / 16; q += kHThreads) dst[q] = src[q];
+    }
+    __syncthreads();
+    {   // expand the 8-byte bucket entries of each profile's (single-eta) pair table
+        const TablesHeader* H0 = reinterpret_cast<const TablesHeader*>(sm);
+        const PairTable* pr = reinterpret_cast<const PairTable*>(sm + H0->off_pair);
+        for (int q = tid; q < P.n_prof * kNB; q += kHThreads) {
+            const uint2 e = pr[q / kNB].ent[q % kNB];
+            Ent4 x;
+            x.T1 = (int)e.x;
+            x.T2 = (int)e.x + (int)(e.y >> 16);
+            x.below = e.y & 0xffu;
+            x.above = (e.y >> 8) & 0xffu;
+            ent4_all[q] = x;
+        }
     }
     if (lane == 0)
-        for (int q0 = 0; q0 < kStages; ++q0) mbar_init(&mbar[q0], 1);
+        for (int q0 = 0; q0 < kHStages; ++q0) mbar_init(&mbar[q0], 1);
     if (lane == 0) fence_mbar_init();
     __syncthreads();
 
@@ -96,8 +138,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
     const ProfileTable* profs = reinterpret_cast<const ProfileTable*>(sm + H->off_prof);
     const PairTable* pairs = reinterpret_cast<const PairTable*>(sm + H->off_pair);
     const float* traces = reinterpret_cast<const float*>(P.traces);
-    const int64_t GW = (int64_t)gridDim.x * kWarpsPerCta;
-    const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    const int64_t GW = (int64_t)gridDim.x * kHWarps;
+    const int64_t gw = (int64_t)blockIdx.x * kHWarps + warp;
     const int nc = P.n_chunks, T = P.T;
 
     auto issue_next = [&]() {  // lane 0: next (trace, chunk) load; cursor in smem
@@ -116,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
             mbar_arrive_expect_tx(&mbar[st], bytes);
         }
         bulk_g2s(dst, psrc, bytes, &mbar[st], policy);
-        ctx->issued = st + 1 == kStages ? 0 : st + 1;
+        ctx->issued = st + 1 == kHStages ? 0 : st + 1;
         if (pc + 1 == nc) {
             ctx->pc = 0;
             ctx->pi = pi + GW;
@@ -132,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
         ctx->issued = 0;
         ctx->psrc = traces + gw * P.ld + P.a0;
         ctx->slow = 0ull;
-        for (int q0 = 0; q0 < kStages; ++q0) issue_next();
+        for (int q0 = 0; q0 < kHStages; ++q0) issue_next();
     }
 
     const int j0 = kChunk * lane;
@@ -209,8 +251,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
                                                                          chb + j0, nullptr, Kc, pf));
                     if (a.bad_pad) atomicAdd(&ctx->slow, (unsigned long long)a.bad_pad);
                 } else {
-                    if (crow) fast_groups<true>(tv, ngr, Ap, wl, invK, pt, pf->line, words, crow, a);
-                    else fast_groups<false>(tv, ngr, Ap, wl, invK, pt, pf->line, words, nullptr, a);
+                    const Ent4* e4 = ent4_all + prof * kNB;
+                    if (crow) fast_groups<true>(tv, ngr, Ap, wl, invK, e4, pt->base, pf->line, words, crow, a);
+                    else fast_groups<false>(tv, ngr, Ap, wl, invK, e4, pt->base, pf->line, words, nullptr, a);
                     if (4 * ngr < nwin)
                         acc_merge(a, fused_generic<true, false, float>(tv, 4 * ngr, nwin, Ap, wl, invK, pt,
                                                                        pf->line, chb + j0, nullptr));
@@ -310,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_fast_kernel(const __grid_co
             }
             __syncwarp();  // every lane is done with stage `st` and the choice buffer
             if (lane == 0) issue_next();
-            if (++st == kStages) {
+            if (++st == kHStages) {
                 st = 0;
                 par ^= 1u;
             }

@@ -105,17 +105,17 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
     if (p.n_traces <= 0) return cudaSuccess;
     if (mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !getenv("CHASE_FORCE_GENERAL")) {
         // the headline shape: lean specialised kernel (k2_fast.cuh)
-        const int smem = fast_smem_total(p.tables_bytes, p.T, p.stage_bytes);
+        const int smem = fast_smem_total(p.tables_bytes, p.T, p.stage_bytes, p.n_prof);
         cudaError_t err = cudaFuncSetAttribute(sweep_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
         int per_sm = 0;
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_fast_kernel, kThreads, smem);
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_fast_kernel, kHThreads, smem);
         if (err != cudaSuccess) return err;
         if (per_sm < 1) return cudaErrorInvalidConfiguration;
         int64_t grid = (int64_t)num_sms() * per_sm;
-        const int64_t need = (p.n_traces + kWarpsPerCta - 1) / kWarpsPerCta;
+        const int64_t need = (p.n_traces + kHWarps - 1) / kHWarps;
         if (grid > need) grid = need;
-        sweep_fast_kernel<<<(unsigned)grid, kThreads, smem, s>>>(p);
+        sweep_fast_kernel<<<(unsigned)grid, kHThreads, smem, s>>>(p);
         ++g_launches;
         return cudaGetLastError();
     }
