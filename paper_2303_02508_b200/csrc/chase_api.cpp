@@ -48,7 +48,7 @@ constexpr size_t kWsAlign = 256;
 // per-(eta, trace) raw replay results [n_eta][n][8] | status [n] |
 // finalize block sums [ceil(n/256)][n_eta][8].
 struct WsLayout {
-    size_t diag, tables, records, raw, status, block_sums, total;
+    size_t diag, tables, records, raw, status, bad_list, block_sums, total;
 };
 
 WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta) {
@@ -59,6 +59,7 @@ WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta) {
     w.records = o; o += round_up(n_traces * kRecDoubles * 8, kWsAlign);
     w.raw = o; o += round_up((int64_t)n_eta * n_traces * kRawDoubles * 8, kWsAlign);
     w.status = o; o += round_up(n_traces, kWsAlign);
+    w.bad_list = o; o += round_up(n_traces * 8, kWsAlign);
     w.block_sums = o; o += round_up((finalize_grid(n_traces) + 1) * n_eta * 8 * 8, kWsAlign);
     w.total = o;
     return w;
@@ -230,6 +231,7 @@ SweepParams base_sweep(const chase_traces_t* t, int L, const WsLayout& WL, uint8
     p.stage_bytes = sweep_stage_bytes(t->dtype == CHASE_F64 ? 8 : 4);
     p.status = ws + WL.status;
     p.diag = reinterpret_cast<chase_diag_t*>(ws + WL.diag);
+    p.bad_list = reinterpret_cast<int64_t*>(ws + WL.bad_list);
     return p;
 }
 
@@ -289,6 +291,7 @@ FinalizeParams make_finalize(const chase_traces_t* t, int L, int n_eta, int n_pr
     f.status = ws + WL.status;
     f.per_trace = per_trace;
     f.block_sums = reinterpret_cast<double*>(ws + WL.block_sums);
+    f.diag = reinterpret_cast<chase_diag_t*>(ws + WL.diag);
     return f;
 }
 
@@ -334,7 +337,7 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     p.ld_f = ld_f;
     e = launch_sweep(MODE_PREDICT, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, s);
     if (e != cudaSuccess) return cuda_fail(e, "predict kernel");
-    e = launch_fixup(p.status, traces->n_traces, nullptr, 0, W, 0, d_forecast, ld_f, p.diag, s);
+    e = launch_fixup(p.status, p.bad_list, traces->n_traces, nullptr, 0, W, 0, d_forecast, ld_f, p.diag, s);
     if (e != cudaSuccess) return cuda_fail(e, "fixup");
     return CHASE_OK;
 }
@@ -422,7 +425,7 @@ chase_status_t chase_replay(const chase_traces_t* traces, int32_t history_len, c
     if (e != cudaSuccess) return cuda_fail(e, "replay kernel");
     FinalizeParams fz = make_finalize(traces, history_len, n_eta, n_profiles, ws, WL, d_profile_id, d_job_samples,
                                       d_per_trace);
-    e = launch_finalize(fz, d_sum, nullptr, 0, 0, nullptr, 0, p.diag, s);
+    e = launch_finalize(fz, p.bad_list, d_sum, nullptr, 0, 0, nullptr, 0, p.diag, s);
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
     return CHASE_OK;
 }
@@ -468,7 +471,7 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     if (e != cudaSuccess) return cuda_fail(e, "sweep kernel");
     FinalizeParams fz = make_finalize(traces, fcfg->history_len, cost->n_eta, n_profiles, ws, WL, d_profile_id,
                                       d_job_samples, d_per_trace);
-    e = launch_finalize(fz, d_sum, d_choice, ld_c, cost->n_eta, d_forecast, ld_f, p.diag, s);
+    e = launch_finalize(fz, p.bad_list, d_sum, d_choice, ld_c, cost->n_eta, d_forecast, ld_f, p.diag, s);
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
     return CHASE_OK;
 }

@@ -90,26 +90,42 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const __grid_cons
         __syncthreads();
     }
     if (valid) p.status[i] = (uint8_t)worst;
+    const unsigned ex = __ballot_sync(0xffffffffu, valid && worst == CHASE_ERR_TRACE_EXHAUSTED);
+    if ((threadIdx.x & 31) == 0 && ex)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&p.diag->n_exhausted), (unsigned long long)__popc(ex));
 }
 
-__global__ void finalize_sums_kernel(const double* block_sums, int64_t grid, int n_eta, chase_sum_t* sum) {
-    const int e = blockIdx.x, r = threadIdx.x;
-    if (e >= n_eta || r >= 8) return;
-    double acc = 0.0;
-    for (int64_t b = 0; b < grid; ++b) acc = __dadd_rn(acc, block_sums[(b * n_eta + e) * 8 + r]);
-    reinterpret_cast<double*>(sum + e)[r] = acc;
+// Per-GPU sums of the finalize blocks' partials: thread t folds the blocks
+// b = t, t + 256, ... in order, then a fixed smem tree (deterministic).
+__global__ void __launch_bounds__(256) finalize_sums_kernel(const double* block_sums, int64_t grid, int n_eta,
+                                                            chase_sum_t* sum) {
+    __shared__ double red[256][8];
+    const int e = blockIdx.x, t = threadIdx.x;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t b = t; b < grid; b += 256) {
+        const double* src = block_sums + (b * n_eta + e) * 8;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc[r] = __dadd_rn(acc[r], src[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) red[t][r] = acc[r];
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (t < w)
+#pragma unroll
+            for (int r = 0; r < 8; ++r) red[t][r] = __dadd_rn(red[t][r], red[t + w][r]);
+        __syncthreads();
+    }
+    if (t < 8) reinterpret_cast<double*>(sum + e)[t] = red[0][t];
 }
 
-// Invalid traces (status 4..7): choices 0xFF, forecasts NaN; count exhausted.
-__global__ void fixup_kernel(const uint8_t* status, int64_t n, uint8_t* choice, int64_t ld_c, int64_t W, int n_eta,
-                             double* forecast, int64_t ld_f, chase_diag_t* diag) {
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const int s = status[i];
-        if (s == CHASE_ERR_TRACE_EXHAUSTED && threadIdx.x == 0)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&diag->n_exhausted), 1ull);
-        if (s < CHASE_ERR_DATA) continue;
-        if (threadIdx.x == 0)
-            atomicMin(reinterpret_cast<unsigned long long*>(&diag->first_bad_trace), (unsigned long long)i);
+// Invalid traces (status 4..7; listed by the sweep kernels as they finish a
+// trace): choices 0xFF, forecasts NaN.
+__global__ void fixup_kernel(const int64_t* bad_list, const chase_diag_t* diag, int64_t n, uint8_t* choice,
+                             int64_t ld_c, int64_t W, int n_eta, double* forecast, int64_t ld_f) {
+    const int64_t n_bad = (int64_t)diag->n_bad;
+    for (int64_t b = blockIdx.x; b < n_bad; b += gridDim.x) {
+        const int64_t i = bad_list[b];
         if (choice)
             for (int e = 0; e < n_eta; ++e)
                 for (int64_t w = threadIdx.x; w < W; w += blockDim.x) choice[((int64_t)e * n + i) * ld_c + w] = 0xff;

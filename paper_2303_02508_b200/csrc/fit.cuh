@@ -4,6 +4,70 @@
 // §3.1: the model is fitted once per trace on its L history points c[0..L)
 // ("one day prior").  One lane per trace, the same
 // sequential order and rounding as oracle_fit (bit-identical records).
+// Normal equations, Cholesky (ridge fallback) and un-standardisation for the
+// 3-column case, unrolled: identical arithmetic to the general path.
+template <typename E>
+__device__ __forceinline__ void fit_solve3(const E* h, int n, int T, int phi0, const double* S, const double* Cc,
+                                           double ridge, double tol_rel, const double* mu, const double* sg, double dn,
+                                           double& c0, double* w, int& status, int& ridge_fired) {
+    double G00 = 0, G10 = 0, G11 = 0, G20 = 0, G21 = 0, G22 = 0, h0 = 0, h1 = 0, h2 = 0;
+    int ph = (phi0 + 1) % T;
+    for (int i = 1; i <= n; ++i) {
+        const double z0 = __ddiv_rn(__dsub_rn(S[ph], mu[0]), sg[0]);
+        const double z1 = __ddiv_rn(__dsub_rn(Cc[ph], mu[1]), sg[1]);
+        const double z2 = __ddiv_rn(__dsub_rn((double)h[i - 1], mu[2]), sg[2]);
+        const double u = __ddiv_rn(__dsub_rn((double)h[i], mu[3]), sg[3]);
+        G00 = __dadd_rn(G00, __dmul_rn(z0, z0));
+        h0 = __dadd_rn(h0, __dmul_rn(z0, u));
+        G10 = __dadd_rn(G10, __dmul_rn(z1, z0));
+        G11 = __dadd_rn(G11, __dmul_rn(z1, z1));
+        h1 = __dadd_rn(h1, __dmul_rn(z1, u));
+        G20 = __dadd_rn(G20, __dmul_rn(z2, z0));
+        G21 = __dadd_rn(G21, __dmul_rn(z2, z1));
+        G22 = __dadd_rn(G22, __dmul_rn(z2, z2));
+        h2 = __dadd_rn(h2, __dmul_rn(z2, u));
+        ph = ph + 1 == T ? 0 : ph + 1;
+    }
+    const double tol = __dmul_rn(tol_rel, dn);
+    double L00 = 0, L10 = 0, L20 = 0, L11 = 0, L21 = 0, L22 = 0;
+    bool ok = false;
+    for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+        if (attempt == 1) {
+            G00 = __dadd_rn(G00, ridge);
+            G11 = __dadd_rn(G11, ridge);
+            G22 = __dadd_rn(G22, ridge);
+            ridge_fired = 1;
+        }
+        double d = G00;
+        if (!(d > tol)) continue;
+        L00 = __dsqrt_rn(d);
+        L10 = __ddiv_rn(G10, L00);
+        L20 = __ddiv_rn(G20, L00);
+        d = __dsub_rn(G11, __dmul_rn(L10, L10));
+        if (!(d > tol)) continue;
+        L11 = __dsqrt_rn(d);
+        L21 = __ddiv_rn(__dsub_rn(G21, __dmul_rn(L20, L10)), L11);
+        d = __dsub_rn(__dsub_rn(G22, __dmul_rn(L20, L20)), __dmul_rn(L21, L21));
+        if (!(d > tol)) continue;
+        L22 = __dsqrt_rn(d);
+        ok = true;
+    }
+    if (!ok) {
+        status = CHASE_ERR_FIT;
+        return;
+    }
+    const double zt0 = __ddiv_rn(h0, L00);
+    const double zt1 = __ddiv_rn(__dsub_rn(h1, __dmul_rn(L10, zt0)), L11);
+    const double zt2 = __ddiv_rn(__dsub_rn(__dsub_rn(h2, __dmul_rn(L20, zt0)), __dmul_rn(L21, zt1)), L22);
+    const double b2 = __ddiv_rn(zt2, L22);
+    const double b1 = __ddiv_rn(__dsub_rn(zt1, __dmul_rn(L21, b2)), L11);
+    const double b0 = __ddiv_rn(__dsub_rn(__dsub_rn(zt0, __dmul_rn(L10, b1)), __dmul_rn(L20, b2)), L00);
+    w[0] = __ddiv_rn(__dmul_rn(sg[3], b0), sg[0]);
+    w[1] = __ddiv_rn(__dmul_rn(sg[3], b1), sg[1]);
+    w[2] = __ddiv_rn(__dmul_rn(sg[3], b2), sg[2]);
+    c0 = __dsub_rn(__dsub_rn(__dsub_rn(mu[3], __dmul_rn(w[0], mu[0])), __dmul_rn(w[1], mu[1])), __dmul_rn(w[2], mu[2]));
+}
+
 template <typename E>
 __device__ void fit_one(const E* h, int L, int T, int phi0, const double* S, const double* Cc, double ridge,
                         double tol_rel, double* rec) {
@@ -50,6 +114,10 @@ __device__ void fit_one(const E* h, int L, int T, int phi0, const double* S, con
         if (!(sg[3] > 0.0)) {
             kind = 1;
             c0 = mu[3];
+        } else if (sg[0] > 0.0 && sg[1] > 0.0 && sg[2] > 0.0) {
+            // all three columns kept (the common case): the same operation
+            // sequence as the general path below, with register-resident 3x3 state
+            fit_solve3(h, n, T, phi0, S, Cc, ridge, tol_rel, mu, sg, dn, c0, w, status, ridge_fired);
         } else {
             int cols[3], m = 0;
             for (int j = 0; j < 3; ++j)

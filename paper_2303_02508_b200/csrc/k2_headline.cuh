@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(con
                 if (lane == 0) {
                     P.status[i] = (uint8_t)status;
                     if (status != 0) {
-                        atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_bad), 1ull);
+                        const unsigned long long slot =
+                            atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_bad), 1ull);
+                        P.bad_list[slot] = i;
                         atomicMin(reinterpret_cast<unsigned long long*>(&P.diag->first_bad_trace),
                                   (unsigned long long)i);
                     }

@@ -146,18 +146,23 @@ cudaError_t launch_plan(const PlanParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_fixup(const uint8_t* status, int64_t n_traces, uint8_t* choice, int64_t ld_c, int64_t W,
-                         int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag, cudaStream_t s) {
+cudaError_t launch_fixup(const uint8_t* status, const int64_t* bad_list, int64_t n_traces, uint8_t* choice,
+                         int64_t ld_c, int64_t W, int n_eta_choice, double* forecast, int64_t ld_f,
+                         chase_diag_t* diag, cudaStream_t s) {
     if (n_traces <= 0) return cudaSuccess;
-    const int64_t g = n_traces < (int64_t)num_sms() * 8 ? n_traces : (int64_t)num_sms() * 8;
-    fixup_kernel<<<(unsigned)g, 128, 0, s>>>(status, n_traces, choice, ld_c, W, n_eta_choice, forecast, ld_f, diag);
+    if (choice || forecast) {
+        fixup_kernel<<<(unsigned)(2 * num_sms()), 256, 0, s>>>(bad_list, diag, n_traces, choice, ld_c, W, n_eta_choice,
+                                                                forecast, ld_f);
+        ++g_launches;
+    }
     diag_status_kernel<<<1, 32, 0, s>>>(status, n_traces, diag);
-    g_launches += 2;
+    ++g_launches;
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const FinalizeParams& p, chase_sum_t* sum, uint8_t* choice, int64_t ld_c,
-                            int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag, cudaStream_t s) {
+cudaError_t launch_finalize(const FinalizeParams& p, const int64_t* bad_list, chase_sum_t* sum, uint8_t* choice,
+                            int64_t ld_c, int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag,
+                            cudaStream_t s) {
     if (p.n_traces > 0) {
         const int64_t grid = finalize_grid(p.n_traces);
         if (p.is_f64) finalize_kernel<double><<<(unsigned)grid, kFinThreads, 0, s>>>(p);
@@ -166,14 +171,14 @@ cudaError_t launch_finalize(const FinalizeParams& p, chase_sum_t* sum, uint8_t* 
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         if (sum) {
-            finalize_sums_kernel<<<p.n_eta, 32, 0, s>>>(p.block_sums, grid, p.n_eta, sum);
+            finalize_sums_kernel<<<p.n_eta, 256, 0, s>>>(p.block_sums, grid, p.n_eta, sum);
             ++g_launches;
         }
     } else if (sum) {
         cudaError_t e = cudaMemsetAsync(sum, 0, sizeof(chase_sum_t) * (size_t)p.n_eta, s);
         if (e != cudaSuccess) return e;
     }
-    return launch_fixup(p.status, p.n_traces, choice, ld_c, p.W, n_eta_choice, forecast, ld_f, diag, s);
+    return launch_fixup(p.status, bad_list, p.n_traces, choice, ld_c, p.W, n_eta_choice, forecast, ld_f, diag, s);
 }
 
 cudaError_t launch_diag_reset(chase_diag_t* diag, cudaStream_t s) {

@@ -51,6 +51,7 @@ struct SweepParams {
     int64_t ld_f;
     uint8_t* status;              // [n]
     chase_diag_t* diag;
+    int64_t* bad_list;            // [n]: traces with status 4..7 (slot = old n_bad)
 };
 
 struct FitParams {
@@ -80,6 +81,7 @@ struct FinalizeParams {
     uint8_t* status;              // in: sweep status; out: final (incl. exhausted)
     chase_totals_t* per_trace;    // may be null
     double* block_sums;           // [grid][n_eta][8]
+    chase_diag_t* diag;
 };
 
 struct PlanParams {
@@ -104,10 +106,12 @@ cudaError_t launch_fit(const FitParams& p, cudaStream_t s);
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s);
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 // per-trace totals + fixed-order per-GPU sums (+ invalid-trace fix-up)
-cudaError_t launch_finalize(const FinalizeParams& p, chase_sum_t* sum, uint8_t* choice, int64_t ld_c,
-                            int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag, cudaStream_t s);
-cudaError_t launch_fixup(const uint8_t* status, int64_t n_traces, uint8_t* choice, int64_t ld_c, int64_t W,
-                         int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag, cudaStream_t s);
+cudaError_t launch_finalize(const FinalizeParams& p, const int64_t* bad_list, chase_sum_t* sum, uint8_t* choice,
+                            int64_t ld_c, int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag,
+                            cudaStream_t s);
+cudaError_t launch_fixup(const uint8_t* status, const int64_t* bad_list, int64_t n_traces, uint8_t* choice,
+                         int64_t ld_c, int64_t W, int n_eta_choice, double* forecast, int64_t ld_f,
+                         chase_diag_t* diag, cudaStream_t s);
 cudaError_t launch_diag_reset(chase_diag_t* diag, cudaStream_t s);
 cudaError_t launch_accumulate(double* acc, const double* add, int n, cudaStream_t s);
 uint64_t kernel_launches();
