@@ -82,8 +82,12 @@ typedef struct {
     int32_t steps_per_day;       /* T = 86400/interval_s (Eq. 2)                   */
     int32_t history_len;         /* L: points before job start, L-1 >= 4 rows */
     int32_t refit_stride;        /* 0 = fit once at job start.
-                                    R >= 1 = rolling refit every R windows on the
-                                    L points before the refit origin (Q1).      */
+                                    R >= 1 = rolling refit: window w uses the model
+                                    fitted on the L points before its origin
+                                    r = s0 + R*floor((w-s0)/R) (Q1);
+                                    MaxCI stays the job-start value.  The
+                                    workspace then also holds an f64 forecast
+                                    scratch of round_up(W,2) per trace.         */
     int32_t reserved;
     double  ridge_lambda;        /* 1e-8                                   */
     double  singular_tol;        /* 1e-12: Cholesky pivot <= tol*(L-1) -> ridge (Q6) */
@@ -220,8 +224,9 @@ uint64_t chase_kernel_launches(void);
 
 /* Optional timing hook: when both are non-NULL cudaEvent_t handles, the next
  * calls record `start` / `stop` on their stream immediately around the
- * dominant kernel (the fused sweep, the replay or the plan kernel), so the
- * caller can time that kernel alone with CUDA events.  Pass NULLs to clear.
+ * dominant kernel (the fused sweep, the replay or the plan kernel; with
+ * refit_stride >= 1, the rolling refit kernel), so the caller can time that
+ * kernel alone with CUDA events.  Pass NULLs to clear.
  * Thread-local. */
 void chase_set_kernel_events(void* start, void* stop);
 

@@ -266,21 +266,21 @@ class Planner:
 
     def __init__(self, traces_tensor, *, n_steps: int, profiles, etas, interval_s=3600, history_len=24,
                  phase0=0, profile_id=None, job_samples=None, want_choice=True, want_forecast=False,
-                 want_per_trace=False, max_power_w=0.0, max_ci=0.0):
+                 want_per_trace=False, max_power_w=0.0, max_ci=0.0, refit_stride=0):
         import torch
         self.x = traces_tensor
         dev = traces_tensor.device
         self.tr = make_traces(traces_tensor, n_steps=n_steps, interval_s=interval_s, phase0=phase0)
-        self.fcfg = make_fcfg(interval_s=interval_s, history_len=history_len)
+        self.fcfg = make_fcfg(interval_s=interval_s, history_len=history_len, refit_stride=refit_stride)
         self.profiles, self.etas = profiles, list(etas)
         n, W = traces_tensor.shape[0], n_steps - history_len
         self.n, self.W = n, W
         self.ld_c = round_up(W, 16)
-        self.ld_f = W
+        self.ld_f = round_up(W, 2)
         self.ws = alloc_workspace(workspace_bytes(self.tr, self.fcfg, len(profiles), len(self.etas)), dev)
         self.sums = torch.zeros((len(self.etas), 8), dtype=torch.float64, device=dev)
         self.choice = torch.empty((len(self.etas), n, self.ld_c), dtype=torch.uint8, device=dev) if want_choice else None
-        self.forecast = torch.empty((n, W), dtype=torch.float64, device=dev) if want_forecast else None
+        self.forecast = torch.empty((n, self.ld_f), dtype=torch.float64, device=dev) if want_forecast else None
         self.per_trace = (torch.empty((len(self.etas), n, 64), dtype=torch.uint8, device=dev)
                           if want_per_trace else None)
         self.profile_id, self.job = profile_id, job_samples

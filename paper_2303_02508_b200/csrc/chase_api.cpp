@@ -48,10 +48,16 @@ constexpr size_t kWsAlign = 256;
 // per-(eta, trace) raw replay results [n_eta][n][8] | status [n] |
 // finalize block sums [ceil(n/256)][n_eta][8].
 struct WsLayout {
-    size_t diag, tables, records, raw, status, bad_list, block_sums, total;
+    size_t diag, tables, records, raw, status, bad_list, block_sums, roll_ptab, roll_fc, total;
+    int64_t ld_roll;  // row stride (doubles) of the rolling forecast scratch
 };
 
-WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta) {
+bool rolling(const chase_forecast_cfg_t* f) { return f && f->refit_stride > 0; }
+
+// Rolling refit (refit_stride >= 1) appends the per-phase fit tables and a
+// forecast scratch [n][round_up(W, 2)] f64 (used when d_forecast is NULL).
+WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta, const chase_traces_t* t = nullptr,
+                   const chase_forecast_cfg_t* f = nullptr) {
     WsLayout w;
     size_t o = 0;
     w.diag = o; o += kWsAlign;
@@ -61,6 +67,13 @@ WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta) {
     w.status = o; o += round_up(n_traces, kWsAlign);
     w.bad_list = o; o += round_up(n_traces * 8, kWsAlign);
     w.block_sums = o; o += round_up((finalize_grid(n_traces) + 1) * n_eta * 8 * 8, kWsAlign);
+    w.roll_ptab = w.roll_fc = o;
+    w.ld_roll = 0;
+    if (rolling(f) && t && f->history_len >= 2 && t->n_steps > f->history_len) {
+        w.roll_ptab = o; o += round_up((int64_t)roll_phase_doubles(T, f->history_len) * 8, kWsAlign);
+        w.ld_roll = round_up(t->n_steps - f->history_len, 2);
+        w.roll_fc = o; o += round_up(n_traces * w.ld_roll * 8, kWsAlign);
+    }
     w.total = o;
     return w;
 }
@@ -90,8 +103,6 @@ chase_status_t check_fcfg(const chase_traces_t* t, const chase_forecast_cfg_t* f
     if (t->n_steps <= f->history_len) return fail(CHASE_ERR_INVALID, "n_steps must exceed history_len (W >= 1)");
     if (f->history_len > 1 << 20) return fail(CHASE_ERR_INVALID, "history_len too large");
     if (f->refit_stride < 0) return fail(CHASE_ERR_INVALID, "refit_stride < 0");
-    if (f->refit_stride > 0)
-        return fail(CHASE_ERR_INVALID, "refit_stride=%d: rolling refit is not available in this build", f->refit_stride);
     if (!(f->ridge_lambda >= 0) || !(f->singular_tol >= 0)) return fail(CHASE_ERR_INVALID, "ridge/tol must be >= 0");
     return CHASE_OK;
 }
@@ -295,20 +306,29 @@ FinalizeParams make_finalize(const chase_traces_t* t, int L, int n_eta, int n_pr
     return f;
 }
 
+cudaError_t launch_rolling_into(const chase_traces_t* t, const chase_forecast_cfg_t* f, uint8_t* ws, const WsLayout& WL,
+                                double max_ci_fixed, double* fc, int64_t ldf, cudaStream_t s) {
+    const int T = f->steps_per_day;
+    const double* phase = reinterpret_cast<const double*>(ws + WL.tables + sizeof(TablesHeader));
+    return launch_rolling(t->data, t->dtype == CHASE_F64, t->ld, t->n_traces, (int)t->n_steps, f->history_len, T,
+                          t->phase0, f->refit_stride, f->ridge_lambda, f->singular_tol, phase,
+                          reinterpret_cast<double*>(ws + WL.roll_ptab), reinterpret_cast<double*>(ws + WL.records),
+                          max_ci_fixed, fc, ldf, s);
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* chase_last_error(void) { return g_err; }
 
-const char* chase_version(void) { return "chase-b200 0.1 (sm_100a, fit-once planner)"; }
+const char* chase_version(void) { return "chase-b200 0.2 (sm_100a; fit-once and rolling-refit planner)"; }
 
 size_t chase_workspace_bytes(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, int32_t n_profiles,
                              int32_t n_eta) {
     if (!traces || traces->interval_s <= 0 || 86400 % traces->interval_s || n_profiles < 0 || n_eta < 0) return 0;
-    (void)fcfg;
     const int T = 86400 / traces->interval_s;
-    return ws_layout(traces->n_traces, T, n_profiles < 1 ? 1 : n_profiles, n_eta < 1 ? 1 : n_eta).total;
+    return ws_layout(traces->n_traces, T, n_profiles < 1 ? 1 : n_profiles, n_eta < 1 ? 1 : n_eta, traces, fcfg).total;
 }
 
 chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_forecast,
@@ -320,7 +340,7 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     if (!d_forecast || ld_f < W) return fail(CHASE_ERR_INVALID, "d_forecast NULL or ld_f < W");
     const int T = fcfg->steps_per_day;
     // layout sized for (1 profile, 1 eta) so one workspace serves every entry point
-    const WsLayout WL = ws_layout(traces->n_traces, T, 1, 1);
+    const WsLayout WL = ws_layout(traces->n_traces, T, 1, 1, traces, fcfg);
     if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
@@ -335,6 +355,13 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     p.n_eta = 1;
     p.forecast = d_forecast;
     p.ld_f = ld_f;
+    if (rolling(fcfg)) {
+        // every origin's fit straight into d_forecast; the predict pass then only validates
+        e = launch_rolling_into(traces, fcfg, ws, WL, 1.0, d_forecast, ld_f, s);
+        if (e != cudaSuccess) return cuda_fail(e, "rolling forecast kernel");
+        p.fc_in = d_forecast;
+        p.ld_fin = ld_f;
+    }
     e = launch_sweep(MODE_PREDICT, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, s);
     if (e != cudaSuccess) return cuda_fail(e, "predict kernel");
     e = launch_fixup(p.status, p.bad_list, traces->n_traces, nullptr, 0, W, 0, d_forecast, ld_f, p.diag, s);
@@ -445,7 +472,7 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
         return fail(CHASE_ERR_INVALID, "d_choice must be 16-byte aligned with ld_c a multiple of 16 >= round_up(W,16)");
     if (d_forecast && ld_f < W) return fail(CHASE_ERR_INVALID, "ld_f < W");
     const int T = fcfg->steps_per_day;
-    const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, cost->n_eta);
+    const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, cost->n_eta, traces, fcfg);
     if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
     std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, cost, cost->n_eta);
     if ((st = check_smem((int)blob.size(), T, traces, cost->n_eta))) return st;
@@ -465,9 +492,24 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     p.ld_c = ld_c;
     p.forecast = d_forecast;
     p.ld_f = ld_f;
-    ev_start(s);
-    e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned_start(traces, fcfg->history_len), p, s);
-    ev_stop(s);
+    bool aligned = aligned_start(traces, fcfg->history_len);
+    if (rolling(fcfg)) {
+        // rolling refit: forecasts of every window first (into d_forecast when given), then the
+        // fused argmin + replay reads them (sweep_kernel<..., FIN>)
+        double* fc = d_forecast ? d_forecast : reinterpret_cast<double*>(ws + WL.roll_fc);
+        const int64_t ldf = d_forecast ? ld_f : WL.ld_roll;
+        ev_start(s);  // rolling mode: the refits dominate (timing hook)
+        e = launch_rolling_into(traces, fcfg, ws, WL, cost->max_ci, fc, ldf, s);
+        ev_stop(s);
+        if (e != cudaSuccess) return cuda_fail(e, "rolling forecast kernel");
+        p.fc_in = fc;
+        p.ld_fin = ldf;
+        p.forecast = nullptr;
+        aligned = aligned && ldf % 2 == 0 && ((uintptr_t)fc & 15) == 0;
+    }
+    if (!rolling(fcfg)) ev_start(s);
+    e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p, s);
+    if (!rolling(fcfg)) ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "sweep kernel");
     FinalizeParams fz = make_finalize(traces, fcfg->history_len, cost->n_eta, n_profiles, ws, WL, d_profile_id,
                                       d_job_samples, d_per_trace);

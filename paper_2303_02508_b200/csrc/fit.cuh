@@ -6,28 +6,12 @@
 // sequential order and rounding as oracle_fit (bit-identical records).
 // Normal equations, Cholesky (ridge fallback) and un-standardisation for the
 // 3-column case, unrolled: identical arithmetic to the general path.
-template <typename E>
-__device__ __forceinline__ void fit_solve3(const E* h, int n, int T, int phi0, const double* S, const double* Cc,
-                                           double ridge, double tol_rel, const double* mu, const double* sg, double dn,
-                                           double& c0, double* w, int& status, int& ridge_fired) {
-    double G00 = 0, G10 = 0, G11 = 0, G20 = 0, G21 = 0, G22 = 0, h0 = 0, h1 = 0, h2 = 0;
-    int ph = (phi0 + 1) % T;
-    for (int i = 1; i <= n; ++i) {
-        const double z0 = __ddiv_rn(__dsub_rn(S[ph], mu[0]), sg[0]);
-        const double z1 = __ddiv_rn(__dsub_rn(Cc[ph], mu[1]), sg[1]);
-        const double z2 = __ddiv_rn(__dsub_rn((double)h[i - 1], mu[2]), sg[2]);
-        const double u = __ddiv_rn(__dsub_rn((double)h[i], mu[3]), sg[3]);
-        G00 = __dadd_rn(G00, __dmul_rn(z0, z0));
-        h0 = __dadd_rn(h0, __dmul_rn(z0, u));
-        G10 = __dadd_rn(G10, __dmul_rn(z1, z0));
-        G11 = __dadd_rn(G11, __dmul_rn(z1, z1));
-        h1 = __dadd_rn(h1, __dmul_rn(z1, u));
-        G20 = __dadd_rn(G20, __dmul_rn(z2, z0));
-        G21 = __dadd_rn(G21, __dmul_rn(z2, z1));
-        G22 = __dadd_rn(G22, __dmul_rn(z2, z2));
-        h2 = __dadd_rn(h2, __dmul_rn(z2, u));
-        ph = ph + 1 == T ? 0 : ph + 1;
-    }
+// Cholesky of the standardised 3x3 Gram (ridge fallback), the two
+// triangular solves and the un-standardisation of oracle_fit (DESIGN Q24).
+__device__ __forceinline__ void chol3_solve(double G00, double G10, double G11, double G20, double G21, double G22,
+                                            double h0, double h1, double h2, double ridge, double tol_rel, double dn,
+                                            const double* mu, const double* sg, double& c0, double* w, int& status,
+                                            int& ridge_fired) {
     const double tol = __dmul_rn(tol_rel, dn);
     double L00 = 0, L10 = 0, L20 = 0, L11 = 0, L21 = 0, L22 = 0;
     bool ok = false;
@@ -66,6 +50,31 @@ __device__ __forceinline__ void fit_solve3(const E* h, int n, int T, int phi0, c
     w[1] = __ddiv_rn(__dmul_rn(sg[3], b1), sg[1]);
     w[2] = __ddiv_rn(__dmul_rn(sg[3], b2), sg[2]);
     c0 = __dsub_rn(__dsub_rn(__dsub_rn(mu[3], __dmul_rn(w[0], mu[0])), __dmul_rn(w[1], mu[1])), __dmul_rn(w[2], mu[2]));
+}
+
+template <typename E>
+__device__ __forceinline__ void fit_solve3(const E* h, int n, int T, int phi0, const double* S, const double* Cc,
+                                           double ridge, double tol_rel, const double* mu, const double* sg, double dn,
+                                           double& c0, double* w, int& status, int& ridge_fired) {
+    double G00 = 0, G10 = 0, G11 = 0, G20 = 0, G21 = 0, G22 = 0, h0 = 0, h1 = 0, h2 = 0;
+    int ph = (phi0 + 1) % T;
+    for (int i = 1; i <= n; ++i) {
+        const double z0 = __ddiv_rn(__dsub_rn(S[ph], mu[0]), sg[0]);
+        const double z1 = __ddiv_rn(__dsub_rn(Cc[ph], mu[1]), sg[1]);
+        const double z2 = __ddiv_rn(__dsub_rn((double)h[i - 1], mu[2]), sg[2]);
+        const double u = __ddiv_rn(__dsub_rn((double)h[i], mu[3]), sg[3]);
+        G00 = __dadd_rn(G00, __dmul_rn(z0, z0));
+        h0 = __dadd_rn(h0, __dmul_rn(z0, u));
+        G10 = __dadd_rn(G10, __dmul_rn(z1, z0));
+        G11 = __dadd_rn(G11, __dmul_rn(z1, z1));
+        h1 = __dadd_rn(h1, __dmul_rn(z1, u));
+        G20 = __dadd_rn(G20, __dmul_rn(z2, z0));
+        G21 = __dadd_rn(G21, __dmul_rn(z2, z1));
+        G22 = __dadd_rn(G22, __dmul_rn(z2, z2));
+        h2 = __dadd_rn(h2, __dmul_rn(z2, u));
+        ph = ph + 1 == T ? 0 : ph + 1;
+    }
+    chol3_solve(G00, G10, G11, G20, G21, G22, h0, h1, h2, ridge, tol_rel, dn, mu, sg, c0, w, status, ridge_fired);
 }
 
 template <typename E>

@@ -257,7 +257,9 @@ __device__ __noinline__ Completion find_completion(const E* tv_src, const uint8_
     return r;
 }
 
-template <int MODE, typename E, bool AL, bool MULTI>
+// FIN (rolling refit): the forecasts come from P.fc_in (rolling_forecast_kernel)
+// instead of the per-trace folded table: Ap = that row, w_lag = 0, so p = fc + 0*lag = fc.
+template <int MODE, typename E, bool AL, bool MULTI, bool FIN = false>
 __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     constexpr int VEC = 16 / (int)sizeof(E);
@@ -358,12 +360,12 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                 smax = profs[prof].smax;
                 J = P.job ? P.job[i] : 0.0;
                 status = (int)rec[5];
-                wl = rec[3];
+                wl = FIN ? 0.0 : rec[3];
                 const double maxci = P.max_ci_fixed > 0.0 ? P.max_ci_fixed : rec[4];
                 if (status == 0 && MODE == MODE_FUSED && !(maxci > 0.0)) status = CHASE_ERR_MAXCI;
                 const int64_t m = (int64_t)rec[8];
                 mb = (J > 0.0 && m >= 1 && m <= P.W) ? m - 1 : P.W;
-                if (status == 0 && MODE != MODE_REPLAY) {
+                if (status == 0 && MODE != MODE_REPLAY && !FIN) {
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
                     const int n_a = aext_len(T);
                     int ph = lane % T;
@@ -395,8 +397,9 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
             const E* tv = reinterpret_cast<const E*>(stage) + off0 + j0;  // tv[jj] = c[w0 + jj]
             int phi0 = phase_c + lane_phase;                              // phase of my first window
             if (phi0 >= T) phi0 -= T;
-            const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;  // 16-byte aligned
             const int64_t jb = (int64_t)c * kWarpW + j0;                  // my first window, from s0
+            const double* Ap = FIN ? P.fc_in + i * P.ld_fin + jb
+                                   : ((phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0);  // 16-byte aligned
             // samples cannot reach J before this many windows: skip the completion test until then
             const int64_t w_through = min((int64_t)P.W, (int64_t)(c + 1) * kWarpW);
             const bool may_complete = J > 0.0 && __dmul_rn(__dmul_rn((double)w_through, smax), 1.000001) >= J;
@@ -458,7 +461,8 @@ __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constan
                     }
                     }
                 } else if (MODE == MODE_PREDICT) {
-                    predict_chunk<E>(tv, nwin, Ap, wl, P.forecast + i * P.ld_f + jb, a);
+                    if (FIN) a.bad |= chunk_has_bad(tv, nwin) ? 1 : 0;  // rolling: forecasts already written
+                    else predict_chunk<E>(tv, nwin, Ap, wl, P.forecast + i * P.ld_f + jb, a);
                 } else {
                     const uint8_t* cin = P.choice_in + ((int64_t)e * P.n_traces + i) * P.ld_c + jb;
                     if (e == 0) replay_chunk<true, E>(tv, nwin, cin, pf->K, pf->line, chb + j0, a);

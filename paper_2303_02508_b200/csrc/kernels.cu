@@ -13,6 +13,9 @@
 //   finalize_kernel   per-trace totals (Eq. 3 stepwise carbon, pro-rata last
 //                     window, max-power baseline) + fixed-order per-GPU sums.
 //   plan_kernel       Eq. 6 argmin from given forecasts (split path).
+//   rolling_*_kernel  rolling refit (refit_stride >= 1): one thread per
+//                     (trace, origin), oracle_fit's exact operation order
+//                     (rolling.cuh); the sweep then reads those forecasts.
 //
 // Arithmetic contract: every fp64 step that decides an output is written with
 // explicit round-to-nearest intrinsics (and the file is built -fmad=false),
@@ -32,6 +35,7 @@ namespace {
 #include "k2_sweep.cuh"
 #include "k2_headline.cuh"
 #include "finalize.cuh"
+#include "rolling.cuh"
 
 int num_sms() {
     int dev = 0, sms = 0;
@@ -40,10 +44,10 @@ int num_sms() {
     return sms > 0 ? sms : 148;
 }
 
-template <int MODE, typename E, bool AL, bool MULTI>
+template <int MODE, typename E, bool AL, bool MULTI, bool FIN = false>
 cudaError_t launch_sweep_t(const SweepParams& p, cudaStream_t s) {
     const int smem = sweep_smem_total(p.tables_bytes, p.T, p.stage_bytes, p.n_eta);
-    auto kern = sweep_kernel<MODE, E, AL, MULTI>;
+    auto kern = sweep_kernel<MODE, E, AL, MULTI, FIN>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;
@@ -103,6 +107,25 @@ cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
 
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
+    if (mode == MODE_PREDICT && p.fc_in) {  // rolling chase_fit_forecast: validation pass only
+        if (f64) return aligned ? launch_sweep_t<MODE_PREDICT, double, true, false, true>(p, s)
+                                : launch_sweep_t<MODE_PREDICT, double, false, false, true>(p, s);
+        return aligned ? launch_sweep_t<MODE_PREDICT, float, true, false, true>(p, s)
+                       : launch_sweep_t<MODE_PREDICT, float, false, false, true>(p, s);
+    }
+    if (mode == MODE_FUSED && p.fc_in) {  // rolling refit: forecasts precomputed by rolling_forecast_kernel
+        const bool multi = p.n_eta > 1;
+        if (f64) {
+            if (multi) return aligned ? launch_sweep_t<MODE_FUSED, double, true, true, true>(p, s)
+                                      : launch_sweep_t<MODE_FUSED, double, false, true, true>(p, s);
+            return aligned ? launch_sweep_t<MODE_FUSED, double, true, false, true>(p, s)
+                           : launch_sweep_t<MODE_FUSED, double, false, false, true>(p, s);
+        }
+        if (multi) return aligned ? launch_sweep_t<MODE_FUSED, float, true, true, true>(p, s)
+                                  : launch_sweep_t<MODE_FUSED, float, false, true, true>(p, s);
+        return aligned ? launch_sweep_t<MODE_FUSED, float, true, false, true>(p, s)
+                       : launch_sweep_t<MODE_FUSED, float, false, false, true>(p, s);
+    }
     if (mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !getenv("CHASE_FORCE_GENERAL")) {
         // the headline shape: lean specialised kernel (k2_fast.cuh)
         const int smem = fast_smem_total(p.tables_bytes, p.T, p.stage_bytes, p.n_prof);
@@ -142,6 +165,43 @@ cudaError_t launch_plan(const PlanParams& p, cudaStream_t s) {
     int64_t grid = (groups + 255) / 256;
     if (grid > (int64_t)num_sms() * 8) grid = (int64_t)num_sms() * 8;
     plan_kernel<<<(unsigned)grid, 256, p.tables_bytes, s>>>(p);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+int roll_phase_doubles(int T, int L) { return T * roll_phase_stride(L); }
+
+cudaError_t launch_rolling(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
+                           int R, double ridge, double tol, const double* phase, double* ptab, double* records,
+                           double max_ci_fixed, double* forecast, int64_t ld_f, cudaStream_t s) {
+    if (n_traces <= 0) return cudaSuccess;
+    rolling_phase_kernel<<<(T + 127) / 128, 128, 0, s>>>(phase, phase + T, T, L, ptab);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    RollParams p;
+    p.traces = traces;
+    p.ld = ld;
+    p.n_traces = n_traces;
+    p.N = N;
+    p.L = L;
+    p.T = T;
+    p.phase0 = phase0;
+    p.R = R;
+    p.n_orig = (N - L + R - 1) / R;
+    p.ridge = ridge;
+    p.tol = tol;
+    p.phase = phase;
+    p.ptab = ptab;
+    p.records = records;
+    p.max_ci_fixed = max_ci_fixed;
+    p.forecast = forecast;
+    p.ld_f = ld_f;
+    const int64_t total = n_traces * (int64_t)p.n_orig;
+    const int64_t grid = (total + 127) / 128;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (f64) rolling_forecast_kernel<double><<<(unsigned)grid, 128, 0, s>>>(p);
+    else rolling_forecast_kernel<float><<<(unsigned)grid, 128, 0, s>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }

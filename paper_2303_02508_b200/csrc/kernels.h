@@ -52,6 +52,8 @@ struct SweepParams {
     uint8_t* status;              // [n]
     chase_diag_t* diag;
     int64_t* bad_list;            // [n]: traces with status 4..7 (slot = old n_bad)
+    const double* fc_in;          // rolling refit: forecasts [n][ld_fin] (null: fit-once fold)
+    int64_t ld_fin;
 };
 
 struct FitParams {
@@ -105,6 +107,11 @@ cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_
 cudaError_t launch_fit(const FitParams& p, cudaStream_t s);
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s);
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
+// rolling refit (refit_stride >= 1): per-phase tables, then one thread per (trace, origin)
+int roll_phase_doubles(int T, int L);
+cudaError_t launch_rolling(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
+                           int R, double ridge, double tol, const double* phase, double* ptab, double* records,
+                           double max_ci_fixed, double* forecast, int64_t ld_f, cudaStream_t s);
 // per-trace totals + fixed-order per-GPU sums (+ invalid-trace fix-up)
 cudaError_t launch_finalize(const FinalizeParams& p, const int64_t* bad_list, chase_sum_t* sum, uint8_t* choice,
                             int64_t ld_c, int n_eta_choice, double* forecast, int64_t ld_f, chase_diag_t* diag,

@@ -164,3 +164,18 @@ def test_envelope_random_profiles():
         for x, k in zip(xs, out):
             if k >= 0:
                 assert k == oracle.choose(P, Th, eta, float(lim[-1]), maxci, x)
+
+
+def test_rolling_workspace_adds_phase_tables_and_forecast_scratch():
+    """Rolling refit (refit_stride >= 1) needs the per-phase fit
+    tables and an f64 forecast scratch of round_up(W, 2) per trace."""
+    cb, x, tr = _args(n=10)
+    a = cb.workspace_bytes(tr, cb.make_fcfg(), 1, 1)
+    b = cb.workspace_bytes(tr, cb.make_fcfg(refit_stride=1), 1, 1)
+    W = tr.n_steps - 24
+    assert b - a >= 10 * ((W + 1) // 2 * 2) * 8
+    with pytest.raises(cb.ChaseError, match="refit_stride"):
+        prof = inputs.make_profile("resnet50", inputs.LIMITS_9)
+        import torch
+        cb.sweep(tr, cb.make_fcfg(refit_stride=-1), [prof], [0.5], _ws(), torch.zeros((1, 8), dtype=torch.float64),
+                 stream=0)

@@ -23,24 +23,26 @@ DEV = torch.device("cuda:0")
 
 
 def run_sweep(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0,
-              dtype=torch.float32, forecast=True):
+              dtype=torch.float32, forecast=True, refit_stride=0):
     x = torch.from_numpy(np.ascontiguousarray(tr_host)).to(DEV, dtype)
     pid_t = None if pid is None else torch.from_numpy(np.ascontiguousarray(pid, np.uint8)).to(DEV)
     J_t = None if J is None else torch.from_numpy(np.ascontiguousarray(J, np.float64)).to(DEV)
     pl = cb.Planner(x, n_steps=N, profiles=profiles, etas=etas, interval_s=interval_s, history_len=L,
                     phase0=phase0, profile_id=pid_t, job_samples=J_t, want_choice=True, want_forecast=forecast,
-                    want_per_trace=True, max_ci=max_ci)
+                    want_per_trace=True, max_ci=max_ci, refit_stride=refit_stride)
     res = pl.run()
     torch.cuda.synchronize()
     out = dict(sums=res.sums.cpu().numpy(), totals=res.per_trace_numpy(),
                choice=res.choice.cpu().numpy()[:, :, :N - L],
-               forecast=None if res.forecast is None else res.forecast.cpu().numpy(), diag=pl.diag())
+               forecast=None if res.forecast is None else res.forecast.cpu().numpy()[:, :N - L], diag=pl.diag())
     return out
 
 
-def run_oracle(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0):
+def run_oracle(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0,
+               refit_stride=0):
     T = 86400 // interval_s
     return oracle.plan_batch(np.ascontiguousarray(tr_host, np.float32), N=N, L=L, T=T, phase0=phase0,
+                             refit_stride=refit_stride,
                              profiles=profiles, profile_id=pid, etas=etas, max_ci=max_ci,
                              delta=float(interval_s), job_samples=J)
 
@@ -375,3 +377,64 @@ def test_full_size_c5_sampled():
     s = res.sums.cpu().numpy()
     assert s[0, 7] == w.n_traces
     assert pl.diag().n_bad == 0
+
+
+# ------------------------------------------------------------------ rolling refit
+@pytest.mark.parametrize("R,L,N,etas,n", [
+    (1, 24, 24 + 700, [0.5], 40),          # a new model every window (rolling, north-star "sliding window")
+    (5, 24, 24 + 1300, [0.5, 0.9], 17),    # stride 5, two etas (multi-eta path), crosses a chunk boundary
+    (24, 24, 24 + 2000, [0.4], 9),         # daily refit
+    (7, 23, 23 + 401, [0.6], 6),           # odd L: unaligned tile path
+    (5000, 24, 24 + 1200, [0.5], 5),       # R > W: one origin = fit once
+])
+def test_rolling_refit_parity(R, L, N, etas, n):
+    """Forecasts bit-identical to oracle_plan_trace's rolling refit, choices
+    and (dyadic) totals exact."""
+    prof = [inputs.make_profile("resnet50", inputs.LIMITS_9)]
+    tr = inputs.synth_traces_host(n, N, seed=100 + R)
+    J = np.full(n, 3600 * (N - L) * prof[0].throughput_sps.min())
+    g = run_sweep(tr, N, prof, etas, J=J, L=L, refit_stride=R)
+    o = run_oracle(tr, N, prof, etas, J=J, L=L, refit_stride=R)
+    assert_parity(g, o)
+    if R >= N - L:   # one origin: identical to fit-once
+        o1 = run_oracle(tr, N, prof, etas, J=J, L=L)
+        assert np.array_equal(o1["choice"], o["choice"])
+    # without a forecast output the sweep reads the workspace scratch
+    g2 = run_sweep(tr, N, prof, etas, J=J, L=L, refit_stride=R, forecast=False)
+    g2["forecast"] = None
+    assert_parity(g2, o)
+
+
+def test_rolling_refit_invalid_traces_and_constant_windows():
+    """Status precedence (DESIGN Q25) and the intercept-only / zero-variance
+    origins: a constant stretch makes every origin inside it a constant-target
+    fit; a bad value later in the trace still gives status 4."""
+    N, n, L = 24 + 500, 6, 24
+    prof = [inputs.make_profile("bert", inputs.LIMITS_9)]
+    tr = inputs.synth_traces_host(n, N, seed=8)
+    tr[1, 100:200] = 300.0             # constant target windows -> kind 1 at those origins
+    tr[2, 400] = -1.0                  # -> 4
+    tr[3, :24] = 0.0                   # MaxCI = 0 -> 5
+    tr[4, 30:90] = 250.0
+    J = np.full(n, 3600 * 500 * prof[0].throughput_sps.min())
+    for R in (1, 3):
+        g = run_sweep(tr, N, prof, [0.5, 0.8], J=J, refit_stride=R)
+        o = run_oracle(tr, N, prof, [0.5, 0.8], J=J, refit_stride=R)
+        assert list(o["totals"]["status"][0]) == [0, 0, 4, 5, 0, 0]
+        assert_parity(g, o)
+
+
+def test_rolling_fit_forecast_split_path_and_f64():
+    w = inputs.workload("C4", n_traces=33)
+    N = 24 + 3000
+    tr = inputs.synth_traces_host(w.n_traces, N, seed=41)
+    for dtype in (torch.float32, torch.float64):
+        x = torch.from_numpy(tr).to(DEV, dtype)
+        t = cb.make_traces(x, n_steps=N)
+        f = cb.make_fcfg(refit_stride=2)
+        ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+        fc = torch.empty((w.n_traces, N - 24 + 1), dtype=torch.float64, device=DEV)
+        cb.fit_forecast(t, f, fc, N - 24 + 1, ws)
+        torch.cuda.synchronize()
+        o = oracle.plan_batch(tr, N=N, L=24, T=24, refit_stride=2, profiles=w.profiles[:1], etas=[0.5])
+        assert np.array_equal(fc.cpu().numpy()[:, :N - 24], o["forecast"])

@@ -151,3 +151,23 @@ def test_rolling_refit_uses_the_L_points_before_each_origin():
         r = L + 7 * ((w - L) // 7)
         m = oracle.fit(c[r - L:r], T=T, phi0=(r - L) % T)
         assert fc[w - L] == oracle.predict(m, S[w % T], C[w % T], c[w - 1])
+
+
+def test_rolling_refit_every_window_matches_numpy_lstsq():
+    """R = 1 (a new model each window): every forecast equals
+    SVD least squares (numpy, a different algorithm) on the L points before
+    that window, clamped at 0."""
+    rng = np.random.default_rng(12)
+    T, L, N = 24, 24, 24 + 120
+    t = np.arange(N)
+    c = np.round((480 + 140 * np.sin(2 * np.pi * (t + 5) / T) + rng.normal(0, 18, N)) * 64) / 64
+    fc, ch, tot, st = oracle.plan_trace(c, L=L, T=T, refit_stride=1, avg_power=[100, 200], thr=[400, 700],
+                                        etas=[0.5], pmax=300.0)
+    assert st == 0
+    S, C = oracle.phase_table(T)
+    for w in range(L, N):
+        rows = np.arange(w - L + 1, w)
+        X = np.column_stack([np.ones(L - 1), S[rows % T], C[rows % T], c[rows - 1]])
+        beta, *_ = np.linalg.lstsq(X, c[rows], rcond=None)
+        ref = beta[0] + beta[1] * S[w % T] + beta[2] * C[w % T] + beta[3] * c[w - 1]
+        assert abs(fc[w - L] - max(ref, 0.0)) <= 1e-9 * max(1.0, abs(ref))

@@ -1,0 +1,53 @@
+// fp64_probe.cu — measures the B200's FP64 vector issue rate (DFMA, DADD,
+// DMUL) to give the rolling-refit kernel an ALU roofline.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/fp64_probe tools/fp64_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int OP>
+__global__ void probe(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (OP == 0) x[k] = __fma_rn(x[k], a, b);
+            else if (OP == 1) x[k] = __dadd_rn(x[k], b);
+            else x[k] = __dmul_rn(x[k], a);
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) out[0] = s;
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    double* d;
+    cudaMalloc(&d, 8);
+    const int iters = 20000, threads = 256, blocks = sms * 8;
+    const char* names[3] = {"dfma", "dadd", "dmul"};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int op = 0; op < 3; ++op) {
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(e0);
+            if (op == 0) probe<0><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
+            else if (op == 1) probe<1><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
+            else probe<2><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double ops = (double)blocks * threads * iters * 8;
+            if (rep == 2)
+                printf("{\"op\": \"%s\", \"thread_ops_per_s\": %.4e, \"per_sm_per_clk_at_1965\": %.2f, \"ms\": %.3f, \"sms\": %d}\n",
+                       names[op], ops / (ms * 1e-3), ops / (ms * 1e-3) / sms / 1.965e9, ms, sms);
+        }
+    }
+    return 0;
+}
