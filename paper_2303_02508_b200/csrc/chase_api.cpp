@@ -479,8 +479,10 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     if ((st = upload_tables(blob, ws, WL, s))) return st;
-    cudaError_t e = launch_fit(make_fit(traces, fcfg->history_len, fcfg, ws, WL, n_profiles, d_profile_id,
-                                        d_job_samples), s);
+    FitParams fp = make_fit(traces, fcfg->history_len, fcfg, ws, WL, n_profiles, d_profile_id, d_job_samples);
+    fp.n_eta = cost->n_eta;
+    fp.max_ci_fixed = cost->max_ci;
+    cudaError_t e = launch_fit(fp, s);
     if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
     SweepParams p = base_sweep(traces, fcfg->history_len, WL, ws, (int)blob.size());
     p.n_eta = cost->n_eta;

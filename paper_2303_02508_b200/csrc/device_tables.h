@@ -4,6 +4,7 @@
 // Blob = TablesHeader | phase S[T], C[T] (f64) | ProfileTable[n_prof] |
 //        PairTable[n_prof * n_eta]     (pair index = p * n_eta + e)
 #pragma once
+#include <stddef.h>
 #include <stdint.h>
 #include <vector_types.h>      // double2, uint2
 #include <vector_functions.h>  // make_double2
@@ -50,6 +51,18 @@ struct alignas(16) PairTable {
     int32_t n_intervals;   // fast intervals (diagnostic)
     uint2 ent[kNB];
 };
+
+// The leading fields of PairTable (everything but the bucket entries): the
+// headline kernel keeps only these in shared memory next to its own expanded
+// entries, and hands them to helpers that never touch `ent`.
+struct PairHead {
+    double a[kMaxK];
+    double kbase;
+    int32_t base, k0, n_test, n_intervals;
+};
+static_assert(offsetof(PairTable, ent) == sizeof(PairHead), "PairHead mirrors PairTable's head");
+static_assert(offsetof(PairTable, kbase) == offsetof(PairHead, kbase), "PairHead layout");
+static_assert(offsetof(PairTable, k0) == offsetof(PairHead, k0), "PairHead layout");
 
 static_assert(sizeof(TablesHeader) % 16 == 0, "header alignment");
 static_assert(sizeof(ProfileTable) % 16 == 0, "profile alignment");

@@ -236,9 +236,27 @@ __global__ void __launch_bounds__(128) fit_kernel(const __grid_constant__ FitPar
         fit_one<E>(h, L, T, p.phase0 % T, tab, tab + T, p.ridge, p.tol, rec);
     }
     const double J = p.job ? p.job[i] : 0.0;
-    if (J > 0.0 && p.n_prof > 0) {
-        int prof = p.profile_id ? (int)p.profile_id[i] : 0;
+    int prof = 0;
+    if (p.n_prof > 0) {
+        prof = p.profile_id ? (int)p.profile_id[i] : 0;
         if (prof >= p.n_prof) prof = 0;
+    }
+    if (p.n_eta > 0 && !p.baseline_only) {
+        // per-trace scalars of the single-eta sweep, one thread per trace here instead of a warp there:
+        // [10] Kc = ((1-eta)*Pmax)*MaxCI   [11] 1/Kc (0: canonical path)   [12] J   [13] profile
+        // [14] J/(1.000001*max_k s_k) (a lower bound on the windows to completion)   [15] MaxCI
+        const PairTable* pt = reinterpret_cast<const PairTable*>(p.tables + H->off_pair) + prof * p.n_eta;
+        const ProfileTable* pf = blob_profiles(p.tables) + prof;
+        const double maxci = p.max_ci_fixed > 0.0 ? p.max_ci_fixed : rec[4];
+        const double Kc = __dmul_rn(pt->kbase, maxci);
+        rec[10] = Kc;
+        rec[11] = per_trace_invK(pt, Kc);
+        rec[12] = J;
+        rec[13] = (double)prof;
+        rec[14] = J > 0.0 ? __ddiv_rn(J, __dmul_rn(pf->smax, 1.000001)) : 0.0;
+        rec[15] = maxci;
+    }
+    if (J > 0.0 && p.n_prof > 0) {
         const ProfileTable* pf = blob_profiles(p.tables) + prof;
         const double sb = pf->line[pf->K - 1].x;
         const double qv = __ddiv_rn(J, sb);

@@ -1,70 +1,124 @@
-// k2_fast.cuh — the headline planner kernel, specialised for the common case
-// (fused plan + replay, fp32 traces with a 16-byte aligned job start, one
-// eta, no forecast output).  Same arithmetic, same decomposition as
-// sweep_kernel (warp-per-trace streaming, TMA bulk-copy ring per warp), with
-// all window bookkeeping in 32-bit registers, the per-lane replay sums in
-// registers, and the choice words stored straight from registers (no smem
-// round trip).  Included by kernels.cu inside its anonymous namespace.
+// k2_headline.cuh — the headline planner kernel, specialised for the common
+// case (fused plan + replay, fp32 traces with a 16-byte aligned job start, one
+// eta, no forecast output).  Same arithmetic as sweep_kernel, same
+// decomposition (warp-per-trace streaming through a per-warp TMA bulk-copy
+// ring), tuned for instruction count and the shared-memory pipe.
+// Included by kernels.cu inside its anonymous namespace.
 //
-// Everything the hot loop does per window (DESIGN §6/§7):
-//   p = A[phi] + w_lag*c[w-1]            (Eq. 1, canonical order)
-//   k = bucket(p / Kc)                   (Eq. 6 envelope; rare windows -> canonical)
-//   S += Thr_k*Delta; E += P_k; C += P_k*c[w]; Cs += c[w]
+// Per window (hot loop):
+//   p = A[phi] + w_lag*c[w-1]                       Eq. 1, canonical order
+//   y = p * (1/Kc); h = hi32(y)                     Eq. 6 envelope key
+//   e = ent8[clamp((h >> 14) - base)]               one LDS.64: {T1, lo16 addr(below) | lo16 addr(above) << 16}
+//   addr = PRMT(e.y, ZB, h < T1 ? below : h > T1 ? above : zero line)
+//   (s_k, P_k) = LDS.128 [addr]                     the line itself, no index arithmetic
+//   S += s_k; E += P_k; C += P_k*c[w]; Cs += c[w]
+// The line table sits in a 256-byte-stride region placed at shared address
+// 0x10000, so byte 1 of a line's address is k: the four choice bytes of a
+// group come out of the addresses with three PRMTs.  Choices are staged per
+// warp in shared memory and written with one TMA bulk store per chunk.
 
 #ifndef CHASE_H_WARPS
-#define CHASE_H_WARPS 6
+#define CHASE_H_WARPS 12
 #endif
 #ifndef CHASE_H_STAGES
 #define CHASE_H_STAGES 2
 #endif
 #ifndef CHASE_H_MINB
-#define CHASE_H_MINB 2
+#define CHASE_H_MINB 1
+#endif
+#ifndef CHASE_H_CHUNK
+#define CHASE_H_CHUNK 36
+#endif
+#ifndef CHASE_H_STG
+#define CHASE_H_STG 0   // 1: choice words stored from registers (per group) instead of a TMA store per chunk
 #endif
 constexpr int kHWarps = CHASE_H_WARPS;    // independent warps per CTA
 constexpr int kHThreads = 32 * kHWarps;
 constexpr int kHStages = CHASE_H_STAGES;  // per-warp TMA ring depth
+constexpr int kHChunk = CHASE_H_CHUNK;    // windows per lane per chunk (4 x odd: conflict-free LDS.128)
+constexpr int kHWarpW = 32 * kHChunk;     // windows per warp chunk
+static_assert(kHChunk % 8 == 4, "kHChunk must be 4 mod 8");
+constexpr int kLineStride = 256;          // bytes between lines k and k+1
+constexpr int kLineRegion = kLineStride * (kMaxK + 1);
+constexpr uint32_t kLineBase = 0x10000;   // shared address of the line region (byte 1 of an address = k)
 
-struct FastLayout {
-    int aext, stage, chb, ctx, mbar, bytes;
+// Line k of profile p: kLineBase + 256 k + 16 ((k + p) mod 16).  The slot
+// rotation puts lines k = 0..7 of a profile in distinct shared-memory banks.
+__host__ __device__ inline int line_off(int p, int k) { return kLineStride * k + 16 * ((k + p) & 15); }
+__host__ __device__ inline int haext_len(int T) { return T + kHChunk + 4; }
+__host__ __device__ inline int hstage_bytes() { return round16((kHWarpW + 8) * 4) + kRecBytes; }
+
+// Shared-memory plan, computed identically on host and device from the CTA's
+// shared-window base address.  The line region sits at kLineBase; the warp
+// blocks and then the tables are placed first-fit in the space before it and
+// after it.  Tables: the blob's header, phase table and profiles (its first
+// `head_bytes` bytes), one PairHead per profile (the pair tables minus their
+// 8-byte entries, replaced by the expanded ent8 table), per-lane phase offsets.
+struct HLayout {
+    int tables, heads, ent8, lph, lines, warp_bytes, total;
+    int n_before, after0;        // warp w's block: w < n_before ? w * warp_bytes : after0 + (w - n_before) * warp_bytes
+    int aext, stage, chb, mbar;  // offsets inside a warp block
+    __host__ __device__ int warp_off(int w) const {
+        return w < n_before ? w * warp_bytes : after0 + (w - n_before) * warp_bytes;
+    }
 };
 
-__host__ __device__ inline FastLayout make_fast_layout(int T, int stage_bytes) {
-    FastLayout L;
-    int o = 0;
-    L.aext = o; o += 2 * round16(aext_len(T) * 8);
-    L.stage = o; o += kHStages * stage_bytes;
-    L.chb = o; o += kWarpW;
-    L.ctx = o; o += (int)sizeof(WarpCtx);
-    L.mbar = o; o += 8 * kHStages;
-    L.bytes = round16(o);
+struct HAlloc {
+    int lo, r0, r1, hi;  // free: [lo, r0) and [hi, inf); the region is [r0, r1)
+    __host__ __device__ int take(int bytes, int align) {
+        const int a = (lo + align - 1) & ~(align - 1);
+        if (a + bytes <= r0) {
+            lo = a + bytes;
+            return a;
+        }
+        const int b = (hi + align - 1) & ~(align - 1);
+        hi = b + bytes;
+        return b;
+    }
+};
+
+__host__ __device__ inline HLayout make_hlayout(int T, int head_bytes, int n_prof, int base) {
+    HLayout L;
+    L.aext = 0;
+    L.stage = 2 * round16(haext_len(T) * 8);
+    L.chb = L.stage + kHStages * hstage_bytes();
+    L.mbar = L.chb + kHWarpW;
+    L.warp_bytes = (L.mbar + 8 * kHStages + 127) & ~127;
+    L.lines = (int)kLineBase - base;
+    HAlloc A{0, L.lines, L.lines + kLineRegion, L.lines + kLineRegion};
+    // warp blocks (128-byte multiples): as many as fit before the region, the rest after it
+    L.n_before = L.lines > 0 ? L.lines / L.warp_bytes : 0;
+    if (L.n_before > kHWarps) L.n_before = kHWarps;
+    A.lo = L.n_before * L.warp_bytes;
+    A.hi = (A.hi + 127) & ~127;
+    L.after0 = A.hi;
+    A.hi += (kHWarps - L.n_before) * L.warp_bytes;
+    L.ent8 = A.take(n_prof * kNB * 8, 16);
+    L.tables = A.take(round16(head_bytes), 16);
+    L.heads = A.take(round16(n_prof * (int)sizeof(PairHead)), 16);
+    L.lph = A.take(2 * 32 * 4, 16);
+    L.total = A.hi;
     return L;
 }
 
-__host__ __device__ inline int fast_ent4_bytes(int n_prof) { return n_prof * kNB * (int)sizeof(int4); }
-__host__ __device__ inline int fast_smem_total(int tables_bytes, int T, int stage_bytes, int n_prof) {
-    return round16(tables_bytes) + fast_ent4_bytes(n_prof) + kHWarps * make_fast_layout(T, stage_bytes).bytes;
+__device__ __forceinline__ double2 lds_line(uint32_t addr) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
 }
 
-// Headline lookup: 16-byte entries {T1, T2, below, above} expanded in smem at
-// kernel start from the blob's 8-byte entries (one LDS.128, 2 ISETP, 2 SEL).
-struct Ent4 {
-    int T1, T2;
-    uint32_t below, above;
-};
-__device__ __forceinline__ uint32_t plan_lookup4(double y, const Ent4* __restrict__ ent, int base) {
-    const int h = __double2hiint(y);
-    const int idx = max(min((h >> kSH) - base, kNBUsed - 1), 0);
-    const int4 e = *reinterpret_cast<const int4*>(ent + idx);
-    return h < e.x ? (uint32_t)e.z : (h > e.y ? (uint32_t)e.w : (uint32_t)kZeroLine);
+// Line address for key h from a bucket entry (below / above / zero line).
+__device__ __forceinline__ uint32_t line_addr(int h, uint2 e, uint32_t ZB) {
+    const uint32_t sel = h < (int)e.x ? 0x7610u : (h > (int)e.x ? 0x7632u : 0x7654u);
+    return __byte_perm(e.y, ZB, sel);
 }
 
-// One full-aligned chunk of ngroups x 4 windows; choice words go to smem
-// (for the completion search) and, when `cdst` is set, straight to global.
-template <bool FIRST_STORE>
-__device__ __forceinline__ void fast_groups(const float* __restrict__ tv, int ngroups, const double* __restrict__ Ap,
-                                            double wl, double invK, const Ent4* __restrict__ ent4, int ebase,
-                                            const double2* __restrict__ lines, uint32_t* __restrict__ words,
-                                            uint32_t* __restrict__ cdst, Acc& a) {
+// One lane's full groups of 4 windows.  Words (4 choice bytes) go to the
+// warp's staging buffer; `a.slow` collects them for the deferred-window test.
+__device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngroups, const double* __restrict__ Ap,
+                                           double wl, double invK, const uint2* __restrict__ ent8, int ebase,
+                                           uint32_t ZB, uint32_t* __restrict__ words, uint32_t* __restrict__ cdst,
+                                           Acc& a) {
     double lag = (double)tv[-1];
 #pragma unroll 1
     for (int g = 0; g < ngroups; ++g) {
@@ -74,150 +128,198 @@ __device__ __forceinline__ void fast_groups(const float* __restrict__ tv, int ng
         const double2 A23 = *reinterpret_cast<const double2*>(Ap + 4 * g + 2);
         const float vv[4] = {v.x, v.y, v.z, v.w};
         const double AA[4] = {A01.x, A01.y, A23.x, A23.y};
-        uint32_t word = 0;
+        uint32_t ad[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const double cw = (double)vv[u];
             const double p = __dadd_rn(AA[u], __dmul_rn(wl, lag));  // Eq. 1, unclamped for the lookup
-            const uint32_t k = plan_lookup4(__dmul_rn(p, invK), ent4, ebase);
-            word |= k << (8 * u);
-            const double2 ln = lines[k];  // (Thr_k * Delta, P_k)
+            const int h = __double2hiint(__dmul_rn(p, invK));
+            const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+            ad[u] = line_addr(h, ent8[idx], ZB);
+            const double2 ln = lds_line(ad[u]);  // (Thr_k * Delta, P_k)
             a.S = __dadd_rn(a.S, ln.x);
             a.E = __dadd_rn(a.E, ln.y);
             a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
             a.Cs = __dadd_rn(a.Cs, cw);
             lag = cw;
         }
+        const uint32_t word = __byte_perm(__byte_perm(ad[0], ad[1], 0x0051u), __byte_perm(ad[2], ad[3], 0x0051u), 0x5410u);
         words[g] = word;
-        if (FIRST_STORE) cdst[g] = word;
+        if (CHASE_H_STG && cdst) cdst[g] = word;
         a.slow |= word;
     }
+}
+
+// Windows [j_begin, nwin) of a lane whose count is not a multiple of 4 (the
+// last chunk only): the same lookup, one window at a time (cold).
+__device__ __noinline__ Acc hot_tail(const float* tv, int j_begin, int nwin, const double* Ap, double wl, double invK,
+                                     const uint2* ent8, int ebase, uint32_t ZB, uint8_t* bytes) {
+    Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
+    double lag = (double)tv[j_begin - 1];
+    for (int jj = j_begin; jj < nwin; ++jj) {
+        const float raw = tv[jj];
+        const double cw = (double)raw;
+        const double p = __dadd_rn(Ap[jj], __dmul_rn(wl, lag));
+        const int h = __double2hiint(__dmul_rn(p, invK));
+        const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+        const uint32_t ad = line_addr(h, ent8[idx], ZB);
+        const uint32_t k = (ad >> 8) & 0xffu;
+        if (k == (uint32_t)kZeroLine) a.slow |= 0x20u;
+        bytes[jj] = (uint8_t)k;
+        const double2 ln = lds_line(ad);
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        a.Cs = __dadd_rn(a.Cs, cw);
+        a.bad |= bad_value(raw) ? 1 : 0;
+        lag = cw;
+    }
+    return a;
+}
+
+// Baseline sum of c over this lane's windows before the baseline's
+// completion window (the chunk that contains it; cold).
+__device__ __noinline__ double partial_cs(const float* tv, int n) {
+    double s = 0.0;
+    for (int jj = 0; jj < n; ++jj) s = __dadd_rn(s, (double)tv[jj]);
+    return s;
 }
 
 __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(const __grid_constant__ SweepParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const FastLayout FL = make_fast_layout(P.T, P.stage_bytes);
-    Ent4* ent4_all = reinterpret_cast<Ent4*>(sm + round16(P.tables_bytes));
-    uint8_t* wbase = sm + round16(P.tables_bytes) + fast_ent4_bytes(P.n_prof) + warp * FL.bytes;
-    const int alen = round16(aext_len(P.T) * 8) / 8;
-    double* A_even = reinterpret_cast<double*>(wbase + FL.aext);
+    const uint32_t sbase = smem_u32(sm);
+    const int head_bytes = reinterpret_cast<const TablesHeader*>(P.tables)->off_pair;
+    const HLayout HL = make_hlayout(P.T, head_bytes, P.n_prof, (int)sbase);
+    if (HL.total > P.smem_total || HL.lines < 0) __trap();  // the host planned for another shared-window base
+    uint2* ent8_all = reinterpret_cast<uint2*>(sm + HL.ent8);
+    int* lph = reinterpret_cast<int*>(sm + HL.lph);
+    uint8_t* wbase = sm + HL.warp_off(warp);
+    const int alen = round16(haext_len(P.T) * 8) / 8;
+    double* A_even = reinterpret_cast<double*>(wbase + HL.aext);
     double* A_odd = A_even + alen;
-    uint8_t* stage0 = wbase + FL.stage;
-    uint8_t* chb = wbase + FL.chb;
-    WarpCtx* ctx = reinterpret_cast<WarpCtx*>(wbase + FL.ctx);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + FL.mbar);
+    uint8_t* stage0 = wbase + HL.stage;
+    uint8_t* chb = wbase + HL.chb;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + HL.mbar);
+    const int T = P.T;
 
-    {   // constant tables -> smem, once per CTA
+    {   // constant tables -> smem, once per CTA: header, phase, profiles; pair heads
         const uint4* src = reinterpret_cast<const uint4*>(P.tables);
-        uint4* dst = reinterpret_cast<uint4*>(sm);
-        for (int q = tid; q < P.tables_bytes / 16; q += kHThreads) dst[q] = src[q];
+        uint4* dst = reinterpret_cast<uint4*>(sm + HL.tables);
+        for (int q = tid; q < head_bytes / 16; q += kHThreads) dst[q] = src[q];
+        const int hw = (int)sizeof(PairHead) / 8;
+        const double* ps = reinterpret_cast<const double*>(P.tables + head_bytes);
+        double* hd = reinterpret_cast<double*>(sm + HL.heads);
+        for (int q = tid; q < P.n_prof * hw; q += kHThreads)
+            hd[q] = ps[(q / hw) * ((int)sizeof(PairTable) / 8) + q % hw];
+        if (tid < 64) lph[tid] = ((tid < 32 ? kHChunk : P.kc_last) * (tid & 31)) % T;  // per-lane phase offsets
     }
     __syncthreads();
-    {   // expand the 8-byte bucket entries of each profile's (single-eta) pair table
-        const TablesHeader* H0 = reinterpret_cast<const TablesHeader*>(sm);
-        const PairTable* pr = reinterpret_cast<const PairTable*>(sm + H0->off_pair);
+    const TablesHeader* H = reinterpret_cast<const TablesHeader*>(sm + HL.tables);
+    const double* phS = reinterpret_cast<const double*>(sm + HL.tables + H->off_phase);
+    const double* phC = phS + T;
+    const ProfileTable* profs = reinterpret_cast<const ProfileTable*>(sm + HL.tables + H->off_prof);
+    // pair heads: only the fields before `ent` are ever read through these pointers
+    const PairHead* heads = reinterpret_cast<const PairHead*>(sm + HL.heads);
+    const PairTable* gpairs = reinterpret_cast<const PairTable*>(P.tables + head_bytes);  // entries: setup only
+    {   // line region: profile p, line k at kLineBase + line_off(p, k) (zero line at k = 32)
+        for (int q = tid; q < P.n_prof * (kMaxK + 1); q += kHThreads) {
+            const int p = q / (kMaxK + 1), k = q % (kMaxK + 1);
+            const double2 v = (k < profs[p].K) ? profs[p].line[k] : make_double2(0.0, 0.0);
+            *reinterpret_cast<double2*>(sm + HL.lines + line_off(p, k)) = v;
+        }
+        // 8-byte bucket entries {T1, lo16(addr below) | lo16(addr above) << 16}
         for (int q = tid; q < P.n_prof * kNB; q += kHThreads) {
-            const uint2 e = pr[q / kNB].ent[q % kNB];
-            Ent4 x;
-            x.T1 = (int)e.x;
-            x.T2 = (int)e.x + (int)(e.y >> 16);
-            x.below = e.y & 0xffu;
-            x.above = (e.y >> 8) & 0xffu;
-            ent4_all[q] = x;
+            const int p = q / kNB;
+            const uint2 e = gpairs[p].ent[q % kNB];
+            const uint32_t below = e.y & 0xffu;
+            const uint32_t above = (e.y >> 16) ? (uint32_t)kZeroLine : ((e.y >> 8) & 0xffu);  // band > 1 unit: slow
+            ent8_all[q] = make_uint2(e.x, (uint32_t)line_off(p, (int)below) | ((uint32_t)line_off(p, (int)above) << 16));
         }
     }
-    if (lane == 0)
+    if (lane == 0) {
         for (int q0 = 0; q0 < kHStages; ++q0) mbar_init(&mbar[q0], 1);
-    if (lane == 0) fence_mbar_init();
+        fence_mbar_init();
+    }
     __syncthreads();
 
-    const TablesHeader* H = reinterpret_cast<const TablesHeader*>(sm);
-    const double* phS = reinterpret_cast<const double*>(sm + H->off_phase);
-    const double* phC = phS + P.T;
-    const ProfileTable* profs = reinterpret_cast<const ProfileTable*>(sm + H->off_prof);
-    const PairTable* pairs = reinterpret_cast<const PairTable*>(sm + H->off_pair);
     const float* traces = reinterpret_cast<const float*>(P.traces);
     const int64_t GW = (int64_t)gridDim.x * kHWarps;
     const int64_t gw = (int64_t)blockIdx.x * kHWarps + warp;
-    const int nc = P.n_chunks, T = P.T;
+    const int nc = P.n_chunks;
+    const bool store_choice = P.choice != nullptr;
+    const int lph_full = lph[lane], lph_last = lph[32 + lane];
 
-    auto issue_next = [&]() {  // lane 0: next (trace, chunk) load; cursor in smem
-        const int64_t pi = ctx->pi;
-        if (pi >= P.n_traces) return;
-        const int pc = ctx->pc;
-        const uint32_t st = ctx->issued;  // stage index (wraps at kStages)
-        const float* psrc = reinterpret_cast<const float*>(ctx->psrc);
-        uint8_t* dst = stage0 + st * P.stage_bytes;
-        const uint32_t bytes = pc == nc - 1 ? P.bytes_last : P.bytes_full;
-        const uint64_t policy = evict_first_policy();
-        if (pc == 0) {
-            mbar_arrive_expect_tx(&mbar[st], bytes + (uint32_t)kRecBytes);
-            bulk_g2s(dst + P.stage_bytes - kRecBytes, P.records + pi * kRecDoubles, kRecBytes, &mbar[st], policy);
-        } else {
-            mbar_arrive_expect_tx(&mbar[st], bytes);
+    // producer cursor (warp-uniform; lane 0 issues)
+    int64_t p_i = gw;
+    int p_c = 0, p_st = 0;
+    const float* p_src = traces + gw * P.ld + P.a0;
+    auto issue_next = [&]() {
+        if (p_i >= P.n_traces) return;
+        if (lane == 0) {
+            const uint64_t policy = evict_first_policy();
+            uint8_t* dst = stage0 + p_st * P.stage_bytes;
+            const uint32_t bytes = p_c == nc - 1 ? P.bytes_last : P.bytes_full;
+            if (p_c == 0) {
+                mbar_arrive_expect_tx(&mbar[p_st], bytes + (uint32_t)kRecBytes);
+                bulk_g2s(dst + P.stage_bytes - kRecBytes, P.records + p_i * kRecDoubles, kRecBytes, &mbar[p_st], policy);
+            } else {
+                mbar_arrive_expect_tx(&mbar[p_st], bytes);
+            }
+            bulk_g2s(dst, p_src, bytes, &mbar[p_st], policy);
         }
-        bulk_g2s(dst, psrc, bytes, &mbar[st], policy);
-        ctx->issued = st + 1 == kHStages ? 0 : st + 1;
-        if (pc + 1 == nc) {
-            ctx->pc = 0;
-            ctx->pi = pi + GW;
-            ctx->psrc = traces + (pi + GW) * P.ld + P.a0;
+        p_st = p_st + 1 == kHStages ? 0 : p_st + 1;
+        if (++p_c == nc) {
+            p_c = 0;
+            p_i += GW;
+            p_src = traces + p_i * P.ld + P.a0;
         } else {
-            ctx->pc = pc + 1;
-            ctx->psrc = psrc + kWarpW;
+            p_src += kHWarpW;
         }
     };
-    if (lane == 0) {
-        ctx->pi = gw;
-        ctx->pc = 0;
-        ctx->issued = 0;
-        ctx->psrc = traces + gw * P.ld + P.a0;
-        ctx->slow = 0ull;
-        for (int q0 = 0; q0 < kHStages; ++q0) issue_next();
-    }
+    for (int q0 = 0; q0 < kHStages; ++q0) issue_next();
 
-    const int j0 = kChunk * lane;
-    const int lane_phase = j0 % T;
     int st = 0;          // stage of the next chunk
     uint32_t par = 0;    // its mbarrier phase parity
+    unsigned n_slow = 0;
 
     for (int64_t i = gw; i < P.n_traces; i += GW) {
-        int status = 0, prof = 0;
-        double wl = 0.0, J = 0.0, smax = 0.0, Kc = 0.0, invK = 0.0;
-        int mb = P.W;
-        double Sl = 0.0, El = 0.0, Cl = 0.0, Cbl = 0.0;
+        int status = 0, c_may = 0, mb = P.W, ebase = 0;
+        double wl = 0.0, J = 0.0, Kc = 0.0, invK = 0.0;
+        double Sl = 0.0, El = 0.0, Cl = 0.0, Cbl = 0.0;  // per-lane running sums
         bool done = false;
         int phase_c = P.phase_start;
-        uint32_t* crow = P.choice ? reinterpret_cast<uint32_t*>(P.choice + i * P.ld_c) + (j0 >> 2) : nullptr;
-        int c_may = 0;   // first chunk in which S can reach J (S <= windows * max_k s_k)
-        for (int c = 0, jb = j0; c < nc; ++c, jb += kWarpW) {
+        uint32_t ZB = 0;
+        const uint2* e8 = ent8_all;
+        const ProfileTable* pf = profs;
+        const PairTable* pt = reinterpret_cast<const PairTable*>(heads);
+        for (int c = 0; c < nc; ++c) {
+            const bool last = c == nc - 1;
             uint8_t* stage = stage0 + st * P.stage_bytes;
+            if (!CHASE_H_STG && store_choice && lane == 0) bulk_wait_read0();  // the previous store has read chb
             mbar_wait(&mbar[st], par);
             if (c == 0) {  // ---- per-trace setup
+                // the record: model (fit_kernel) and this trace's eta-0 scalars (record [10..15], kernels.h)
                 const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
-                prof = P.profile_id ? (int)P.profile_id[i] : 0;
-                if (prof >= P.n_prof) prof = 0;
-                smax = profs[prof].smax;
-                J = P.job ? P.job[i] : 0.0;
+                const int prof = (int)rec[13];
+                pf = profs + prof;
+                pt = reinterpret_cast<const PairTable*>(heads + prof);
+                e8 = ent8_all + prof * kNB;
+                ebase = pt->base;
+                ZB = kLineBase | (uint32_t)line_off(prof, kZeroLine);
+                J = rec[12];
                 status = (int)rec[5];
                 wl = rec[3];
-                const double maxci = P.max_ci_fixed > 0.0 ? P.max_ci_fixed : rec[4];
-                if (status == 0 && !(maxci > 0.0)) status = CHASE_ERR_MAXCI;
-                const int64_t m = (int64_t)rec[8];
-                mb = (J > 0.0 && m >= 1 && m <= P.W) ? (int)(m - 1) : P.W;
-                const PairTable* pt0 = pairs + prof;
-                Kc = __dmul_rn(pt0->kbase, maxci);
-                invK = per_trace_invK(pt0, Kc);
-                if (J > 0.0) {
-                    const double wmin = __ddiv_rn(J, __dmul_rn(smax, 1.000001));  // windows needed, rounded down
-                    c_may = wmin >= (double)P.W ? nc - 1 : max(0, (int)(wmin / kWarpW) - 1);
-                } else {
-                    c_may = nc;  // fixed duration: never completes
-                }
+                if (status == 0 && !(rec[15] > 0.0)) status = CHASE_ERR_MAXCI;
+                const int m = (int)rec[8];
+                mb = (J > 0.0 && m >= 1 && m <= P.W) ? m - 1 : P.W;
+                Kc = rec[10];
+                invK = rec[11];
+                // first chunk in which S can reach J: from a lower bound on the windows needed
+                c_may = J > 0.0 ? (rec[14] >= (double)P.W ? nc - 1 : max(0, (int)(rec[14] * (1.0 / kHWarpW)) - 1)) : nc;
                 if (status == 0) {
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
-                    const int n_a = aext_len(T);
+                    const int n_a = haext_len(T);
                     int ph = lane % T;
                     for (int j = lane; j < n_a; j += 32) {
                         // A(phi) = (c0 + w_sin*S[phi]) + w_cos*C[phi]  (canonical fold of Eq. 1)
@@ -233,53 +335,42 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(con
                 phase_c += P.phase_step;
                 if (phase_c >= T) phase_c -= T;
             }
-            const int nwin = max(0, min(kChunk, P.W - jb));
-            const float* tv = reinterpret_cast<const float*>(stage) + P.off0 + j0;  // tv[jj] = c[s0 + jb + jj]
-            int phi0 = phase_c + lane_phase;
+            const int kc = last ? P.kc_last : kHChunk;
+            const int j0 = kc * lane;
+            const int nwin = max(0, min(kc, (last ? P.W_last : kHWarpW) - j0));
+            const float* tv = reinterpret_cast<const float*>(stage) + P.off0 + j0;  // tv[jj] = c[s0 + c*kHWarpW + j0 + jj]
+            int phi0 = phase_c + (last ? lph_last : lph_full);
             if (phi0 >= T) phi0 -= T;
             const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;
-            const PairTable* pt = pairs + prof;
-            const ProfileTable* pf = profs + prof;
 
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
-                uint32_t* words = reinterpret_cast<uint32_t*>(chb + j0);
-                int ngr = nwin >> 2;
-                if (invK == 0.0) {
-                    ngr = 0;  // Kc outside [2^-900, 2^900]: every window on the canonical rule
-                    acc_merge(a, fused_generic<true, false, float, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line,
-                                                                         chb + j0, nullptr, Kc, pf));
-                    if (a.bad_pad) atomicAdd(&ctx->slow, (unsigned long long)a.bad_pad);
-                } else {
-                    const Ent4* e4 = ent4_all + prof * kNB;
-                    if (crow) fast_groups<true>(tv, ngr, Ap, wl, invK, e4, pt->base, pf->line, words, crow, a);
-                    else fast_groups<false>(tv, ngr, Ap, wl, invK, e4, pt->base, pf->line, words, nullptr, a);
-                    if (4 * ngr < nwin)
-                        acc_merge(a, fused_generic<true, false, float>(tv, 4 * ngr, nwin, Ap, wl, invK, pt,
-                                                                       pf->line, chb + j0, nullptr));
-                    if (a.slow & 0x20202020u) {
-                        const SlowFix fx = fix_slow<float>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0);
-                        a.S = __dadd_rn(a.S, fx.S);
-                        a.E = __dadd_rn(a.E, fx.E);
-                        a.C = __dadd_rn(a.C, fx.C);
-                        atomicAdd(&ctx->slow, (unsigned long long)fx.n);
+                const int ngr = invK == 0.0 ? 0 : nwin >> 2;
+                uint32_t* cdst = (CHASE_H_STG && store_choice)
+                                     ? reinterpret_cast<uint32_t*>(P.choice + i * P.ld_c + c * kHWarpW + j0) : nullptr;
+                hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), cdst, a);
+                if (4 * ngr < nwin) {  // cold: a ragged last chunk, or Kc outside [2^-900, 2^900]
+                    if (invK == 0.0) {
+                        a = fused_generic<true, false, float, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line, chb + j0,
+                                                                    nullptr, Kc, pf);
+                        n_slow += (unsigned)a.bad_pad;
+                    } else {
+                        acc_merge(a, hot_tail(tv, 4 * ngr, nwin, Ap, wl, invK, e8, ebase, ZB, chb + j0));
                     }
                 }
-                // choice words not written from registers (canonical / tail / fixed windows)
-                if (crow && (4 * ngr < nwin || (a.slow & 0x20202020u) || invK == 0.0))
-                    for (int g = (a.slow & 0x20202020u) || invK == 0.0 ? 0 : ngr; 4 * g < nwin; ++g)
-                        crow[g] = words[g];
+                if (a.slow & 0x20202020u) {  // deferred windows: the canonical K-way rule
+                    const SlowFix fx = fix_slow<float>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0);
+                    a.S = __dadd_rn(a.S, fx.S);
+                    a.E = __dadd_rn(a.E, fx.E);
+                    a.C = __dadd_rn(a.C, fx.C);
+                    n_slow += (unsigned)fx.n;
+                }
                 // validation: negatives via vmin, NaN/inf via the sum of c
-                const int flag = (ngr > 0 && (!(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX))) ? 1 : a.bad;
-                if (__any_sync(kFull, flag)) status = CHASE_ERR_DATA;
+                if (__any_sync(kFull, !(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX) || a.bad)) status = CHASE_ERR_DATA;
                 if (status == 0) {
                     // baseline: sum of c over the windows before w*_b
-                    double Cbt = 0.0;
-                    if (jb + nwin <= mb) Cbt = a.Cs;
-                    else if (jb < mb)
-                        for (int jj = 0; jj < mb - jb; ++jj) Cbt = __dadd_rn(Cbt, (double)tv[jj]);
-                    Cbl = __dadd_rn(Cbl, Cbt);
-                    bool completed = false;
+                    const int jb = c * kHWarpW + j0;
+                    Cbl = __dadd_rn(Cbl, jb + nwin <= mb ? a.Cs : (jb < mb ? partial_cs(tv, mb - jb) : 0.0));
                     if (!done && c >= c_may) {
                         const double S_prev = warp_sum(Sl);
                         if (__dadd_rn(S_prev, warp_sum(a.S)) >= J) {
@@ -288,14 +379,14 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(con
                             const double before = __dadd_rn(S_prev, lane == 0 ? 0.0 : ex);
                             const bool full = __dadd_rn(before, a.S) < J;
                             const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
-                            if (who != 0) {
+                            if (who != 0) {  // this chunk completes the job
                                 __syncwarp();
                                 const double Eb = warp_sum(full ? __dadd_rn(El, a.E) : El);
                                 const double Cb = warp_sum(full ? __dadd_rn(Cl, a.C) : Cl);
                                 const int src = __ffs(who) - 1;
-                                const int nw_src = max(0, min(kChunk, P.W - (jb - j0) - kChunk * src));
+                                const int nw_src = max(0, min(kc, (last ? P.W_last : kHWarpW) - kc * src));
                                 const Completion cp = find_completion<float>(
-                                    tv + kChunk * (src - lane), chb + kChunk * src, nw_src,
+                                    tv + kc * (src - lane), chb + kc * src, nw_src,
                                     __shfl_sync(kFull, before, src), J, pf->line, lane);
                                 if (lane == 0) {
                                     double* r = P.raw + i * kRawDoubles;
@@ -303,39 +394,54 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(con
                                     r[1] = __dadd_rn(Cb, cp.Cp);
                                     r[2] = J;
                                     r[3] = cp.f;
-                                    r[4] = (double)((int64_t)P.L + (jb - j0) + kChunk * src + cp.w);
+                                    r[4] = (double)((int64_t)P.L + c * kHWarpW + kc * src + cp.w);
                                     r[5] = cp.Pk;
                                     r[6] = cp.cw;
                                     r[7] = 1.0;
                                 }
-                                done = completed = true;
+                                done = true;
                             }
                             // else: no window reached J in the scan order (non-dyadic rounding): carry on
                         }
                     }
-                    if (!done && !completed) {
+                    if (!done) {
                         Sl = __dadd_rn(Sl, a.S);
                         El = __dadd_rn(El, a.E);
                         Cl = __dadd_rn(Cl, a.C);
+                    }
+                    if (CHASE_H_STG && store_choice && (4 * ngr < nwin || (a.slow & 0x20202020u))) {
+                        // words not stored from registers (ragged tail, canonical or corrected windows)
+                        uint32_t* cd = reinterpret_cast<uint32_t*>(P.choice + i * P.ld_c + c * kHWarpW + j0);
+                        const uint32_t* wd = reinterpret_cast<const uint32_t*>(chb + j0);
+                        for (int g = (a.slow & 0x20202020u) || invK == 0.0 ? 0 : ngr; 4 * g < nwin; ++g) cd[g] = wd[g];
+                    }
+                    if (!CHASE_H_STG && store_choice) {  // the chunk's choices: one TMA bulk store from the staging buffer
+                        __syncwarp();
+                        if (lane == 0) {
+                            fence_proxy_async();
+                            bulk_s2g(P.choice + i * P.ld_c + c * kHWarpW, chb,
+                                     (uint32_t)(last ? (P.W_last + 15) & ~15 : kHWarpW));
+                            bulk_commit();
+                        }
                     }
                 }
             } else if (status == CHASE_ERR_MAXCI || status == CHASE_ERR_FIT) {
                 // S:29 precedence: a bad value anywhere makes the trace status 4
                 if (__any_sync(kFull, chunk_has_bad(tv, nwin))) status = CHASE_ERR_DATA;
             }
-            if (crow) crow += kWarpW / 4;
 
-            if (c == nc - 1) {  // ---- end of trace
+            if (last) {  // ---- end of trace: one transposed reduction of the four running sums
                 if (status == 0) {
-                    const double Cb = warp_sum(Cbl);
-                    const double Sx = warp_sum(Sl), Ex = warp_sum(El), Cx = warp_sum(Cl);
+                    const double t4 = warp_sum4(Sl, El, Cl, Cbl, lane);  // totals in lanes 0, 8, 16, 24
+                    const double Ex = __shfl_sync(kFull, t4, 8), Cx = __shfl_sync(kFull, t4, 16);
+                    const double Cb = __shfl_sync(kFull, t4, 24);
                     if (lane == 0) {
                         P.records[i * kRecDoubles + 9] = Cb;
                         if (!done) {
                             double* r = P.raw + i * kRawDoubles;
                             r[0] = Ex;
                             r[1] = Cx;
-                            r[2] = Sx;
+                            r[2] = t4;
                             r[3] = 0.0;
                             r[4] = -1.0;
                             r[5] = r[6] = r[7] = 0.0;
@@ -353,14 +459,16 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(con
                     }
                 }
             }
-            __syncwarp();  // every lane is done with stage `st` and the choice buffer
-            if (lane == 0) issue_next();
+            __syncwarp();  // every lane is done with stage `st`
+            issue_next();
             if (++st == kHStages) {
                 st = 0;
                 par ^= 1u;
             }
         }
     }
-    if (lane == 0 && ctx->slow)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_slow_windows), ctx->slow);
+    if (store_choice && lane == 0) bulk_wait_read0();  // staging buffers stay valid until read
+    n_slow = __reduce_add_sync(kFull, n_slow);
+    if (lane == 0 && n_slow)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_slow_windows), (unsigned long long)n_slow);
 }

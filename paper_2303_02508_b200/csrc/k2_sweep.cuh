@@ -262,7 +262,6 @@ __device__ __noinline__ Completion find_completion(const E* tv_src, const uint8_
 template <int MODE, typename E, bool AL, bool MULTI, bool FIN = false>
 __global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
-    constexpr int VEC = 16 / (int)sizeof(E);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const WarpLayout WL = make_warp_layout(P.T, P.stage_bytes, P.n_eta);
     uint8_t* wbase = sm + round16(P.tables_bytes) + warp * WL.bytes;

@@ -127,8 +127,35 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
                        : launch_sweep_t<MODE_FUSED, float, false, false, true>(p, s);
     }
     if (mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !getenv("CHASE_FORCE_GENERAL")) {
-        // the headline shape: lean specialised kernel (k2_fast.cuh)
-        const int smem = fast_smem_total(p.tables_bytes, p.T, p.stage_bytes, p.n_prof);
+        // the headline shape: lean specialised kernel (k2_headline.cuh), with its own chunk geometry
+        SweepParams q = p;
+        {
+            const int64_t L = p.L, W = p.W, vec = 4;
+            q.n_chunks = (int32_t)((W + kHWarpW - 1) / kHWarpW);
+            q.a0 = (int32_t)(L - vec);
+            q.off0 = (int32_t)vec;
+            q.W_last = (int32_t)(W - (int64_t)(q.n_chunks - 1) * kHWarpW);
+            q.bytes_full = (uint32_t)((kHWarpW + vec) * 4);
+            int64_t last_end = (L + (int64_t)(q.n_chunks - 1) * kHWarpW + q.W_last + vec - 1) / vec * vec;
+            if (last_end > p.ld) last_end = p.ld;
+            q.bytes_last = (uint32_t)((last_end - (q.a0 + (int64_t)(q.n_chunks - 1) * kHWarpW)) * 4);
+            q.phase_step = kHWarpW % p.T;
+            q.stage_bytes = hstage_bytes();
+            // last chunk: the fewest windows per lane (4 mod 8: conflict-free LDS.128) covering W_last
+            int k = (q.W_last + 31) / 32;
+            k = k < 4 ? 4 : k;
+            while (k % 8 != 4) ++k;
+            q.kc_last = k > kHChunk ? kHChunk : k;
+        }
+        // blob bytes before the pair tables (header, phase, profiles): see make_hlayout
+        const int head_bytes = (int)sizeof(TablesHeader) + ((2 * p.T * 8) + 15) / 16 * 16 +
+                               p.n_prof * (int)sizeof(ProfileTable);
+        int smem = 0;  // the layout depends on the shared-window base: plan for the worst candidate
+        for (int base = 0; base <= 8192; base += 16) {
+            const int t = make_hlayout(p.T, head_bytes, p.n_prof, base).total;
+            smem = t > smem ? t : smem;
+        }
+        q.smem_total = smem;
         cudaError_t err = cudaFuncSetAttribute(sweep_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
         int per_sm = 0;
@@ -136,9 +163,9 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
         if (err != cudaSuccess) return err;
         if (per_sm < 1) return cudaErrorInvalidConfiguration;
         int64_t grid = (int64_t)num_sms() * per_sm;
-        const int64_t need = (p.n_traces + kHWarps - 1) / kHWarps;
+        const int64_t need = (p.n_traces + kHWarps - 1) / kHWarps;  // one trace per warp at least
         if (grid > need) grid = need;
-        sweep_fast_kernel<<<(unsigned)grid, kHThreads, smem, s>>>(p);
+        sweep_fast_kernel<<<(unsigned)grid, kHThreads, smem, s>>>(q);
         ++g_launches;
         return cudaGetLastError();
     }

@@ -23,6 +23,8 @@ constexpr int kFinThreads = 256;           // finalize CTA size
 //  [0] c0 [1] w_sin [2] w_cos [3] w_lag [4] max_ci(history) [5] status
 //  [6] ridge [7] kind [8] m_base (baseline completion count, 0: J <= 0)
 //  [9] Cb (baseline sum of c over the windows before w*_b; sweep writes)
+//  [10..15] eta-0 scalars for the headline sweep: Kc, 1/Kc, J, profile,
+//           windows-to-completion lower bound, resolved MaxCI
 // Raw per (eta, trace) (sweep writes, finalize reads):
 //  [0] E [1] C [2] S [3] f [4] w* [5] P_k* [6] c[w*] [7] done
 enum SweepMode { MODE_FUSED = 0, MODE_PREDICT = 1, MODE_REPLAY = 2 };
@@ -54,6 +56,8 @@ struct SweepParams {
     int64_t* bad_list;            // [n]: traces with status 4..7 (slot = old n_bad)
     const double* fc_in;          // rolling refit: forecasts [n][ld_fin] (null: fit-once fold)
     int64_t ld_fin;
+    int32_t kc_last;              // headline kernel: windows per lane in the last chunk (4 mod 8)
+    int32_t smem_total;           // headline kernel: dynamic shared memory planned by the host
 };
 
 struct FitParams {
@@ -68,6 +72,9 @@ struct FitParams {
     double* records;              // [n][16]
     double* models_out;           // optional user copy [n][8]
     double* max_ci_out;           // optional [n]
+    int32_t n_eta;                // > 0: also the single-eta sweep's per-trace scalars (record [10..15])
+    int32_t reserved;
+    double max_ci_fixed;          // > 0: fixed MaxCI
 };
 
 struct FinalizeParams {
