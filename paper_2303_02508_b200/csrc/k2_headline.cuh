@@ -21,13 +21,16 @@
 #define CHASE_H_WARPS 12
 #endif
 #ifndef CHASE_H_STAGES
-#define CHASE_H_STAGES 2
+#define CHASE_H_STAGES 1
 #endif
 #ifndef CHASE_H_MINB
 #define CHASE_H_MINB 1
 #endif
 #ifndef CHASE_H_CHUNK
-#define CHASE_H_CHUNK 36
+#define CHASE_H_CHUNK 84
+#endif
+#ifndef CHASE_H_PREFETCH
+#define CHASE_H_PREFETCH 1  // load group g+1's trace values and A terms during group g
 #endif
 #ifndef CHASE_H_STG
 #define CHASE_H_STG 0   // 1: choice words stored from registers (per group) instead of a TMA store per chunk
@@ -115,17 +118,28 @@ __device__ __forceinline__ uint32_t line_addr(int h, uint2 e, uint32_t ZB) {
 
 // One lane's full groups of 4 windows.  Words (4 choice bytes) go to the
 // warp's staging buffer; `a.slow` collects them for the deferred-window test.
+// The trace values and A terms of group g+1 are loaded while group g computes
+// (the reads past the last group stay inside the stage / A-table buffers).
 __device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngroups, const double* __restrict__ Ap,
                                            double wl, double invK, const uint2* __restrict__ ent8, int ebase,
                                            uint32_t ZB, uint32_t* __restrict__ words, uint32_t* __restrict__ cdst,
                                            Acc& a) {
     double lag = (double)tv[-1];
+    float4 v = *reinterpret_cast<const float4*>(tv);
+    double2 A01 = *reinterpret_cast<const double2*>(Ap);
+    double2 A23 = *reinterpret_cast<const double2*>(Ap + 2);
 #pragma unroll 1
     for (int g = 0; g < ngroups; ++g) {
-        const float4 v = *reinterpret_cast<const float4*>(tv + 4 * g);
+#if CHASE_H_PREFETCH
+        const float4 vn = *reinterpret_cast<const float4*>(tv + 4 * g + 4);
+        const double2 A01n = *reinterpret_cast<const double2*>(Ap + 4 * g + 4);
+        const double2 A23n = *reinterpret_cast<const double2*>(Ap + 4 * g + 6);
+#else
+        v = *reinterpret_cast<const float4*>(tv + 4 * g);
+        A01 = *reinterpret_cast<const double2*>(Ap + 4 * g);
+        A23 = *reinterpret_cast<const double2*>(Ap + 4 * g + 2);
+#endif
         a.vmin = fminf(fminf(fminf(a.vmin, v.x), v.y), fminf(v.z, v.w));  // FMNMX3 x2
-        const double2 A01 = *reinterpret_cast<const double2*>(Ap + 4 * g);
-        const double2 A23 = *reinterpret_cast<const double2*>(Ap + 4 * g + 2);
         const float vv[4] = {v.x, v.y, v.z, v.w};
         const double AA[4] = {A01.x, A01.y, A23.x, A23.y};
         uint32_t ad[4];
@@ -147,6 +161,11 @@ __device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngr
         words[g] = word;
         if (CHASE_H_STG && cdst) cdst[g] = word;
         a.slow |= word;
+#if CHASE_H_PREFETCH
+        v = vn;
+        A01 = A01n;
+        A23 = A23n;
+#endif
     }
 }
 
@@ -185,7 +204,12 @@ __device__ __noinline__ double partial_cs(const float* tv, int n) {
     return s;
 }
 
-__global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(const __grid_constant__ SweepParams P) {
+#ifdef CHASE_H_MAXNREG
+__global__ void __maxnreg__(CHASE_H_MAXNREG) sweep_fast_kernel(
+#else
+__global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
+#endif
+    const __grid_constant__ SweepParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t sbase = smem_u32(sm);
