@@ -18,7 +18,7 @@
 // warp in shared memory and written with one TMA bulk store per chunk.
 
 #ifndef CHASE_H_WARPS
-#define CHASE_H_WARPS 12
+#define CHASE_H_WARPS 16
 #endif
 #ifndef CHASE_H_STAGES
 #define CHASE_H_STAGES 1
@@ -27,7 +27,7 @@
 #define CHASE_H_MINB 1
 #endif
 #ifndef CHASE_H_CHUNK
-#define CHASE_H_CHUNK 84
+#define CHASE_H_CHUNK 60
 #endif
 #ifndef CHASE_H_PREFETCH
 #define CHASE_H_PREFETCH 1  // load group g+1's trace values and A terms during group g

@@ -14,4 +14,5 @@ nvcc $ARCH -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v -Xcompiler -fPIC -I $
 nvcc $ARCH -O2 -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -I $ROOT/include -I $C "$@" -c $C/chase_api.cpp -o $O/api.o
 nvcc $ARCH -O2 -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -I $ROOT/include -I $C -c $C/envelope.cpp -o $O/env.o
 nvcc $ARCH -shared -cudart static -o $ROOT/build/variants/libchase_$name.so $O/kernels.o $O/api.o $O/env.o
+rm -rf "$O"
 echo built $ROOT/build/variants/libchase_$name.so
