@@ -20,9 +20,7 @@
 #ifndef CHASE_H_WARPS
 #define CHASE_H_WARPS 16
 #endif
-#ifndef CHASE_H_STAGES
-#define CHASE_H_STAGES 1
-#endif
+#define CHASE_H_STAGES 1  // one stage per warp (see the chunk loop)
 #ifndef CHASE_H_MINB
 #define CHASE_H_MINB 1
 #endif
@@ -262,7 +260,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         }
     }
     if (lane == 0) {
-        for (int q0 = 0; q0 < kHStages; ++q0) mbar_init(&mbar[q0], 1);
+        mbar_init(mbar, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -274,37 +272,23 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
     const bool store_choice = P.choice != nullptr;
     const int lph_full = lph[lane], lph_last = lph[32 + lane];
 
-    // producer cursor (warp-uniform; lane 0 issues)
-    int64_t p_i = gw;
-    int p_c = 0, p_st = 0;
-    const float* p_src = traces + gw * P.ld + P.a0;
-    auto issue_next = [&]() {
-        if (p_i >= P.n_traces) return;
-        if (lane == 0) {
-            const uint64_t policy = evict_first_policy();
-            uint8_t* dst = stage0 + p_st * P.stage_bytes;
-            const uint32_t bytes = p_c == nc - 1 ? P.bytes_last : P.bytes_full;
-            if (p_c == 0) {
-                mbar_arrive_expect_tx(&mbar[p_st], bytes + (uint32_t)kRecBytes);
-                bulk_g2s(dst + P.stage_bytes - kRecBytes, P.records + p_i * kRecDoubles, kRecBytes, &mbar[p_st], policy);
-            } else {
-                mbar_arrive_expect_tx(&mbar[p_st], bytes);
-            }
-            bulk_g2s(dst, p_src, bytes, &mbar[p_st], policy);
-        }
-        p_st = p_st + 1 == kHStages ? 0 : p_st + 1;
-        if (++p_c == nc) {
-            p_c = 0;
-            p_i += GW;
-            p_src = traces + p_i * P.ld + P.a0;
+    // One stage per warp: the load of chunk c+1 (or of the next trace's first
+    // chunk, with its record) is issued once chunk c is consumed (lane 0).
+    auto issue = [&](int64_t ti, int tc) {
+        if (ti >= P.n_traces || lane != 0) return;
+        const uint64_t policy = evict_first_policy();
+        const uint32_t bytes = tc == nc - 1 ? P.bytes_last : P.bytes_full;
+        if (tc == 0) {
+            mbar_arrive_expect_tx(mbar, bytes + (uint32_t)kRecBytes);
+            bulk_g2s(stage0 + P.stage_bytes - kRecBytes, P.records + ti * kRecDoubles, kRecBytes, mbar, policy);
         } else {
-            p_src += kHWarpW;
+            mbar_arrive_expect_tx(mbar, bytes);
         }
+        bulk_g2s(stage0, traces + ti * P.ld + P.a0 + (int64_t)tc * kHWarpW, bytes, mbar, policy);
     };
-    for (int q0 = 0; q0 < kHStages; ++q0) issue_next();
+    issue(gw, 0);
 
-    int st = 0;          // stage of the next chunk
-    uint32_t par = 0;    // its mbarrier phase parity
+    uint32_t par = 0;    // mbarrier phase parity of the next chunk
     unsigned n_slow = 0;
 
     for (int64_t i = gw; i < P.n_traces; i += GW) {
@@ -319,9 +303,9 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         const PairTable* pt = reinterpret_cast<const PairTable*>(heads);
         for (int c = 0; c < nc; ++c) {
             const bool last = c == nc - 1;
-            uint8_t* stage = stage0 + st * P.stage_bytes;
+            uint8_t* stage = stage0;
             if (!CHASE_H_STG && store_choice && lane == 0) bulk_wait_read0();  // the previous store has read chb
-            mbar_wait(&mbar[st], par);
+            mbar_wait(mbar, par);
             if (c == 0) {  // ---- per-trace setup
                 // the record: model (fit_kernel) and this trace's eta-0 scalars (record [10..15], kernels.h)
                 const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
@@ -367,6 +351,10 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             if (phi0 >= T) phi0 -= T;
             const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;
 
+            // The next chunk's load can be issued as soon as the hot loop is done with the
+            // stage, unless this chunk still reads it afterwards (the baseline's or the job's
+            // completion window may lie in it, or the trace is being validated only)
+            const bool early = status == 0 && !(c * kHWarpW <= mb && mb < (c + 1) * kHWarpW) && (done || c < c_may);
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
                 const int ngr = invK == 0.0 ? 0 : nwin >> 2;
@@ -388,6 +376,11 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     a.E = __dadd_rn(a.E, fx.E);
                     a.C = __dadd_rn(a.C, fx.C);
                     n_slow += (unsigned)fx.n;
+                }
+                if (early) {
+                    __syncwarp();  // every lane is done with the stage
+                    if (last) issue(i + GW, 0);
+                    else issue(i, c + 1);
                 }
                 // validation: negatives via vmin, NaN/inf via the sum of c
                 if (__any_sync(kFull, !(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX) || a.bad)) status = CHASE_ERR_DATA;
@@ -483,12 +476,12 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     }
                 }
             }
-            __syncwarp();  // every lane is done with stage `st`
-            issue_next();
-            if (++st == kHStages) {
-                st = 0;
-                par ^= 1u;
+            if (!early) {
+                __syncwarp();  // every lane is done with the stage
+                if (last) issue(i + GW, 0);
+                else issue(i, c + 1);
             }
+            par ^= 1u;
         }
     }
     if (store_choice && lane == 0) bulk_wait_read0();  // staging buffers stay valid until read
