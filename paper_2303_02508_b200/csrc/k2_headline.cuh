@@ -324,7 +324,9 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 Kc = rec[10];
                 invK = rec[11];
                 // first chunk in which S can reach J: from a lower bound on the windows needed
-                c_may = J > 0.0 ? (rec[14] >= (double)P.W ? nc - 1 : max(0, (int)(rec[14] * (1.0 / kHWarpW)) - 1)) : nc;
+                // the completion window w* (from s0) has (w*+1)*max_k s_k >= J, so w* >= rec[14] - 1
+                // (rec[14] = J/(1.000001 max_k s_k) absorbs the roundings): its chunk is at least c_may
+                c_may = J > 0.0 ? (rec[14] >= (double)P.W ? nc - 1 : (int)(fmax(rec[14] - 1.0, 0.0) * (1.0 / kHWarpW))) : nc;
                 if (status == 0) {
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
                     const int n_a = haext_len(T);
@@ -351,10 +353,10 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             if (phi0 >= T) phi0 -= T;
             const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;
 
-            // The next chunk's load can be issued as soon as the hot loop is done with the
-            // stage, unless this chunk still reads it afterwards (the baseline's or the job's
-            // completion window may lie in it, or the trace is being validated only)
-            const bool early = status == 0 && !(c * kHWarpW <= mb && mb < (c + 1) * kHWarpW) && (done || c < c_may);
+            // The next chunk's load is issued as soon as nothing reads the stage any more:
+            // right after the hot loop and the two sums that may still read it (the
+            // baseline's completion chunk), except in the chunk where the job completes.
+            bool issued = false;
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
                 const int ngr = invK == 0.0 ? 0 : nwin >> 2;
@@ -377,49 +379,56 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     a.C = __dadd_rn(a.C, fx.C);
                     n_slow += (unsigned)fx.n;
                 }
-                if (early) {
+                // validation (S:29): negatives via vmin, NaN/inf via the sum of c
+                const bool bad = __any_sync(kFull, !(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX) || a.bad);
+                // baseline: sum of c over the windows before w*_b
+                const int jb = c * kHWarpW + j0;
+                const double Cbt = jb + nwin <= mb ? a.Cs : (jb < mb ? partial_cs(tv, mb - jb) : 0.0);
+                // does the job complete in this chunk? (warp totals of the samples done)
+                double S_prev = 0.0;
+                bool completes = false;
+                if (!bad && !done && c >= c_may) {
+                    S_prev = warp_sum(Sl);
+                    completes = __dadd_rn(S_prev, warp_sum(a.S)) >= J;
+                }
+                if (!completes) {
                     __syncwarp();  // every lane is done with the stage
                     if (last) issue(i + GW, 0);
                     else issue(i, c + 1);
+                    issued = true;
                 }
-                // validation (S:29): negatives via vmin, NaN/inf via the sum of c
-                if (__any_sync(kFull, !(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX) || a.bad)) status = CHASE_ERR_DATA;
+                if (bad) status = CHASE_ERR_DATA;
                 if (status == 0) {
-                    // baseline: sum of c over the windows before w*_b
-                    const int jb = c * kHWarpW + j0;
-                    Cbl = __dadd_rn(Cbl, jb + nwin <= mb ? a.Cs : (jb < mb ? partial_cs(tv, mb - jb) : 0.0));
-                    if (!done && c >= c_may) {
-                        const double S_prev = warp_sum(Sl);
-                        if (__dadd_rn(S_prev, warp_sum(a.S)) >= J) {
-                            const double incl = warp_incl_scan(a.S, lane);
-                            const double ex = __shfl_up_sync(kFull, incl, 1);
-                            const double before = __dadd_rn(S_prev, lane == 0 ? 0.0 : ex);
-                            const bool full = __dadd_rn(before, a.S) < J;
-                            const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
-                            if (who != 0) {  // this chunk completes the job
-                                __syncwarp();
-                                const double Eb = warp_sum(full ? __dadd_rn(El, a.E) : El);
-                                const double Cb = warp_sum(full ? __dadd_rn(Cl, a.C) : Cl);
-                                const int src = __ffs(who) - 1;
-                                const int nw_src = max(0, min(kc, (last ? P.W_last : kHWarpW) - kc * src));
-                                const Completion cp = find_completion<float>(
-                                    tv + kc * (src - lane), chb + kc * src, nw_src,
-                                    __shfl_sync(kFull, before, src), J, pf->line, lane);
-                                if (lane == 0) {
-                                    double* r = P.raw + i * kRawDoubles;
-                                    r[0] = __dadd_rn(Eb, cp.Ep);
-                                    r[1] = __dadd_rn(Cb, cp.Cp);
-                                    r[2] = J;
-                                    r[3] = cp.f;
-                                    r[4] = (double)((int64_t)P.L + c * kHWarpW + kc * src + cp.w);
-                                    r[5] = cp.Pk;
-                                    r[6] = cp.cw;
-                                    r[7] = 1.0;
-                                }
-                                done = true;
+                    Cbl = __dadd_rn(Cbl, Cbt);
+                    if (completes) {
+                        const double incl = warp_incl_scan(a.S, lane);
+                        const double ex = __shfl_up_sync(kFull, incl, 1);
+                        const double before = __dadd_rn(S_prev, lane == 0 ? 0.0 : ex);
+                        const bool full = __dadd_rn(before, a.S) < J;
+                        const unsigned who = __ballot_sync(kFull, !full && before < J && nwin > 0);
+                        if (who != 0) {  // this chunk completes the job
+                            __syncwarp();
+                            const double Eb = warp_sum(full ? __dadd_rn(El, a.E) : El);
+                            const double Cb = warp_sum(full ? __dadd_rn(Cl, a.C) : Cl);
+                            const int src = __ffs(who) - 1;
+                            const int nw_src = max(0, min(kc, (last ? P.W_last : kHWarpW) - kc * src));
+                            const Completion cp = find_completion<float>(
+                                tv + kc * (src - lane), chb + kc * src, nw_src,
+                                __shfl_sync(kFull, before, src), J, pf->line, lane);
+                            if (lane == 0) {
+                                double* r = P.raw + i * kRawDoubles;
+                                r[0] = __dadd_rn(Eb, cp.Ep);
+                                r[1] = __dadd_rn(Cb, cp.Cp);
+                                r[2] = J;
+                                r[3] = cp.f;
+                                r[4] = (double)((int64_t)P.L + c * kHWarpW + kc * src + cp.w);
+                                r[5] = cp.Pk;
+                                r[6] = cp.cw;
+                                r[7] = 1.0;
                             }
-                            // else: no window reached J in the scan order (non-dyadic rounding): carry on
+                            done = true;
                         }
+                        // else: no window reached J in the scan order (non-dyadic rounding): carry on
                     }
                     if (!done) {
                         Sl = __dadd_rn(Sl, a.S);
@@ -476,7 +485,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     }
                 }
             }
-            if (!early) {
+            if (!issued) {
                 __syncwarp();  // every lane is done with the stage
                 if (last) issue(i + GW, 0);
                 else issue(i, c + 1);
