@@ -199,6 +199,133 @@ __device__ void fit_one(const E* h, int L, int T, int phi0, const double* S, con
     rec[7] = (double)kind;
 }
 
+// Phase columns of a fit whose first history point has phase rho (rows
+// i = 1..n, phase (rho + i) mod T): their means, population sigmas, z-scores
+// and the phase-only Gram entries G00, G10, G11, each computed with
+// oracle_fit's own sequential operations.  Every accumulator of the fit is a
+// separate sequential sum over the rows, so taking these from a table changes
+// no rounding.  Record layout (phase_stride(L) doubles):
+//   [mu0, mu1, sg0, sg1, G00, G10, G11, ok] z0[1..n] z1[1..n]
+__host__ __device__ inline int phase_stride(int L) { return 8 + 2 * (L - 1); }
+
+__device__ void phase_record(const double* S, const double* Cc, int T, int L, int rho, double* out) {
+    const int n = L - 1;
+    const double dn = (double)n;
+    double s0 = 0.0, s1 = 0.0;
+    int ph = (rho + 1) % T;
+    for (int i = 1; i <= n; ++i) {
+        s0 = __dadd_rn(s0, S[ph]);
+        s1 = __dadd_rn(s1, Cc[ph]);
+        ph = ph + 1 == T ? 0 : ph + 1;
+    }
+    const double mu0 = __ddiv_rn(s0, dn), mu1 = __ddiv_rn(s1, dn);
+    double q0 = 0.0, q1 = 0.0;
+    ph = (rho + 1) % T;
+    for (int i = 1; i <= n; ++i) {
+        const double d0 = __dsub_rn(S[ph], mu0), d1 = __dsub_rn(Cc[ph], mu1);
+        q0 = __dadd_rn(q0, __dmul_rn(d0, d0));
+        q1 = __dadd_rn(q1, __dmul_rn(d1, d1));
+        ph = ph + 1 == T ? 0 : ph + 1;
+    }
+    const double sg0 = __dsqrt_rn(__ddiv_rn(q0, dn)), sg1 = __dsqrt_rn(__ddiv_rn(q1, dn));
+    const bool ok = sg0 > 0.0 && sg1 > 0.0;
+    double G00 = 0.0, G10 = 0.0, G11 = 0.0;
+    double* z0 = out + 8;
+    double* z1 = z0 + n;
+    ph = (rho + 1) % T;
+    for (int i = 1; i <= n; ++i) {
+        const double a = ok ? __ddiv_rn(__dsub_rn(S[ph], mu0), sg0) : 0.0;
+        const double b = ok ? __ddiv_rn(__dsub_rn(Cc[ph], mu1), sg1) : 0.0;
+        z0[i - 1] = a;
+        z1[i - 1] = b;
+        G00 = __dadd_rn(G00, __dmul_rn(a, a));
+        G10 = __dadd_rn(G10, __dmul_rn(b, a));
+        G11 = __dadd_rn(G11, __dmul_rn(b, b));
+        ph = ph + 1 == T ? 0 : ph + 1;
+    }
+    out[0] = mu0;
+    out[1] = mu1;
+    out[2] = sg0;
+    out[3] = sg1;
+    out[4] = G00;
+    out[5] = G10;
+    out[6] = G11;
+    out[7] = ok ? 1.0 : 0.0;
+}
+
+// fit_one with the phase columns from a phase_record `pt` (same results,
+// bit for bit, with half the divides): rec[0..7] as fit_one.
+template <typename E>
+__device__ void fit_phase(const E* h, int L, int T, int rho, const double* pt, const double* S, const double* Cc,
+                          double ridge, double tol_rel, double* rec) {
+    const int n = L - 1;
+    const double dn = (double)n;
+    double maxci = (double)h[0];
+    int bad = 0;
+    for (int t = 0; t < L; ++t) {
+        const E v = h[t];
+        bad |= bad_value(v);
+        if ((double)v > maxci) maxci = (double)v;
+    }
+    double c0 = 0.0, w[3] = {0.0, 0.0, 0.0};
+    int status = bad ? CHASE_ERR_DATA : 0, ridge_fired = 0, kind = 0;
+    bool constant = true;
+    for (int i = 2; i <= n; ++i)
+        if ((double)h[i] != (double)h[1]) { constant = false; break; }
+    if (status == 0 && constant) {  // F2: intercept-only model
+        kind = 1;
+        c0 = (double)h[1];
+    } else if (status == 0) {
+        double sl = 0.0, sy = 0.0;
+        for (int i = 1; i <= n; ++i) {
+            sl = __dadd_rn(sl, (double)h[i - 1]);
+            sy = __dadd_rn(sy, (double)h[i]);
+        }
+        const double mu2 = __ddiv_rn(sl, dn), mu3 = __ddiv_rn(sy, dn);
+        double ql = 0.0, qy = 0.0;
+        for (int i = 1; i <= n; ++i) {
+            const double d2 = __dsub_rn((double)h[i - 1], mu2), d3 = __dsub_rn((double)h[i], mu3);
+            ql = __dadd_rn(ql, __dmul_rn(d2, d2));
+            qy = __dadd_rn(qy, __dmul_rn(d3, d3));
+        }
+        const double sg2 = __dsqrt_rn(__ddiv_rn(ql, dn)), sg3 = __dsqrt_rn(__ddiv_rn(qy, dn));
+        if (!(sg3 > 0.0)) {  // numerically constant target
+            kind = 1;
+            c0 = mu3;
+        } else if (pt[7] != 0.0 && sg2 > 0.0) {
+            const double mu[4] = {pt[0], pt[1], mu2, mu3};
+            const double sg[4] = {pt[2], pt[3], sg2, sg3};
+            const double* z0 = pt + 8;
+            const double* z1 = z0 + n;
+            double h0 = 0.0, h1 = 0.0, h2 = 0.0, G20 = 0.0, G21 = 0.0, G22 = 0.0;
+            for (int i = 1; i <= n; ++i) {
+                const double a = z0[i - 1], b = z1[i - 1];
+                const double z2 = __ddiv_rn(__dsub_rn((double)h[i - 1], mu2), sg2);
+                const double u = __ddiv_rn(__dsub_rn((double)h[i], mu3), sg3);
+                h0 = __dadd_rn(h0, __dmul_rn(a, u));
+                h1 = __dadd_rn(h1, __dmul_rn(b, u));
+                G20 = __dadd_rn(G20, __dmul_rn(z2, a));
+                G21 = __dadd_rn(G21, __dmul_rn(z2, b));
+                G22 = __dadd_rn(G22, __dmul_rn(z2, z2));
+                h2 = __dadd_rn(h2, __dmul_rn(z2, u));
+            }
+            chol3_solve(pt[4], pt[5], pt[6], G20, G21, G22, h0, h1, h2, ridge, tol_rel, dn, mu, sg, c0, w, status,
+                        ridge_fired);
+        } else {  // a zero-variance column: the general path (cold)
+            fit_one<E>(h, L, T, rho, S, Cc, ridge, tol_rel, rec);
+            return;
+        }
+    }
+    rec[0] = c0;
+    rec[1] = w[0];
+    rec[2] = w[1];
+    rec[3] = w[2];
+    rec[4] = maxci;
+    rec[5] = (double)status;
+    rec[6] = (double)ridge_fired;
+    rec[7] = (double)kind;
+}
+
 // Fit kernel: stage the CTA's 128 histories (L <= 64) into smem with coalesced
 // loads (odd row stride), one lane per trace runs the canonical fit; also the
 // max-power baseline's completion count m: the first m with
@@ -208,6 +335,7 @@ __global__ void __launch_bounds__(128) fit_kernel(const __grid_constant__ FitPar
     extern __shared__ __align__(16) uint8_t fsm[];
     E* hs = reinterpret_cast<E*>(fsm);
     double* tab = reinterpret_cast<double*>(fsm + round16(128 * 65 * (int)sizeof(E)));
+    double* prec = tab + 2 * p.T;  // the phase record of phase0 (staged path: L <= 64)
     const TablesHeader* H = reinterpret_cast<const TablesHeader*>(p.tables);
     const int L = p.L, T = p.T;
     const int64_t first = (int64_t)blockIdx.x * 128;
@@ -226,6 +354,8 @@ __global__ void __launch_bounds__(128) fit_kernel(const __grid_constant__ FitPar
         }
     }
     __syncthreads();
+    if (staged && threadIdx.x == 0) phase_record(tab, tab + T, T, L, p.phase0 % T, prec);
+    __syncthreads();
     const int64_t i = first + threadIdx.x;
     if (i >= p.n_traces) return;
     double rec[kRecDoubles];
@@ -233,7 +363,8 @@ __global__ void __launch_bounds__(128) fit_kernel(const __grid_constant__ FitPar
     for (int q = 0; q < kRecDoubles; ++q) rec[q] = 0.0;
     if (!p.baseline_only) {
         const E* h = staged ? hs + threadIdx.x * (L | 1) : tr + i * p.ld;
-        fit_one<E>(h, L, T, p.phase0 % T, tab, tab + T, p.ridge, p.tol, rec);
+        if (staged) fit_phase<E>(h, L, T, p.phase0 % T, prec, tab, tab + T, p.ridge, p.tol, rec);
+        else fit_one<E>(h, L, T, p.phase0 % T, tab, tab + T, p.ridge, p.tol, rec);
     }
     const double J = p.job ? p.job[i] : 0.0;
     int prof = 0;

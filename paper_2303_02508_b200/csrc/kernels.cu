@@ -92,7 +92,7 @@ cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_
 cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
     const int esz = p.is_f64 ? 8 : 4;
-    const int smem = round16(128 * 65 * esz) + 2 * p.T * 8;
+    const int smem = round16(128 * 65 * esz) + 2 * p.T * 8 + (p.L <= 64 ? phase_stride(p.L) * 8 : 0);
     const unsigned grid = (unsigned)((p.n_traces + 127) / 128);
     if (p.is_f64) {
         cudaFuncSetAttribute(fit_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -17,56 +17,14 @@
 // sum over rows, so splitting them off changes no rounding.  Per origin this
 // leaves 2(L-1) divides (lag and target z-scores) instead of 4(L-1).
 
-// Per-rho record: [mu0, mu1, sg0, sg1, G00, G10, G11, ok] then z0[1..n], z1[1..n].
-__host__ __device__ inline int roll_phase_stride(int L) { return 8 + 2 * (L - 1); }
+// One phase_record (fit.cuh) per first-point phase rho.
+__host__ __device__ inline int roll_phase_stride(int L) { return phase_stride(L); }
 
 __global__ void rolling_phase_kernel(const double* __restrict__ S, const double* __restrict__ Cc, int T, int L,
                                      double* __restrict__ tab) {
     const int rho = blockIdx.x * blockDim.x + threadIdx.x;
     if (rho >= T) return;
-    const int n = L - 1;
-    const double dn = (double)n;
-    double* out = tab + (int64_t)rho * roll_phase_stride(L);
-    double s0 = 0.0, s1 = 0.0;
-    int ph = (rho + 1) % T;
-    for (int i = 1; i <= n; ++i) {
-        s0 = __dadd_rn(s0, S[ph]);
-        s1 = __dadd_rn(s1, Cc[ph]);
-        ph = ph + 1 == T ? 0 : ph + 1;
-    }
-    const double mu0 = __ddiv_rn(s0, dn), mu1 = __ddiv_rn(s1, dn);
-    double q0 = 0.0, q1 = 0.0;
-    ph = (rho + 1) % T;
-    for (int i = 1; i <= n; ++i) {
-        const double d0 = __dsub_rn(S[ph], mu0), d1 = __dsub_rn(Cc[ph], mu1);
-        q0 = __dadd_rn(q0, __dmul_rn(d0, d0));
-        q1 = __dadd_rn(q1, __dmul_rn(d1, d1));
-        ph = ph + 1 == T ? 0 : ph + 1;
-    }
-    const double sg0 = __dsqrt_rn(__ddiv_rn(q0, dn)), sg1 = __dsqrt_rn(__ddiv_rn(q1, dn));
-    const bool ok = sg0 > 0.0 && sg1 > 0.0;
-    double G00 = 0.0, G10 = 0.0, G11 = 0.0;
-    double* z0 = out + 8;
-    double* z1 = z0 + n;
-    ph = (rho + 1) % T;
-    for (int i = 1; i <= n; ++i) {
-        const double a = ok ? __ddiv_rn(__dsub_rn(S[ph], mu0), sg0) : 0.0;
-        const double b = ok ? __ddiv_rn(__dsub_rn(Cc[ph], mu1), sg1) : 0.0;
-        z0[i - 1] = a;
-        z1[i - 1] = b;
-        G00 = __dadd_rn(G00, __dmul_rn(a, a));
-        G10 = __dadd_rn(G10, __dmul_rn(b, a));
-        G11 = __dadd_rn(G11, __dmul_rn(b, b));
-        ph = ph + 1 == T ? 0 : ph + 1;
-    }
-    out[0] = mu0;
-    out[1] = mu1;
-    out[2] = sg0;
-    out[3] = sg1;
-    out[4] = G00;
-    out[5] = G10;
-    out[6] = G11;
-    out[7] = ok ? 1.0 : 0.0;
+    phase_record(S, Cc, T, L, rho, tab + (int64_t)rho * phase_stride(L));
 }
 
 struct RollParams {
@@ -83,62 +41,12 @@ struct RollParams {
 };
 
 // Fit of one origin (history h[0..L), first-point phase rho): model in
-// (c0, w[3]); returns the status (0 or CHASE_ERR_FIT).
+// (c0, w[3]); returns the status (0 or CHASE_ERR_FIT; bad values are left to
+// the sweep's validation of the whole trace).
 template <typename E>
 __device__ int rolling_fit(const E* h, int L, int T, int rho, const RollParams& p, double& c0, double* w) {
-    const int n = L - 1;
-    const double dn = (double)n;
-    w[0] = w[1] = w[2] = 0.0;
-    bool constant = true;
-    for (int i = 2; i <= n; ++i)
-        if ((double)h[i] != (double)h[1]) { constant = false; break; }
-    if (constant) {  // F2: intercept-only model
-        c0 = (double)h[1];
-        return 0;
-    }
-    const double* pt = p.ptab + (int64_t)rho * roll_phase_stride(L);
-    double sl = 0.0, sy = 0.0;
-    for (int i = 1; i <= n; ++i) {
-        sl = __dadd_rn(sl, (double)h[i - 1]);
-        sy = __dadd_rn(sy, (double)h[i]);
-    }
-    const double mu2 = __ddiv_rn(sl, dn), mu3 = __ddiv_rn(sy, dn);
-    double ql = 0.0, qy = 0.0;
-    for (int i = 1; i <= n; ++i) {
-        const double d2 = __dsub_rn((double)h[i - 1], mu2), d3 = __dsub_rn((double)h[i], mu3);
-        ql = __dadd_rn(ql, __dmul_rn(d2, d2));
-        qy = __dadd_rn(qy, __dmul_rn(d3, d3));
-    }
-    const double sg2 = __dsqrt_rn(__ddiv_rn(ql, dn)), sg3 = __dsqrt_rn(__ddiv_rn(qy, dn));
-    if (!(sg3 > 0.0)) {  // numerically constant target
-        c0 = mu3;
-        return 0;
-    }
-    if (pt[7] != 0.0 && sg2 > 0.0) {
-        const double mu[4] = {pt[0], pt[1], mu2, mu3};
-        const double sg[4] = {pt[2], pt[3], sg2, sg3};
-        const double* z0 = pt + 8;
-        const double* z1 = z0 + n;
-        double h0 = 0.0, h1 = 0.0, h2 = 0.0, G20 = 0.0, G21 = 0.0, G22 = 0.0;
-        for (int i = 1; i <= n; ++i) {
-            const double a = __ldg(z0 + i - 1), b = __ldg(z1 + i - 1);
-            const double z2 = __ddiv_rn(__dsub_rn((double)h[i - 1], mu2), sg2);
-            const double u = __ddiv_rn(__dsub_rn((double)h[i], mu3), sg3);
-            h0 = __dadd_rn(h0, __dmul_rn(a, u));
-            h1 = __dadd_rn(h1, __dmul_rn(b, u));
-            G20 = __dadd_rn(G20, __dmul_rn(z2, a));
-            G21 = __dadd_rn(G21, __dmul_rn(z2, b));
-            G22 = __dadd_rn(G22, __dmul_rn(z2, z2));
-            h2 = __dadd_rn(h2, __dmul_rn(z2, u));
-        }
-        int status = 0, ridge_fired = 0;
-        chol3_solve(pt[4], pt[5], pt[6], G20, G21, G22, h0, h1, h2, p.ridge, p.tol, dn, mu, sg, c0, w, status,
-                    ridge_fired);
-        return status;
-    }
-    // a zero-variance column: the general path of fit_one (cold)
     double rec[kRecDoubles];
-    fit_one<E>(h, L, T, rho, p.phase, p.phase + T, p.ridge, p.tol, rec);
+    fit_phase<E>(h, L, T, rho, p.ptab + (int64_t)rho * phase_stride(L), p.phase, p.phase + T, p.ridge, p.tol, rec);
     c0 = rec[0];
     w[0] = rec[1];
     w[1] = rec[2];
