@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
     const int nc = P.n_chunks;
     const bool store_choice = P.choice != nullptr;
     const int lph_full = lph[lane], lph_last = lph[32 + lane];
+    const int lane_mod_T = lane % T;
 
     // One stage per warp: the load of chunk c+1 (or of the next trace's first
     // chunk, with its record) is issued once chunk c is consumed (lane 0).
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 if (status == 0) {
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
                     const int n_a = haext_len(T);
-                    int ph = lane % T;
+                    int ph = lane_mod_T;
                     for (int j = lane; j < n_a; j += 32) {
                         // A(phi) = (c0 + w_sin*S[phi]) + w_cos*C[phi]  (canonical fold of Eq. 1)
                         const int ph1 = ph + 1 == T ? 0 : ph + 1;
@@ -385,12 +386,8 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 const int jb = c * kHWarpW + j0;
                 const double Cbt = jb + nwin <= mb ? a.Cs : (jb < mb ? partial_cs(tv, mb - jb) : 0.0);
                 // does the job complete in this chunk? (warp totals of the samples done)
-                double S_prev = 0.0;
                 bool completes = false;
-                if (!bad && !done && c >= c_may) {
-                    S_prev = warp_sum(Sl);
-                    completes = __dadd_rn(S_prev, warp_sum(a.S)) >= J;
-                }
+                if (!bad && !done && c >= c_may) completes = warp_sum(__dadd_rn(Sl, a.S)) >= J;
                 if (!completes) {
                     __syncwarp();  // every lane is done with the stage
                     if (last) issue(i + GW, 0);
@@ -401,6 +398,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 if (status == 0) {
                     Cbl = __dadd_rn(Cbl, Cbt);
                     if (completes) {
+                        const double S_prev = warp_sum(Sl);
                         const double incl = warp_incl_scan(a.S, lane);
                         const double ex = __shfl_up_sync(kFull, incl, 1);
                         const double before = __dadd_rn(S_prev, lane == 0 ? 0.0 : ex);
