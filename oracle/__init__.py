@@ -56,10 +56,10 @@ def lib():
         L.oracle_total_cost.restype = f64
         L.oracle_replay.argtypes = [vp, i32, i32, vp, vp, vp, f64, f64, vp, ctypes.POINTER(i32)]
         L.oracle_replay.restype = i32
-        L.oracle_plan_trace.argtypes = [vp, i32, i32, i32, i32, i32, f64, f64, vp, vp, i32, vp, vp,
+        L.oracle_plan_trace.argtypes = [vp, i32, i32, i32, i32, i32, i32, f64, f64, vp, vp, i32, vp, vp,
                                         i32, vp, f64, f64, f64, f64, vp, vp, vp]
         L.oracle_plan_trace.restype = i32
-        L.oracle_plan_batch_f32.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, f64, f64, i32,
+        L.oracle_plan_batch_f32.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, i32, f64, f64, i32,
                                             vp, vp, vp, vp, vp, vp, i32, vp, f64, f64, f64, vp, vp,
                                             vp, vp, vp, i32]
         L.oracle_plan_batch_f32.restype = i32
@@ -117,7 +117,7 @@ def replay(c, s0, choice, avg_power, thr, delta, J):
     return out, w.value, st
 
 
-def plan_trace(c, *, L, T, phase0=0, refit_stride=0, ridge=1e-8, tol=1e-12, avg_power, thr,
+def plan_trace(c, *, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-8, tol=1e-12, avg_power, thr,
                etas, pmax, max_ci=0.0, delta=3600.0, J=0.0):
     c = _f64(c)
     N = len(c)
@@ -127,14 +127,14 @@ def plan_trace(c, *, L, T, phase0=0, refit_stride=0, ridge=1e-8, tol=1e-12, avg_
     fc = np.empty(W)
     ch = np.empty((len(E), W), dtype=np.uint8)
     tot = np.zeros(len(E), dtype=TOTALS_DTYPE)
-    st = lib().oracle_plan_trace(c.ctypes.data, N, L, T, phase0, refit_stride, ridge, tol,
+    st = lib().oracle_plan_trace(c.ctypes.data, N, L, T, phase0, refit_stride, period, ridge, tol,
                                  S.ctypes.data, C.ctypes.data, len(P), P.ctypes.data, Th.ctypes.data,
                                  len(E), E.ctypes.data, pmax, max_ci, delta, J,
                                  fc.ctypes.data, ch.ctypes.data, tot.ctypes.data)
     return fc, ch, tot, st
 
 
-def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, ridge=1e-8, tol=1e-12, profiles,
+def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-8, tol=1e-12, profiles,
                profile_id=None, etas, pmax=0.0, max_ci=0.0, delta=3600.0, job_samples=None,
                want_forecast=True, want_choice=True, threads=0):
     """traces: float32 [n][ld].  profiles: list of objects with limit_w,
@@ -155,7 +155,7 @@ def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, ridge=1e-8, tol=1e-
     tot = np.zeros((len(E), n), dtype=TOTALS_DTYPE)
     sums = np.zeros((len(E), 8))
     used = lib().oracle_plan_batch_f32(
-        tr.ctypes.data, n, N, ld, L, T, phase0, refit_stride, ridge, tol, len(profiles),
+        tr.ctypes.data, n, N, ld, L, T, phase0, refit_stride, period, ridge, tol, len(profiles),
         Ks.ctypes.data, offs.ctypes.data, P.ctypes.data, Th.ctypes.data, pm.ctypes.data,
         None if pid is None else pid.ctypes.data, len(E), E.ctypes.data, pmax, max_ci, delta,
         None if job is None else job.ctypes.data,

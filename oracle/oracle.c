@@ -245,7 +245,7 @@ int32_t oracle_replay(const double* c, int32_t N, int32_t s0,
 
 /* ---------------------------------------------------------------- planner */
 int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
-                          int32_t phase0, int32_t refit_stride,
+                          int32_t phase0, int32_t refit_stride, int32_t period,
                           double ridge_lambda, double singular_tol,
                           const double* S, const double* Cc,
                           int32_t K, const double* avg_power, const double* thr,
@@ -273,7 +273,15 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
 
     oracle_model_t m;
     int32_t origin = -1;
-    for (int32_t w = s0; status == 0 && w < N; ++w) {
+    /* One decision per period of `period` trace steps ("the
+     * period between forecasts and power limit adjustments"; <= 1: one step).
+     * At the period start w the forecaster runs recursively over the horizon
+     * n = min(period, N - w) from the last OBSERVED value (S:158-166
+     * forecast_horizon: prediction k feeds the lag of prediction k+1), and
+     * Eq. 6 takes the mean of the horizon forecasts.  The period's
+     * windows all get that decision; forecast[] holds the decision value. */
+    const int32_t P = period > 1 ? period : 1;
+    for (int32_t w = s0; status == 0 && w < N; w += P) {
         int32_t r = refit_stride > 0 ? s0 + refit_stride * ((w - s0) / refit_stride) : s0;
         if (r != origin) {
             origin = r;
@@ -281,12 +289,21 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
             if (oracle_fit(c + (r - L), L, T, phi0, S, Cc, ridge_lambda,
                            singular_tol, &m) != 0) { status = 6; break; }
         }
-        int32_t phi = (int32_t)(((int64_t)phase0 + w) % T);
-        double chat = oracle_predict(&m, S[phi], Cc[phi], c[w - 1]);
-        if (forecast) forecast[w - s0] = chat;
-        for (int e = 0; e < n_eta; ++e)
-            choice[(size_t)e * W + (w - s0)] =
-                (uint8_t)oracle_choose(K, avg_power, thr, eta[e], pmax, maxci, chat);
+        const int32_t n = N - w < P ? N - w : P;
+        double prev = c[w - 1], sum = 0.0;
+        for (int32_t k = 0; k < n; ++k) {
+            int32_t phi = (int32_t)(((int64_t)phase0 + w + k) % T);
+            double f = oracle_predict(&m, S[phi], Cc[phi], prev);
+            sum = sum + f;
+            prev = f;
+        }
+        double chat = sum / (double)n;
+        for (int32_t k = 0; k < n; ++k) {
+            if (forecast) forecast[w - s0 + k] = chat;
+            for (int e = 0; e < n_eta; ++e)
+                choice[(size_t)e * W + (w - s0 + k)] =
+                    (uint8_t)oracle_choose(K, avg_power, thr, eta[e], pmax, maxci, chat);
+        }
     }
 
     if (status != 0) {
@@ -328,7 +345,7 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
 
 int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
                               int64_t ld, int32_t L, int32_t T, int32_t phase0,
-                              int32_t refit_stride, double ridge_lambda,
+                              int32_t refit_stride, int32_t period, double ridge_lambda,
                               double singular_tol, int32_t n_profiles,
                               const int32_t* prof_K, const int32_t* prof_off,
                               const double* avg_power, const double* thr,
@@ -371,7 +388,7 @@ int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
             /* MaxPower defaults to the highest power limit */
             double pmax = pmax_cfg > 0.0 ? pmax_cfg : prof_pmax[p];
             double J = job_samples ? job_samples[i] : 0.0;
-            oracle_plan_trace(c, (int32_t)N, L, T, phase0, refit_stride,
+            oracle_plan_trace(c, (int32_t)N, L, T, phase0, refit_stride, period,
                               ridge_lambda, singular_tol, S, Cc, K, P, Th,
                               n_eta, eta, pmax, max_ci_cfg, delta, J,
                               forecast ? forecast + i * W : NULL, ch, tt);

@@ -83,6 +83,9 @@ int32_t oracle_replay(const double* c, int32_t N, int32_t s0,
 
 /* Whole planner for one trace: fit (once, or rolling with refit_stride R),
  * predict every window, choose for every eta, replay aware + baseline.
+ * period > 1: one decision per period of that many steps, on the mean of the
+ * recursive horizon forecast; forecast[]
+ * then holds each window's decision value (the period mean).
  *   c[N]            trace (g/kWh)
  *   forecast[W]     out, may be NULL
  *   choice[n_eta*W] out, may be NULL (then an internal buffer is used)
@@ -90,7 +93,7 @@ int32_t oracle_replay(const double* c, int32_t N, int32_t s0,
  * max_ci_cfg <= 0 -> MaxCI = max(c[0..L));
    pmax: the resolved MaxPower (> 0; the batch driver applies the P:183 default). */
 int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
-                          int32_t phase0, int32_t refit_stride,
+                          int32_t phase0, int32_t refit_stride, int32_t period,
                           double ridge_lambda, double singular_tol,
                           const double* S, const double* Cc,
                           int32_t K, const double* avg_power, const double* thr,
@@ -110,7 +113,7 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
  * Returns the number of threads used. */
 int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
                               int64_t ld, int32_t L, int32_t T, int32_t phase0,
-                              int32_t refit_stride, double ridge_lambda,
+                              int32_t refit_stride, int32_t period, double ridge_lambda,
                               double singular_tol, int32_t n_profiles,
                               const int32_t* prof_K, const int32_t* prof_off,
                               const double* avg_power, const double* thr,
