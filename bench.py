@@ -46,6 +46,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--e2e-traces", type=int, default=None)
+    ap.add_argument("--period-steps", type=int, default=0,
+                    help="P > 1: one decision per period of P steps on the mean recursive forecast (f1)")
     ap.add_argument("--refit-stride", type=int, default=0,
                     help="0: fit once at job start (headline); R >= 1: rolling refit every R windows (FP64-bound)")
     return ap.parse_args(argv)
@@ -135,8 +137,8 @@ class OracleSample:
     """A bounded prefix sample of the workload, generated once on the host,
     planned by the CPU oracle as it stands (OpenMP across traces)."""
 
-    def __init__(self, w: inputs.Workload, n: int, R: int = 0):
-        self.w, self.n, self.R = w, n, R
+    def __init__(self, w: inputs.Workload, n: int, R: int = 0, P: int = 0):
+        self.w, self.n, self.R, self.P = w, n, R, P
         self.tr = inputs.synth_traces_host(n, w.n_steps, seed=w.seed, mode=w.mode)
         self.pid = (inputs.profile_ids_host(n, seed=w.seed, n_profiles=len(w.profiles))
                     if len(w.profiles) > 1 else None)
@@ -147,30 +149,31 @@ class OracleSample:
         import oracle
         w = self.w
         t0 = time.perf_counter()
-        r = oracle.plan_batch(self.tr, N=w.n_steps, L=w.history_len, T=w.T, refit_stride=self.R, profiles=w.profiles,
+        r = oracle.plan_batch(self.tr, N=w.n_steps, L=w.history_len, T=w.T, refit_stride=self.R, period=self.P,
+                              profiles=w.profiles,
                               profile_id=self.pid, etas=w.etas, delta=float(w.interval_s), job_samples=self.J,
                               want_forecast=False, want_choice=False)
         self.cores = r["threads"]
         return time.perf_counter() - t0
 
 
-def calibrated_sample(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0) -> OracleSample:
+def calibrated_sample(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0, P: int = 0) -> OracleSample:
     """Two-stage calibration: a tiny probe (dominated by thread start-up)
     sizes a ~1 s probe, whose rate sizes the sample to ~target_s."""
     n0 = min(max_traces, 256 if R == 0 else 4)
-    probe = OracleSample(w, n0, R)
+    probe = OracleSample(w, n0, R, P)
     dt = probe.run()
     n1 = int(min(max_traces, max(n0, n0 * min(1.0, target_s) / max(dt, 1e-3))))
     if n1 > n0:
-        probe = OracleSample(w, n1, R)
+        probe = OracleSample(w, n1, R, P)
         dt = probe.run()
         n0 = n1
     n = int(min(max_traces, max(n0, n0 * target_s / max(dt, 1e-3))))
-    return probe if n <= n0 else OracleSample(w, n, R)
+    return probe if n <= n0 else OracleSample(w, n, R, P)
 
 
-def oracle_sample_rate(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0):
-    s = calibrated_sample(w, target_s, max_traces, R)
+def oracle_sample_rate(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0, P: int = 0):
+    s = calibrated_sample(w, target_s, max_traces, R, P)
     dt = s.run()
     return s.n * w.W / dt, s.cores, s.n, dt
 
@@ -184,7 +187,7 @@ def main_reference(args):
         return 0
     w = inputs.workload(args.config, n_traces=args.traces)
     per_step = min(10.0, 150.0 / max(1, args.steps + args.warmup))
-    s = calibrated_sample(w, per_step, w.n_traces, args.refit_stride)
+    s = calibrated_sample(w, per_step, w.n_traces, args.refit_stride, args.period_steps)
     times = []
     for k in range(args.warmup + args.steps):
         dt = s.run()
@@ -198,7 +201,7 @@ def main_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(w, args.gpus, args.refit_stride),
+        "config": workload_config(w, args.gpus, args.refit_stride, args.period_steps),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": s.cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -230,7 +233,9 @@ def fp64_peak():
     return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz)"
 
 
-def planner_kernel_name(w: inputs.Workload, R: int = 0) -> str:
+def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0) -> str:
+    if P > 1:
+        return "sweep_kernel<FUSED, FIN> (Eq. 6 argmin + replay on the period decision forecasts)"
     if R > 0:
         return "rolling_forecast_kernel (one thread per (trace, refit origin), oracle_fit's exact fp64 sequence)"
     if len(w.etas) == 1 and w.history_len % 4 == 0:
@@ -238,15 +243,17 @@ def planner_kernel_name(w: inputs.Workload, R: int = 0) -> str:
     return "sweep_kernel<FUSED> (fused predict + Eq. 6 argmin + replay)"
 
 
-def workload_config(w: inputs.Workload, n_gpus: int, R: int = 0):
+def workload_config(w: inputs.Workload, n_gpus: int, R: int = 0, P: int = 0):
     fc = ("fit once per trace on the 24 h before job start (P:67), least squares (Table 1 LR)" if R == 0 else
           f"rolling refit every {R} window(s) on the {w.history_len} points before each origin (P:78-79)")
+    if P > 1:
+        fc += f"; one decision per {P}-step period on the mean recursive forecast (P:130, S:158-166)"
     return {
         "workload": f"{w.name}: {w.description}",
         "traces_per_gpu": w.n_traces, "steps_per_trace": w.n_steps, "history_len": w.history_len,
         "windows_per_trace": w.W, "interval_s": w.interval_s, "n_eta": len(w.etas),
         "n_limits": int(w.profiles[0].K), "profiles": [p.name for p in w.profiles],
-        "forecaster": fc, "refit_stride": R,
+        "forecaster": fc, "refit_stride": R, "period_steps": max(P, 1),
         "l2": f"inputs larger than L2 ({w.n_traces * w.ld * 4 / 1e9:.1f} GB of fp32 traces per GPU vs 126 MB L2)",
         "parallelism": f"dp{n_gpus} (trace-sharded; NCCL all-reduce of per-GPU totals)",
     }
@@ -283,7 +290,7 @@ def main_chase(args):
 
     planner = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, interval_s=w.interval_s,
                          history_len=w.history_len, profile_id=pid, job_samples=J, want_choice=True,
-                         refit_stride=args.refit_stride)
+                         refit_stride=args.refit_stride, period_steps=args.period_steps)
 
     def step():
         planner.run()
@@ -340,7 +347,7 @@ def main_chase(args):
         tpw = ncu_traffic_per_window(args.config)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": None if tpw is None else tpw * n * W,
-                    "kernel": planner_kernel_name(w),
+                    "kernel": planner_kernel_name(w, 0, args.period_steps),
                     "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
                     "algorithmic_bytes_per_launch": alg_bytes, "bytes_per_window": BYTES_PER_WINDOW,
                     "peak_source": peak_src}
@@ -360,7 +367,7 @@ def main_chase(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, ns, dt = oracle_sample_rate(w, args.cpu_seconds, n, args.refit_stride)
+        rate, cores, ns, dt = oracle_sample_rate(w, args.cpu_seconds, n, args.refit_stride, args.period_steps)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {ns} of {n} traces ({ns * W:.3g} windows, {dt:.1f} s on {cores} threads)"}
 
@@ -369,7 +376,7 @@ def main_chase(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based generator, inputs/)",
-            "config": workload_config(w, world, args.refit_stride), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "config": workload_config(w, world, args.refit_stride, args.period_steps), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk,
             "check": {"n_ok": float(sums0[0, 7]), "n_slow_windows": int(diag.n_slow_windows)},
         }
@@ -399,7 +406,8 @@ def bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev):
     chunk = min(n_e2e, 32768)
     ht = cb.make_traces(h, n_steps=w.n_steps, interval_s=w.interval_s)
     tc = cb.make_traces(h[:chunk], n_steps=w.n_steps, interval_s=w.interval_s)
-    fcfg = cb.make_fcfg(interval_s=w.interval_s, history_len=w.history_len, refit_stride=args.refit_stride)
+    fcfg = cb.make_fcfg(interval_s=w.interval_s, history_len=w.history_len, refit_stride=args.refit_stride,
+                        period_steps=args.period_steps)
     ws = cb.alloc_workspace(cb.workspace_bytes(tc, fcfg, len(w.profiles), len(w.etas)), dev)
     stg = cb.alloc_workspace(cb.sweep_host_staging_bytes(ht, chunk, len(w.etas)), dev)
 

@@ -88,7 +88,14 @@ typedef struct {
                                     MaxCI stays the job-start value.  The
                                     workspace then also holds an f64 forecast
                                     scratch of round_up(W,2) per trace.         */
-    int32_t reserved;
+    int32_t period_steps;        /* <= 1: a decision every trace step.
+                                    P > 1: one decision per period of P steps
+                                    (P:78-79), on the mean of the
+                                    recursive forecast over the period
+                                    (S:158-166); d_forecast then holds
+                                    each window's decision value.  Needs
+                                    refit_stride == 0; uses the same forecast
+                                    scratch as the rolling refit.               */
     double  ridge_lambda;        /* 1e-8                                   */
     double  singular_tol;        /* 1e-12: Cholesky pivot <= tol*(L-1) -> ridge (Q6) */
 } chase_forecast_cfg_t;

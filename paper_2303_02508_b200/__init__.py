@@ -35,7 +35,7 @@ class Traces(ctypes.Structure):
 
 
 class ForecastCfg(ctypes.Structure):
-    _fields_ = [("steps_per_day", i32), ("history_len", i32), ("refit_stride", i32), ("reserved", i32),
+    _fields_ = [("steps_per_day", i32), ("history_len", i32), ("refit_stride", i32), ("period_steps", i32),
                 ("ridge_lambda", f64), ("singular_tol", f64)]
 
 
@@ -130,9 +130,9 @@ def make_traces(x, *, n_steps: int | None = None, interval_s: int = 3600, phase0
     return Traces(x.data_ptr(), dt, interval_s, x.shape[0], n_steps or x.shape[1], x.shape[1], phase0, 0)
 
 
-def make_fcfg(*, interval_s: int = 3600, history_len: int = 24, refit_stride: int = 0, ridge: float = 1e-8,
-              tol: float = 1e-12) -> ForecastCfg:
-    return ForecastCfg(86400 // interval_s, history_len, refit_stride, 0, ridge, tol)
+def make_fcfg(*, interval_s: int = 3600, history_len: int = 24, refit_stride: int = 0, period_steps: int = 0,
+              ridge: float = 1e-8, tol: float = 1e-12) -> ForecastCfg:
+    return ForecastCfg(86400 // interval_s, history_len, refit_stride, period_steps, ridge, tol)
 
 
 class _Profiles:
@@ -266,12 +266,13 @@ class Planner:
 
     def __init__(self, traces_tensor, *, n_steps: int, profiles, etas, interval_s=3600, history_len=24,
                  phase0=0, profile_id=None, job_samples=None, want_choice=True, want_forecast=False,
-                 want_per_trace=False, max_power_w=0.0, max_ci=0.0, refit_stride=0):
+                 want_per_trace=False, max_power_w=0.0, max_ci=0.0, refit_stride=0, period_steps=0):
         import torch
         self.x = traces_tensor
         dev = traces_tensor.device
         self.tr = make_traces(traces_tensor, n_steps=n_steps, interval_s=interval_s, phase0=phase0)
-        self.fcfg = make_fcfg(interval_s=interval_s, history_len=history_len, refit_stride=refit_stride)
+        self.fcfg = make_fcfg(interval_s=interval_s, history_len=history_len, refit_stride=refit_stride,
+                              period_steps=period_steps)
         self.profiles, self.etas = profiles, list(etas)
         n, W = traces_tensor.shape[0], n_steps - history_len
         self.n, self.W = n, W

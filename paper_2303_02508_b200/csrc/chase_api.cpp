@@ -53,6 +53,9 @@ struct WsLayout {
 };
 
 bool rolling(const chase_forecast_cfg_t* f) { return f && f->refit_stride > 0; }
+bool periods(const chase_forecast_cfg_t* f) { return f && f->period_steps > 1; }
+// forecasts precomputed per window (rolling refit or decision periods), then read by the sweep
+bool fc_first(const chase_forecast_cfg_t* f) { return rolling(f) || periods(f); }
 
 // Rolling refit (refit_stride >= 1) appends the per-phase fit tables and a
 // forecast scratch [n][round_up(W, 2)] f64 (used when d_forecast is NULL).
@@ -69,8 +72,8 @@ WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta, const chase_t
     w.block_sums = o; o += round_up((finalize_grid(n_traces) + 1) * n_eta * 8 * 8, kWsAlign);
     w.roll_ptab = w.roll_fc = o;
     w.ld_roll = 0;
-    if (rolling(f) && t && f->history_len >= 2 && t->n_steps > f->history_len) {
-        w.roll_ptab = o; o += round_up((int64_t)roll_phase_doubles(T, f->history_len) * 8, kWsAlign);
+    if (fc_first(f) && t && f->history_len >= 2 && t->n_steps > f->history_len) {
+        if (rolling(f)) { w.roll_ptab = o; o += round_up((int64_t)roll_phase_doubles(T, f->history_len) * 8, kWsAlign); }
         w.ld_roll = round_up(t->n_steps - f->history_len, 2);
         w.roll_fc = o; o += round_up(n_traces * w.ld_roll * 8, kWsAlign);
     }
@@ -103,6 +106,9 @@ chase_status_t check_fcfg(const chase_traces_t* t, const chase_forecast_cfg_t* f
     if (t->n_steps <= f->history_len) return fail(CHASE_ERR_INVALID, "n_steps must exceed history_len (W >= 1)");
     if (f->history_len > 1 << 20) return fail(CHASE_ERR_INVALID, "history_len too large");
     if (f->refit_stride < 0) return fail(CHASE_ERR_INVALID, "refit_stride < 0");
+    if (f->period_steps < 0) return fail(CHASE_ERR_INVALID, "period_steps < 0");
+    if (f->period_steps > 1 && f->refit_stride > 0)
+        return fail(CHASE_ERR_INVALID, "period_steps > 1 with refit_stride > 0 is not supported");
     if (!(f->ridge_lambda >= 0) || !(f->singular_tol >= 0)) return fail(CHASE_ERR_INVALID, "ridge/tol must be >= 0");
     return CHASE_OK;
 }
@@ -310,6 +316,10 @@ cudaError_t launch_rolling_into(const chase_traces_t* t, const chase_forecast_cf
                                 double max_ci_fixed, double* fc, int64_t ldf, cudaStream_t s) {
     const int T = f->steps_per_day;
     const double* phase = reinterpret_cast<const double*>(ws + WL.tables + sizeof(TablesHeader));
+    if (periods(f))  // decision periods: the recursive horizon means of the fit-once model
+        return launch_periods(t->data, t->dtype == CHASE_F64, t->ld, t->n_traces, (int)t->n_steps, f->history_len, T,
+                              t->phase0, f->period_steps, phase, reinterpret_cast<const double*>(ws + WL.records), fc,
+                              ldf, s);
     return launch_rolling(t->data, t->dtype == CHASE_F64, t->ld, t->n_traces, (int)t->n_steps, f->history_len, T,
                           t->phase0, f->refit_stride, f->ridge_lambda, f->singular_tol, phase,
                           reinterpret_cast<double*>(ws + WL.roll_ptab), reinterpret_cast<double*>(ws + WL.records),
@@ -355,8 +365,8 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     p.n_eta = 1;
     p.forecast = d_forecast;
     p.ld_f = ld_f;
-    if (rolling(fcfg)) {
-        // every origin's fit straight into d_forecast; the predict pass then only validates
+    if (fc_first(fcfg)) {
+        // every window's forecast straight into d_forecast; the predict pass then only validates
         e = launch_rolling_into(traces, fcfg, ws, WL, 1.0, d_forecast, ld_f, s);
         if (e != cudaSuccess) return cuda_fail(e, "rolling forecast kernel");
         p.fc_in = d_forecast;
@@ -495,14 +505,14 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     p.forecast = d_forecast;
     p.ld_f = ld_f;
     bool aligned = aligned_start(traces, fcfg->history_len);
-    if (rolling(fcfg)) {
-        // rolling refit: forecasts of every window first (into d_forecast when given), then the
-        // fused argmin + replay reads them (sweep_kernel<..., FIN>)
+    if (fc_first(fcfg)) {
+        // rolling refit / decision periods: forecasts of every window first (into d_forecast when
+        // given), then the fused argmin + replay reads them (sweep_kernel<..., FIN>)
         double* fc = d_forecast ? d_forecast : reinterpret_cast<double*>(ws + WL.roll_fc);
         const int64_t ldf = d_forecast ? ld_f : WL.ld_roll;
-        ev_start(s);  // rolling mode: the refits dominate (timing hook)
+        if (rolling(fcfg)) ev_start(s);  // rolling mode: the refits dominate (timing hook)
         e = launch_rolling_into(traces, fcfg, ws, WL, cost->max_ci, fc, ldf, s);
-        ev_stop(s);
+        if (rolling(fcfg)) ev_stop(s);
         if (e != cudaSuccess) return cuda_fail(e, "rolling forecast kernel");
         p.fc_in = fc;
         p.ld_fin = ldf;

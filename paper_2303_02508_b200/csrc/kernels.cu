@@ -233,6 +233,32 @@ cudaError_t launch_rolling(const void* traces, bool f64, int64_t ld, int64_t n_t
     return cudaGetLastError();
 }
 
+cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
+                           int P, const double* phase, const double* records, double* forecast, int64_t ld_f,
+                           cudaStream_t s) {
+    if (n_traces <= 0) return cudaSuccess;
+    PeriodParams p;
+    p.traces = traces;
+    p.ld = ld;
+    p.n_traces = n_traces;
+    p.N = N;
+    p.L = L;
+    p.T = T;
+    p.phase0 = phase0;
+    p.P = P;
+    p.n_per = (N - L + P - 1) / P;
+    p.phase = phase;
+    p.records = records;
+    p.forecast = forecast;
+    p.ld_f = ld_f;
+    const int64_t grid = (n_traces * (int64_t)p.n_per + 127) / 128;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (f64) period_forecast_kernel<double><<<(unsigned)grid, 128, 0, s>>>(p);
+    else period_forecast_kernel<float><<<(unsigned)grid, 128, 0, s>>>(p);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fixup(const uint8_t* status, const int64_t* bad_list, int64_t n_traces, uint8_t* choice,
                          int64_t ld_c, int64_t W, int n_eta_choice, double* forecast, int64_t ld_f,
                          chase_diag_t* diag, cudaStream_t s) {

@@ -86,3 +86,51 @@ __global__ void __launch_bounds__(128) rolling_forecast_kernel(const __grid_cons
         ph = ph + 1 == T ? 0 : ph + 1;
     }
 }
+
+// ------------------------------------------------------------------ decision periods
+// period_steps P > 1 ("the period between forecasts and power
+// limit adjustments"): at each period start b = s0 + jP the fit-once model
+// forecasts recursively over n = min(P, N - b) steps from the last observed
+// value (SPEC forecast_horizon: prediction k is the lag of prediction k+1,
+// clamped at 0), and Eq. 6 decides on the mean of those n forecasts.
+// One thread per (trace, period) writes that decision value to the period's n
+// windows; the FIN sweep then takes the same decision for each of them.
+// oracle_plan_trace's operation order throughout (bit-identical).
+struct PeriodParams {
+    const void* traces;
+    int64_t ld, n_traces;
+    int32_t N, L, T, phase0, P, n_per;   // n_per = ceil(W / P)
+    const double* phase;                 // S[T], C[T]
+    const double* records;               // fit-once models [n][16]
+    double* forecast;                    // [n][ld_f]: the decision value of every window
+    int64_t ld_f;
+};
+
+template <typename E>
+__global__ void __launch_bounds__(128) period_forecast_kernel(const __grid_constant__ PeriodParams p) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= p.n_traces * (int64_t)p.n_per) return;
+    const int64_t i = idx / p.n_per;
+    const int j = (int)(idx - i * p.n_per);
+    const int s0 = p.L, T = p.T;
+    const int b = s0 + j * p.P;
+    const int n = min(p.P, p.N - b);
+    const E* row = reinterpret_cast<const E*>(p.traces) + i * p.ld;
+    const double* rec = p.records + i * kRecDoubles;
+    const double c0 = rec[0], ws = rec[1], wc = rec[2], wl = rec[3];
+    const double* S = p.phase;
+    const double* C = p.phase + T;
+    int ph = (int)(((int64_t)p.phase0 + b) % T);
+    double prev = (double)row[b - 1], sum = 0.0;
+    for (int k = 0; k < n; ++k) {
+        const double A = __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, S[ph])), __dmul_rn(wc, C[ph]));
+        const double pr = __dadd_rn(A, __dmul_rn(wl, prev));
+        const double f = pr > 0.0 ? pr : 0.0;
+        sum = __dadd_rn(sum, f);
+        prev = f;
+        ph = ph + 1 == T ? 0 : ph + 1;
+    }
+    const double chat = __ddiv_rn(sum, (double)n);
+    double* out = p.forecast + i * p.ld_f + (b - s0);
+    for (int k = 0; k < n; ++k) out[k] = chat;
+}

@@ -179,3 +179,18 @@ def test_rolling_workspace_adds_phase_tables_and_forecast_scratch():
         import torch
         cb.sweep(tr, cb.make_fcfg(refit_stride=-1), [prof], [0.5], _ws(), torch.zeros((1, 8), dtype=torch.float64),
                  stream=0)
+
+
+def test_decision_periods_validation_and_workspace():
+    import torch
+    cb, x, tr = _args(n=10)
+    a = cb.workspace_bytes(tr, cb.make_fcfg(), 1, 1)
+    b = cb.workspace_bytes(tr, cb.make_fcfg(period_steps=24), 1, 1)
+    W = tr.n_steps - 24
+    assert b - a >= 10 * ((W + 1) // 2 * 2) * 8
+    prof = inputs.make_profile("resnet50", inputs.LIMITS_9)
+    s = torch.zeros((1, 8), dtype=torch.float64)
+    for f, needle in [(cb.make_fcfg(period_steps=-1), "period_steps"),
+                      (cb.make_fcfg(period_steps=4, refit_stride=2), "refit_stride")]:
+        with pytest.raises(cb.ChaseError, match=needle):
+            cb.sweep(tr, f, [prof], [0.5], _ws(), s, stream=0)

@@ -23,13 +23,13 @@ DEV = torch.device("cuda:0")
 
 
 def run_sweep(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0,
-              dtype=torch.float32, forecast=True, refit_stride=0):
+              dtype=torch.float32, forecast=True, refit_stride=0, period_steps=0):
     x = torch.from_numpy(np.ascontiguousarray(tr_host)).to(DEV, dtype)
     pid_t = None if pid is None else torch.from_numpy(np.ascontiguousarray(pid, np.uint8)).to(DEV)
     J_t = None if J is None else torch.from_numpy(np.ascontiguousarray(J, np.float64)).to(DEV)
     pl = cb.Planner(x, n_steps=N, profiles=profiles, etas=etas, interval_s=interval_s, history_len=L,
                     phase0=phase0, profile_id=pid_t, job_samples=J_t, want_choice=True, want_forecast=forecast,
-                    want_per_trace=True, max_ci=max_ci, refit_stride=refit_stride)
+                    want_per_trace=True, max_ci=max_ci, refit_stride=refit_stride, period_steps=period_steps)
     res = pl.run()
     torch.cuda.synchronize()
     out = dict(sums=res.sums.cpu().numpy(), totals=res.per_trace_numpy(),
@@ -39,10 +39,10 @@ def run_sweep(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=
 
 
 def run_oracle(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0,
-               refit_stride=0):
+               refit_stride=0, period_steps=0):
     T = 86400 // interval_s
     return oracle.plan_batch(np.ascontiguousarray(tr_host, np.float32), N=N, L=L, T=T, phase0=phase0,
-                             refit_stride=refit_stride,
+                             refit_stride=refit_stride, period=period_steps,
                              profiles=profiles, profile_id=pid, etas=etas, max_ci=max_ci,
                              delta=float(interval_s), job_samples=J)
 
@@ -438,3 +438,45 @@ def test_rolling_fit_forecast_split_path_and_f64():
         torch.cuda.synchronize()
         o = oracle.plan_batch(tr, N=N, L=24, T=24, refit_stride=2, profiles=w.profiles[:1], etas=[0.5])
         assert np.array_equal(fc.cpu().numpy()[:, :N - 24], o["forecast"])
+
+
+# ------------------------------------------------------------------ decision periods
+@pytest.mark.parametrize("P,L,N,etas,n", [
+    (2, 24, 24 + 701, [0.5], 21),          # ragged last period (W = 701)
+    (24, 24, 24 + 2000, [0.4, 0.8], 9),    # daily decisions, two etas
+    (7, 23, 23 + 400, [0.6], 5),           # odd L: unaligned tile path
+    (168, 24, 24 + 8760, [0.5], 3),        # weekly decisions over a year
+])
+def test_decision_periods_parity(P, L, N, etas, n):
+    """One decision per period on the mean of the recursive horizon forecast:
+    decision values bit-identical to the oracle, choices and totals exact."""
+    prof = [inputs.make_profile("vit", inputs.LIMITS_9)]
+    tr = inputs.synth_traces_host(n, N, seed=300 + P)
+    J = np.full(n, 3600 * (N - L) * prof[0].throughput_sps.min())
+    g = run_sweep(tr, N, prof, etas, J=J, L=L, period_steps=P)
+    o = run_oracle(tr, N, prof, etas, J=J, L=L, period_steps=P)
+    assert_parity(g, o)
+    for start in range(0, N - L, P):   # constant within each period
+        assert len(set(g["choice"][0, 0, start:start + P])) == 1
+    g2 = run_sweep(tr, N, prof, etas, J=J, L=L, period_steps=P, forecast=False)
+    g2["forecast"] = None
+    assert_parity(g2, o)
+
+
+def test_decision_periods_fit_forecast_split_path():
+    w = inputs.workload("C4", n_traces=17)
+    N = 24 + 1000
+    tr = inputs.synth_traces_host(w.n_traces, N, seed=43)
+    tr[3, 500] = -1.0
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=N)
+    f = cb.make_fcfg(period_steps=6)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    fc = torch.empty((w.n_traces, N - 24), dtype=torch.float64, device=DEV)
+    cb.fit_forecast(t, f, fc, N - 24, ws)
+    torch.cuda.synchronize()
+    o = oracle.plan_batch(tr, N=N, L=24, T=24, period=6, profiles=w.profiles[:1], etas=[0.5])
+    fg = fc.cpu().numpy()
+    assert np.array_equal(np.isnan(fg), np.isnan(o["forecast"]))
+    ok = ~np.isnan(o["forecast"])
+    assert np.array_equal(fg[ok], o["forecast"][ok])
