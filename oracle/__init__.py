@@ -63,6 +63,12 @@ def lib():
                                             vp, vp, vp, vp, vp, vp, i32, vp, f64, f64, f64, vp, vp,
                                             vp, vp, vp, i32]
         L.oracle_plan_batch_f32.restype = i32
+        L.oracle_mape.argtypes = [vp, vp, i64]
+        L.oracle_mape.restype = f64
+        L.oracle_evaluate.argtypes = [vp, i32, i32, i32, i32, f64, f64, vp, vp, vp]
+        L.oracle_evaluate.restype = i32
+        L.oracle_evaluate_batch_f32.argtypes = [vp, i64, i64, i64, i32, i32, i32, f64, f64, vp, vp, i32]
+        L.oracle_evaluate_batch_f32.restype = i32
         _LIB = L
     return _LIB
 
@@ -162,3 +168,31 @@ def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-
         None if fc is None else fc.ctypes.data, None if ch is None else ch.ctypes.data,
         tot.ctypes.data, sums.ctypes.data, threads)
     return dict(forecast=fc, choice=ch, totals=tot, sums=sums, threads=used)
+
+
+def mape(actual, predicted) -> float:
+    """SPEC mape: 100/n * sum |a - p| / |a|; NaN if undefined."""
+    a, p = _f64(actual), _f64(predicted)
+    assert len(a) == len(p)
+    return float(lib().oracle_mape(a.ctypes.data, p.ctypes.data, len(a)))
+
+
+def evaluate(c, *, L, T, phase0=0, ridge=1e-8, tol=1e-12):
+    """SPEC evaluate_models for one trace: (status, mape_linear, mape_persistence)."""
+    c = _f64(c)
+    S, C = phase_table(T)
+    out = np.empty(2)
+    st = lib().oracle_evaluate(c.ctypes.data, len(c), L, T, phase0, ridge, tol, S.ctypes.data, C.ctypes.data,
+                               out.ctypes.data)
+    return st, float(out[0]), float(out[1])
+
+
+def evaluate_batch(traces, *, N, L, T, phase0=0, ridge=1e-8, tol=1e-12, threads=0):
+    """fp32 traces [n][ld] -> (mape [n][2], status [n], threads used)."""
+    tr = np.ascontiguousarray(traces, dtype=np.float32)
+    n, ld = tr.shape
+    out = np.empty((n, 2))
+    st = np.empty(n, dtype=np.int32)
+    used = lib().oracle_evaluate_batch_f32(tr.ctypes.data, n, N, ld, L, T, phase0, ridge, tol, out.ctypes.data,
+                                           st.ctypes.data, threads)
+    return out, st, used

@@ -421,3 +421,66 @@ int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
     free(S); free(Cc);
     return used;
 }
+
+
+/* ---------------------------------------------------------------- forecast evaluation */
+/* SPEC mape: 100/n * sum |a_i - p_i| / |a_i|, sequential sum. */
+double oracle_mape(const double* actual, const double* predicted, int64_t n) {
+    if (n < 1) return NAN;
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (actual[i] == 0.0) return NAN;
+        s = s + fabs(actual[i] - predicted[i]) / fabs(actual[i]);
+    }
+    return (100.0 / (double)n) * s;
+}
+
+/* SPEC evaluate_models: fit once on the first L points, walk
+ * forward with the true lag; linear vs persistence. */
+int32_t oracle_evaluate(const double* c, int32_t N, int32_t L, int32_t T, int32_t phase0,
+                        double ridge_lambda, double singular_tol, const double* S,
+                        const double* Cc, double* out2) {
+    out2[0] = out2[1] = NAN;
+    for (int32_t t = 0; t < N; ++t)
+        if (!(c[t] >= 0.0) || !isfinite(c[t])) return 4;
+    oracle_model_t m;
+    if (oracle_fit(c, L, T, phase0 % T, S, Cc, ridge_lambda, singular_tol, &m) != 0) return 6;
+    const int32_t n = N - L;
+    double* pl = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int32_t w = L; w < N; ++w) {
+        int32_t phi = (int32_t)(((int64_t)phase0 + w) % T);
+        pl[w - L] = oracle_predict(&m, S[phi], Cc[phi], c[w - 1]);
+    }
+    out2[0] = oracle_mape(c + L, pl, n);
+    out2[1] = oracle_mape(c + L, c + L - 1, n);   /* persistence: p(w) = c[w-1] */
+    free(pl);
+    return isnan(out2[0]) ? 8 : 0;
+}
+
+int32_t oracle_evaluate_batch_f32(const float* traces, int64_t n_traces, int64_t N, int64_t ld,
+                                  int32_t L, int32_t T, int32_t phase0, double ridge_lambda,
+                                  double singular_tol, double* out, int32_t* status, int32_t threads) {
+    double* S = (double*)malloc(sizeof(double) * (size_t)T);
+    double* Cc = (double*)malloc(sizeof(double) * (size_t)T);
+    oracle_phase_table(T, S, Cc);
+    int32_t used = 1;
+#ifdef _OPENMP
+    if (threads <= 0) threads = omp_get_max_threads();
+    used = threads;
+#else
+    threads = 1;
+#endif
+    #pragma omp parallel num_threads(threads)
+    {
+        double* c = (double*)malloc(sizeof(double) * (size_t)N);
+        #pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < n_traces; ++i) {
+            for (int64_t t = 0; t < N; ++t) c[t] = (double)traces[i * ld + t];
+            status[i] = oracle_evaluate(c, (int32_t)N, L, T, phase0, ridge_lambda, singular_tol, S, Cc,
+                                        out + 2 * i);
+        }
+        free(c);
+    }
+    free(S); free(Cc);
+    return used;
+}

@@ -125,6 +125,26 @@ int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
                               uint8_t* choice, oracle_totals_t* totals,
                               double* sums, int32_t threads);
 
+/* SPEC mape (Table 1 metric P:159-161): 100/n * sum |a_i - p_i| / |a_i|.
+ * Returns NaN when n < 1 or some a_i == 0 ("errors: zero actual"). */
+double oracle_mape(const double* actual, const double* predicted, int64_t n);
+
+/* SPEC evaluate_models (P:159-161 walk-forward, Table 1) for one
+ * trace: fit Eq. 1 once on c[0..L), then one-step predictions of every
+ * window w = L..N-1 with the TRUE lag c[w-1] (the first seeded by the last
+ * fit point: N - L predictions, Open Question S:211-212), next to the
+ * persistence baseline p(w) = c[w-1].  out2 = {MAPE linear, MAPE persistence}
+ * (percent; NaN if undefined).  Returns 0, 4 (negative / non-finite value),
+ * 6 (fit failed) or 8 (a zero actual: MAPE undefined). */
+int32_t oracle_evaluate(const double* c, int32_t N, int32_t L, int32_t T, int32_t phase0,
+                        double ridge_lambda, double singular_tol, const double* S,
+                        const double* Cc, double* out2);
+
+/* Batch of fp32 traces [n][ld] (OpenMP across traces): out[n][2], status[n]. */
+int32_t oracle_evaluate_batch_f32(const float* traces, int64_t n_traces, int64_t N, int64_t ld,
+                                  int32_t L, int32_t T, int32_t phase0, double ridge_lambda,
+                                  double singular_tol, double* out, int32_t* status, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif
