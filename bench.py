@@ -46,6 +46,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--e2e-traces", type=int, default=None)
+    ap.add_argument("--mode", choices=["plan", "mape"], default="plan",
+                    help="plan: the planner (headline); mape: the walk-forward forecast-evaluation sweep (f3)")
     ap.add_argument("--period-steps", type=int, default=0,
                     help="P > 1: one decision per period of P steps on the mean recursive forecast (f1)")
     ap.add_argument("--refit-stride", type=int, default=0,
@@ -439,10 +441,137 @@ def bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev):
             "api": "chase_sweep_host (pinned host inputs, double-buffered H2D on a second stream)"}
 
 
+MAPE_METRIC = "trace-windows evaluated/sec (walk-forward MAPE, linear + persistence)"
+
+
+def main_mape(args):
+    """Forecast-evaluation sweep (the Table 1 experiment,
+    P:159-161, on synthetic traces): chase_forecast_mape over this GPU's traces.
+    Roofline: HBM, 4 B per window (the trace value; 16 B per trace of output)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_02508_b200 as cb
+    from paper_2303_02508_b200.parallel import shard_bounds
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = inputs.workload(args.config, n_traces=args.traces)
+    n, W = w.n_traces, w.W
+    trace0, _ = shard_bounds(n * world, rank, world)
+    x = torch.empty((n, w.ld), dtype=torch.float32, device=dev)
+    inputs.synth_traces_device(x, w.n_steps, seed=w.seed, mode=w.mode, trace0=trace0)
+    t = cb.make_traces(x, n_steps=w.n_steps, interval_s=w.interval_s)
+    f = cb.make_fcfg(interval_s=w.interval_s, history_len=w.history_len)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), dev)
+    mp = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    st = torch.empty(n, dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        cb.forecast_mape(t, f, mp, ws, status=st)
+    torch.cuda.synchronize()
+    if int((st != 0).sum()) != 0:
+        raise RuntimeError("forecast_mape reported invalid traces on the synthetic workload")
+    stream = torch.cuda.current_stream(dev)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:
+        a.record(stream)
+        b.record(stream)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = cb.kernel_launches()
+    t0.record(stream)
+    for k in range(args.steps):
+        cb.set_kernel_events(*kev[k])
+        cb.forecast_mape(t, f, mp, ws, status=st)
+    t1.record(stream)
+    cb.set_kernel_events(None, None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = cb.kernel_launches() - launches0
+    clk = clocks.stop()
+    tm = torch.tensor([t0.elapsed_time(t1), float(np.mean([a.elapsed_time(b) for a, b in kev]))],
+                      dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms_per_step, kern_ms = float(tm[0]) / args.steps, float(tm[1])
+    value = float(n) * W * world / (ms_per_step / 1e3)
+    peak, peak_src = measured_peaks()
+    alg = n * W * 4.0
+    achieved = alg / (kern_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "mape_kernel (warp per trace, walk-forward predict + MAPE sums)",
+                "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
+                "algorithmic_bytes_per_launch": alg, "bytes_per_window": 4.0, "peak_source": peak_src}
+    e2e = None
+    if not args.no_e2e:   # host traces -> device (chunked, pinned) -> chase_forecast_mape -> host results
+        chunk = min(n, 65536)
+        h = torch.empty((chunk, w.ld), dtype=torch.float32).pin_memory()
+        h.copy_(x[:chunk])
+        hm = torch.empty((chunk, 2), dtype=torch.float64).pin_memory()
+        xd = torch.empty_like(x[:chunk])
+        tc = cb.make_traces(xd, n_steps=w.n_steps, interval_s=w.interval_s)
+        wsc = cb.alloc_workspace(cb.workspace_bytes(tc, f, 1, 1), dev)
+        mc = torch.empty((chunk, 2), dtype=torch.float64, device=dev)
+        reps = max(1, n // chunk)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            xd.copy_(h, non_blocking=True)
+            cb.forecast_mape(tc, f, mc, wsc)
+            hm.copy_(mc, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        e2e = {"value": reps * chunk * W / (ms / 1e3), "unit": "trace-windows/s",
+               "h2d_bytes_per_step": int(reps * chunk * w.ld * 4), "d2h_bytes_per_step": int(reps * chunk * 16),
+               "api": "chase_forecast_mape on chunks copied from pinned host memory"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        ns = 256
+        tr_h = inputs.synth_traces_host(ns, w.n_steps, seed=w.seed, mode=w.mode)
+        t_0 = time.perf_counter()
+        _, _, cores = oracle.evaluate_batch(tr_h, N=w.n_steps, L=w.history_len, T=w.T)
+        dt = time.perf_counter() - t_0
+        ns = int(min(n, ns * max(1.0, args.cpu_seconds / max(dt, 1e-3))))
+        tr_h = inputs.synth_traces_host(ns, w.n_steps, seed=w.seed, mode=w.mode)
+        t_0 = time.perf_counter()
+        _, _, cores = oracle.evaluate_batch(tr_h, N=w.n_steps, L=w.history_len, T=w.T)
+        dt = time.perf_counter() - t_0
+        cpu = {"value": ns * W / dt, "unit": "trace-windows/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {ns} of {n} traces ({ns * W:.3g} windows, {dt:.1f} s on {cores} threads)"}
+    if rank == 0:
+        cfg = workload_config(w, world)
+        cfg["workload"] = f"{w.name} traces, walk-forward forecast evaluation (Table 1 shape, P:159-161)"
+        line = {"metric": MAPE_METRIC, "value": value, "unit": "trace-windows/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded counter-based generator, inputs/)", "config": cfg,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk, "check": {"mean_mape_linear": float(mp[:, 0].mean()),
+                                         "mean_mape_persistence": float(mp[:, 1].mean())}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main(argv=None):
     args = parse_args(argv)
     if args.impl == "reference":
         return main_reference(args)
+    if args.mode == "mape":
+        return main_mape(args)
     return main_chase(args)
 
 

@@ -53,6 +53,7 @@ typedef enum {
     CHASE_ERR_MAXCI = 5,            /* S:292 MaxCarbonIntensity must be > 0    */
     CHASE_ERR_FIT = 6,              /* S:135 rank-deficient after ridge        */
     CHASE_ERR_CHOICE = 7,           /* chase_replay: choice index out of range */
+    CHASE_ERR_ZERO_ACTUAL = 8,      /* chase_forecast_mape: a zero intensity */
     CHASE_ERR_CUDA = 10,
     CHASE_ERR_NCCL = 11,
     CHASE_ERR_WORKSPACE = 12        /* workspace NULL, misaligned or too small */
@@ -206,6 +207,21 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
                            uint8_t* d_choice, int64_t ld_c, double* d_forecast, int64_t ld_f,
                            chase_totals_t* d_per_trace, chase_sum_t* d_sum,
                            void* nccl_comm, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Forecast-evaluation sweep (the walk-forward Table 1 experiment, P:159-161;
+ * SPEC evaluate_models S:175-184, mape S:167-174): the Eq. 1 model fitted once
+ * on the L history points predicts every window w = L..n_steps-1 from the TRUE
+ * previous intensity (the first seeded by the last history point), and the
+ * MAPE of those predictions and of persistence (p(w) = c[w-1]) is written per
+ * trace:
+ *   d_mape   [n_traces][2] f64 out: {MAPE linear, MAPE persistence} in percent,
+ *            NaN where undefined;
+ *   d_status [n_traces] int32 out or NULL: 0, 4 (negative / non-finite value),
+ *            6 (fit failed) or 8 (a zero intensity: MAPE undefined).
+ * Needs refit_stride == 0 and period_steps <= 1.  Predictions are bit-identical
+ * to the oracle's; the MAPE sums agree to <= 1e-9 relative. */
+chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_mape,
+                                   int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 
 /* End-to-end variant with HOST inputs (the public call a user makes when the
  * traces live in host memory; bench.py's "e2e" figure): streams chunks of

@@ -25,7 +25,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 i32, i64, f64, vp, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
 
 CHASE_F32, CHASE_F64 = 0, 1
-STATUS = {0: "OK", 2: "INVALID", 3: "TRACE_EXHAUSTED", 4: "DATA", 5: "MAXCI", 6: "FIT", 7: "CHOICE",
+STATUS = {0: "OK", 2: "INVALID", 3: "TRACE_EXHAUSTED", 4: "DATA", 5: "MAXCI", 6: "FIT", 7: "CHOICE", 8: "ZERO_ACTUAL",
           10: "CUDA", 11: "NCCL", 12: "WORKSPACE"}
 
 
@@ -72,6 +72,8 @@ _lib.chase_replay.restype = ctypes.c_int
 _lib.chase_sweep.argtypes = [_P(Traces), _P(ForecastCfg), _P(Profile), i32, vp, _P(CostCfg), vp, vp, i64, vp, i64,
                              vp, vp, vp, vp, sz, vp]
 _lib.chase_sweep.restype = ctypes.c_int
+_lib.chase_forecast_mape.argtypes = [_P(Traces), _P(ForecastCfg), vp, vp, vp, sz, vp]
+_lib.chase_forecast_mape.restype = ctypes.c_int
 _lib.chase_diag_read.argtypes = [vp, _P(Diag), vp]
 _lib.chase_diag_read.restype = ctypes.c_int
 _lib.chase_sweep_host_staging_bytes.argtypes = [_P(Traces), i64, i32]
@@ -86,7 +88,8 @@ _lib.chase_last_error.restype = ctypes.c_char_p
 _lib.chase_version.restype = ctypes.c_char_p
 
 EXPORTED = ("chase_workspace_bytes", "chase_fit_forecast", "chase_plan_power_limits", "chase_replay",
-            "chase_sweep", "chase_sweep_host", "chase_sweep_host_staging_bytes", "chase_kernel_launches",
+            "chase_sweep", "chase_sweep_host", "chase_sweep_host_staging_bytes", "chase_forecast_mape",
+            "chase_kernel_launches",
             "chase_set_kernel_events", "chase_diag_read", "chase_last_error", "chase_version")
 
 
@@ -202,6 +205,13 @@ def sweep(traces: Traces, fcfg: ForecastCfg, profiles, etas, workspace, out_sum,
                             ctypes.byref(C.cfg), _ptr(job_samples), _ptr(choice), ld_c, _ptr(forecast), ld_f,
                             _ptr(per_trace), _ptr(out_sum), None, _ptr(workspace), workspace.numel(),
                             _stream(stream)), "chase_sweep")
+
+
+def forecast_mape(traces: Traces, fcfg: ForecastCfg, mape, workspace, *, status=None, stream=None):
+    """chase_forecast_mape: walk-forward MAPE of the fit-once model and of
+    persistence per trace (mape: f64 [n][2] device tensor; status: int32 [n])."""
+    _check(_lib.chase_forecast_mape(ctypes.byref(traces), ctypes.byref(fcfg), _ptr(mape), _ptr(status),
+                                    _ptr(workspace), workspace.numel(), _stream(stream)), "chase_forecast_mape")
 
 
 def kernel_launches() -> int:

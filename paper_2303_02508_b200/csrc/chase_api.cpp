@@ -379,6 +379,32 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     return CHASE_OK;
 }
 
+chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_mape,
+                                   int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+    chase_status_t st;
+    if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
+    if (fc_first(fcfg)) return fail(CHASE_ERR_INVALID, "chase_forecast_mape evaluates the fit-once forecaster "
+                                                       "(refit_stride 0, period_steps <= 1)");
+    if (traces->n_traces > 0 && !d_mape) return fail(CHASE_ERR_INVALID, "d_mape is NULL");
+    const int T = fcfg->steps_per_day;
+    const WsLayout WL = ws_layout(traces->n_traces, T, 1, 1, traces, fcfg);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, nullptr, 0, nullptr, 0);
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    cudaError_t e = launch_fit(make_fit(traces, fcfg->history_len, fcfg, ws, WL, 0, nullptr, nullptr), s);
+    if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
+    const double* phase = reinterpret_cast<const double*>(ws + WL.tables + sizeof(TablesHeader));
+    ev_start(s);
+    e = launch_mape(traces->data, traces->dtype == CHASE_F64, traces->ld, traces->n_traces, (int)traces->n_steps,
+                    fcfg->history_len, T, traces->phase0, phase, reinterpret_cast<const double*>(ws + WL.records),
+                    d_mape, d_status, s);
+    ev_stop(s);
+    if (e != cudaSuccess) return cuda_fail(e, "mape kernel");
+    return CHASE_OK;
+}
+
 chase_status_t chase_plan_power_limits(const double* d_forecast, int64_t n_traces, int64_t W, int64_t ld_f,
                                        const chase_profile_t* profiles, int32_t n_profiles,
                                        const uint8_t* d_profile_id, const chase_cost_cfg_t* cost,

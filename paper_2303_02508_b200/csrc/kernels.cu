@@ -22,6 +22,7 @@
 // in the same order as the oracle (DESIGN.md §3 Q9), so forecasts and choices
 // are bit-identical and dyadic replay totals are exact.
 #include <cfloat>
+#include <math_constants.h>
 #include <cstdlib>
 #include <cstring>
 
@@ -36,6 +37,7 @@ namespace {
 #include "k2_headline.cuh"
 #include "finalize.cuh"
 #include "rolling.cuh"
+#include "mape.cuh"
 
 int num_sms() {
     int dev = 0, sms = 0;
@@ -255,6 +257,31 @@ cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_t
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     if (f64) period_forecast_kernel<double><<<(unsigned)grid, 128, 0, s>>>(p);
     else period_forecast_kernel<float><<<(unsigned)grid, 128, 0, s>>>(p);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
+                        const double* phase, const double* records, double* out, int32_t* status, cudaStream_t s) {
+    if (n_traces <= 0) return cudaSuccess;
+    MapeParams p;
+    p.traces = traces;
+    p.ld = ld;
+    p.n_traces = n_traces;
+    p.N = N;
+    p.L = L;
+    p.T = T;
+    p.phase0 = phase0;
+    p.phase = phase;
+    p.records = records;
+    p.out = out;
+    p.status = status;
+    int64_t grid = (n_traces + 7) / 8;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    if (grid > cap) grid = cap;
+    const int smem = 2 * T * 8;
+    if (f64) mape_kernel<double><<<(unsigned)grid, 256, smem, s>>>(p);
+    else mape_kernel<float><<<(unsigned)grid, 256, smem, s>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }

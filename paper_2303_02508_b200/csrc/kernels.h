@@ -116,6 +116,9 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 // rolling refit (refit_stride >= 1): per-phase tables, then one thread per (trace, origin)
 int roll_phase_doubles(int T, int L);
+// forecast-evaluation sweep: walk-forward MAPE of the fit-once model and of persistence
+cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
+                        const double* phase, const double* records, double* out, int32_t* status, cudaStream_t s);
 // decision periods (period_steps > 1): one thread per (trace, period) writes the period's decision forecast
 cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
                            int P, const double* phase, const double* records, double* forecast, int64_t ld_f,

@@ -480,3 +480,29 @@ def test_decision_periods_fit_forecast_split_path():
     assert np.array_equal(np.isnan(fg), np.isnan(o["forecast"]))
     ok = ~np.isnan(o["forecast"])
     assert np.array_equal(fg[ok], o["forecast"][ok])
+
+
+# ------------------------------------------------------------------ forecast-evaluation sweep
+@pytest.mark.parametrize("T,L,N,n", [(24, 24, 24 + 8760, 40), (48, 48, 552, 7), (24, 23, 23 + 301, 5)])
+def test_forecast_mape_matches_oracle(T, L, N, n):
+    """Per-trace MAPE of the walk-forward fit-once forecaster and of
+    persistence (Table 1 shape) within 1e-9 of the oracle; statuses exact."""
+    interval = 86400 // T
+    tr = inputs.synth_traces_host(n, N, seed=500 + T, T=T)
+    tr[1, N // 2] = 0.0                       # zero actual: MAPE undefined (S:171)
+    tr[2, L + 3] = -5.0                       # negative: status 4
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=N, interval_s=interval)
+    f = cb.make_fcfg(interval_s=interval, history_len=L)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    mp = torch.empty((n, 2), dtype=torch.float64, device=DEV)
+    st = torch.empty(n, dtype=torch.int32, device=DEV)
+    cb.forecast_mape(t, f, mp, ws, status=st)
+    torch.cuda.synchronize()
+    om, ost, _ = oracle.evaluate_batch(tr, N=N, L=L, T=T)
+    g, gs = mp.cpu().numpy(), st.cpu().numpy()
+    assert list(gs) == list(ost)
+    assert np.array_equal(np.isnan(g), np.isnan(om))
+    ok = ~np.isnan(om)
+    np.testing.assert_allclose(g[ok], om[ok], rtol=1e-9, atol=0)
+    assert gs[1] == 8 and gs[2] == 4
