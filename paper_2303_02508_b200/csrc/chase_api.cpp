@@ -531,7 +531,10 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     p.forecast = d_forecast;
     p.ld_f = ld_f;
     bool aligned = aligned_start(traces, fcfg->history_len);
-    if (fc_first(fcfg)) {
+    // decision periods in the headline kernel itself (decided per chunk, then replayed)
+    const bool per_inplace = periods(fcfg) && headline_eligible(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p);
+    if (per_inplace) p.period = fcfg->period_steps;
+    if (fc_first(fcfg) && !per_inplace) {
         // rolling refit / decision periods: forecasts of every window first (into d_forecast when
         // given), then the fused argmin + replay reads them (sweep_kernel<..., FIN>)
         double* fc = d_forecast ? d_forecast : reinterpret_cast<double*>(ws + WL.roll_fc);

@@ -202,6 +202,89 @@ __device__ __noinline__ double partial_cs(const float* tv, int n) {
     return s;
 }
 
+// ---- decision periods (period_steps P > 1) ----------------
+// The choices of a chunk are decided before its replay: every period that
+// starts in the chunk forecasts recursively from the value before its start
+// (in the stage: the chunk's lag slot or a chunk value), Eq. 6 decides on the
+// horizon mean (the envelope lookup, else the canonical rule), and the period's
+// windows in this chunk get that byte; windows before the chunk's first period
+// start continue the previous chunk's last period (its byte, carried).  The
+// hot loop then only replays.  Same operation order as oracle_plan_trace.
+__device__ __noinline__ void period_decisions(const float* stagev, int cs, int wc, int Wt, int Pp, int phase_start,
+                                              int T, const double* Aeven, double wl, double invK, double Kc,
+                                              const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
+                                              const ProfileTable* pf, uint32_t k_carry, uint8_t* chb, int lane,
+                                              unsigned& n_slow) {
+    const int ce = cs + wc;
+    const int jf = (cs + Pp - 1) / Pp;
+    const int bf = min(jf * Pp, ce);
+    for (int q = lane; q < bf - cs; q += 32) chb[q] = (uint8_t)k_carry;
+    for (int j = jf + lane; j * Pp < ce; j += 32) {
+        const int b = j * Pp;
+        const int n = min(Pp, Wt - b);
+        int ph = (phase_start + b) % T;
+        double prev = (double)stagev[b - cs - 1], sum = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const double pr = __dadd_rn(Aeven[ph], __dmul_rn(wl, prev));  // Eq. 1, oracle_predict's order
+            const double f = pr > 0.0 ? pr : 0.0;
+            sum = __dadd_rn(sum, f);
+            prev = f;
+            ph = ph + 1 == T ? 0 : ph + 1;
+        }
+        const double chat = __ddiv_rn(sum, (double)n);
+        uint32_t k;
+        if (invK == 0.0) {
+            k = canonical_choose(chat, Kc, pt->a, pf->thr, pf->K);
+            ++n_slow;
+        } else {
+            const int h = __double2hiint(__dmul_rn(chat, invK));
+            const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+            k = (line_addr(h, ent8[idx], ZB) >> 8) & 0xffu;
+            if (k == (uint32_t)kZeroLine) {
+                k = canonical_choose(chat, Kc, pt->a, pf->thr, pf->K);
+                ++n_slow;
+            }
+        }
+        const int e = min(b + Pp, ce);
+        for (int q = b; q < e; ++q) chb[q - cs] = (uint8_t)k;
+    }
+}
+
+// Replay of one lane's windows from the staged choice bytes (period mode).
+__device__ __forceinline__ void replay_groups(const float* __restrict__ tv, int nwin, const uint8_t* __restrict__ bytes,
+                                              int prof, Acc& a) {
+    const int ngr = nwin >> 2;
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(bytes);
+#pragma unroll 1
+    for (int g = 0; g < ngr; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(tv + 4 * g);
+        a.vmin = fminf(fminf(fminf(a.vmin, v.x), v.y), fminf(v.z, v.w));
+        const uint32_t word = words[g];
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = (int)((word >> (8 * u)) & 0xffu);
+            const double cw = (double)vv[u];
+            const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, k));
+            a.S = __dadd_rn(a.S, ln.x);
+            a.E = __dadd_rn(a.E, ln.y);
+            a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+            a.Cs = __dadd_rn(a.Cs, cw);
+        }
+    }
+    for (int jj = 4 * ngr; jj < nwin; ++jj) {
+        const float raw = tv[jj];
+        const double cw = (double)raw;
+        const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, bytes[jj]));
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        a.Cs = __dadd_rn(a.Cs, cw);
+        a.bad |= bad_value(raw) ? 1 : 0;
+    }
+}
+
+template <bool PER>
 #ifdef CHASE_H_MAXNREG
 __global__ void __maxnreg__(CHASE_H_MAXNREG) sweep_fast_kernel(
 #else
@@ -302,6 +385,8 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         const uint2* e8 = ent8_all;
         const ProfileTable* pf = profs;
         const PairTable* pt = reinterpret_cast<const PairTable*>(heads);
+        int prof_i = 0;
+        uint32_t k_carry = 0;  // period mode: the decision of the period running into the next chunk
         for (int c = 0; c < nc; ++c) {
             const bool last = c == nc - 1;
             uint8_t* stage = stage0;
@@ -311,6 +396,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 // the record: model (fit_kernel) and this trace's eta-0 scalars (record [10..15], kernels.h)
                 const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
                 const int prof = (int)rec[13];
+                prof_i = prof;
                 pf = profs + prof;
                 pt = reinterpret_cast<const PairTable*>(heads + prof);
                 e8 = ent8_all + prof * kNB;
@@ -360,11 +446,20 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             bool issued = false;
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
-                const int ngr = invK == 0.0 ? 0 : nwin >> 2;
+                const int ngr = (PER || invK == 0.0) ? 0 : nwin >> 2;
+                if (PER) {  // decisions for the chunk's periods first, then the replay
+                    const int wc = last ? P.W_last : kHWarpW;
+                    period_decisions(reinterpret_cast<const float*>(stage) + P.off0, c * kHWarpW, wc, P.W, P.period,
+                                     P.phase_start, T, A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, k_carry, chb, lane,
+                                     n_slow);
+                    __syncwarp();
+                    k_carry = chb[wc - 1];
+                    replay_groups(tv, nwin, chb + j0, prof_i, a);
+                }
                 uint32_t* cdst = (CHASE_H_STG && store_choice)
                                      ? reinterpret_cast<uint32_t*>(P.choice + i * P.ld_c + c * kHWarpW + j0) : nullptr;
-                hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), cdst, a);
-                if (4 * ngr < nwin) {  // cold: a ragged last chunk, or Kc outside [2^-900, 2^900]
+                if (!PER) hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), cdst, a);
+                if (!PER && 4 * ngr < nwin) {  // cold: a ragged last chunk, or Kc outside [2^-900, 2^900]
                     if (invK == 0.0) {
                         a = fused_generic<true, false, float, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line, chb + j0,
                                                                     nullptr, Kc, pf);
@@ -373,7 +468,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                         acc_merge(a, hot_tail(tv, 4 * ngr, nwin, Ap, wl, invK, e8, ebase, ZB, chb + j0));
                     }
                 }
-                if (a.slow & 0x20202020u) {  // deferred windows: the canonical K-way rule
+                if (!PER && (a.slow & 0x20202020u)) {  // deferred windows: the canonical K-way rule
                     const SlowFix fx = fix_slow<float>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0);
                     a.S = __dadd_rn(a.S, fx.S);
                     a.E = __dadd_rn(a.E, fx.E);

@@ -107,6 +107,11 @@ cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+bool headline_eligible(int mode, bool f64, bool aligned, const SweepParams& p) {
+    return mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !p.fc_in &&
+           !getenv("CHASE_FORCE_GENERAL");
+}
+
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
     if (mode == MODE_PREDICT && p.fc_in) {  // rolling chase_fit_forecast: validation pass only
@@ -128,7 +133,7 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
         return aligned ? launch_sweep_t<MODE_FUSED, float, true, false, true>(p, s)
                        : launch_sweep_t<MODE_FUSED, float, false, false, true>(p, s);
     }
-    if (mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !getenv("CHASE_FORCE_GENERAL")) {
+    if (headline_eligible(mode, f64, aligned, p)) {
         // the headline shape: lean specialised kernel (k2_headline.cuh), with its own chunk geometry
         SweepParams q = p;
         {
@@ -158,16 +163,18 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
             smem = t > smem ? t : smem;
         }
         q.smem_total = smem;
-        cudaError_t err = cudaFuncSetAttribute(sweep_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const bool per = p.period > 1;
+        auto kern = per ? sweep_fast_kernel<true> : sweep_fast_kernel<false>;
+        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
         int per_sm = 0;
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_fast_kernel, kHThreads, smem);
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kHThreads, smem);
         if (err != cudaSuccess) return err;
         if (per_sm < 1) return cudaErrorInvalidConfiguration;
         int64_t grid = (int64_t)num_sms() * per_sm;
         const int64_t need = (p.n_traces + kHWarps - 1) / kHWarps;  // one trace per warp at least
         if (grid > need) grid = need;
-        sweep_fast_kernel<<<(unsigned)grid, kHThreads, smem, s>>>(q);
+        kern<<<(unsigned)grid, kHThreads, smem, s>>>(q);
         ++g_launches;
         return cudaGetLastError();
     }
@@ -253,7 +260,8 @@ cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_t
     p.records = records;
     p.forecast = forecast;
     p.ld_f = ld_f;
-    const int64_t grid = (n_traces * (int64_t)p.n_per + 127) / 128;
+    const int64_t warps = n_traces * (int64_t)((p.n_per + 31) / 32);
+    const int64_t grid = (warps + 3) / 4;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     if (f64) period_forecast_kernel<double><<<(unsigned)grid, 128, 0, s>>>(p);
     else period_forecast_kernel<float><<<(unsigned)grid, 128, 0, s>>>(p);

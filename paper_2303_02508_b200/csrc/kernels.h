@@ -58,6 +58,7 @@ struct SweepParams {
     int64_t ld_fin;
     int32_t kc_last;              // headline kernel: windows per lane in the last chunk (4 mod 8)
     int32_t smem_total;           // headline kernel: dynamic shared memory planned by the host
+    int32_t period;               // > 1: one decision per period of this many windows (headline kernel)
 };
 
 struct FitParams {
@@ -112,6 +113,9 @@ int64_t finalize_grid(int64_t n_traces);
 
 cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_t s);
 cudaError_t launch_fit(const FitParams& p, cudaStream_t s);
+// the specialised headline kernel applies (fp32, aligned, one eta, no forecast in/out); it also
+// runs decision periods in place (p.period > 1), every other period path is forecast-first
+bool headline_eligible(int mode, bool f64, bool aligned, const SweepParams& p);
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s);
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 // rolling refit (refit_stride >= 1): per-phase tables, then one thread per (trace, origin)

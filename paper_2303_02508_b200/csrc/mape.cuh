@@ -28,7 +28,6 @@ __global__ void __launch_bounds__(256) mape_kernel(const __grid_constant__ MapeP
     const int64_t GW = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int s0 = p.L;
     const int64_t n = p.N - s0;
-    const int step = 32 % T;
     for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < p.n_traces; i += GW) {
         const double* rec = p.records + i * kRecDoubles;
         int st = (int)rec[5];
@@ -36,24 +35,37 @@ __global__ void __launch_bounds__(256) mape_kernel(const __grid_constant__ MapeP
         const E* row = reinterpret_cast<const E*>(p.traces) + i * p.ld;
         double el = 0.0, ep = 0.0;
         int bad = 0, zero = 0;
+        // 4 windows per lane per iteration (w = base + lane + 32u): 8 independent loads in flight
         int ph = (int)(((int64_t)p.phase0 + s0 + lane) % T);
-        for (int base = s0; base < p.N; base += 32) {
-            const int w = base + lane;
-            if (w < p.N) {
-                const E raw = row[w];
-                const double cw = (double)raw, lag = (double)row[w - 1];
-                bad |= bad_value(raw) ? 1 : 0;
-                zero |= cw == 0.0 ? 1 : 0;
-                // Eq. 1 prediction, oracle_predict's rounding order
-                const double A = __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, ph_sm[ph])), __dmul_rn(wc, ph_sm[T + ph]));
-                const double pr = __dadd_rn(A, __dmul_rn(wl, lag));
-                const double pred = pr > 0.0 ? pr : 0.0;
-                const double r = __drcp_rn(cw);
-                el = __dadd_rn(el, __dmul_rn(fabs(__dsub_rn(cw, pred)), r));
-                ep = __dadd_rn(ep, __dmul_rn(fabs(__dsub_rn(cw, lag)), r));
+        const int step32 = 32 % T;
+        for (int base = s0; base < p.N; base += 128) {
+            E raw[4], lagr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int w = base + lane + 32 * u;
+                raw[u] = w < p.N ? row[w] : (E)1;
+                lagr[u] = w < p.N ? row[w - 1] : (E)1;
             }
-            ph += step;
-            if (ph >= T) ph -= T;
+            int phu = ph;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int w = base + lane + 32 * u;
+                if (w < p.N) {
+                    const double cw = (double)raw[u], lag = (double)lagr[u];
+                    bad |= bad_value(raw[u]) ? 1 : 0;
+                    zero |= cw == 0.0 ? 1 : 0;
+                    // Eq. 1 prediction, oracle_predict's rounding order
+                    const double A = __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, ph_sm[phu])), __dmul_rn(wc, ph_sm[T + phu]));
+                    const double pr = __dadd_rn(A, __dmul_rn(wl, lag));
+                    const double pred = pr > 0.0 ? pr : 0.0;
+                    const double r = __drcp_rn(cw);
+                    el = __dadd_rn(el, __dmul_rn(fabs(__dsub_rn(cw, pred)), r));
+                    ep = __dadd_rn(ep, __dmul_rn(fabs(__dsub_rn(cw, lag)), r));
+                }
+                phu += step32;
+                if (phu >= T) phu -= T;
+            }
+            ph = phu;
         }
         el = warp_sum(el);
         ep = warp_sum(ep);

@@ -108,29 +108,43 @@ struct PeriodParams {
 
 template <typename E>
 __global__ void __launch_bounds__(128) period_forecast_kernel(const __grid_constant__ PeriodParams p) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= p.n_traces * (int64_t)p.n_per) return;
-    const int64_t i = idx / p.n_per;
-    const int j = (int)(idx - i * p.n_per);
-    const int s0 = p.L, T = p.T;
-    const int b = s0 + j * p.P;
-    const int n = min(p.P, p.N - b);
+    // one warp per (trace, group of 32 periods): lane j forecasts period 32g + j, then the
+    // warp writes the group's decision values with coalesced stores (one period at a time)
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int n_grp = (p.n_per + 31) >> 5;
+    if (wid >= p.n_traces * (int64_t)n_grp) return;
+    const int64_t i = wid / n_grp;
+    const int g = (int)(wid - i * n_grp);
+    const int s0 = p.L, T = p.T, W = p.N - p.L;
+    const int j = 32 * g + lane;
     const E* row = reinterpret_cast<const E*>(p.traces) + i * p.ld;
     const double* rec = p.records + i * kRecDoubles;
     const double c0 = rec[0], ws = rec[1], wc = rec[2], wl = rec[3];
     const double* S = p.phase;
     const double* C = p.phase + T;
-    int ph = (int)(((int64_t)p.phase0 + b) % T);
-    double prev = (double)row[b - 1], sum = 0.0;
-    for (int k = 0; k < n; ++k) {
-        const double A = __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, S[ph])), __dmul_rn(wc, C[ph]));
-        const double pr = __dadd_rn(A, __dmul_rn(wl, prev));
-        const double f = pr > 0.0 ? pr : 0.0;
-        sum = __dadd_rn(sum, f);
-        prev = f;
-        ph = ph + 1 == T ? 0 : ph + 1;
+    double chat = 0.0;
+    if (j < p.n_per) {
+        const int b = s0 + j * p.P;
+        const int n = min(p.P, p.N - b);
+        int ph = (int)(((int64_t)p.phase0 + b) % T);
+        double prev = (double)row[b - 1], sum = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const double A = __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, S[ph])), __dmul_rn(wc, C[ph]));
+            const double pr = __dadd_rn(A, __dmul_rn(wl, prev));
+            const double f = pr > 0.0 ? pr : 0.0;
+            sum = __dadd_rn(sum, f);
+            prev = f;
+            ph = ph + 1 == T ? 0 : ph + 1;
+        }
+        chat = __ddiv_rn(sum, (double)n);
     }
-    const double chat = __ddiv_rn(sum, (double)n);
-    double* out = p.forecast + i * p.ld_f + (b - s0);
-    for (int k = 0; k < n; ++k) out[k] = chat;
+    double* out = p.forecast + i * p.ld_f;
+    const int jmax = min(32, p.n_per - 32 * g);
+    for (int jj = 0; jj < jmax; ++jj) {
+        const double v = __shfl_sync(kFull, chat, jj);
+        const int b = (32 * g + jj) * p.P;
+        const int n = min(p.P, W - b);
+        for (int k = lane; k < n; k += 32) out[b + k] = v;
+    }
 }
