@@ -63,6 +63,8 @@ def lib():
                                             vp, vp, vp, vp, vp, vp, i32, vp, f64, f64, f64, vp, vp,
                                             vp, vp, vp, i32]
         L.oracle_plan_batch_f32.restype = i32
+        L.oracle_timeline.argtypes = [vp, i32, i32, i32, vp, vp, i32, vp, vp, vp, f64, f64, vp]
+        L.oracle_timeline.restype = i32
         L.oracle_mape.argtypes = [vp, vp, i64]
         L.oracle_mape.restype = f64
         L.oracle_evaluate.argtypes = [vp, i32, i32, i32, i32, f64, f64, vp, vp, vp]
@@ -196,3 +198,24 @@ def evaluate_batch(traces, *, N, L, T, phase0=0, ridge=1e-8, tol=1e-12, threads=
     used = lib().oracle_evaluate_batch_f32(tr.ctypes.data, n, N, ld, L, T, phase0, ridge, tol, out.ctypes.data,
                                            st.ctypes.data, threads)
     return out, st, used
+
+
+def timeline(c, *, L, period=1, choice=None, forecast=None, limit_w, avg_power, thr, delta=3600.0, J=0.0):
+    """SPEC emit_timeline: rows [n_periods][8] = period_start,
+    forecast_ci, actual_mean_ci, chosen_limit_w, avg_power_w, samples_done,
+    energy_j, carbon_g (choice None: the max-limit baseline)."""
+    c = _f64(c)
+    N = len(c)
+    W = N - L
+    P = max(int(period), 1)
+    n_per = -(-W // P)
+    rows = np.empty((n_per, 8))
+    ch = None if choice is None else np.ascontiguousarray(choice, dtype=np.uint8)
+    fc = None if forecast is None else _f64(forecast)
+    lim = np.ascontiguousarray(limit_w, dtype=np.int32)
+    pw, th = _f64(avg_power), _f64(thr)
+    n = lib().oracle_timeline(c.ctypes.data, N, L, P, None if ch is None else ch.ctypes.data,
+                              None if fc is None else fc.ctypes.data, len(pw), lim.ctypes.data, pw.ctypes.data,
+                              th.ctypes.data, delta, J, rows.ctypes.data)
+    assert n == n_per
+    return rows

@@ -484,3 +484,49 @@ int32_t oracle_evaluate_batch_f32(const float* traces, int64_t n_traces, int64_t
     free(S); free(Cc);
     return used;
 }
+
+
+/* ---------------------------------------------------------------- timeline */
+/* SPEC emit_timeline: per-period rows of a planned replay. */
+int32_t oracle_timeline(const double* c, int32_t N, int32_t L, int32_t period, const uint8_t* choice,
+                        const double* forecast, int32_t K, const int32_t* limit_w, const double* avg_power,
+                        const double* thr, double delta, double J, double* rows) {
+    const int32_t s0 = L, W = N - L, P = period > 1 ? period : 1;
+    double S = 0.0;
+    int done = 0, np = 0;
+    for (int32_t b = 0; b < W; b += P, ++np) {
+        const int32_t n = W - b < P ? W - b : P;
+        double* r = rows + 8 * (size_t)np;
+        int k = choice ? choice[b] : K - 1;
+        double csum = 0.0, samples = 0.0, E = 0.0, C = 0.0;
+        for (int32_t q = 0; q < n; ++q) {
+            const int32_t w = s0 + b + q;
+            csum = csum + c[w];
+            if (done) continue;
+            int kw = choice ? choice[b + q] : K - 1;
+            double sk = thr[kw] * delta;
+            double prevS = S;
+            S = S + sk;
+            if (J > 0.0 && S >= J) {
+                double f = (J - prevS) / sk;
+                samples = samples + (J - prevS);
+                E = E + f * avg_power[kw];
+                C = C + f * (avg_power[kw] * c[w]);
+                done = 1;
+                continue;
+            }
+            samples = samples + sk;
+            E = E + avg_power[kw];
+            C = C + avg_power[kw] * c[w];
+        }
+        r[0] = (double)(s0 + b);
+        r[1] = forecast ? forecast[b] : NAN;
+        r[2] = csum / (double)n;
+        r[3] = (double)limit_w[k];
+        r[4] = avg_power[k];
+        r[5] = samples;
+        r[6] = E * delta;
+        r[7] = (C * delta) / 3.6e6;
+    }
+    return np;
+}

@@ -125,6 +125,22 @@ int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
                               uint8_t* choice, oracle_totals_t* totals,
                               double* sums, int32_t threads);
 
+/* SPEC emit_timeline (Figure 1/2 rows) for one trace:
+ * one row per decision period of `period` steps (<= 1: per window) starting
+ * at the job start s0 = L, from the planned choices (choice[W]; NULL: the
+ * max-limit baseline) and the decision forecasts (forecast[W] or
+ * NULL: NaN):
+ *   {period_start (absolute step), forecast_ci, actual_mean_ci (mean of c
+ *    over the period's windows), chosen_limit_w, avg_power_w, samples_done,
+ *    energy_j, carbon_g}
+ * with the fixed-work replay of oracle_replay split by period: full windows
+ * count s_k, P_k*Delta and P_k*Delta*c/3.6e6; the completion window its
+ * fraction f (samples J - S_before, so they sum to J exactly); later windows
+ * nothing.  rows[n_periods][8]; returns n_periods. */
+int32_t oracle_timeline(const double* c, int32_t N, int32_t L, int32_t period, const uint8_t* choice,
+                        const double* forecast, int32_t K, const int32_t* limit_w, const double* avg_power,
+                        const double* thr, double delta, double J, double* rows);
+
 /* SPEC mape (Table 1 metric P:159-161): 100/n * sum |a_i - p_i| / |a_i|.
  * Returns NaN when n < 1 or some a_i == 0 ("errors: zero actual"). */
 double oracle_mape(const double* actual, const double* predicted, int64_t n);
