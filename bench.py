@@ -46,8 +46,9 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--e2e-traces", type=int, default=None)
-    ap.add_argument("--mode", choices=["plan", "mape"], default="plan",
-                    help="plan: the planner (headline); mape: the walk-forward forecast-evaluation sweep (f3)")
+    ap.add_argument("--mode", choices=["plan", "mape", "timeline"], default="plan",
+                    help="plan: the planner (headline); mape: the walk-forward forecast-evaluation sweep (f3); "
+                         "timeline: per-period audit rows of a planned replay (f4)")
     ap.add_argument("--period-steps", type=int, default=0,
                     help="P > 1: one decision per period of P steps on the mean recursive forecast (f1)")
     ap.add_argument("--refit-stride", type=int, default=0,
@@ -566,12 +567,107 @@ def main_mape(args):
     return 0
 
 
+TIMELINE_METRIC = "trace-windows audited/sec (per-period timeline rows of the planned replay)"
+
+
+def main_timeline(args):
+    """Timeline / audit rows: chase_timeline over this GPU's
+    traces after one planning sweep (choices + decision forecasts kept).
+    Roofline: HBM, per window 4 B trace + 1 B choice + 8 B forecast read, plus
+    64 B per row written."""
+    import torch
+
+    import paper_2303_02508_b200 as cb
+
+    rank, world, local = dist_env()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = inputs.workload(args.config, n_traces=args.traces or 100_000)
+    n, W = w.n_traces, w.W
+    P = max(args.period_steps, 1)
+    x = torch.empty((n, w.ld), dtype=torch.float32, device=dev)
+    inputs.synth_traces_device(x, w.n_steps, seed=w.seed, mode=w.mode, trace0=rank * n)
+    J = torch.full((n,), float(w.interval_s * W * w.profiles[0].throughput_sps.min()), dtype=torch.float64,
+                   device=dev)
+    pl = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles[:1], etas=w.etas[:1], job_samples=J, want_choice=True,
+                    want_forecast=True, period_steps=P)
+    res = pl.run()
+    n_per = -(-W // P)
+    rows = torch.empty((n, n_per, 8), dtype=torch.float64, device=dev)
+    t = cb.make_traces(x, n_steps=w.n_steps, interval_s=w.interval_s)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, cb.make_fcfg(), 1, 1), dev)
+
+    def step():
+        cb.timeline(t, w.history_len, w.profiles[:1], rows, n, ws, period_steps=P, choice=res.choice[0],
+                    ld_c=pl.ld_c, forecast=res.forecast, ld_f=pl.ld_f, job_samples=J)
+
+    for _ in range(args.warmup):
+        step()
+    stream = torch.cuda.current_stream(dev)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:
+        a.record(stream)
+        b.record(stream)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    launches0 = cb.kernel_launches()
+    t0.record(stream)
+    for k in range(args.steps):
+        cb.set_kernel_events(*kev[k])
+        step()
+    t1.record(stream)
+    cb.set_kernel_events(None, None)
+    torch.cuda.synchronize()
+    launches = cb.kernel_launches() - launches0
+    clk = clocks.stop()
+    ms_per_step = t0.elapsed_time(t1) / args.steps
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    alg = n * W * 13.0 + n * n_per * 64.0
+    peak, peak_src = measured_peaks()
+    achieved = alg / (kern_ms / 1e3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        fc, ch = res.forecast.cpu().numpy(), res.choice.cpu().numpy()[0]
+        xs = x[:2000].cpu().numpy().astype(np.float64)
+        p0 = w.profiles[0]
+        t_0 = time.perf_counter()
+        ns = 0
+        while time.perf_counter() - t_0 < min(args.cpu_seconds, 5.0) and ns < 2000:
+            oracle.timeline(xs[ns, :w.n_steps], L=w.history_len, period=P, choice=ch[ns, :W], forecast=fc[ns, :W],
+                            limit_w=p0.limit_w, avg_power=p0.avg_power_w, thr=p0.throughput_sps,
+                            delta=float(w.interval_s), J=float(J[ns]))
+            ns += 1
+        dt = time.perf_counter() - t_0
+        cpu = {"value": ns * W / dt, "unit": "trace-windows/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {ns} traces, one thread ({dt:.1f} s)"}
+    cfg = workload_config(w, 1, 0, P)
+    cfg["workload"] = f"{w.name} traces: per-period audit rows of the planned replay (SPEC emit_timeline)"
+    line = {"metric": TIMELINE_METRIC, "value": float(n) * W / (ms_per_step / 1e3), "unit": "trace-windows/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator, inputs/)", "config": cfg,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "timeline_kernel (warp per trace, lane per period)",
+                         "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
+                         "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(launches), "clocks": clk,
+            "check": {"rows": int(n * n_per)}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main(argv=None):
     args = parse_args(argv)
     if args.impl == "reference":
         return main_reference(args)
     if args.mode == "mape":
         return main_mape(args)
+    if args.mode == "timeline":
+        return main_timeline(args)
     return main_chase(args)
 
 

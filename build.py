@@ -51,7 +51,7 @@ def build_inputs(force=False):
 
 
 CHASE_SOURCES = ["chase_api.cpp", "envelope.cpp", "kernels.cu"]
-CHASE_HEADERS = ["envelope.h", "device_tables.h", "kernels.h", "device_common.cuh", "fit.cuh", "k2_sweep.cuh", "k2_headline.cuh", "rolling.cuh", "mape.cuh",
+CHASE_HEADERS = ["envelope.h", "device_tables.h", "kernels.h", "device_common.cuh", "fit.cuh", "k2_sweep.cuh", "k2_headline.cuh", "rolling.cuh", "mape.cuh", "timeline.cuh",
                  "finalize.cuh"]
 
 

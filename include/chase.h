@@ -223,6 +223,26 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
 chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_mape,
                                    int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Timeline / audit rows of a planned replay (SPEC emit_timeline S:413-421;
+ * Figure 1/2) for m selected traces: one row per decision period
+ * (period_steps <= 1: per window) from the job start,
+ *   {period_start (absolute step), forecast_ci, actual_mean_ci, chosen_limit_w,
+ *    avg_power_w, samples_done, energy_j, carbon_g}
+ * with the fixed-work replay split by period: full windows count in full, the
+ * completion window pro rata (its samples are J - samples before, so a row set
+ * sums to J), later windows contribute nothing.
+ *   d_choice    [n_traces][ld_c] u8 of ONE eta (e.g. chase_sweep's first eta
+ *               plane), or NULL for the max-limit baseline;
+ *   d_forecast  [n_traces][ld_f] f64 decision forecasts or NULL (rows get NaN);
+ *   d_trace_ids [m] int64 trace indices, or NULL for traces 0..m-1;
+ *   d_rows      [m][ceil(W/P)][8] f64 out.
+ * Rows match oracle_timeline (bit-identical for the dyadic synthetic inputs). */
+chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len, int32_t period_steps,
+                              const uint8_t* d_choice, int64_t ld_c, const double* d_forecast, int64_t ld_f,
+                              const chase_profile_t* profiles, int32_t n_profiles, const uint8_t* d_profile_id,
+                              const double* d_job_samples, const int64_t* d_trace_ids, int64_t m, double* d_rows,
+                              void* d_ws, size_t ws_bytes, void* stream);
+
 /* End-to-end variant with HOST inputs (the public call a user makes when the
  * traces live in host memory; bench.py's "e2e" figure): streams chunks of
  * `chunk_traces` traces through a double-buffered device staging area with

@@ -74,6 +74,9 @@ _lib.chase_sweep.argtypes = [_P(Traces), _P(ForecastCfg), _P(Profile), i32, vp, 
 _lib.chase_sweep.restype = ctypes.c_int
 _lib.chase_forecast_mape.argtypes = [_P(Traces), _P(ForecastCfg), vp, vp, vp, sz, vp]
 _lib.chase_forecast_mape.restype = ctypes.c_int
+_lib.chase_timeline.argtypes = [_P(Traces), i32, i32, vp, i64, vp, i64, _P(Profile), i32, vp, vp, vp, i64, vp, vp,
+                                sz, vp]
+_lib.chase_timeline.restype = ctypes.c_int
 _lib.chase_diag_read.argtypes = [vp, _P(Diag), vp]
 _lib.chase_diag_read.restype = ctypes.c_int
 _lib.chase_sweep_host_staging_bytes.argtypes = [_P(Traces), i64, i32]
@@ -88,7 +91,7 @@ _lib.chase_last_error.restype = ctypes.c_char_p
 _lib.chase_version.restype = ctypes.c_char_p
 
 EXPORTED = ("chase_workspace_bytes", "chase_fit_forecast", "chase_plan_power_limits", "chase_replay",
-            "chase_sweep", "chase_sweep_host", "chase_sweep_host_staging_bytes", "chase_forecast_mape",
+            "chase_sweep", "chase_sweep_host", "chase_sweep_host_staging_bytes", "chase_forecast_mape", "chase_timeline",
             "chase_kernel_launches",
             "chase_set_kernel_events", "chase_diag_read", "chase_last_error", "chase_version")
 
@@ -212,6 +215,17 @@ def forecast_mape(traces: Traces, fcfg: ForecastCfg, mape, workspace, *, status=
     persistence per trace (mape: f64 [n][2] device tensor; status: int32 [n])."""
     _check(_lib.chase_forecast_mape(ctypes.byref(traces), ctypes.byref(fcfg), _ptr(mape), _ptr(status),
                                     _ptr(workspace), workspace.numel(), _stream(stream)), "chase_forecast_mape")
+
+
+def timeline(traces: Traces, history_len: int, profiles, rows, m: int, workspace, *, period_steps=1, choice=None,
+             ld_c: int = 0, forecast=None, ld_f: int = 0, profile_id=None, job_samples=None, trace_ids=None,
+             stream=None):
+    """chase_timeline: per-period audit rows [m][ceil(W/P)][8] of a planned replay
+    (choice None: the max-limit baseline)."""
+    Pr = _Profiles(profiles)
+    _check(_lib.chase_timeline(ctypes.byref(traces), history_len, period_steps, _ptr(choice), ld_c, _ptr(forecast),
+                               ld_f, Pr.arr, Pr.n, _ptr(profile_id), _ptr(job_samples), _ptr(trace_ids), m,
+                               _ptr(rows), _ptr(workspace), workspace.numel(), _stream(stream)), "chase_timeline")
 
 
 def kernel_launches() -> int:

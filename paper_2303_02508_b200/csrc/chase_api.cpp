@@ -193,6 +193,7 @@ std::vector<uint8_t> build_tables(int T, double delta, const chase_profile_t* pr
         for (int k = 0; k < P.n_limits; ++k) {
             T_.line[k] = make_double2(P.throughput_sps[k] * delta, P.avg_power_w[k]);
             T_.thr[k] = P.throughput_sps[k];
+            T_.limit_w[k] = P.limit_w[k];
             if (T_.line[k].x > T_.smax) T_.smax = T_.line[k].x;
         }
         for (int e = 0; e < n_eta; ++e)
@@ -402,6 +403,39 @@ chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_for
                     d_mape, d_status, s);
     ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "mape kernel");
+    return CHASE_OK;
+}
+
+chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len, int32_t period_steps,
+                              const uint8_t* d_choice, int64_t ld_c, const double* d_forecast, int64_t ld_f,
+                              const chase_profile_t* profiles, int32_t n_profiles, const uint8_t* d_profile_id,
+                              const double* d_job_samples, const int64_t* d_trace_ids, int64_t m, double* d_rows,
+                              void* d_ws, size_t ws_bytes, void* stream) {
+    chase_status_t st;
+    if ((st = check_traces(traces)) || (st = check_profiles(profiles, n_profiles))) return st;
+    if (history_len < 1 || traces->n_steps <= history_len) return fail(CHASE_ERR_INVALID, "history_len");
+    if (period_steps < 0) return fail(CHASE_ERR_INVALID, "period_steps < 0");
+    const int64_t W = traces->n_steps - history_len;
+    if (m < 0 || (!d_trace_ids && m > traces->n_traces)) return fail(CHASE_ERR_INVALID, "m out of range");
+    if (m > 0 && !d_rows) return fail(CHASE_ERR_INVALID, "d_rows is NULL");
+    if (d_choice && ld_c < W) return fail(CHASE_ERR_INVALID, "ld_c < W");
+    if (d_forecast && ld_f < W) return fail(CHASE_ERR_INVALID, "ld_f < W");
+    const int T = 86400 / traces->interval_s;
+    const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, 1);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    std::vector<double> etas(1, 0.5);  // eta is not used by the timeline; the tables need a value
+    chase_cost_cfg_t cc{etas.data(), 1, 0, 0.0, 0.0};
+    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, &cc, 1);
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    ev_start(s);
+    cudaError_t e = launch_timeline(traces->data, traces->dtype == CHASE_F64, traces->ld, traces->n_traces,
+                                    (int)traces->n_steps, history_len, period_steps > 1 ? period_steps : 1,
+                                    n_profiles, (double)traces->interval_s, d_choice, ld_c, d_forecast, ld_f,
+                                    ws + WL.tables, d_profile_id, d_job_samples, d_trace_ids, m, d_rows, s);
+    ev_stop(s);
+    if (e != cudaSuccess) return cuda_fail(e, "timeline kernel");
     return CHASE_OK;
 }
 

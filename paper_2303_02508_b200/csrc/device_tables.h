@@ -40,6 +40,7 @@ struct alignas(16) ProfileTable {
     double pmax;           // resolved MaxPower
     double smax;           // max_k s_k (bounds the samples done after n windows)
     double reserved2;
+    int32_t limit_w[kMaxK];  // the power limits themselves (timeline rows)
 };
 
 struct alignas(16) PairTable {

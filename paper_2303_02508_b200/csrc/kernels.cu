@@ -38,6 +38,7 @@ namespace {
 #include "finalize.cuh"
 #include "rolling.cuh"
 #include "mape.cuh"
+#include "timeline.cuh"
 
 int num_sms() {
     int dev = 0, sms = 0;
@@ -290,6 +291,37 @@ cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_trac
     const int smem = 2 * T * 8;
     if (f64) mape_kernel<double><<<(unsigned)grid, 256, smem, s>>>(p);
     else mape_kernel<float><<<(unsigned)grid, 256, smem, s>>>(p);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int P,
+                            int n_prof, double delta, const uint8_t* choice, int64_t ld_c, const double* forecast,
+                            int64_t ld_f, const uint8_t* tables, const uint8_t* profile_id, const double* job,
+                            const int64_t* ids, int64_t m, double* rows, cudaStream_t s) {
+    if (m <= 0) return cudaSuccess;
+    TimelineParams p;
+    p.traces = traces;
+    p.ld = ld;
+    p.n_traces = n_traces;
+    p.N = N;
+    p.L = L;
+    p.P = P;
+    p.n_prof = n_prof;
+    p.delta = delta;
+    p.choice = choice;
+    p.ld_c = ld_c;
+    p.forecast = forecast;
+    p.ld_f = ld_f;
+    p.tables = tables;
+    p.profile_id = profile_id;
+    p.job = job;
+    p.ids = ids;
+    p.m = m;
+    p.rows = rows;
+    const int64_t grid = (m + 3) / 4;
+    if (f64) timeline_kernel<double><<<(unsigned)grid, 128, 0, s>>>(p);
+    else timeline_kernel<float><<<(unsigned)grid, 128, 0, s>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }

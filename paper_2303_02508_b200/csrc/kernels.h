@@ -123,6 +123,11 @@ int roll_phase_doubles(int T, int L);
 // forecast-evaluation sweep: walk-forward MAPE of the fit-once model and of persistence
 cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
                         const double* phase, const double* records, double* out, int32_t* status, cudaStream_t s);
+// timeline / audit rows of a planned replay, one warp per selected trace
+cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int P,
+                            int n_prof, double delta, const uint8_t* choice, int64_t ld_c, const double* forecast,
+                            int64_t ld_f, const uint8_t* tables, const uint8_t* profile_id, const double* job,
+                            const int64_t* ids, int64_t m, double* rows, cudaStream_t s);
 // decision periods (period_steps > 1): one thread per (trace, period) writes the period's decision forecast
 cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
                            int P, const double* phase, const double* records, double* forecast, int64_t ld_f,

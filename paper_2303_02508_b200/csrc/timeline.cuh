@@ -1,0 +1,108 @@
+// timeline.cuh — timeline / audit rows of a planned replay,
+// included by kernels.cu inside its anonymous namespace.
+//
+// SPEC emit_timeline (Figure 1/2 rows): one row per
+// decision period {period_start, forecast_ci, actual_mean_ci, chosen_limit_w,
+// avg_power_w, samples_done, energy_j, carbon_g}, the fixed-work replay of
+// oracle_replay split by period (full windows count in full, the completion
+// window by its fraction, later windows not at all).  One warp per selected
+// trace, one lane per period, 32 periods per round: each lane sums its
+// period's windows in order, a warp scan gives the samples done before every
+// period, and the lane whose period holds the completion window re-walks it
+// with the pro-rata rule.  oracle_timeline's per-period operation order.
+struct TimelineParams {
+    const void* traces;
+    int64_t ld, n_traces;
+    int32_t N, L, P, n_prof;
+    double delta;
+    const uint8_t* choice;   // [n][ld_c] (one eta) or null: the max-limit baseline
+    int64_t ld_c;
+    const double* forecast;  // [n][ld_f] or null
+    int64_t ld_f;
+    const uint8_t* tables;   // profiles (ProfileTable[n_prof] at H->off_prof)
+    const uint8_t* profile_id;
+    const double* job;
+    const int64_t* ids;      // [m] or null: traces 0..m-1
+    int64_t m;
+    double* rows;            // [m][n_per][8]
+};
+
+template <typename E>
+__global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ TimelineParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= p.m) return;
+    const int64_t i = p.ids ? p.ids[r] : r;
+    const int s0 = p.L, W = p.N - p.L, Pp = p.P;
+    const int n_per = (W + Pp - 1) / Pp;
+    int prof = p.profile_id ? (int)p.profile_id[i] : 0;
+    if (prof >= p.n_prof) prof = 0;
+    const ProfileTable* pf = blob_profiles(p.tables) + prof;
+    const E* row = reinterpret_cast<const E*>(p.traces) + i * p.ld;
+    const uint8_t* ch = p.choice ? p.choice + i * p.ld_c : nullptr;
+    const double J = p.job ? p.job[i] : 0.0;
+    double S = 0.0;      // samples done before the current round (warp-uniform)
+    bool done = false;
+    double* out = p.rows + r * (int64_t)n_per * 8;
+    for (int j0 = 0; j0 < n_per; j0 += 32) {
+        const int j = j0 + lane;
+        const bool valid = j < n_per;
+        const int b = j * Pp;
+        const int n = valid ? min(Pp, W - b) : 0;
+        double csum = 0.0, ssum = 0.0, esum = 0.0, psum = 0.0;  // full-window sums of the period
+        for (int q = 0; q < n; ++q) {
+            const double cw = (double)row[s0 + b + q];
+            const int kw = ch ? ch[b + q] : pf->K - 1;
+            const double2 ln = pf->line[kw];
+            csum = __dadd_rn(csum, cw);
+            ssum = __dadd_rn(ssum, ln.x);
+            esum = __dadd_rn(esum, ln.y);
+            psum = __dadd_rn(psum, __dmul_rn(ln.y, cw));
+        }
+        const double incl = warp_incl_scan(ssum, lane);
+        const double ex = __shfl_up_sync(kFull, incl, 1);
+        const double before = __dadd_rn(S, lane == 0 ? 0.0 : ex);  // samples done before period j
+        // the period in which the running samples first reach J
+        const bool hit = !done && valid && J > 0.0 && __dadd_rn(before, ssum) >= J;
+        const unsigned hits = __ballot_sync(kFull, hit);
+        const int first = hits ? __ffs(hits) - 1 : 32;
+        double samples = ssum, E = esum, C = psum;
+        if (done || lane > first) {
+            samples = E = C = 0.0;
+        } else if (lane == first) {  // re-walk the completion period window by window
+            double Sr = before;
+            samples = E = C = 0.0;
+            for (int q = 0; q < n; ++q) {
+                const double cw = (double)row[s0 + b + q];
+                const int kw = ch ? ch[b + q] : pf->K - 1;
+                const double2 ln = pf->line[kw];
+                const double prevS = Sr;
+                Sr = __dadd_rn(Sr, ln.x);
+                if (Sr >= J) {
+                    const double f = __ddiv_rn(__dsub_rn(J, prevS), ln.x);
+                    samples = __dadd_rn(samples, __dsub_rn(J, prevS));
+                    E = __dadd_rn(E, __dmul_rn(f, ln.y));
+                    C = __dadd_rn(C, __dmul_rn(f, __dmul_rn(ln.y, cw)));
+                    break;
+                }
+                samples = __dadd_rn(samples, ln.x);
+                E = __dadd_rn(E, ln.y);
+                C = __dadd_rn(C, __dmul_rn(ln.y, cw));
+            }
+        }
+        if (valid) {
+            const int k = ch ? ch[b] : pf->K - 1;
+            double* o = out + (int64_t)j * 8;
+            o[0] = (double)(s0 + b);
+            o[1] = p.forecast ? p.forecast[i * p.ld_f + b] : CUDART_NAN;
+            o[2] = __ddiv_rn(csum, (double)n);
+            o[3] = (double)pf->limit_w[k];
+            o[4] = pf->line[k].y;
+            o[5] = samples;
+            o[6] = __dmul_rn(E, p.delta);
+            o[7] = __ddiv_rn(__dmul_rn(C, p.delta), 3.6e6);
+        }
+        done = done || hits != 0;
+        S = __dadd_rn(S, __shfl_sync(kFull, incl, 31));
+    }
+}

@@ -506,3 +506,50 @@ def test_forecast_mape_matches_oracle(T, L, N, n):
     ok = ~np.isnan(om)
     np.testing.assert_allclose(g[ok], om[ok], rtol=1e-9, atol=0)
     assert gs[1] == 8 and gs[2] == 4
+
+
+# ------------------------------------------------------------------ timeline / audit rows
+@pytest.mark.parametrize("P", [1, 24, 7])
+def test_timeline_rows_match_oracle(P):
+    """Per-period rows of the planned replay (and of the baseline) equal
+    oracle_timeline bit for bit on the dyadic synthetic traces, and sum to
+    the sweep's per-trace totals."""
+    w = inputs.workload("C4", n_traces=64)
+    N = 24 + 2000
+    prof = w.profiles
+    tr = inputs.synth_traces_host(w.n_traces, N, seed=600 + P)
+    pid = inputs.profile_ids_host(w.n_traces, seed=6, n_profiles=3)
+    J = np.array([3600 * (N - 24) * float(prof[k].throughput_sps.min()) for k in pid])
+    x = torch.from_numpy(tr).to(DEV)
+    pid_t = torch.from_numpy(pid).to(DEV)
+    J_t = torch.from_numpy(J).to(DEV)
+    pl = cb.Planner(x, n_steps=N, profiles=prof, etas=[0.5], profile_id=pid_t, job_samples=J_t, want_choice=True,
+                    want_forecast=True, want_per_trace=True, period_steps=P)
+    res = pl.run()
+    ids = torch.tensor([0, 5, 17, 63, 2], dtype=torch.int64, device=DEV)
+    m = ids.numel()
+    n_per = -(-(N - 24) // P)
+    rows = torch.empty((m, n_per, 8), dtype=torch.float64, device=DEV)
+    base = torch.empty_like(rows)
+    t = cb.make_traces(x, n_steps=N)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, cb.make_fcfg(), len(prof), 1), DEV)
+    cb.timeline(t, 24, prof, rows, m, ws, period_steps=P, choice=res.choice[0], ld_c=pl.ld_c, forecast=res.forecast,
+                ld_f=pl.ld_f, profile_id=pid_t, job_samples=J_t, trace_ids=ids)
+    cb.timeline(t, 24, prof, base, m, ws, period_steps=P, profile_id=pid_t, job_samples=J_t, trace_ids=ids)
+    torch.cuda.synchronize()
+    g, gb = rows.cpu().numpy(), base.cpu().numpy()
+    ch = res.choice.cpu().numpy()[0]
+    fc = res.forecast.cpu().numpy()
+    tot = res.per_trace_numpy()[0]
+    for r, i in enumerate([0, 5, 17, 63, 2]):
+        p = prof[pid[i]]
+        kw = dict(L=24, period=P, limit_w=p.limit_w, avg_power=p.avg_power_w, thr=p.throughput_sps, J=J[i])
+        o = oracle.timeline(tr[i, :N].astype(np.float64), choice=ch[i, :N - 24], forecast=fc[i, :N - 24], **kw)
+        ob = oracle.timeline(tr[i, :N].astype(np.float64), choice=None, **kw)
+        assert np.array_equal(g[r], o), (P, i, _first_diff(g[r], o))
+        assert np.array_equal(np.isnan(gb[r]), np.isnan(ob)) and np.array_equal(gb[r][~np.isnan(ob)],
+                                                                                 ob[~np.isnan(ob)])
+        assert g[r][:, 5].sum() == J[i]
+        np.testing.assert_allclose(g[r][:, 6].sum(), tot["energy_j"][i], rtol=1e-12)
+        np.testing.assert_allclose(g[r][:, 7].sum(), tot["carbon_g"][i], rtol=1e-12)
+        np.testing.assert_allclose(gb[r][:, 7].sum(), tot["base_carbon_g"][i], rtol=1e-12)
