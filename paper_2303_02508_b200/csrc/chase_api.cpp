@@ -48,7 +48,7 @@ constexpr size_t kWsAlign = 256;
 // per-(eta, trace) raw replay results [n_eta][n][8] | status [n] |
 // finalize block sums [ceil(n/256)][n_eta][8].
 struct WsLayout {
-    size_t diag, tables, records, raw, status, bad_list, block_sums, roll_ptab, roll_fc, total;
+    size_t diag, tables, records, raw, status, bad_list, block_sums, fit_prec, roll_ptab, roll_fc, total;
     int64_t ld_roll;  // row stride (doubles) of the rolling forecast scratch
 };
 
@@ -70,6 +70,7 @@ WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta, const chase_t
     w.status = o; o += round_up(n_traces, kWsAlign);
     w.bad_list = o; o += round_up(n_traces * 8, kWsAlign);
     w.block_sums = o; o += round_up((finalize_grid(n_traces) + 1) * n_eta * 8 * 8, kWsAlign);
+    w.fit_prec = o; o += round_up(8 + 2 * 63, 32) * 8;  // the job-start phase record (fit kernel, L <= 64)
     w.roll_ptab = w.roll_fc = o;
     w.ld_roll = 0;
     if (fc_first(f) && t && f->history_len >= 2 && t->n_steps > f->history_len) {
@@ -285,6 +286,7 @@ FitParams make_fit(const chase_traces_t* t, int L, const chase_forecast_cfg_t* f
     fp.profile_id = pid;
     fp.job = job;
     fp.records = reinterpret_cast<double*>(ws + WL.records);
+    fp.prec = reinterpret_cast<double*>(ws + WL.fit_prec);
     return fp;
 }
 

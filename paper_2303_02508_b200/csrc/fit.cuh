@@ -326,6 +326,13 @@ __device__ void fit_phase(const E* h, int L, int T, int rho, const double* pt, c
     rec[7] = (double)kind;
 }
 
+// The phase record of the fit-once job start (one thread, once per call).
+__global__ void fit_phase_kernel(const uint8_t* tables, int T, int L, int phase0, double* out) {
+    const TablesHeader* H = reinterpret_cast<const TablesHeader*>(tables);
+    const double* ph = reinterpret_cast<const double*>(tables + H->off_phase);
+    phase_record(ph, ph + T, T, L, phase0 % T, out);
+}
+
 // Fit kernel: stage the CTA's 128 histories (L <= 64) into smem with coalesced
 // loads (odd row stride), one lane per trace runs the canonical fit; also the
 // max-power baseline's completion count m: the first m with
@@ -354,7 +361,9 @@ __global__ void __launch_bounds__(128) fit_kernel(const __grid_constant__ FitPar
         }
     }
     __syncthreads();
-    if (staged && threadIdx.x == 0) phase_record(tab, tab + T, T, L, p.phase0 % T, prec);
+    if (staged) {  // the job-start phase record (fit_phase_kernel, once per call)
+        for (int q = threadIdx.x; q < phase_stride(L); q += blockDim.x) prec[q] = p.prec[q];
+    }
     __syncthreads();
     const int64_t i = first + threadIdx.x;
     if (i >= p.n_traces) return;

@@ -94,6 +94,10 @@ cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_
 
 cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
+    if (!p.baseline_only && p.L <= 64) {
+        fit_phase_kernel<<<1, 1, 0, s>>>(p.tables, p.T, p.L, p.phase0, p.prec);
+        ++g_launches;
+    }
     const int esz = p.is_f64 ? 8 : 4;
     const int smem = round16(128 * 65 * esz) + 2 * p.T * 8 + (p.L <= 64 ? phase_stride(p.L) * 8 : 0);
     const unsigned grid = (unsigned)((p.n_traces + 127) / 128);

@@ -73,6 +73,7 @@ struct FitParams {
     double* records;              // [n][16]
     double* models_out;           // optional user copy [n][8]
     double* max_ci_out;           // optional [n]
+    double* prec;                 // workspace slot for the job-start phase record (phase_stride(64) doubles)
     int32_t n_eta;                // > 0: also the single-eta sweep's per-trace scalars (record [10..15])
     int32_t reserved;
     double max_ci_fixed;          // > 0: fixed MaxCI
