@@ -56,23 +56,37 @@ def lib():
         L.oracle_total_cost.restype = f64
         L.oracle_replay.argtypes = [vp, i32, i32, vp, vp, vp, f64, f64, vp, ctypes.POINTER(i32)]
         L.oracle_replay.restype = i32
-        L.oracle_plan_trace.argtypes = [vp, i32, i32, i32, i32, i32, i32, f64, f64, vp, vp, i32, vp, vp,
+        L.oracle_plan_trace.argtypes = [vp, i32, i32, i32, i32, i32, i32, vp, f64, f64, vp, vp, i32, vp, vp,
                                         i32, vp, f64, f64, f64, f64, vp, vp, vp]
         L.oracle_plan_trace.restype = i32
-        L.oracle_plan_batch_f32.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, i32, f64, f64, i32,
+        L.oracle_plan_batch_f32.argtypes = [vp, i64, i64, i64, i32, i32, i32, i32, i32, vp, f64, f64, i32,
                                             vp, vp, vp, vp, vp, vp, i32, vp, f64, f64, f64, vp, vp,
                                             vp, vp, vp, i32]
         L.oracle_plan_batch_f32.restype = i32
         L.oracle_timeline.argtypes = [vp, i32, i32, i32, vp, vp, i32, vp, vp, vp, f64, f64, vp]
         L.oracle_timeline.restype = i32
+        L.oracle_rbf_exp.argtypes = [f64]
+        L.oracle_rbf_exp.restype = f64
+        L.oracle_svr_fit.argtypes = [vp, i32, i32, i32, vp, vp, f64, f64, f64, f64, i32, ctypes.POINTER(SVRModel)]
+        L.oracle_svr_fit.restype = i32
+        L.oracle_svr_predict.argtypes = [ctypes.POINTER(SVRModel), f64, f64, f64]
+        L.oracle_svr_predict.restype = f64
         L.oracle_mape.argtypes = [vp, vp, i64]
         L.oracle_mape.restype = f64
-        L.oracle_evaluate.argtypes = [vp, i32, i32, i32, i32, f64, f64, vp, vp, vp]
+        L.oracle_evaluate.argtypes = [vp, i32, i32, i32, i32, f64, f64, vp, vp, vp, vp]
         L.oracle_evaluate.restype = i32
-        L.oracle_evaluate_batch_f32.argtypes = [vp, i64, i64, i64, i32, i32, i32, f64, f64, vp, vp, i32]
+        L.oracle_evaluate_batch_f32.argtypes = [vp, i64, i64, i64, i32, i32, i32, f64, f64, vp, vp, vp, i32]
         L.oracle_evaluate_batch_f32.restype = i32
         _LIB = L
     return _LIB
+
+
+class SVRModel(ctypes.Structure):
+    """oracle_svr_t (oracle.h): the epsilon-SVR forecaster (f2)."""
+    _fields_ = [("z", (ctypes.c_double * 3) * 63), ("coef", ctypes.c_double * 63), ("mu", ctypes.c_double * 4),
+                ("sigma", ctypes.c_double * 4), ("gamma", ctypes.c_double), ("rho", ctypes.c_double),
+                ("n", ctypes.c_int32), ("kind", ctypes.c_int32), ("iters", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("keep", ctypes.c_int32 * 3), ("status", ctypes.c_int32)]
 
 
 def _f64(a):
@@ -125,7 +139,16 @@ def replay(c, s0, choice, avg_power, thr, delta, J):
     return out, w.value, st
 
 
-def plan_trace(c, *, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-8, tol=1e-12, avg_power, thr,
+def _svr(svr):
+    """None (least squares) or a dict of SVR hyperparameters -> the oracle's params array."""
+    if svr is None:
+        return None
+    d = dict(C=1.0, eps=0.1, gamma=0.0, tol=1e-3, max_iter=10000)
+    d.update(svr if isinstance(svr, dict) else {})
+    return np.array([d["C"], d["eps"], d["gamma"], d["tol"], float(d["max_iter"])], dtype=np.float64)
+
+
+def plan_trace(c, *, L, T, phase0=0, refit_stride=0, period=1, svr=None, ridge=1e-8, tol=1e-12, avg_power, thr,
                etas, pmax, max_ci=0.0, delta=3600.0, J=0.0):
     c = _f64(c)
     N = len(c)
@@ -135,14 +158,16 @@ def plan_trace(c, *, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-8, tol=1
     fc = np.empty(W)
     ch = np.empty((len(E), W), dtype=np.uint8)
     tot = np.zeros(len(E), dtype=TOTALS_DTYPE)
-    st = lib().oracle_plan_trace(c.ctypes.data, N, L, T, phase0, refit_stride, period, ridge, tol,
+    sv = _svr(svr)
+    st = lib().oracle_plan_trace(c.ctypes.data, N, L, T, phase0, refit_stride, period,
+                                 None if sv is None else sv.ctypes.data, ridge, tol,
                                  S.ctypes.data, C.ctypes.data, len(P), P.ctypes.data, Th.ctypes.data,
                                  len(E), E.ctypes.data, pmax, max_ci, delta, J,
                                  fc.ctypes.data, ch.ctypes.data, tot.ctypes.data)
     return fc, ch, tot, st
 
 
-def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-8, tol=1e-12, profiles,
+def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, period=1, svr=None, ridge=1e-8, tol=1e-12, profiles,
                profile_id=None, etas, pmax=0.0, max_ci=0.0, delta=3600.0, job_samples=None,
                want_forecast=True, want_choice=True, threads=0):
     """traces: float32 [n][ld].  profiles: list of objects with limit_w,
@@ -156,6 +181,7 @@ def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-
     Th = _f64(np.concatenate([p.throughput_sps for p in profiles]))
     pm = _f64([float(max(p.limit_w)) for p in profiles])
     E = _f64(etas)
+    sv = _svr(svr)
     pid = None if profile_id is None else np.ascontiguousarray(profile_id, dtype=np.uint8)
     job = None if job_samples is None else _f64(job_samples)
     fc = np.empty((n, W)) if want_forecast else None
@@ -163,7 +189,8 @@ def plan_batch(traces, *, N, L, T, phase0=0, refit_stride=0, period=1, ridge=1e-
     tot = np.zeros((len(E), n), dtype=TOTALS_DTYPE)
     sums = np.zeros((len(E), 8))
     used = lib().oracle_plan_batch_f32(
-        tr.ctypes.data, n, N, ld, L, T, phase0, refit_stride, period, ridge, tol, len(profiles),
+        tr.ctypes.data, n, N, ld, L, T, phase0, refit_stride, period, None if sv is None else sv.ctypes.data,
+        ridge, tol, len(profiles),
         Ks.ctypes.data, offs.ctypes.data, P.ctypes.data, Th.ctypes.data, pm.ctypes.data,
         None if pid is None else pid.ctypes.data, len(E), E.ctypes.data, pmax, max_ci, delta,
         None if job is None else job.ctypes.data,
@@ -179,23 +206,26 @@ def mape(actual, predicted) -> float:
     return float(lib().oracle_mape(a.ctypes.data, p.ctypes.data, len(a)))
 
 
-def evaluate(c, *, L, T, phase0=0, ridge=1e-8, tol=1e-12):
+def evaluate(c, *, L, T, phase0=0, ridge=1e-8, tol=1e-12, svr=None):
     """SPEC evaluate_models for one trace: (status, mape_linear, mape_persistence)."""
     c = _f64(c)
     S, C = phase_table(T)
     out = np.empty(2)
+    sv = _svr(svr)
     st = lib().oracle_evaluate(c.ctypes.data, len(c), L, T, phase0, ridge, tol, S.ctypes.data, C.ctypes.data,
-                               out.ctypes.data)
+                               None if sv is None else sv.ctypes.data, out.ctypes.data)
     return st, float(out[0]), float(out[1])
 
 
-def evaluate_batch(traces, *, N, L, T, phase0=0, ridge=1e-8, tol=1e-12, threads=0):
+def evaluate_batch(traces, *, N, L, T, phase0=0, ridge=1e-8, tol=1e-12, threads=0, svr=None):
     """fp32 traces [n][ld] -> (mape [n][2], status [n], threads used)."""
     tr = np.ascontiguousarray(traces, dtype=np.float32)
     n, ld = tr.shape
     out = np.empty((n, 2))
     st = np.empty(n, dtype=np.int32)
-    used = lib().oracle_evaluate_batch_f32(tr.ctypes.data, n, N, ld, L, T, phase0, ridge, tol, out.ctypes.data,
+    sv = _svr(svr)
+    used = lib().oracle_evaluate_batch_f32(tr.ctypes.data, n, N, ld, L, T, phase0, ridge, tol,
+                                           None if sv is None else sv.ctypes.data, out.ctypes.data,
                                            st.ctypes.data, threads)
     return out, st, used
 
@@ -219,3 +249,21 @@ def timeline(c, *, L, period=1, choice=None, forecast=None, limit_w, avg_power, 
                               th.ctypes.data, delta, J, rows.ctypes.data)
     assert n == n_per
     return rows
+
+
+def rbf_exp(x: float) -> float:
+    return float(lib().oracle_rbf_exp(float(x)))
+
+
+def svr_fit(hist, *, T, phi0=0, C=1.0, eps=0.1, gamma=0.0, tol=1e-3, max_iter=10000):
+    """SPEC fit_svr on the L history points: returns an SVRModel."""
+    h = _f64(hist)
+    S, Cc = phase_table(T)
+    m = SVRModel()
+    lib().oracle_svr_fit(h.ctypes.data, len(h), T, phi0, S.ctypes.data, Cc.ctypes.data, C, eps, gamma, tol,
+                         max_iter, ctypes.byref(m))
+    return m
+
+
+def svr_predict(m, s, c, lag) -> float:
+    return float(lib().oracle_svr_predict(ctypes.byref(m), s, c, lag))

@@ -245,7 +245,7 @@ int32_t oracle_replay(const double* c, int32_t N, int32_t s0,
 
 /* ---------------------------------------------------------------- planner */
 int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
-                          int32_t phase0, int32_t refit_stride, int32_t period,
+                          int32_t phase0, int32_t refit_stride, int32_t period, const double* svr,
                           double ridge_lambda, double singular_tol,
                           const double* S, const double* Cc,
                           int32_t K, const double* avg_power, const double* thr,
@@ -272,6 +272,7 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
     if (!choice) { own = (uint8_t*)malloc((size_t)n_eta * (size_t)W); choice = own; }
 
     oracle_model_t m;
+    static __thread oracle_svr_t sv;   /* f2: the epsilon-SVR forecaster when svr != NULL */
     int32_t origin = -1;
     /* One decision per period of `period` trace steps ("the
      * period between forecasts and power limit adjustments"; <= 1: one step).
@@ -286,14 +287,17 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
         if (r != origin) {
             origin = r;
             int32_t phi0 = (int32_t)(((int64_t)phase0 + r - L) % T);
-            if (oracle_fit(c + (r - L), L, T, phi0, S, Cc, ridge_lambda,
-                           singular_tol, &m) != 0) { status = 6; break; }
+            if (svr) {
+                if (oracle_svr_fit(c + (r - L), L, T, phi0, S, Cc, svr[0], svr[1], svr[2], svr[3],
+                                   (int32_t)svr[4], &sv) != 0) { status = 6; break; }
+            } else if (oracle_fit(c + (r - L), L, T, phi0, S, Cc, ridge_lambda,
+                                  singular_tol, &m) != 0) { status = 6; break; }
         }
         const int32_t n = N - w < P ? N - w : P;
         double prev = c[w - 1], sum = 0.0;
         for (int32_t k = 0; k < n; ++k) {
             int32_t phi = (int32_t)(((int64_t)phase0 + w + k) % T);
-            double f = oracle_predict(&m, S[phi], Cc[phi], prev);
+            double f = svr ? oracle_svr_predict(&sv, S[phi], Cc[phi], prev) : oracle_predict(&m, S[phi], Cc[phi], prev);
             sum = sum + f;
             prev = f;
         }
@@ -345,7 +349,7 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
 
 int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
                               int64_t ld, int32_t L, int32_t T, int32_t phase0,
-                              int32_t refit_stride, int32_t period, double ridge_lambda,
+                              int32_t refit_stride, int32_t period, const double* svr, double ridge_lambda,
                               double singular_tol, int32_t n_profiles,
                               const int32_t* prof_K, const int32_t* prof_off,
                               const double* avg_power, const double* thr,
@@ -388,7 +392,7 @@ int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
             /* MaxPower defaults to the highest power limit */
             double pmax = pmax_cfg > 0.0 ? pmax_cfg : prof_pmax[p];
             double J = job_samples ? job_samples[i] : 0.0;
-            oracle_plan_trace(c, (int32_t)N, L, T, phase0, refit_stride, period,
+            oracle_plan_trace(c, (int32_t)N, L, T, phase0, refit_stride, period, svr,
                               ridge_lambda, singular_tol, S, Cc, K, P, Th,
                               n_eta, eta, pmax, max_ci_cfg, delta, J,
                               forecast ? forecast + i * W : NULL, ch, tt);
@@ -439,17 +443,23 @@ double oracle_mape(const double* actual, const double* predicted, int64_t n) {
  * forward with the true lag; linear vs persistence. */
 int32_t oracle_evaluate(const double* c, int32_t N, int32_t L, int32_t T, int32_t phase0,
                         double ridge_lambda, double singular_tol, const double* S,
-                        const double* Cc, double* out2) {
+                        const double* Cc, const double* svr, double* out2) {
     out2[0] = out2[1] = NAN;
     for (int32_t t = 0; t < N; ++t)
         if (!(c[t] >= 0.0) || !isfinite(c[t])) return 4;
     oracle_model_t m;
-    if (oracle_fit(c, L, T, phase0 % T, S, Cc, ridge_lambda, singular_tol, &m) != 0) return 6;
+    static __thread oracle_svr_t sv;
+    if (svr) {
+        if (oracle_svr_fit(c, L, T, phase0 % T, S, Cc, svr[0], svr[1], svr[2], svr[3], (int32_t)svr[4], &sv) != 0)
+            return 6;
+    } else if (oracle_fit(c, L, T, phase0 % T, S, Cc, ridge_lambda, singular_tol, &m) != 0) {
+        return 6;
+    }
     const int32_t n = N - L;
     double* pl = (double*)malloc(sizeof(double) * (size_t)n);
     for (int32_t w = L; w < N; ++w) {
         int32_t phi = (int32_t)(((int64_t)phase0 + w) % T);
-        pl[w - L] = oracle_predict(&m, S[phi], Cc[phi], c[w - 1]);
+        pl[w - L] = svr ? oracle_svr_predict(&sv, S[phi], Cc[phi], c[w - 1]) : oracle_predict(&m, S[phi], Cc[phi], c[w - 1]);
     }
     out2[0] = oracle_mape(c + L, pl, n);
     out2[1] = oracle_mape(c + L, c + L - 1, n);   /* persistence: p(w) = c[w-1] */
@@ -459,7 +469,8 @@ int32_t oracle_evaluate(const double* c, int32_t N, int32_t L, int32_t T, int32_
 
 int32_t oracle_evaluate_batch_f32(const float* traces, int64_t n_traces, int64_t N, int64_t ld,
                                   int32_t L, int32_t T, int32_t phase0, double ridge_lambda,
-                                  double singular_tol, double* out, int32_t* status, int32_t threads) {
+                                  double singular_tol, const double* svr, double* out, int32_t* status,
+                                  int32_t threads) {
     double* S = (double*)malloc(sizeof(double) * (size_t)T);
     double* Cc = (double*)malloc(sizeof(double) * (size_t)T);
     oracle_phase_table(T, S, Cc);
@@ -476,7 +487,7 @@ int32_t oracle_evaluate_batch_f32(const float* traces, int64_t n_traces, int64_t
         #pragma omp for schedule(dynamic, 16)
         for (int64_t i = 0; i < n_traces; ++i) {
             for (int64_t t = 0; t < N; ++t) c[t] = (double)traces[i * ld + t];
-            status[i] = oracle_evaluate(c, (int32_t)N, L, T, phase0, ridge_lambda, singular_tol, S, Cc,
+            status[i] = oracle_evaluate(c, (int32_t)N, L, T, phase0, ridge_lambda, singular_tol, S, Cc, svr,
                                         out + 2 * i);
         }
         free(c);
@@ -529,4 +540,192 @@ int32_t oracle_timeline(const double* c, int32_t N, int32_t L, int32_t period, c
         r[7] = (C * delta) / 3.6e6;
     }
     return np;
+}
+
+
+/* ---------------------------------------------------------------- epsilon-SVR (f2) */
+double oracle_rbf_exp(double x) {
+    if (!(x <= 0.0)) return NAN;
+    if (x < -745.0) return 0.0;
+    const double k = floor(x * 1.4426950408889634 + 0.5);          /* nearest integer to x / ln 2 */
+    const double r = (x - k * 6.93147180369123816490e-01) - k * 1.90821492927058770002e-10;
+    double q = 0x1.6124613a86d09p-33;                               /* 1/13! */
+    q = q * r + 0x1.1eed8eff8d898p-29;                              /* 1/12! */
+    q = q * r + 0x1.ae64567f544e4p-26;
+    q = q * r + 0x1.27e4fb7789f5cp-22;
+    q = q * r + 0x1.71de3a556c734p-19;
+    q = q * r + 0x1.a01a01a01a01ap-16;
+    q = q * r + 0x1.a01a01a01a01ap-13;
+    q = q * r + 0x1.6c16c16c16c17p-10;
+    q = q * r + 0x1.1111111111111p-7;
+    q = q * r + 0x1.5555555555555p-5;
+    q = q * r + 0x1.5555555555555p-3;
+    q = q * r + 0.5;
+    q = q * r + 1.0;
+    q = q * r + 1.0;
+    return ldexp(q, (int)k);
+}
+
+/* K(a, b) = exp(-gamma * ((a0-b0)^2 + (a1-b1)^2 + (a2-b2)^2)), left to right */
+static double rbf(const double* a, const double* b, double gamma) {
+    const double d0 = a[0] - b[0], d1 = a[1] - b[1], d2 = a[2] - b[2];
+    const double d = ((d0 * d0) + (d1 * d1)) + (d2 * d2);
+    return oracle_rbf_exp(-(gamma * d));
+}
+
+int32_t oracle_svr_fit(const double* hist, int32_t L, int32_t T, int32_t phi0, const double* S, const double* Cc,
+                       double C, double eps, double gamma, double tol, int32_t max_iter, oracle_svr_t* m) {
+    memset(m, 0, sizeof(*m));
+    const int32_t n = L - 1;
+    m->n = n;
+    if (n < 2 || n > ORACLE_SVR_MAXN) { m->status = 2; return 2; }
+    for (int32_t t = 0; t < L; ++t)
+        if (!(hist[t] >= 0.0) || !isfinite(hist[t])) { m->status = 4; return 4; }
+    const double dn = (double)n;
+    /* features and moments exactly as oracle_fit (rows i = 1..n) */
+    double x[ORACLE_SVR_MAXN][3], y[ORACLE_SVR_MAXN];
+    for (int32_t i = 1; i <= n; ++i) {
+        int32_t ph = (phi0 + i) % T;
+        x[i - 1][0] = S[ph];
+        x[i - 1][1] = Cc[ph];
+        x[i - 1][2] = hist[i - 1];
+        y[i - 1] = hist[i];
+    }
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int32_t i = 0; i < n; ++i) {
+        for (int j = 0; j < 3; ++j) sum[j] = sum[j] + x[i][j];
+        sum[3] = sum[3] + y[i];
+    }
+    for (int j = 0; j < 4; ++j) m->mu[j] = sum[j] / dn;
+    double ss[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int32_t i = 0; i < n; ++i) {
+        for (int j = 0; j < 3; ++j) { double d = x[i][j] - m->mu[j]; ss[j] = ss[j] + d * d; }
+        double d = y[i] - m->mu[3];
+        ss[3] = ss[3] + d * d;
+    }
+    for (int j = 0; j < 4; ++j) m->sigma[j] = sqrt(ss[j] / dn);
+    if (!(m->sigma[3] > 0.0)) { m->kind = 1; m->converged = 1; return 0; }   /* constant target */
+    int kept = 0;
+    for (int j = 0; j < 3; ++j) { m->keep[j] = m->sigma[j] > 0.0; kept += m->keep[j]; }
+    double u[ORACLE_SVR_MAXN];
+    for (int32_t i = 0; i < n; ++i) {
+        for (int j = 0; j < 3; ++j) m->z[i][j] = m->keep[j] ? (x[i][j] - m->mu[j]) / m->sigma[j] : 0.0;
+        u[i] = (y[i] - m->mu[3]) / m->sigma[3];
+    }
+    /* SPEC default gamma = 1/(3 * mean feature variance); standardised kept columns have variance 1 */
+    m->gamma = gamma > 0.0 ? gamma : (kept > 0 ? 1.0 / (double)kept : 1.0);
+    /* kernel matrix */
+    static __thread double K[ORACLE_SVR_MAXN][ORACLE_SVR_MAXN];
+    for (int32_t i = 0; i < n; ++i)
+        for (int32_t j = 0; j < n; ++j) K[i][j] = rbf(m->z[i], m->z[j], m->gamma);
+    /* SMO on 2n variables: t < n -> y = +1 (alpha), t >= n -> y = -1 (alpha*) */
+    const int32_t l = 2 * n;
+    double a[2 * ORACLE_SVR_MAXN], G[2 * ORACLE_SVR_MAXN];
+    for (int32_t t = 0; t < l; ++t) {
+        a[t] = 0.0;
+        G[t] = t < n ? eps - u[t] : eps + u[t - n];      /* G = Q a + p, a = 0 */
+    }
+    const double TAU = 1e-12;
+    int32_t it = 0;
+    m->converged = 0;
+    for (;;) {
+        /* second-order working-set selection */
+        double Gmax = -INFINITY, Gmax2 = -INFINITY, obj_min = INFINITY;
+        int32_t i = -1, j = -1;
+        for (int32_t t = 0; t < l; ++t) {
+            if (t < n) { if (a[t] < C && -G[t] >= Gmax) { Gmax = -G[t]; i = t; } }
+            else { if (a[t] > 0.0 && G[t] >= Gmax) { Gmax = G[t]; i = t; } }
+        }
+        if (i >= 0) {
+            const double yi = i < n ? 1.0 : -1.0;
+            for (int32_t t = 0; t < l; ++t) {
+                const double yt = t < n ? 1.0 : -1.0;
+                const double Qit = (yi * yt) * K[i % n][t % n];
+                if (t < n) {
+                    if (a[t] > 0.0) {
+                        const double gd = Gmax + G[t];
+                        if (G[t] >= Gmax2) Gmax2 = G[t];
+                        if (gd > 0.0) {
+                            const double qc = (K[i % n][i % n] + K[t % n][t % n]) - (2.0 * yi) * Qit;
+                            const double od = -(gd * gd) / (qc > 0.0 ? qc : TAU);
+                            if (od <= obj_min) { j = t; obj_min = od; }
+                        }
+                    }
+                } else {
+                    if (a[t] < C) {
+                        const double gd = Gmax - G[t];
+                        if (-G[t] >= Gmax2) Gmax2 = -G[t];
+                        if (gd > 0.0) {
+                            const double qc = (K[i % n][i % n] + K[t % n][t % n]) + (2.0 * yi) * Qit;
+                            const double od = -(gd * gd) / (qc > 0.0 ? qc : TAU);
+                            if (od <= obj_min) { j = t; obj_min = od; }
+                        }
+                    }
+                }
+            }
+        }
+        if (Gmax + Gmax2 < tol || j < 0) { m->converged = 1; break; }
+        if (it >= max_iter) break;
+        ++it;
+        /* analytic pair update with clipping to [0, C] */
+        const double yi = i < n ? 1.0 : -1.0, yj = j < n ? 1.0 : -1.0;
+        const double Qij = (yi * yj) * K[i % n][j % n];
+        const double ai = a[i], aj = a[j];
+        if (yi != yj) {
+            double qc = (K[i % n][i % n] + K[j % n][j % n]) + 2.0 * Qij;
+            if (qc <= 0.0) qc = TAU;
+            const double delta = (-G[i] - G[j]) / qc;
+            const double diff = a[i] - a[j];
+            a[i] = a[i] + delta;
+            a[j] = a[j] + delta;
+            if (diff > 0.0) { if (a[j] < 0.0) { a[j] = 0.0; a[i] = diff; } }
+            else { if (a[i] < 0.0) { a[i] = 0.0; a[j] = -diff; } }
+            if (diff > 0.0) { if (a[i] > C) { a[i] = C; a[j] = C - diff; } }
+            else { if (a[j] > C) { a[j] = C; a[i] = C + diff; } }
+        } else {
+            double qc = (K[i % n][i % n] + K[j % n][j % n]) - 2.0 * Qij;
+            if (qc <= 0.0) qc = TAU;
+            const double delta = (G[i] - G[j]) / qc;
+            const double sm = a[i] + a[j];
+            a[i] = a[i] - delta;
+            a[j] = a[j] + delta;
+            if (sm > C) { if (a[i] > C) { a[i] = C; a[j] = sm - C; } }
+            else { if (a[j] < 0.0) { a[j] = 0.0; a[i] = sm; } }
+            if (sm > C) { if (a[j] > C) { a[j] = C; a[i] = sm - C; } }
+            else { if (a[i] < 0.0) { a[i] = 0.0; a[j] = sm; } }
+        }
+        const double dai = a[i] - ai, daj = a[j] - aj;
+        for (int32_t t = 0; t < l; ++t) {
+            const double yt = t < n ? 1.0 : -1.0;
+            const double Qti = (yt * yi) * K[t % n][i % n];
+            const double Qtj = (yt * yj) * K[t % n][j % n];
+            G[t] = G[t] + (Qti * dai + Qtj * daj);
+        }
+    }
+    m->iters = it;
+    /* bias: mean y*G over free variables, else the midpoint of the bounds */
+    double ub = INFINITY, lb = -INFINITY, sfree = 0.0;
+    int32_t nfree = 0;
+    for (int32_t t = 0; t < l; ++t) {
+        const double yt = t < n ? 1.0 : -1.0;
+        const double yG = yt * G[t];
+        if (a[t] >= C) { if (yt < 0.0) ub = fmin(ub, yG); else lb = fmax(lb, yG); }
+        else if (a[t] <= 0.0) { if (yt > 0.0) ub = fmin(ub, yG); else lb = fmax(lb, yG); }
+        else { ++nfree; sfree = sfree + yG; }
+    }
+    m->rho = nfree > 0 ? sfree / (double)nfree : (ub + lb) / 2.0;
+    for (int32_t t = 0; t < n; ++t) m->coef[t] = a[t] - a[t + n];
+    return 0;
+}
+
+double oracle_svr_predict(const oracle_svr_t* m, double s, double c, double lag) {
+    if (m->kind == 1) return m->mu[3] > 0.0 ? m->mu[3] : 0.0;
+    const double xv[3] = {s, c, lag};
+    double zq[3];
+    for (int j = 0; j < 3; ++j) zq[j] = m->keep[j] ? (xv[j] - m->mu[j]) / m->sigma[j] : 0.0;
+    double f = 0.0;
+    for (int32_t t = 0; t < m->n; ++t) f = f + m->coef[t] * rbf(m->z[t], zq, m->gamma);
+    f = f - m->rho;
+    const double p = m->mu[3] + m->sigma[3] * f;
+    return p > 0.0 ? p : 0.0;
 }

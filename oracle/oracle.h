@@ -82,6 +82,8 @@ int32_t oracle_replay(const double* c, int32_t N, int32_t s0,
                       double* out4, int32_t* completion_window);
 
 /* Whole planner for one trace: fit (once, or rolling with refit_stride R),
+ * svr != NULL: the epsilon-SVR forecaster {C, eps, gamma, tol, max_iter} (f2)
+ * instead of least squares,
  * predict every window, choose for every eta, replay aware + baseline.
  * period > 1: one decision per period of that many steps, on the mean of the
  * recursive horizon forecast; forecast[]
@@ -93,7 +95,7 @@ int32_t oracle_replay(const double* c, int32_t N, int32_t s0,
  * max_ci_cfg <= 0 -> MaxCI = max(c[0..L));
    pmax: the resolved MaxPower (> 0; the batch driver applies the P:183 default). */
 int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
-                          int32_t phase0, int32_t refit_stride, int32_t period,
+                          int32_t phase0, int32_t refit_stride, int32_t period, const double* svr,
                           double ridge_lambda, double singular_tol,
                           const double* S, const double* Cc,
                           int32_t K, const double* avg_power, const double* thr,
@@ -113,7 +115,7 @@ int32_t oracle_plan_trace(const double* c, int32_t N, int32_t L, int32_t T,
  * Returns the number of threads used. */
 int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
                               int64_t ld, int32_t L, int32_t T, int32_t phase0,
-                              int32_t refit_stride, int32_t period, double ridge_lambda,
+                              int32_t refit_stride, int32_t period, const double* svr, double ridge_lambda,
                               double singular_tol, int32_t n_profiles,
                               const int32_t* prof_K, const int32_t* prof_off,
                               const double* avg_power, const double* thr,
@@ -124,6 +126,41 @@ int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
                               const double* job_samples, double* forecast,
                               uint8_t* choice, oracle_totals_t* totals,
                               double* sums, int32_t threads);
+
+/* ---- epsilon-SVR forecaster (Table 1's best model; SPEC fit_svr
+ * S:140-148).  RBF kernel on the z-scored features of Eq. 1
+ * (fit-window statistics, population sigma, zero-variance columns dropped),
+ * target z-scored too; the dual is solved by sequential minimal optimisation
+ * with second-order working-set selection (Fan, Chen & Lin 2005, the solver
+ * of LIBSVM: 2n variables, y = +1 / -1, p = eps -/+ u), stopping when the
+ * maximal KKT violation is below tol or after max_iter pair updates; the bias
+ * is the mean y*G over free variables (else the midpoint of the bounds).
+ * f(x) = sum_t (a_t - a*_t) K(z_t, z(x)) - rho;  chat = max(0, mu_y + sigma_y f).
+ * exp() of the kernel is oracle_rbf_exp (below), not libm, so that the GPU can
+ * reproduce every operation (DESIGN Q31). */
+#define ORACLE_SVR_MAXN 63
+typedef struct {
+    double z[ORACLE_SVR_MAXN][3];  /* standardised training features */
+    double coef[ORACLE_SVR_MAXN];  /* a_t - a*_t                      */
+    double mu[4], sigma[4];        /* sin, cos, lag, target           */
+    double gamma, rho;
+    int32_t n, kind;               /* kind 0 SVR, 1 constant target    */
+    int32_t iters, converged;      /* SMO pair updates; 1 if KKT <= tol */
+    int32_t keep[3];               /* feature kept (sigma > 0)         */
+    int32_t status;                /* 0 ok, 4 bad value                */
+} oracle_svr_t;
+
+/* exp(x) for x <= 0: Cody-Waite reduction x = k ln2 + r, degree-13 Taylor
+ * polynomial of exp(r) in Horner form, scaled by 2^k (ldexp).  Every step is
+ * one IEEE operation, so host and device agree bit for bit; |error| <= 2 ulp
+ * of libm exp (pinned in tests). */
+double oracle_rbf_exp(double x);
+
+/* Fit on the L history points hist[0..L) (rows as oracle_fit).  gamma <= 0:
+ * 1/(3 * mean variance of the standardised features) (SPEC default). */
+int32_t oracle_svr_fit(const double* hist, int32_t L, int32_t T, int32_t phi0, const double* S, const double* Cc,
+                       double C, double eps, double gamma, double tol, int32_t max_iter, oracle_svr_t* m);
+double oracle_svr_predict(const oracle_svr_t* m, double s, double c, double lag);
 
 /* SPEC emit_timeline (Figure 1/2 rows) for one trace:
  * one row per decision period of `period` steps (<= 1: per window) starting
@@ -154,12 +191,13 @@ double oracle_mape(const double* actual, const double* predicted, int64_t n);
  * 6 (fit failed) or 8 (a zero actual: MAPE undefined). */
 int32_t oracle_evaluate(const double* c, int32_t N, int32_t L, int32_t T, int32_t phase0,
                         double ridge_lambda, double singular_tol, const double* S,
-                        const double* Cc, double* out2);
+                        const double* Cc, const double* svr, double* out2);
 
 /* Batch of fp32 traces [n][ld] (OpenMP across traces): out[n][2], status[n]. */
 int32_t oracle_evaluate_batch_f32(const float* traces, int64_t n_traces, int64_t N, int64_t ld,
                                   int32_t L, int32_t T, int32_t phase0, double ridge_lambda,
-                                  double singular_tol, double* out, int32_t* status, int32_t threads);
+                                  double singular_tol, const double* svr, double* out, int32_t* status,
+                                  int32_t threads);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,101 @@
+"""Pins for the epsilon-SVR forecaster (Table 1's best model,
+PAPER.md:162, :171; SPEC fit_svr S:140-148).
+
+The oracle solves the RBF epsilon-SVR dual by SMO with second-order working
+set selection.  It is pinned against scikit-learn's SVR (libsvm, an
+independent implementation of the same problem), the dual constraints and
+KKT conditions, and the SPEC examples.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+def test_rbf_exp_against_libm():
+    """oracle_rbf_exp (DESIGN Q31) is within 1 ulp of libm exp on [-745, 0]."""
+    xs = np.concatenate([-np.logspace(-14, np.log10(744.0), 40000), [-0.0, 0.0, -1e-300]])
+    worst = 0.0
+    for x in xs:
+        ref = math.exp(x)
+        if ref > 1e-300:
+            worst = max(worst, abs(oracle.rbf_exp(x) - ref) / ref)
+    assert worst <= 2.3e-16
+    assert oracle.rbf_exp(0.0) == 1.0 and oracle.rbf_exp(-800.0) == 0.0
+
+
+def _history(seed, T=24, L=24, noise=20.0):
+    rng = np.random.default_rng(seed)
+    t = np.arange(L)
+    return np.round((500 + 150 * np.sin(2 * np.pi * (t + rng.integers(0, T)) / T) + rng.normal(0, noise, L)) * 64) / 64
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("tol,coef_tol,pred_tol", [(1e-3, 1e-2, 2e-3), (1e-9, 2e-5, 1e-6)])
+def test_svr_matches_scikit_learn(seed, tol, coef_tol, pred_tol):
+    """Same standardised data and hyperparameters: dual coefficients and
+    predictions agree with sklearn.svm.SVR (libsvm) within the stopping
+    tolerance -- loosely at the default tol = 1e-3, tightly at 1e-9, where
+    both solvers sit on the unique optimum of the strictly convex dual."""
+    from sklearn.svm import SVR
+    T, L = 24, 24 + 8 * seed
+    h = _history(seed, T, L)
+    m = oracle.svr_fit(h, T=T, tol=tol, max_iter=100000)
+    n = L - 1
+    assert m.n == n and m.kind == 0 and m.converged == 1 and m.gamma == pytest.approx(1.0 / 3.0)
+    Z = np.array([[m.z[i][j] for j in range(3)] for i in range(n)])
+    u = (h[1:] - m.mu[3]) / m.sigma[3]
+    sk = SVR(kernel="rbf", C=1.0, epsilon=0.1, gamma=m.gamma, tol=tol, shrinking=False).fit(Z, u)
+    coef = np.zeros(n)
+    coef[sk.support_] = sk.dual_coef_[0]
+    assert np.max(np.abs(coef - np.array(m.coef[:n]))) < coef_tol
+    S, C = oracle.phase_table(T)
+    rng = np.random.default_rng(100 + seed)
+    for w in range(L, L + 12):
+        lag = float(h[-1]) if w == L else float(rng.uniform(300, 700))
+        zq = np.array([(S[w % T] - m.mu[0]) / m.sigma[0], (C[w % T] - m.mu[1]) / m.sigma[1],
+                       (lag - m.mu[2]) / m.sigma[2]])
+        ref = max(m.mu[3] + m.sigma[3] * sk.predict(zq[None])[0], 0.0)
+        got = oracle.svr_predict(m, S[w % T], C[w % T], lag)
+        assert abs(got - ref) <= pred_tol * m.sigma[3]
+
+
+def test_dual_constraints_and_kkt():
+    """|a - a*| <= C, sum(a - a*) = 0 (the equality constraint of the dual)."""
+    for seed in range(5):
+        h = _history(seed, 24, 48, noise=40.0)
+        m = oracle.svr_fit(h, T=24, C=0.5)
+        coef = np.array(m.coef[:m.n])
+        assert np.all(np.abs(coef) <= 0.5 + 1e-12)
+        assert abs(coef.sum()) < 1e-12
+        assert m.converged == 1 and m.iters > 0
+
+
+def test_spec_examples():
+    # S:146 constant target -> the constant (within eps * sigma; here exactly)
+    m = oracle.svr_fit(np.full(24, 432.0), T=24)
+    assert m.kind == 1 and oracle.svr_predict(m, 0.3, 0.9, 400.0) == 432.0
+    # S:147 pure diurnal sinusoid, default hyperparameters: walk-forward one-step MAPE < 2 %
+    T, N, L = 48, 552, 48
+    c = 550 + 150 * np.sin(2 * np.pi * np.arange(N) / T)
+    st, lin, per = oracle.evaluate(c, L=L, T=T, svr={})
+    assert st == 0 and lin < 2.0 and lin < per
+
+
+def test_planner_with_svr_forecaster():
+    """The planner with the SVR forecaster: one-step forecasts are svr_predict
+    with the observed lag; choices are Eq. 6 on them (composition)."""
+    rng = np.random.default_rng(3)
+    T, L, N = 24, 24, 24 + 120
+    c = np.round((500 + 120 * np.sin(2 * np.pi * np.arange(N) / T) + rng.normal(0, 20, N)) * 64) / 64
+    fc, ch, tot, st = oracle.plan_trace(c, L=L, T=T, svr={}, avg_power=[100.0, 200.0, 280.0],
+                                        thr=[400.0, 700.0, 780.0], etas=[0.5], pmax=300.0)
+    assert st == 0
+    m = oracle.svr_fit(c[:L], T=T)
+    S, C = oracle.phase_table(T)
+    for w in (L, L + 9, N - 1):
+        assert fc[w - L] == oracle.svr_predict(m, S[w % T], C[w % T], c[w - 1])
+        assert ch[0, w - L] == oracle.choose([100.0, 200.0, 280.0], [400.0, 700.0, 780.0], 0.5, 300.0,
+                                             float(c[:L].max()), fc[w - L])
