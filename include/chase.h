@@ -99,7 +99,22 @@ typedef struct {
                                     scratch as the rolling refit.               */
     double  ridge_lambda;        /* 1e-8                                   */
     double  singular_tol;        /* 1e-12: Cholesky pivot <= tol*(L-1) -> ridge (Q6) */
+    int32_t forecaster;          /* CHASE_FC_LINEAR (0): Eq. 1 least squares (§3.1).
+                                    CHASE_FC_SVR (1): the epsilon-SVR with an RBF
+                                    kernel on the same three features, z-scored on
+                                    the fit window (Table 1's best model, P:162,
+                                    P:171; SPEC fit_svr S:140-148), solved by SMO
+                                    with second-order working-set selection
+                                    (DESIGN §6.8).  Needs refit_stride == 0 and
+                                    history_len <= 64; combines with period_steps. */
+    int32_t svr_max_iter;        /* SMO iteration cap (>= 0; 10000 in the binding) */
+    double  svr_C;               /* box constraint C > 0 (1.0)                     */
+    double  svr_eps;             /* epsilon-tube half width >= 0, in z-units (0.1) */
+    double  svr_gamma;           /* RBF gamma >= 0; 0 = 1/(#non-constant features)  */
+    double  svr_tol;             /* KKT stopping tolerance > 0 (1e-3)              */
 } chase_forecast_cfg_t;
+
+enum { CHASE_FC_LINEAR = 0, CHASE_FC_SVR = 1 };
 
 /* D2 PowerProfile, HOST memory, copied during the call.
  * limit_w strictly increasing, n_limits in [2, 32], avg_power_w > 0 and
@@ -162,7 +177,9 @@ size_t chase_workspace_bytes(const chase_traces_t* traces, const chase_forecast_
  *   d_max_ci   [n_traces] f64 or NULL: max of the L history points;
  *   d_models   [n_traces][8] f64 or NULL: job-start model
  *              {c0, w_sin, w_cos, w_lag, max_ci, status, ridge, kind}
- *              with forecast = max(0, ((c0 + w_sin*S) + w_cos*C) + w_lag*lag). */
+ *              with forecast = max(0, ((c0 + w_sin*S) + w_cos*C) + w_lag*lag).
+ *              Must be NULL with the SVR forecaster (its dual lives in the
+ *              workspace). */
 chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg,
                                   double* d_forecast, int64_t ld_f, double* d_max_ci,
                                   double* d_models, void* d_ws, size_t ws_bytes, void* stream);
@@ -218,8 +235,10 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
  *            NaN where undefined;
  *   d_status [n_traces] int32 out or NULL: 0, 4 (negative / non-finite value),
  *            6 (fit failed) or 8 (a zero intensity: MAPE undefined).
- * Needs refit_stride == 0 and period_steps <= 1.  Predictions are bit-identical
- * to the oracle's; the MAPE sums agree to <= 1e-9 relative. */
+ * fcfg->forecaster selects the model (CHASE_FC_SVR: the first column is the
+ * SVR's MAPE, Table 1's comparison).  Needs refit_stride == 0 and
+ * period_steps <= 1.  Predictions are bit-identical to the oracle's; the MAPE
+ * sums agree to <= 1e-9 relative. */
 chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_mape,
                                    int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 

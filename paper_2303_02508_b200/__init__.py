@@ -36,7 +36,12 @@ class Traces(ctypes.Structure):
 
 class ForecastCfg(ctypes.Structure):
     _fields_ = [("steps_per_day", i32), ("history_len", i32), ("refit_stride", i32), ("period_steps", i32),
-                ("ridge_lambda", f64), ("singular_tol", f64)]
+                ("ridge_lambda", f64), ("singular_tol", f64), ("forecaster", i32), ("svr_max_iter", i32),
+                ("svr_C", f64), ("svr_eps", f64), ("svr_gamma", f64), ("svr_tol", f64)]
+
+
+FC_LINEAR, FC_SVR = 0, 1
+SVR_DEFAULTS = dict(C=1.0, eps=0.1, gamma=0.0, tol=1e-3, max_iter=10000)
 
 
 class Profile(ctypes.Structure):
@@ -137,8 +142,16 @@ def make_traces(x, *, n_steps: int | None = None, interval_s: int = 3600, phase0
 
 
 def make_fcfg(*, interval_s: int = 3600, history_len: int = 24, refit_stride: int = 0, period_steps: int = 0,
-              ridge: float = 1e-8, tol: float = 1e-12) -> ForecastCfg:
-    return ForecastCfg(86400 // interval_s, history_len, refit_stride, period_steps, ridge, tol)
+              ridge: float = 1e-8, tol: float = 1e-12, svr=None) -> ForecastCfg:
+    """svr: None for the Eq. 1 least-squares forecaster, else a dict of SVR
+    hyperparameters (keys of SVR_DEFAULTS; {} = the defaults)."""
+    if svr is None:
+        return ForecastCfg(86400 // interval_s, history_len, refit_stride, period_steps, ridge, tol, FC_LINEAR, 0,
+                           0.0, 0.0, 0.0, 0.0)
+    h = dict(SVR_DEFAULTS)
+    h.update(svr)
+    return ForecastCfg(86400 // interval_s, history_len, refit_stride, period_steps, ridge, tol, FC_SVR,
+                       int(h["max_iter"]), float(h["C"]), float(h["eps"]), float(h["gamma"]), float(h["tol"]))
 
 
 class _Profiles:
@@ -290,13 +303,13 @@ class Planner:
 
     def __init__(self, traces_tensor, *, n_steps: int, profiles, etas, interval_s=3600, history_len=24,
                  phase0=0, profile_id=None, job_samples=None, want_choice=True, want_forecast=False,
-                 want_per_trace=False, max_power_w=0.0, max_ci=0.0, refit_stride=0, period_steps=0):
+                 want_per_trace=False, max_power_w=0.0, max_ci=0.0, refit_stride=0, period_steps=0, svr=None):
         import torch
         self.x = traces_tensor
         dev = traces_tensor.device
         self.tr = make_traces(traces_tensor, n_steps=n_steps, interval_s=interval_s, phase0=phase0)
         self.fcfg = make_fcfg(interval_s=interval_s, history_len=history_len, refit_stride=refit_stride,
-                              period_steps=period_steps)
+                              period_steps=period_steps, svr=svr)
         self.profiles, self.etas = profiles, list(etas)
         n, W = traces_tensor.shape[0], n_steps - history_len
         self.n, self.W = n, W

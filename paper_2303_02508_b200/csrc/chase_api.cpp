@@ -48,14 +48,15 @@ constexpr size_t kWsAlign = 256;
 // per-(eta, trace) raw replay results [n_eta][n][8] | status [n] |
 // finalize block sums [ceil(n/256)][n_eta][8].
 struct WsLayout {
-    size_t diag, tables, records, raw, status, bad_list, block_sums, fit_prec, roll_ptab, roll_fc, total;
+    size_t diag, tables, records, raw, status, bad_list, block_sums, fit_prec, roll_ptab, roll_fc, svr_models, total;
     int64_t ld_roll;  // row stride (doubles) of the rolling forecast scratch
 };
 
 bool rolling(const chase_forecast_cfg_t* f) { return f && f->refit_stride > 0; }
 bool periods(const chase_forecast_cfg_t* f) { return f && f->period_steps > 1; }
-// forecasts precomputed per window (rolling refit or decision periods), then read by the sweep
-bool fc_first(const chase_forecast_cfg_t* f) { return rolling(f) || periods(f); }
+bool svr(const chase_forecast_cfg_t* f) { return f && f->forecaster == CHASE_FC_SVR; }
+// forecasts precomputed per window (rolling refit, decision periods or the SVR), then read by the sweep
+bool fc_first(const chase_forecast_cfg_t* f) { return rolling(f) || periods(f) || svr(f); }
 
 // Rolling refit (refit_stride >= 1) appends the per-phase fit tables and a
 // forecast scratch [n][round_up(W, 2)] f64 (used when d_forecast is NULL).
@@ -71,12 +72,13 @@ WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta, const chase_t
     w.bad_list = o; o += round_up(n_traces * 8, kWsAlign);
     w.block_sums = o; o += round_up((finalize_grid(n_traces) + 1) * n_eta * 8 * 8, kWsAlign);
     w.fit_prec = o; o += round_up(8 + 2 * 63, 32) * 8;  // the job-start phase record (fit kernel, L <= 64)
-    w.roll_ptab = w.roll_fc = o;
+    w.roll_ptab = w.roll_fc = w.svr_models = o;
     w.ld_roll = 0;
     if (fc_first(f) && t && f->history_len >= 2 && t->n_steps > f->history_len) {
         if (rolling(f)) { w.roll_ptab = o; o += round_up((int64_t)roll_phase_doubles(T, f->history_len) * 8, kWsAlign); }
         w.ld_roll = round_up(t->n_steps - f->history_len, 2);
         w.roll_fc = o; o += round_up(n_traces * w.ld_roll * 8, kWsAlign);
+        if (svr(f)) { w.svr_models = o; o += round_up(n_traces * kSvrModelDoubles * 8, kWsAlign); }
     }
     w.total = o;
     return w;
@@ -111,6 +113,16 @@ chase_status_t check_fcfg(const chase_traces_t* t, const chase_forecast_cfg_t* f
     if (f->period_steps > 1 && f->refit_stride > 0)
         return fail(CHASE_ERR_INVALID, "period_steps > 1 with refit_stride > 0 is not supported");
     if (!(f->ridge_lambda >= 0) || !(f->singular_tol >= 0)) return fail(CHASE_ERR_INVALID, "ridge/tol must be >= 0");
+    if (f->forecaster != CHASE_FC_LINEAR && f->forecaster != CHASE_FC_SVR)
+        return fail(CHASE_ERR_INVALID, "forecaster=%d (0 least squares, 1 SVR)", f->forecaster);
+    if (svr(f)) {
+        if (f->refit_stride > 0) return fail(CHASE_ERR_INVALID, "the SVR forecaster is fitted once (refit_stride 0)");
+        if (f->history_len > 64) return fail(CHASE_ERR_INVALID, "the SVR forecaster needs history_len <= 64");
+        if (!(f->svr_C > 0) || !std::isfinite(f->svr_C) || !(f->svr_eps >= 0) || !std::isfinite(f->svr_eps) ||
+            !(f->svr_gamma >= 0) || !std::isfinite(f->svr_gamma) || !(f->svr_tol > 0) || !std::isfinite(f->svr_tol) ||
+            f->svr_max_iter < 0)
+            return fail(CHASE_ERR_INVALID, "SVR hyperparameters: need C > 0, eps >= 0, gamma >= 0, tol > 0, max_iter >= 0");
+    }
     return CHASE_OK;
 }
 
@@ -319,6 +331,11 @@ cudaError_t launch_rolling_into(const chase_traces_t* t, const chase_forecast_cf
                                 double max_ci_fixed, double* fc, int64_t ldf, cudaStream_t s) {
     const int T = f->steps_per_day;
     const double* phase = reinterpret_cast<const double*>(ws + WL.tables + sizeof(TablesHeader));
+    if (svr(f))  // the SVR forecaster (fit once; one-step or per-period horizon means)
+        return launch_svr(t->data, t->dtype == CHASE_F64, t->ld, t->n_traces, (int)t->n_steps, f->history_len, T,
+                          t->phase0, f->period_steps > 1 ? f->period_steps : 1, f->svr_C, f->svr_eps, f->svr_gamma,
+                          f->svr_tol, f->svr_max_iter, phase, reinterpret_cast<double*>(ws + WL.records),
+                          reinterpret_cast<double*>(ws + WL.svr_models), fc, ldf, s);
     if (periods(f))  // decision periods: the recursive horizon means of the fit-once model
         return launch_periods(t->data, t->dtype == CHASE_F64, t->ld, t->n_traces, (int)t->n_steps, f->history_len, T,
                               t->phase0, f->period_steps, phase, reinterpret_cast<const double*>(ws + WL.records), fc,
@@ -335,7 +352,7 @@ extern "C" {
 
 const char* chase_last_error(void) { return g_err; }
 
-const char* chase_version(void) { return "chase-b200 0.2 (sm_100a; fit-once and rolling-refit planner)"; }
+const char* chase_version(void) { return "chase-b200 0.3 (sm_100a; least-squares and SVR forecasters, fit-once / rolling / periods)"; }
 
 size_t chase_workspace_bytes(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, int32_t n_profiles,
                              int32_t n_eta) {
@@ -351,6 +368,7 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
     const int64_t W = traces->n_steps - fcfg->history_len;
     if (!d_forecast || ld_f < W) return fail(CHASE_ERR_INVALID, "d_forecast NULL or ld_f < W");
+    if (svr(fcfg) && d_models) return fail(CHASE_ERR_INVALID, "d_models must be NULL with the SVR forecaster");
     const int T = fcfg->steps_per_day;
     // layout sized for (1 profile, 1 eta) so one workspace serves every entry point
     const WsLayout WL = ws_layout(traces->n_traces, T, 1, 1, traces, fcfg);
@@ -386,8 +404,9 @@ chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_for
                                    int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
-    if (fc_first(fcfg)) return fail(CHASE_ERR_INVALID, "chase_forecast_mape evaluates the fit-once forecaster "
-                                                       "(refit_stride 0, period_steps <= 1)");
+    if (rolling(fcfg) || periods(fcfg))
+        return fail(CHASE_ERR_INVALID, "chase_forecast_mape evaluates the fit-once one-step forecaster "
+                                       "(refit_stride 0, period_steps <= 1)");
     if (traces->n_traces > 0 && !d_mape) return fail(CHASE_ERR_INVALID, "d_mape is NULL");
     const int T = fcfg->steps_per_day;
     const WsLayout WL = ws_layout(traces->n_traces, T, 1, 1, traces, fcfg);
@@ -399,10 +418,16 @@ chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_for
     cudaError_t e = launch_fit(make_fit(traces, fcfg->history_len, fcfg, ws, WL, 0, nullptr, nullptr), s);
     if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
     const double* phase = reinterpret_cast<const double*>(ws + WL.tables + sizeof(TablesHeader));
+    const double* fc = nullptr;
     ev_start(s);
+    if (svr(fcfg)) {  // Table 1's SVR column: its one-step forecasts first, then the same MAPE pass
+        e = launch_rolling_into(traces, fcfg, ws, WL, 1.0, reinterpret_cast<double*>(ws + WL.roll_fc), WL.ld_roll, s);
+        if (e != cudaSuccess) return cuda_fail(e, "svr kernels");
+        fc = reinterpret_cast<const double*>(ws + WL.roll_fc);
+    }
     e = launch_mape(traces->data, traces->dtype == CHASE_F64, traces->ld, traces->n_traces, (int)traces->n_steps,
                     fcfg->history_len, T, traces->phase0, phase, reinterpret_cast<const double*>(ws + WL.records),
-                    d_mape, d_status, s);
+                    fc, WL.ld_roll, d_mape, d_status, s);
     ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "mape kernel");
     return CHASE_OK;
@@ -568,25 +593,26 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     p.ld_f = ld_f;
     bool aligned = aligned_start(traces, fcfg->history_len);
     // decision periods in the headline kernel itself (decided per chunk, then replayed)
-    const bool per_inplace = periods(fcfg) && headline_eligible(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p);
+    const bool per_inplace = periods(fcfg) && !svr(fcfg) && headline_eligible(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p);
     if (per_inplace) p.period = fcfg->period_steps;
     if (fc_first(fcfg) && !per_inplace) {
         // rolling refit / decision periods: forecasts of every window first (into d_forecast when
         // given), then the fused argmin + replay reads them (sweep_kernel<..., FIN>)
         double* fc = d_forecast ? d_forecast : reinterpret_cast<double*>(ws + WL.roll_fc);
         const int64_t ldf = d_forecast ? ld_f : WL.ld_roll;
-        if (rolling(fcfg)) ev_start(s);  // rolling mode: the refits dominate (timing hook)
+        // rolling refit / SVR: the forecaster dominates (timing hook)
+        if (rolling(fcfg) || svr(fcfg)) ev_start(s);
         e = launch_rolling_into(traces, fcfg, ws, WL, cost->max_ci, fc, ldf, s);
-        if (rolling(fcfg)) ev_stop(s);
+        if (rolling(fcfg) || svr(fcfg)) ev_stop(s);
         if (e != cudaSuccess) return cuda_fail(e, "rolling forecast kernel");
         p.fc_in = fc;
         p.ld_fin = ldf;
         p.forecast = nullptr;
         aligned = aligned && ldf % 2 == 0 && ((uintptr_t)fc & 15) == 0;
     }
-    if (!rolling(fcfg)) ev_start(s);
+    if (!rolling(fcfg) && !svr(fcfg)) ev_start(s);
     e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p, s);
-    if (!rolling(fcfg)) ev_stop(s);
+    if (!rolling(fcfg) && !svr(fcfg)) ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "sweep kernel");
     FinalizeParams fz = make_finalize(traces, fcfg->history_len, cost->n_eta, n_profiles, ws, WL, d_profile_id,
                                       d_job_samples, d_per_trace);

@@ -39,6 +39,7 @@ namespace {
 #include "rolling.cuh"
 #include "mape.cuh"
 #include "timeline.cuh"
+#include "svr.cuh"
 
 int num_sms() {
     int dev = 0, sms = 0;
@@ -275,7 +276,8 @@ cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_t
 }
 
 cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
-                        const double* phase, const double* records, double* out, int32_t* status, cudaStream_t s) {
+                        const double* phase, const double* records, const double* fc_in, int64_t ld_fin, double* out,
+                        int32_t* status, cudaStream_t s) {
     if (n_traces <= 0) return cudaSuccess;
     MapeParams p;
     p.traces = traces;
@@ -287,6 +289,8 @@ cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_trac
     p.phase0 = phase0;
     p.phase = phase;
     p.records = records;
+    p.fc_in = fc_in;
+    p.ld_fin = ld_fin;
     p.out = out;
     p.status = status;
     int64_t grid = (n_traces + 7) / 8;
@@ -295,6 +299,54 @@ cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_trac
     const int smem = 2 * T * 8;
     if (f64) mape_kernel<double><<<(unsigned)grid, 256, smem, s>>>(p);
     else mape_kernel<float><<<(unsigned)grid, 256, smem, s>>>(p);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_svr(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
+                       int P, double C, double eps, double gamma, double tol, int max_iter, const double* phase,
+                       double* records, double* models, double* forecast, int64_t ld_f, cudaStream_t s) {
+    static_assert(kSvrModelDoubles == kSvrDoubles, "model record size");
+    if (n_traces <= 0) return cudaSuccess;
+    if (L - 1 > kSvrMaxN || L < 3) return cudaErrorInvalidValue;
+    SvrParams p;
+    p.traces = traces;
+    p.ld = ld;
+    p.n_traces = n_traces;
+    p.N = N;
+    p.L = L;
+    p.T = T;
+    p.phase0 = phase0;
+    p.max_iter = max_iter;
+    p.P = P < 1 ? 1 : P;
+    p.n_per = (N - L + p.P - 1) / p.P;
+    p.C = C;
+    p.eps = eps;
+    p.gamma = gamma;
+    p.tol = tol;
+    p.phase = phase;
+    p.models = models;
+    p.records = records;
+    p.forecast = forecast;
+    p.ld_f = ld_f;
+    const int smem = kSvrWarps * svr_smem_doubles(L) * 8;
+    const int64_t grid = (n_traces + kSvrWarps - 1) / kSvrWarps;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (f64) {
+        cudaFuncSetAttribute(svr_fit_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        svr_fit_kernel<double><<<(unsigned)grid, 32 * kSvrWarps, smem, s>>>(p);
+    } else {
+        cudaFuncSetAttribute(svr_fit_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        svr_fit_kernel<float><<<(unsigned)grid, 32 * kSvrWarps, smem, s>>>(p);
+    }
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t threads = n_traces * (int64_t)p.n_per;
+    const int64_t g2 = (threads + 255) / 256;
+    if (g2 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (f64) svr_forecast_kernel<double><<<(unsigned)g2, 256, 0, s>>>(p);
+    else svr_forecast_kernel<float><<<(unsigned)g2, 256, 0, s>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }

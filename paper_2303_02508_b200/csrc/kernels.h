@@ -122,8 +122,16 @@ cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 // rolling refit (refit_stride >= 1): per-phase tables, then one thread per (trace, origin)
 int roll_phase_doubles(int T, int L);
 // forecast-evaluation sweep: walk-forward MAPE of the fit-once model and of persistence
+// fc_in != null: the predictions are read from fc_in [n][ld_fin] (the SVR forecaster's)
 cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
-                        const double* phase, const double* records, double* out, int32_t* status, cudaStream_t s);
+                        const double* phase, const double* records, const double* fc_in, int64_t ld_fin, double* out,
+                        int32_t* status, cudaStream_t s);
+// epsilon-SVR forecaster (f2): per-trace SMO fit (warp per trace) into models [n][kSvrModelDoubles],
+// then the per-period forecasts into forecast [n][ld_f]; records[.][5] is the status
+constexpr int kSvrModelDoubles = 268;
+cudaError_t launch_svr(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
+                       int P, double C, double eps, double gamma, double tol, int max_iter, const double* phase,
+                       double* records, double* models, double* forecast, int64_t ld_f, cudaStream_t s);
 // timeline / audit rows of a planned replay, one warp per selected trace
 cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int P,
                             int n_prof, double delta, const uint8_t* choice, int64_t ld_c, const double* forecast,

@@ -14,6 +14,8 @@ struct MapeParams {
     int32_t N, L, T, phase0;
     const double* phase;    // S[T], C[T]
     const double* records;  // fit-once models [n][16]
+    const double* fc_in;    // [n][ld_fin] predictions (the SVR's) or null: Eq. 1 from the record
+    int64_t ld_fin;
     double* out;            // [n][2]: MAPE linear, MAPE persistence (percent; NaN if undefined)
     int32_t* status;        // [n] or null: 0, 4 bad value, 6 fit failed, 8 zero actual
 };
@@ -54,10 +56,15 @@ __global__ void __launch_bounds__(256) mape_kernel(const __grid_constant__ MapeP
                     const double cw = (double)raw[u], lag = (double)lagr[u];
                     bad |= bad_value(raw[u]) ? 1 : 0;
                     zero |= cw == 0.0 ? 1 : 0;
-                    // Eq. 1 prediction, oracle_predict's rounding order
-                    const double A = __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, ph_sm[phu])), __dmul_rn(wc, ph_sm[T + phu]));
-                    const double pr = __dadd_rn(A, __dmul_rn(wl, lag));
-                    const double pred = pr > 0.0 ? pr : 0.0;
+                    double pred;
+                    if (p.fc_in) {
+                        pred = p.fc_in[i * p.ld_fin + (w - s0)];
+                    } else {  // Eq. 1 prediction, oracle_predict's rounding order
+                        const double A =
+                            __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, ph_sm[phu])), __dmul_rn(wc, ph_sm[T + phu]));
+                        const double pr = __dadd_rn(A, __dmul_rn(wl, lag));
+                        pred = pr > 0.0 ? pr : 0.0;
+                    }
                     const double r = __drcp_rn(cw);
                     el = __dadd_rn(el, __dmul_rn(fabs(__dsub_rn(cw, pred)), r));
                     ep = __dadd_rn(ep, __dmul_rn(fabs(__dsub_rn(cw, lag)), r));

@@ -194,3 +194,32 @@ def test_decision_periods_validation_and_workspace():
                       (cb.make_fcfg(period_steps=4, refit_stride=2), "refit_stride")]:
         with pytest.raises(cb.ChaseError, match=needle):
             cb.sweep(tr, f, [prof], [0.5], _ws(), s, stream=0)
+
+
+def test_svr_forecaster_validation_and_workspace():
+    """f2: the SVR forecaster adds the per-trace dual models and the forecast
+    scratch to the workspace, and rejects what it does not support."""
+    import torch
+    cb, x, tr = _args(n=10)
+    a = cb.workspace_bytes(tr, cb.make_fcfg(), 1, 1)
+    b = cb.workspace_bytes(tr, cb.make_fcfg(svr={}), 1, 1)
+    W = tr.n_steps - 24
+    assert b - a >= 10 * ((W + 1) // 2 * 2) * 8 + 10 * 268 * 8
+    f = cb.make_fcfg(svr={})
+    assert (f.forecaster, f.svr_C, f.svr_eps, f.svr_gamma, f.svr_tol, f.svr_max_iter) == (1, 1.0, 0.1, 0.0, 1e-3, 10000)
+    prof = inputs.make_profile("resnet50", inputs.LIMITS_9)
+    s = torch.zeros((1, 8), dtype=torch.float64)
+    bad_kind = cb.make_fcfg()
+    bad_kind.forecaster = 7
+    for f, needle in [(bad_kind, "forecaster"),
+                      (cb.make_fcfg(svr={}, refit_stride=24), "refit_stride"),
+                      (cb.make_fcfg(svr={}, history_len=65), "history_len"),
+                      (cb.make_fcfg(svr={"C": 0.0}), "hyperparameters"),
+                      (cb.make_fcfg(svr={"eps": -1.0}), "hyperparameters"),
+                      (cb.make_fcfg(svr={"tol": 0.0}), "hyperparameters"),
+                      (cb.make_fcfg(svr={"gamma": float("nan")}), "hyperparameters"),
+                      (cb.make_fcfg(svr={"max_iter": -1}), "hyperparameters")]:
+        with pytest.raises(cb.ChaseError, match=needle):
+            cb.sweep(tr, f, [prof], [0.5], _ws(), s, stream=0)
+    with pytest.raises(cb.ChaseError, match="d_models"):
+        cb.fit_forecast(tr, cb.make_fcfg(svr={}), _ws(), W, _ws(), models=_ws(), stream=0)

@@ -23,13 +23,14 @@ DEV = torch.device("cuda:0")
 
 
 def run_sweep(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0,
-              dtype=torch.float32, forecast=True, refit_stride=0, period_steps=0):
+              dtype=torch.float32, forecast=True, refit_stride=0, period_steps=0, svr=None):
     x = torch.from_numpy(np.ascontiguousarray(tr_host)).to(DEV, dtype)
     pid_t = None if pid is None else torch.from_numpy(np.ascontiguousarray(pid, np.uint8)).to(DEV)
     J_t = None if J is None else torch.from_numpy(np.ascontiguousarray(J, np.float64)).to(DEV)
     pl = cb.Planner(x, n_steps=N, profiles=profiles, etas=etas, interval_s=interval_s, history_len=L,
                     phase0=phase0, profile_id=pid_t, job_samples=J_t, want_choice=True, want_forecast=forecast,
-                    want_per_trace=True, max_ci=max_ci, refit_stride=refit_stride, period_steps=period_steps)
+                    want_per_trace=True, max_ci=max_ci, refit_stride=refit_stride, period_steps=period_steps,
+                    svr=svr)
     res = pl.run()
     torch.cuda.synchronize()
     out = dict(sums=res.sums.cpu().numpy(), totals=res.per_trace_numpy(),
@@ -39,10 +40,10 @@ def run_sweep(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=
 
 
 def run_oracle(tr_host, N, profiles, etas, *, pid=None, J=None, L=24, interval_s=3600, phase0=0, max_ci=0.0,
-               refit_stride=0, period_steps=0):
+               refit_stride=0, period_steps=0, svr=None):
     T = 86400 // interval_s
     return oracle.plan_batch(np.ascontiguousarray(tr_host, np.float32), N=N, L=L, T=T, phase0=phase0,
-                             refit_stride=refit_stride, period=period_steps,
+                             refit_stride=refit_stride, period=period_steps, svr=svr,
                              profiles=profiles, profile_id=pid, etas=etas, max_ci=max_ci,
                              delta=float(interval_s), job_samples=J)
 
@@ -553,3 +554,87 @@ def test_timeline_rows_match_oracle(P):
         np.testing.assert_allclose(g[r][:, 6].sum(), tot["energy_j"][i], rtol=1e-12)
         np.testing.assert_allclose(g[r][:, 7].sum(), tot["carbon_g"][i], rtol=1e-12)
         np.testing.assert_allclose(gb[r][:, 7].sum(), tot["base_carbon_g"][i], rtol=1e-12)
+
+
+# ------------------------------------------------------------------ epsilon-SVR forecaster
+@pytest.mark.parametrize("P,L,N,etas,n,interval", [
+    (1, 24, 24 + 500, [0.5], 33, 3600),        # one-step, several CTAs of fit warps, ragged tail
+    (24, 24, 24 + 2000, [0.4, 0.8], 9, 3600),  # daily decisions on the recursive SVR horizon
+    (1, 23, 23 + 301, [0.6], 5, 3600),         # odd L: unaligned tiles
+    (1, 64, 64 + 600, [0.5], 6, 3600),         # the largest SVR history (n = 63 dual pairs)
+    (5, 48, 48 + 504, [0.3], 7, 1800),         # T = 48 (the paper's 30-minute split)
+])
+def test_svr_forecaster_parity(P, L, N, etas, n, interval):
+    """The SVR fit (SMO on the dual), its forecasts and the plan: forecasts
+    bit-identical to the oracle's, choices and totals exact."""
+    prof = [inputs.make_profile("bert", inputs.LIMITS_9)]
+    T = 86400 // interval
+    tr = inputs.synth_traces_host(n, N, seed=700 + L + P, T=T)
+    J = np.full(n, interval * (N - L) * prof[0].throughput_sps.min() * 0.8)
+    g = run_sweep(tr, N, prof, etas, J=J, L=L, interval_s=interval, period_steps=P, svr={})
+    o = run_oracle(tr, N, prof, etas, J=J, L=L, interval_s=interval, period_steps=P, svr={})
+    assert np.all(o["totals"]["status"] == 0)
+    assert_parity(g, o)
+    # the SVR forecasts differ from the least-squares ones (a different model actually ran)
+    lin = run_oracle(tr, N, prof, etas, J=J, L=L, interval_s=interval, period_steps=P)
+    assert not np.array_equal(lin["forecast"], o["forecast"])
+
+
+@pytest.mark.parametrize("hp", [dict(C=0.5, eps=0.05), dict(gamma=0.7, tol=1e-6), dict(max_iter=3),
+                                dict(C=20.0, eps=0.0, tol=1e-9, max_iter=100000)])
+def test_svr_hyperparameters_parity(hp):
+    """Box constraint, tube width, gamma, tolerance and the iteration cap all
+    reach the device solver unchanged (bit-identical forecasts)."""
+    prof = [inputs.make_profile("resnet50", inputs.LIMITS_9)]
+    N, n = 24 + 300, 12
+    tr = inputs.synth_traces_host(n, N, seed=91)
+    g = run_sweep(tr, N, prof, [0.5], svr=hp)
+    o = run_oracle(tr, N, prof, [0.5], svr=hp)
+    assert_parity(g, o)
+
+
+def test_svr_degenerate_and_invalid_traces():
+    """Constant history (the constant model), a constant phase column cannot
+    occur at T = 24, a negative value in the history (status 4) and in the
+    future (status 4), f64 traces."""
+    prof = [inputs.make_profile("vit", inputs.LIMITS_9)]
+    N, n = 24 + 200, 8
+    tr = inputs.synth_traces_host(n, N, seed=17)
+    tr[1, :24] = 412.5                          # constant history -> kind 1, forecast = the constant
+    tr[2, 5] = -1.0                             # bad history value
+    tr[3, 100] = float("nan")                   # bad future value
+    tr[4, :] = 300.0                            # constant everywhere
+    J = np.full(n, 3600 * 150 * prof[0].throughput_sps.max())
+    for dt in (torch.float32, torch.float64):
+        g = run_sweep(tr, N, prof, [0.5, 0.9], J=J, dtype=dt, svr={})
+        o = run_oracle(tr, N, prof, [0.5, 0.9], J=J, svr={})
+        assert list(o["totals"]["status"][0][:5]) == [0, 0, 4, 4, 0]
+        assert_parity(g, o)
+        assert np.all(g["forecast"][1] == 412.5) and np.all(g["forecast"][4] == 300.0)
+
+
+def test_svr_fit_forecast_and_mape():
+    """chase_fit_forecast and chase_forecast_mape with the SVR forecaster:
+    forecasts bit-identical, MAPE within 1e-9 (Table 1's SVR column)."""
+    T, L, N, n = 48, 48, 552, 9
+    tr = inputs.synth_traces_host(n, N, seed=23, T=T)
+    tr[2, 300] = 0.0                            # zero actual: MAPE undefined
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=N, interval_s=1800)
+    f = cb.make_fcfg(interval_s=1800, history_len=L, svr={})
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    fc = torch.empty((n, N - L), dtype=torch.float64, device=DEV)
+    cb.fit_forecast(t, f, fc, N - L, ws)
+    mp = torch.empty((n, 2), dtype=torch.float64, device=DEV)
+    st = torch.empty(n, dtype=torch.int32, device=DEV)
+    cb.forecast_mape(t, f, mp, ws, status=st)
+    torch.cuda.synchronize()
+    o = oracle.plan_batch(tr, N=N, L=L, T=T, svr={}, profiles=[inputs.make_profile("bert", inputs.LIMITS_9)],
+                          etas=[0.5], delta=1800.0)
+    assert np.array_equal(fc.cpu().numpy(), o["forecast"])
+    om, ost, _ = oracle.evaluate_batch(tr, N=N, L=L, T=T, svr={})
+    g, gs = mp.cpu().numpy(), st.cpu().numpy()
+    assert list(gs) == list(ost) and gs[2] == 8
+    assert np.array_equal(np.isnan(g), np.isnan(om))
+    ok = ~np.isnan(om)
+    np.testing.assert_allclose(g[ok], om[ok], rtol=1e-9, atol=0)
