@@ -51,6 +51,8 @@ def parse_args(argv=None):
                          "timeline: per-period audit rows of a planned replay (f4)")
     ap.add_argument("--period-steps", type=int, default=0,
                     help="P > 1: one decision per period of P steps on the mean recursive forecast (f1)")
+    ap.add_argument("--forecaster", choices=["linear", "svr"], default="linear",
+                    help="linear: Eq. 1 least squares (headline); svr: the epsilon-SVR of Table 1 (FP64-bound)")
     ap.add_argument("--refit-stride", type=int, default=0,
                     help="0: fit once at job start (headline); R >= 1: rolling refit every R windows (FP64-bound)")
     return ap.parse_args(argv)
@@ -140,8 +142,8 @@ class OracleSample:
     """A bounded prefix sample of the workload, generated once on the host,
     planned by the CPU oracle as it stands (OpenMP across traces)."""
 
-    def __init__(self, w: inputs.Workload, n: int, R: int = 0, P: int = 0):
-        self.w, self.n, self.R, self.P = w, n, R, P
+    def __init__(self, w: inputs.Workload, n: int, R: int = 0, P: int = 0, svr=None):
+        self.w, self.n, self.R, self.P, self.svr = w, n, R, P, svr
         self.tr = inputs.synth_traces_host(n, w.n_steps, seed=w.seed, mode=w.mode)
         self.pid = (inputs.profile_ids_host(n, seed=w.seed, n_profiles=len(w.profiles))
                     if len(w.profiles) > 1 else None)
@@ -153,30 +155,31 @@ class OracleSample:
         w = self.w
         t0 = time.perf_counter()
         r = oracle.plan_batch(self.tr, N=w.n_steps, L=w.history_len, T=w.T, refit_stride=self.R, period=self.P,
-                              profiles=w.profiles,
+                              svr=self.svr, profiles=w.profiles,
                               profile_id=self.pid, etas=w.etas, delta=float(w.interval_s), job_samples=self.J,
                               want_forecast=False, want_choice=False)
         self.cores = r["threads"]
         return time.perf_counter() - t0
 
 
-def calibrated_sample(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0, P: int = 0) -> OracleSample:
+def calibrated_sample(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0, P: int = 0,
+                      svr=None) -> OracleSample:
     """Two-stage calibration: a tiny probe (dominated by thread start-up)
     sizes a ~1 s probe, whose rate sizes the sample to ~target_s."""
-    n0 = min(max_traces, 256 if R == 0 else 4)
-    probe = OracleSample(w, n0, R, P)
+    n0 = min(max_traces, 256 if R == 0 and svr is None else 4)
+    probe = OracleSample(w, n0, R, P, svr)
     dt = probe.run()
     n1 = int(min(max_traces, max(n0, n0 * min(1.0, target_s) / max(dt, 1e-3))))
     if n1 > n0:
-        probe = OracleSample(w, n1, R, P)
+        probe = OracleSample(w, n1, R, P, svr)
         dt = probe.run()
         n0 = n1
     n = int(min(max_traces, max(n0, n0 * target_s / max(dt, 1e-3))))
-    return probe if n <= n0 else OracleSample(w, n, R, P)
+    return probe if n <= n0 else OracleSample(w, n, R, P, svr)
 
 
-def oracle_sample_rate(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0, P: int = 0):
-    s = calibrated_sample(w, target_s, max_traces, R, P)
+def oracle_sample_rate(w: inputs.Workload, target_s: float, max_traces: int, R: int = 0, P: int = 0, svr=None):
+    s = calibrated_sample(w, target_s, max_traces, R, P, svr)
     dt = s.run()
     return s.n * w.W / dt, s.cores, s.n, dt
 
@@ -190,7 +193,7 @@ def main_reference(args):
         return 0
     w = inputs.workload(args.config, n_traces=args.traces)
     per_step = min(10.0, 150.0 / max(1, args.steps + args.warmup))
-    s = calibrated_sample(w, per_step, w.n_traces, args.refit_stride, args.period_steps)
+    s = calibrated_sample(w, per_step, w.n_traces, args.refit_stride, args.period_steps, svr_arg(args))
     times = []
     for k in range(args.warmup + args.steps):
         dt = s.run()
@@ -204,7 +207,7 @@ def main_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(w, args.gpus, args.refit_stride, args.period_steps),
+        "config": workload_config(w, args.gpus, args.refit_stride, args.period_steps, svr_arg(args)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": s.cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -223,6 +226,24 @@ def rolling_flops(w: inputs.Workload, R: int) -> float:
     return float(w.n_traces) * (origins * (42 * n + 56) + 6 * w.W)
 
 
+def svr_arg(args):
+    """The SVR hyperparameters (the binding's defaults: C 1, eps 0.1, gamma 1/3, tol 1e-3) or None."""
+    return {} if getattr(args, "forecaster", "linear") == "svr" else None
+
+
+def svr_flops(w: inputs.Workload) -> float:
+    """Algorithmic fp64 operations of the SVR forecaster per launch pair
+    (DESIGN §6.8), a LOWER bound, an fma counted as 2: per trace the kernel
+    matrix, n^2 RBF entries of 42 flops (squared distance 3 sub + 1 mul + 2 fma
+    = 8, gamma 1, exp 33: reduction 3 fma, 13 Horner fma, the 2^k scaling 1
+    mul -- floor is not counted), plus per window one prediction of 44n + 9
+    flops (z-scores 6, n x (RBF 42 + the coef fma 2), bias and
+    un-standardisation 3).  The SMO iterations are not counted (their number
+    depends on the data)."""
+    n = w.history_len - 1
+    return float(w.n_traces) * (42.0 * n * n + w.W * (44.0 * n + 9.0))
+
+
 def fp64_peak():
     """FP64 vector peak in TFLOP/s (a DFMA = 2 flops): the DFMA rate measured
     by tools/fp64_probe.cu (profiles/fp64_probe.json) when present, else
@@ -236,7 +257,10 @@ def fp64_peak():
     return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz)"
 
 
-def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0) -> str:
+def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0, svr=None) -> str:
+    if svr is not None:
+        return ("svr_fit_kernel (warp per trace, SMO on the RBF dual, kernel matrix in smem) + "
+                "svr_forecast_kernel (thread per window / period)")
     if P > 1:
         return "sweep_kernel<FUSED, FIN> (Eq. 6 argmin + replay on the period decision forecasts)"
     if R > 0:
@@ -246,9 +270,12 @@ def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0) -> str:
     return "sweep_kernel<FUSED> (fused predict + Eq. 6 argmin + replay)"
 
 
-def workload_config(w: inputs.Workload, n_gpus: int, R: int = 0, P: int = 0):
+def workload_config(w: inputs.Workload, n_gpus: int, R: int = 0, P: int = 0, svr=None):
     fc = ("fit once per trace on the 24 h before job start (P:67), least squares (Table 1 LR)" if R == 0 else
           f"rolling refit every {R} window(s) on the {w.history_len} points before each origin (P:78-79)")
+    if svr is not None:
+        fc = ("fit once per trace on the 24 h before job start (P:67), epsilon-SVR with an RBF kernel "
+              "(Table 1's best model, P:162; C=1, eps=0.1, gamma=1/3, tol=1e-3)")
     if P > 1:
         fc += f"; one decision per {P}-step period on the mean recursive forecast (P:130, S:158-166)"
     return {
@@ -293,7 +320,7 @@ def main_chase(args):
 
     planner = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, interval_s=w.interval_s,
                          history_len=w.history_len, profile_id=pid, job_samples=J, want_choice=True,
-                         refit_stride=args.refit_stride, period_steps=args.period_steps)
+                         refit_stride=args.refit_stride, period_steps=args.period_steps, svr=svr_arg(args))
 
     def step():
         planner.run()
@@ -343,7 +370,16 @@ def main_chase(args):
     value = total_windows / (ms_per_step / 1e3)
 
     R = args.refit_stride
-    if R == 0:
+    if svr_arg(args) is not None:
+        peak, peak_src = fp64_peak()
+        flops = svr_flops(w)
+        achieved = flops / (kern_ms / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": planner_kernel_name(w, R, args.period_steps, {}),
+                    "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
+                    "algorithmic_flops_per_launch": flops, "flops_note": "lower bound: SMO iterations not counted",
+                    "peak_source": peak_src}
+    elif R == 0:
         peak, peak_src = measured_peaks()
         alg_bytes = n * W * BYTES_PER_WINDOW
         achieved = alg_bytes / (kern_ms / 1e3) / 1e9
@@ -370,7 +406,8 @@ def main_chase(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, ns, dt = oracle_sample_rate(w, args.cpu_seconds, n, args.refit_stride, args.period_steps)
+        rate, cores, ns, dt = oracle_sample_rate(w, args.cpu_seconds, n, args.refit_stride, args.period_steps,
+                                                 svr_arg(args))
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {ns} of {n} traces ({ns * W:.3g} windows, {dt:.1f} s on {cores} threads)"}
 
@@ -379,7 +416,8 @@ def main_chase(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based generator, inputs/)",
-            "config": workload_config(w, world, args.refit_stride, args.period_steps), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "config": workload_config(w, world, args.refit_stride, args.period_steps, svr_arg(args)),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk,
             "check": {"n_ok": float(sums0[0, 7]), "n_slow_windows": int(diag.n_slow_windows)},
         }
@@ -410,7 +448,7 @@ def bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev):
     ht = cb.make_traces(h, n_steps=w.n_steps, interval_s=w.interval_s)
     tc = cb.make_traces(h[:chunk], n_steps=w.n_steps, interval_s=w.interval_s)
     fcfg = cb.make_fcfg(interval_s=w.interval_s, history_len=w.history_len, refit_stride=args.refit_stride,
-                        period_steps=args.period_steps)
+                        period_steps=args.period_steps, svr=svr_arg(args))
     ws = cb.alloc_workspace(cb.workspace_bytes(tc, fcfg, len(w.profiles), len(w.etas)), dev)
     stg = cb.alloc_workspace(cb.sweep_host_staging_bytes(ht, chunk, len(w.etas)), dev)
 
@@ -467,7 +505,8 @@ def main_mape(args):
     x = torch.empty((n, w.ld), dtype=torch.float32, device=dev)
     inputs.synth_traces_device(x, w.n_steps, seed=w.seed, mode=w.mode, trace0=trace0)
     t = cb.make_traces(x, n_steps=w.n_steps, interval_s=w.interval_s)
-    f = cb.make_fcfg(interval_s=w.interval_s, history_len=w.history_len)
+    sv = svr_arg(args)
+    f = cb.make_fcfg(interval_s=w.interval_s, history_len=w.history_len, svr=sv)
     ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), dev)
     mp = torch.empty((n, 2), dtype=torch.float64, device=dev)
     st = torch.empty(n, dtype=torch.int32, device=dev)
@@ -505,13 +544,23 @@ def main_mape(args):
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     ms_per_step, kern_ms = float(tm[0]) / args.steps, float(tm[1])
     value = float(n) * W * world / (ms_per_step / 1e3)
-    peak, peak_src = measured_peaks()
-    alg = n * W * 4.0
-    achieved = alg / (kern_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "mape_kernel (warp per trace, walk-forward predict + MAPE sums)",
-                "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
-                "algorithmic_bytes_per_launch": alg, "bytes_per_window": 4.0, "peak_source": peak_src}
+    if sv is None:
+        peak, peak_src = measured_peaks()
+        alg = n * W * 4.0
+        achieved = alg / (kern_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": "mape_kernel (warp per trace, walk-forward predict + MAPE sums)",
+                    "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
+                    "algorithmic_bytes_per_launch": alg, "bytes_per_window": 4.0, "peak_source": peak_src}
+    else:
+        peak, peak_src = fp64_peak()
+        flops = svr_flops(w)
+        achieved = flops / (kern_ms / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": None, "kernel": planner_kernel_name(w, 0, 0, sv) + " + mape_kernel",
+                    "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
+                    "algorithmic_flops_per_launch": flops, "flops_note": "lower bound: SMO iterations not counted",
+                    "peak_source": peak_src}
     e2e = None
     if not args.no_e2e:   # host traces -> device (chunked, pinned) -> chase_forecast_mape -> host results
         chunk = min(n, 65536)
@@ -539,20 +588,20 @@ def main_mape(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
-        ns = 256
+        ns = 256 if sv is None else 16
         tr_h = inputs.synth_traces_host(ns, w.n_steps, seed=w.seed, mode=w.mode)
         t_0 = time.perf_counter()
-        _, _, cores = oracle.evaluate_batch(tr_h, N=w.n_steps, L=w.history_len, T=w.T)
+        _, _, cores = oracle.evaluate_batch(tr_h, N=w.n_steps, L=w.history_len, T=w.T, svr=sv)
         dt = time.perf_counter() - t_0
         ns = int(min(n, ns * max(1.0, args.cpu_seconds / max(dt, 1e-3))))
         tr_h = inputs.synth_traces_host(ns, w.n_steps, seed=w.seed, mode=w.mode)
         t_0 = time.perf_counter()
-        _, _, cores = oracle.evaluate_batch(tr_h, N=w.n_steps, L=w.history_len, T=w.T)
+        _, _, cores = oracle.evaluate_batch(tr_h, N=w.n_steps, L=w.history_len, T=w.T, svr=sv)
         dt = time.perf_counter() - t_0
         cpu = {"value": ns * W / dt, "unit": "trace-windows/s", "cores": cores, "kind": "oracle",
                "sample": f"first {ns} of {n} traces ({ns * W:.3g} windows, {dt:.1f} s on {cores} threads)"}
     if rank == 0:
-        cfg = workload_config(w, world)
+        cfg = workload_config(w, world, 0, 0, sv)
         cfg["workload"] = f"{w.name} traces, walk-forward forecast evaluation (Table 1 shape, P:159-161)"
         line = {"metric": MAPE_METRIC, "value": value, "unit": "trace-windows/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

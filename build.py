@@ -51,8 +51,8 @@ def build_inputs(force=False):
 
 
 CHASE_SOURCES = ["chase_api.cpp", "envelope.cpp", "kernels.cu"]
-CHASE_HEADERS = ["envelope.h", "device_tables.h", "kernels.h", "device_common.cuh", "fit.cuh", "k2_sweep.cuh", "k2_headline.cuh", "rolling.cuh", "mape.cuh", "timeline.cuh",
-                 "finalize.cuh"]
+CHASE_HEADERS = sorted(f for f in os.listdir(os.path.join(ROOT, "paper_2303_02508_b200", "csrc"))
+                       if f.endswith((".h", ".cuh")))  # every header: a change to any rebuilds
 
 
 def build_chase(force=False):

@@ -105,8 +105,9 @@ typedef struct {
                                     the fit window (Table 1's best model, P:162,
                                     P:171; SPEC fit_svr S:140-148), solved by SMO
                                     with second-order working-set selection
-                                    (DESIGN §6.8).  Needs refit_stride == 0 and
-                                    history_len <= 64; combines with period_steps. */
+                                    (DESIGN §6.8).  Needs refit_stride == 0,
+                                    history_len <= 64 and steps_per_day <= 8192;
+                                    combines with period_steps.                  */
     int32_t svr_max_iter;        /* SMO iteration cap (>= 0; 10000 in the binding) */
     double  svr_C;               /* box constraint C > 0 (1.0)                     */
     double  svr_eps;             /* epsilon-tube half width >= 0, in z-units (0.1) */

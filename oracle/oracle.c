@@ -544,32 +544,40 @@ int32_t oracle_timeline(const double* c, int32_t N, int32_t L, int32_t period, c
 
 
 /* ---------------------------------------------------------------- epsilon-SVR (f2) */
+/* exp(x) for x <= 0 (DESIGN Q31): x = k ln2 + r with k the nearest integer to
+ * x/ln2 and ln2 split in two (Cody-Waite), exp(r) by its degree-13 Taylor
+ * polynomial in Horner form, then the exact scaling by 2^k.  Every step is one
+ * correctly rounded operation: fma(a, b, c) is (a*b + c) rounded once. */
 double oracle_rbf_exp(double x) {
     if (!(x <= 0.0)) return NAN;
     if (x < -745.0) return 0.0;
-    const double k = floor(x * 1.4426950408889634 + 0.5);          /* nearest integer to x / ln 2 */
-    const double r = (x - k * 6.93147180369123816490e-01) - k * 1.90821492927058770002e-10;
+    /* k = the integer nearest x / ln 2 (ties to even): x*log2(e) + 1.5*2^52 rounded
+     * once lands on an integer (ulp 1 there), and removing 1.5*2^52 again is exact */
+    const double k = fma(x, 1.4426950408889634, 0x1.8p52) - 0x1.8p52;
+    double r = fma(-k, 6.93147180369123816490e-01, x);              /* x - k ln2_hi (exact) */
+    r = fma(-k, 1.90821492927058770002e-10, r);                     /* - k ln2_lo */
     double q = 0x1.6124613a86d09p-33;                               /* 1/13! */
-    q = q * r + 0x1.1eed8eff8d898p-29;                              /* 1/12! */
-    q = q * r + 0x1.ae64567f544e4p-26;
-    q = q * r + 0x1.27e4fb7789f5cp-22;
-    q = q * r + 0x1.71de3a556c734p-19;
-    q = q * r + 0x1.a01a01a01a01ap-16;
-    q = q * r + 0x1.a01a01a01a01ap-13;
-    q = q * r + 0x1.6c16c16c16c17p-10;
-    q = q * r + 0x1.1111111111111p-7;
-    q = q * r + 0x1.5555555555555p-5;
-    q = q * r + 0x1.5555555555555p-3;
-    q = q * r + 0.5;
-    q = q * r + 1.0;
-    q = q * r + 1.0;
+    q = fma(q, r, 0x1.1eed8eff8d898p-29);                           /* 1/12! */
+    q = fma(q, r, 0x1.ae64567f544e4p-26);
+    q = fma(q, r, 0x1.27e4fb7789f5cp-22);
+    q = fma(q, r, 0x1.71de3a556c734p-19);
+    q = fma(q, r, 0x1.a01a01a01a01ap-16);
+    q = fma(q, r, 0x1.a01a01a01a01ap-13);
+    q = fma(q, r, 0x1.6c16c16c16c17p-10);
+    q = fma(q, r, 0x1.1111111111111p-7);
+    q = fma(q, r, 0x1.5555555555555p-5);
+    q = fma(q, r, 0x1.5555555555555p-3);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    q = fma(q, r, 1.0);
     return ldexp(q, (int)k);
 }
 
-/* K(a, b) = exp(-gamma * ((a0-b0)^2 + (a1-b1)^2 + (a2-b2)^2)), left to right */
+/* K(a, b) = exp(-gamma * ||a - b||^2), the squared distance accumulated left
+ * to right: d0*d0, then + d1*d1, then + d2*d2 (each add fused with its product). */
 static double rbf(const double* a, const double* b, double gamma) {
     const double d0 = a[0] - b[0], d1 = a[1] - b[1], d2 = a[2] - b[2];
-    const double d = ((d0 * d0) + (d1 * d1)) + (d2 * d2);
+    const double d = fma(d2, d2, fma(d1, d1, d0 * d0));
     return oracle_rbf_exp(-(gamma * d));
 }
 
@@ -724,7 +732,7 @@ double oracle_svr_predict(const oracle_svr_t* m, double s, double c, double lag)
     double zq[3];
     for (int j = 0; j < 3; ++j) zq[j] = m->keep[j] ? (xv[j] - m->mu[j]) / m->sigma[j] : 0.0;
     double f = 0.0;
-    for (int32_t t = 0; t < m->n; ++t) f = f + m->coef[t] * rbf(m->z[t], zq, m->gamma);
+    for (int32_t t = 0; t < m->n; ++t) f = fma(m->coef[t], rbf(m->z[t], zq, m->gamma), f);  /* f += coef*K, one rounding */
     f = f - m->rho;
     const double p = m->mu[3] + m->sigma[3] * f;
     return p > 0.0 ? p : 0.0;

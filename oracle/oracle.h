@@ -150,10 +150,13 @@ typedef struct {
     int32_t status;                /* 0 ok, 4 bad value                */
 } oracle_svr_t;
 
-/* exp(x) for x <= 0: Cody-Waite reduction x = k ln2 + r, degree-13 Taylor
+/* exp(x) for x <= 0: Cody-Waite reduction x = k ln2 + r (k the integer
+ * nearest x/ln2, found by the 1.5*2^52 shift), degree-13 Taylor
  * polynomial of exp(r) in Horner form, scaled by 2^k (ldexp).  Every step is
- * one IEEE operation, so host and device agree bit for bit; |error| <= 2 ulp
- * of libm exp (pinned in tests). */
+ * one correctly rounded IEEE operation (the reduction and the Horner steps are
+ * fma: a*b + c rounded once), so host and device agree bit for bit; |error|
+ * <= 1 ulp of libm exp (pinned in tests).  The kernel's squared distance and
+ * the prediction's sum of coef*K accumulate with fma as well. */
 double oracle_rbf_exp(double x);
 
 /* Fit on the L history points hist[0..L) (rows as oracle_fit).  gamma <= 0:

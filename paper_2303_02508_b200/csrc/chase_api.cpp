@@ -118,6 +118,7 @@ chase_status_t check_fcfg(const chase_traces_t* t, const chase_forecast_cfg_t* f
     if (svr(f)) {
         if (f->refit_stride > 0) return fail(CHASE_ERR_INVALID, "the SVR forecaster is fitted once (refit_stride 0)");
         if (f->history_len > 64) return fail(CHASE_ERR_INVALID, "the SVR forecaster needs history_len <= 64");
+        if (f->steps_per_day > 8192) return fail(CHASE_ERR_INVALID, "the SVR forecaster needs steps_per_day <= 8192");
         if (!(f->svr_C > 0) || !std::isfinite(f->svr_C) || !(f->svr_eps >= 0) || !std::isfinite(f->svr_eps) ||
             !(f->svr_gamma >= 0) || !std::isfinite(f->svr_gamma) || !(f->svr_tol > 0) || !std::isfinite(f->svr_tol) ||
             f->svr_max_iter < 0)

@@ -342,11 +342,16 @@ cudaError_t launch_svr(const void* traces, bool f64, int64_t ld, int64_t n_trace
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int64_t threads = n_traces * (int64_t)p.n_per;
-    const int64_t g2 = (threads + 255) / 256;
-    if (g2 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    if (f64) svr_forecast_kernel<double><<<(unsigned)g2, 256, 0, s>>>(p);
-    else svr_forecast_kernel<float><<<(unsigned)g2, 256, 0, s>>>(p);
+    const int64_t chunks = (p.n_per + kSvrFcThreads * kSvrFcPer - 1) / (kSvrFcThreads * kSvrFcPer);
+    if (n_traces > 0x7fffffffLL || chunks > 65535) return cudaErrorInvalidConfiguration;
+    const dim3 g2((unsigned)n_traces, (unsigned)chunks);
+    const int smem2 = svr_fc_smem_doubles(L, T) * 8;
+    if (smem2 > 48 * 1024) {
+        cudaFuncSetAttribute(svr_forecast_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        cudaFuncSetAttribute(svr_forecast_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    }
+    if (f64) svr_forecast_kernel<double><<<g2, kSvrFcThreads, smem2, s>>>(p);
+    else svr_forecast_kernel<float><<<g2, kSvrFcThreads, smem2, s>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }

@@ -17,33 +17,49 @@ constexpr int kSvrZ = 0, kSvrCoef = 3 * kSvrMaxN, kSvrMu = kSvrCoef + kSvrMaxN, 
 constexpr int kSvrGamma = kSvrSigma + 4, kSvrRho = kSvrGamma + 1, kSvrN = kSvrRho + 1, kSvrKind = kSvrN + 1;
 constexpr int kSvrKeep = kSvrKind + 1, kSvrIters = kSvrKeep + 3, kSvrDoubles = (kSvrIters + 1 + 1) & ~1;
 
-__device__ __forceinline__ double svr_exp(double x) {
-    if (!(x <= 0.0)) return CUDART_NAN;
-    if (x < -745.0) return 0.0;
-    const double k = floor(__dadd_rn(__dmul_rn(x, 1.4426950408889634), 0.5));
-    const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(k, 6.93147180369123816490e-01)),
-                               __dmul_rn(k, 1.90821492927058770002e-10));
-    double q = 0x1.6124613a86d09p-33;
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.1eed8eff8d898p-29);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.ae64567f544e4p-26);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.27e4fb7789f5cp-22);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.71de3a556c734p-19);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.a01a01a01a01ap-16);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.a01a01a01a01ap-13);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.6c16c16c16c17p-10);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.1111111111111p-7);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.5555555555555p-5);
-    q = __dadd_rn(__dmul_rn(q, r), 0x1.5555555555555p-3);
-    q = __dadd_rn(__dmul_rn(q, r), 0.5);
-    q = __dadd_rn(__dmul_rn(q, r), 1.0);
-    q = __dadd_rn(__dmul_rn(q, r), 1.0);
-    return ldexp(q, (int)k);
+// oracle_rbf_exp's constants in the constant bank: the fma's take them as
+// c[][] operands (no per-use uniform-register moves in the issue stream)
+__constant__ double c_svr_exp[17] = {
+    1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
+    0x1.6124613a86d09p-33, 0x1.1eed8eff8d898p-29, 0x1.ae64567f544e4p-26, 0x1.27e4fb7789f5cp-22,
+    0x1.71de3a556c734p-19, 0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-13, 0x1.6c16c16c16c17p-10,
+    0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.5555555555555p-3, 0.5, 1.0, 1.0};
+
+// q * 2^k (k <= 0 an integer, q in [0.70, 1.42]) rounded once: oracle_rbf_exp's
+// ldexp.  For k >= -1021 the product is normal and exact, so k is added to the
+// exponent field (integer pipe); below that (rare) two multiplications, the
+// first exact, the second rounding the exact value once.
+__device__ __forceinline__ double svr_scale2k(double q, int ki) {
+    if (ki >= -1021) return __hiloint2double(__double2hiint(q) + (ki << 20), __double2loint(q));
+    return __dmul_rn(__dmul_rn(q, 0x1p-600), __hiloint2double((ki + 600 + 1023) << 20, 0));
 }
 
+// oracle_rbf_exp(-y), operation for operation (fma = one rounding on both sides).
+// The oracle's guards on x = -y, !(x <= 0) -> NaN and x < -745 -> 0, are decided
+// on the bit pattern of y (integer pipe; the fp64 pipe is this kernel's bound),
+// k comes from the 1.5*2^52 shift: its low word is k, no float->int conversion.
+__device__ __forceinline__ double svr_exp_neg(double y) {
+    const unsigned long long v = (unsigned long long)__double_as_longlong(y);
+    const double m = __fma_rn(-y, c_svr_exp[0], 0x1.8p52);
+    const double k = __dsub_rn(m, 0x1.8p52);
+    double r = __fma_rn(-k, c_svr_exp[1], -y);
+    r = __fma_rn(-k, c_svr_exp[2], r);
+    double q = c_svr_exp[3];
+#pragma unroll
+    for (int j = 4; j < 17; ++j) q = __fma_rn(q, r, c_svr_exp[j]);
+    // x <= 0  <=>  y in [+0, +inf] or y == -0;  x < -745  <=>  y > 745 (not NaN)
+    if (!(v <= 0x7FF0000000000000ull || v == 0x8000000000000000ull)) return CUDART_NAN;
+    if (v > 0x4087480000000000ull) return 0.0;
+    return svr_scale2k(q, __double2loint(m));
+}
+
+__device__ __forceinline__ double svr_exp(double x) { return svr_exp_neg(-x); }
+
+// oracle rbf(): exp(-gamma * ((d0*d0 + d1*d1) + d2*d2)), each add fused with its product
 __device__ __forceinline__ double svr_rbf(const double* a, const double* b, double gamma) {
     const double d0 = __dsub_rn(a[0], b[0]), d1 = __dsub_rn(a[1], b[1]), d2 = __dsub_rn(a[2], b[2]);
-    const double d = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
-    return svr_exp(-__dmul_rn(gamma, d));
+    const double d = __fma_rn(d2, d2, __fma_rn(d1, d1, __dmul_rn(d0, d0)));
+    return svr_exp_neg(__dmul_rn(gamma, d));
 }
 
 struct SvrParams {
@@ -282,46 +298,89 @@ __global__ void __launch_bounds__(32 * kSvrWarps) svr_fit_kernel(const __grid_co
     }
 }
 
-// oracle_svr_predict for window w of trace i (thread per window).
-__device__ __forceinline__ double svr_predict(const double* M, double s, double c, double lag) {
-    if (M[kSvrKind] != 0.0) return M[kSvrMu + 3] > 0.0 ? M[kSvrMu + 3] : 0.0;
-    const double xv[3] = {s, c, lag};
-    double zq[3];
-    for (int j = 0; j < 3; ++j)
-        zq[j] = M[kSvrKeep + j] != 0.0 ? __ddiv_rn(__dsub_rn(xv[j], M[kSvrMu + j]), M[kSvrSigma + j]) : 0.0;
-    const int n = (int)M[kSvrN];
-    const double gamma = M[kSvrGamma];
-    double f = 0.0;
-    for (int t = 0; t < n; ++t) f = __dadd_rn(f, __dmul_rn(M[kSvrCoef + t], svr_rbf(M + kSvrZ + 3 * t, zq, gamma)));
-    f = __dsub_rn(f, M[kSvrRho]);
-    const double pr = __dadd_rn(M[kSvrMu + 3], __dmul_rn(M[kSvrSigma + 3], f));
-    return pr > 0.0 ? pr : 0.0;
-}
+// svr_forecast_kernel's shared memory (doubles): z[3n] | coef[n] | zs[T] | zc[T]
+__host__ __device__ inline int svr_fc_smem_doubles(int L, int T) { return 4 * (L - 1) + 2 * T; }
+constexpr int kSvrFcThreads = 128, kSvrFcPer = 8;  // 128 threads x 8 periods per block
 
-// One thread per (trace, decision period): the recursive horizon of
+// One block per (trace, 1024 decision periods): the trace's support vectors,
+// coefficients and the z-scored phase features of every phase are staged in
+// shared memory once; one thread per period runs the recursive horizon of
 // oracle_plan_trace (prediction k is the lag of prediction k+1, from the last
-// observed value), its mean written to every window of the period.  P = 1 is
-// the one-step forecast with the observed lag.
+// observed value) and writes its mean to every window of the period.  P = 1 is
+// the one-step forecast with the observed lag.  Each prediction is
+// oracle_svr_predict: f = sum_t coef_t K(z_t, zq) (fma, in t order) - rho,
+// mu_y + sigma_y f clamped at 0; two kernel terms are evaluated per loop step
+// (independent exp chains) and accumulated in order.
 template <typename E>
-__global__ void __launch_bounds__(256) svr_forecast_kernel(const __grid_constant__ SvrParams p) {
-    const int W = p.N - p.L, P = p.P;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= p.n_traces * (int64_t)p.n_per) return;
-    const int64_t i = idx / p.n_per;
-    const int b = (int)(idx - i * p.n_per) * P;
+__global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __grid_constant__ SvrParams p) {
+    extern __shared__ __align__(16) double vsm[];
+    const int64_t i = blockIdx.x;
     if (p.records[i * kRecDoubles + 5] != 0.0) return;  // bad history: no model (the sweep reports it)
-    const E* row = reinterpret_cast<const E*>(p.traces) + i * p.ld;
     const double* M = p.models + i * kSvrDoubles;
-    const int n = W - b < P ? W - b : P;
-    double prev = (double)row[p.L + b - 1], sum = 0.0;
-    int ph = (int)(((int64_t)p.phase0 + p.L + b) % p.T);
-    for (int k = 0; k < n; ++k) {
-        const double f = svr_predict(M, p.phase[ph], p.phase[p.T + ph], prev);
-        sum = __dadd_rn(sum, f);
-        prev = f;
-        ph = ph + 1 == p.T ? 0 : ph + 1;
+    const int n = (int)M[kSvrN], T = p.T;
+    double* z = vsm;
+    double* cf = z + 3 * n;
+    double* zs = cf + n;
+    double* zc = zs + T;
+    const bool constant = M[kSvrKind] != 0.0;
+    const double mu0 = M[kSvrMu], mu1 = M[kSvrMu + 1], mu2 = M[kSvrMu + 2], mu3 = M[kSvrMu + 3];
+    const double sg0 = M[kSvrSigma], sg1 = M[kSvrSigma + 1], sg2 = M[kSvrSigma + 2], sg3 = M[kSvrSigma + 3];
+    const bool k0 = M[kSvrKeep] != 0.0, k1 = M[kSvrKeep + 1] != 0.0, k2 = M[kSvrKeep + 2] != 0.0;
+    const double gamma = M[kSvrGamma], rho = M[kSvrRho];
+    if (!constant) {
+        for (int q = threadIdx.x; q < 3 * n; q += blockDim.x) z[q] = M[kSvrZ + q];
+        for (int q = threadIdx.x; q < n; q += blockDim.x) cf[q] = M[kSvrCoef + q];
+        for (int q = threadIdx.x; q < T; q += blockDim.x) {
+            zs[q] = k0 ? __ddiv_rn(__dsub_rn(p.phase[q], mu0), sg0) : 0.0;
+            zc[q] = k1 ? __ddiv_rn(__dsub_rn(p.phase[T + q], mu1), sg1) : 0.0;
+        }
     }
-    const double chat = __ddiv_rn(sum, (double)n);
-    double* out = p.forecast + i * p.ld_f + b;
-    for (int k = 0; k < n; ++k) out[k] = chat;
+    __syncthreads();
+    const int W = p.N - p.L, P = p.P;
+    const E* row = reinterpret_cast<const E*>(p.traces) + i * p.ld;
+    const int per_end = min(p.n_per, (int)(blockIdx.y + 1) * kSvrFcThreads * kSvrFcPer);
+    for (int per = blockIdx.y * kSvrFcThreads * kSvrFcPer + threadIdx.x; per < per_end; per += kSvrFcThreads) {
+        const int b = per * P;
+        const int nw = W - b < P ? W - b : P;
+        double prev = (double)row[p.L + b - 1], sum = 0.0;
+        int ph = (int)(((int64_t)p.phase0 + p.L + b) % T);
+        for (int k = 0; k < nw; ++k) {
+            double pr;
+            if (constant) {
+                pr = mu3;
+            } else {
+                const double q0 = zs[ph], q1 = zc[ph];
+                const double q2 = k2 ? __ddiv_rn(__dsub_rn(prev, mu2), sg2) : 0.0;
+                double f = 0.0;
+                int t = 0;
+                for (; t + 1 < n; t += 2) {
+                    const double a0 = __dsub_rn(z[3 * t], q0), a1 = __dsub_rn(z[3 * t + 1], q1),
+                                 a2 = __dsub_rn(z[3 * t + 2], q2);
+                    const double b0 = __dsub_rn(z[3 * t + 3], q0), b1 = __dsub_rn(z[3 * t + 4], q1),
+                                 b2 = __dsub_rn(z[3 * t + 5], q2);
+                    const double da = __fma_rn(a2, a2, __fma_rn(a1, a1, __dmul_rn(a0, a0)));
+                    const double db = __fma_rn(b2, b2, __fma_rn(b1, b1, __dmul_rn(b0, b0)));
+                    const double Ka = svr_exp_neg(__dmul_rn(gamma, da));
+                    const double Kb = svr_exp_neg(__dmul_rn(gamma, db));
+                    f = __fma_rn(cf[t], Ka, f);
+                    f = __fma_rn(cf[t + 1], Kb, f);
+                }
+                if (t < n) {
+                    const double a0 = __dsub_rn(z[3 * t], q0), a1 = __dsub_rn(z[3 * t + 1], q1),
+                                 a2 = __dsub_rn(z[3 * t + 2], q2);
+                    const double da = __fma_rn(a2, a2, __fma_rn(a1, a1, __dmul_rn(a0, a0)));
+                    f = __fma_rn(cf[t], svr_exp_neg(__dmul_rn(gamma, da)), f);
+                }
+                f = __dsub_rn(f, rho);
+                pr = __dadd_rn(mu3, __dmul_rn(sg3, f));
+            }
+            const double fk = pr > 0.0 ? pr : 0.0;
+            sum = __dadd_rn(sum, fk);
+            prev = fk;
+            ph = ph + 1 == T ? 0 : ph + 1;
+        }
+        const double chat = __ddiv_rn(sum, (double)nw);
+        double* out = p.forecast + i * p.ld_f + b;
+        for (int k = 0; k < nw; ++k) out[k] = chat;
+    }
 }

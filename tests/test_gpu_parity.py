@@ -581,7 +581,8 @@ def test_svr_forecaster_parity(P, L, N, etas, n, interval):
 
 
 @pytest.mark.parametrize("hp", [dict(C=0.5, eps=0.05), dict(gamma=0.7, tol=1e-6), dict(max_iter=3),
-                                dict(C=20.0, eps=0.0, tol=1e-9, max_iter=100000)])
+                                dict(C=20.0, eps=0.0, tol=1e-9, max_iter=100000),
+                                dict(gamma=60.0), dict(gamma=300.0)])   # RBF entries in exp's subnormal / zero ranges
 def test_svr_hyperparameters_parity(hp):
     """Box constraint, tube width, gamma, tolerance and the iteration cap all
     reach the device solver unchanged (bit-identical forecasts)."""

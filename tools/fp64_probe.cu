@@ -14,7 +14,10 @@ __global__ void probe(double* out, int iters, double a, double b) {
         for (int k = 0; k < 8; ++k) {
             if (OP == 0) x[k] = __fma_rn(x[k], a, b);
             else if (OP == 1) x[k] = __dadd_rn(x[k], b);
-            else x[k] = __dmul_rn(x[k], a);
+            else if (OP == 2) x[k] = __dmul_rn(x[k], a);
+            else if (OP == 3) x[k] = floor(__dadd_rn(x[k], b));                       // DADD + FRND
+            else if (OP == 4) x[k] = __dadd_rn(x[k], (double)(__double2int_rn(x[k]) & 1));  // F2I + I2F + DADD
+            else x[k] = __dadd_rn(x[k], x[k] > a ? b : a);                            // DSETP + DADD
         }
     }
     double s = 0;
@@ -29,16 +32,19 @@ int main() {
     double* d;
     cudaMalloc(&d, 8);
     const int iters = 20000, threads = 256, blocks = sms * 8;
-    const char* names[3] = {"dfma", "dadd", "dmul"};
+    const char* names[6] = {"dfma", "dadd", "dmul", "dadd+frnd", "f2i+i2f+dadd", "dsetp+dadd"};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int op = 0; op < 3; ++op) {
+    for (int op = 0; op < 6; ++op) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaEventRecord(e0);
             if (op == 0) probe<0><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
             else if (op == 1) probe<1><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
-            else probe<2><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
+            else if (op == 2) probe<2><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
+            else if (op == 3) probe<3><<<blocks, threads>>>(d, iters, 0.999999, 1.5);
+            else if (op == 4) probe<4><<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
+            else probe<5><<<blocks, threads>>>(d, iters, 0.5, 1e-9);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms = 0;

@@ -54,11 +54,13 @@ def main():
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--windows", type=float, default=8.76e9)
     ap.add_argument("--config", default="C5")
+    ap.add_argument("--kernel", default="sweep_fast", help="file-name stem of the captured kernel")
+    ap.add_argument("--no-traffic", action="store_true", help="do not update ncu_traffic.json (ALU-bound kernels)")
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
 
     m = raw_metrics(a.rep)
-    with open(os.path.join(prof, f"{a.tag}_sweep_fast_metrics.csv"), "w") as f:
+    with open(os.path.join(prof, f"{a.tag}_{a.kernel}_metrics.csv"), "w") as f:
         f.write("metric,unit,value\n")
         for k, _ in KEYS:
             if k in m:
@@ -68,7 +70,7 @@ def main():
                         key=lambda kv: -kv[1])[:8]
         for k, v in stalls:
             f.write(f"{k},ratio,{v:.4f}\n")
-    with open(os.path.join(prof, f"{a.tag}_sweep_fast_details.txt"), "w") as f:
+    with open(os.path.join(prof, f"{a.tag}_{a.kernel}_details.txt"), "w") as f:
         f.write(ncu("-i", a.rep, "--page", "details"))
 
     def gb(k):
@@ -78,11 +80,13 @@ def main():
     rd, wr = gb("dram__bytes_read.sum"), gb("dram__bytes_write.sum")
     path = os.path.join(prof, "ncu_traffic.json")
     d = json.load(open(path)) if os.path.exists(path) else {}
-    d[a.config] = {"dram_bytes_per_window": (rd + wr) / a.windows, "dram_read_bytes": rd, "dram_write_bytes": wr,
+    entry = {"dram_bytes_per_window": (rd + wr) / a.windows, "dram_read_bytes": rd, "dram_write_bytes": wr,
                    "windows": a.windows,
                    "source": f"ncu --set full --clock-control none, sweep_fast_kernel "
-                             f"(profiles/{a.tag}_sweep_fast_metrics.csv)"}
-    json.dump(d, open(path, "w"), indent=1)
+                             f"(profiles/{a.tag}_{a.kernel}_metrics.csv)"}
+    if not a.no_traffic:
+        d[a.config] = entry
+        json.dump(d, open(path, "w"), indent=1)
 
     # launch list: keep the CSV rows, add per-kernel totals of the last bench step
     text = open(a.launches).read()
@@ -108,7 +112,7 @@ def main():
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
             share = f"{v / s:.4f}" if "chase::" in k and "chasegen" not in k else "setup"
             w.writerow([k, f"{v:.1f}", share])
-    print(json.dumps(d[a.config]))
+    print(json.dumps(entry))
 
 
 if __name__ == "__main__":
