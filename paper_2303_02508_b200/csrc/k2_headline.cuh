@@ -27,9 +27,6 @@
 #ifndef CHASE_H_CHUNK
 #define CHASE_H_CHUNK 60
 #endif
-#ifndef CHASE_H_PREFETCH
-#define CHASE_H_PREFETCH 1  // load group g+1's trace values and A terms during group g
-#endif
 #ifndef CHASE_H_STG
 #define CHASE_H_STG 0   // 1: choice words stored from registers (per group) instead of a TMA store per chunk
 #endif
@@ -114,56 +111,69 @@ __device__ __forceinline__ uint32_t line_addr(int h, uint2 e, uint32_t ZB) {
     return __byte_perm(e.y, ZB, sel);
 }
 
+// One group of 4 windows: predict, envelope lookup, line load, running sums;
+// returns the group's word of 4 choice bytes (byte 1 of each line address).
+__device__ __forceinline__ uint32_t hot_group(const float4 v, const double2 A01, const double2 A23, double& lag,
+                                              double wl, double invK, const uint2* __restrict__ ent8, int ebase,
+                                              uint32_t ZB, Acc& a) {
+    a.vmin = fminf(fminf(fminf(a.vmin, v.x), v.y), fminf(v.z, v.w));  // FMNMX3 x2
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    const double AA[4] = {A01.x, A01.y, A23.x, A23.y};
+    uint32_t ad[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const double cw = (double)vv[u];
+        const double p = __dadd_rn(AA[u], __dmul_rn(wl, lag));  // Eq. 1, unclamped for the lookup
+        const int h = __double2hiint(__dmul_rn(p, invK));
+        const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+        ad[u] = line_addr(h, ent8[idx], ZB);
+        const double2 ln = lds_line(ad[u]);  // (Thr_k * Delta, P_k)
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        a.Cs = __dadd_rn(a.Cs, cw);
+        lag = cw;
+    }
+    const uint32_t word = __byte_perm(__byte_perm(ad[0], ad[1], 0x0051u), __byte_perm(ad[2], ad[3], 0x0051u), 0x5410u);
+    a.slow |= word;
+    return word;
+}
+
 // One lane's full groups of 4 windows.  Words (4 choice bytes) go to the
 // warp's staging buffer; `a.slow` collects them for the deferred-window test.
-// The trace values and A terms of group g+1 are loaded while group g computes
-// (the reads past the last group stay inside the stage / A-table buffers).
+// Two register sets alternate (unrolled by 2): the trace values and A terms of
+// group g+1 are loaded while group g computes, with no register moves (the
+// reads at most one group past the last stay inside the stage / A buffers).
 __device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngroups, const double* __restrict__ Ap,
                                            double wl, double invK, const uint2* __restrict__ ent8, int ebase,
                                            uint32_t ZB, uint32_t* __restrict__ words, uint32_t* __restrict__ cdst,
                                            Acc& a) {
     double lag = (double)tv[-1];
-    float4 v = *reinterpret_cast<const float4*>(tv);
-    double2 A01 = *reinterpret_cast<const double2*>(Ap);
-    double2 A23 = *reinterpret_cast<const double2*>(Ap + 2);
+    float4 vx = *reinterpret_cast<const float4*>(tv);
+    double2 Ax0 = *reinterpret_cast<const double2*>(Ap);
+    double2 Ax1 = *reinterpret_cast<const double2*>(Ap + 2);
+    int g = 0;
 #pragma unroll 1
-    for (int g = 0; g < ngroups; ++g) {
-#if CHASE_H_PREFETCH
-        const float4 vn = *reinterpret_cast<const float4*>(tv + 4 * g + 4);
-        const double2 A01n = *reinterpret_cast<const double2*>(Ap + 4 * g + 4);
-        const double2 A23n = *reinterpret_cast<const double2*>(Ap + 4 * g + 6);
-#else
-        v = *reinterpret_cast<const float4*>(tv + 4 * g);
-        A01 = *reinterpret_cast<const double2*>(Ap + 4 * g);
-        A23 = *reinterpret_cast<const double2*>(Ap + 4 * g + 2);
-#endif
-        a.vmin = fminf(fminf(fminf(a.vmin, v.x), v.y), fminf(v.z, v.w));  // FMNMX3 x2
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        const double AA[4] = {A01.x, A01.y, A23.x, A23.y};
-        uint32_t ad[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const double cw = (double)vv[u];
-            const double p = __dadd_rn(AA[u], __dmul_rn(wl, lag));  // Eq. 1, unclamped for the lookup
-            const int h = __double2hiint(__dmul_rn(p, invK));
-            const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
-            ad[u] = line_addr(h, ent8[idx], ZB);
-            const double2 ln = lds_line(ad[u]);  // (Thr_k * Delta, P_k)
-            a.S = __dadd_rn(a.S, ln.x);
-            a.E = __dadd_rn(a.E, ln.y);
-            a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
-            a.Cs = __dadd_rn(a.Cs, cw);
-            lag = cw;
+    for (; g + 1 < ngroups; g += 2) {
+        const float4 vy = *reinterpret_cast<const float4*>(tv + 4 * g + 4);
+        const double2 Ay0 = *reinterpret_cast<const double2*>(Ap + 4 * g + 4);
+        const double2 Ay1 = *reinterpret_cast<const double2*>(Ap + 4 * g + 6);
+        const uint32_t w0 = hot_group(vx, Ax0, Ax1, lag, wl, invK, ent8, ebase, ZB, a);
+        vx = *reinterpret_cast<const float4*>(tv + 4 * g + 8);
+        Ax0 = *reinterpret_cast<const double2*>(Ap + 4 * g + 8);
+        Ax1 = *reinterpret_cast<const double2*>(Ap + 4 * g + 10);
+        const uint32_t w1 = hot_group(vy, Ay0, Ay1, lag, wl, invK, ent8, ebase, ZB, a);
+        words[g] = w0;  // (lane blocks are 4 mod 8 bytes apart: two 4-byte stores)
+        words[g + 1] = w1;
+        if (CHASE_H_STG && cdst) {
+            cdst[g] = w0;
+            cdst[g + 1] = w1;
         }
-        const uint32_t word = __byte_perm(__byte_perm(ad[0], ad[1], 0x0051u), __byte_perm(ad[2], ad[3], 0x0051u), 0x5410u);
-        words[g] = word;
-        if (CHASE_H_STG && cdst) cdst[g] = word;
-        a.slow |= word;
-#if CHASE_H_PREFETCH
-        v = vn;
-        A01 = A01n;
-        A23 = A23n;
-#endif
+    }
+    if (g < ngroups) {
+        const uint32_t w0 = hot_group(vx, Ax0, Ax1, lag, wl, invK, ent8, ebase, ZB, a);
+        words[g] = w0;
+        if (CHASE_H_STG && cdst) cdst[g] = w0;
     }
 }
 
