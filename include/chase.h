@@ -237,8 +237,8 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
  *   d_status [n_traces] int32 out or NULL: 0, 4 (negative / non-finite value),
  *            6 (fit failed) or 8 (a zero intensity: MAPE undefined).
  * fcfg->forecaster selects the model (CHASE_FC_SVR: the first column is the
- * SVR's MAPE, Table 1's comparison).  Needs refit_stride == 0 and
- * period_steps <= 1.  Predictions are bit-identical to the oracle's; the MAPE
+ * SVR's MAPE, Table 1's comparison).  Needs refit_stride == 0,
+ * period_steps <= 1 and steps_per_day <= 2048.  Predictions are bit-identical to the oracle's; the MAPE
  * sums agree to <= 1e-9 relative. */
 chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_mape,
                                    int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);

@@ -409,6 +409,7 @@ chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_for
         return fail(CHASE_ERR_INVALID, "chase_forecast_mape evaluates the fit-once one-step forecaster "
                                        "(refit_stride 0, period_steps <= 1)");
     if (traces->n_traces > 0 && !d_mape) return fail(CHASE_ERR_INVALID, "d_mape is NULL");
+    if (fcfg->steps_per_day > 2048) return fail(CHASE_ERR_INVALID, "chase_forecast_mape needs steps_per_day <= 2048");
     const int T = fcfg->steps_per_day;
     const WsLayout WL = ws_layout(traces->n_traces, T, 1, 1, traces, fcfg);
     if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;

@@ -296,7 +296,11 @@ cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_trac
     int64_t grid = (n_traces + 7) / 8;
     const int64_t cap = (int64_t)num_sms() * 8;
     if (grid > cap) grid = cap;
-    const int smem = 2 * T * 8;
+    const int smem = mape_smem_bytes(T);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(mape_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(mape_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    }
     if (f64) mape_kernel<double><<<(unsigned)grid, 256, smem, s>>>(p);
     else mape_kernel<float><<<(unsigned)grid, 256, smem, s>>>(p);
     ++g_launches;

@@ -509,6 +509,37 @@ def test_forecast_mape_matches_oracle(T, L, N, n):
     assert gs[1] == 8 and gs[2] == 4
 
 
+@pytest.mark.parametrize("L", [27, 28])
+def test_forecast_mape_special_values(L):
+    """The vectorised MAPE path converts floats on the integer pipe: subnormal
+    values (exact fallback), -0.0 (valid, a zero actual), inf / NaN (status 4)
+    and ragged ends all match the oracle (L = 28: the job start is 16-byte
+    aligned, the first lag comes from the lane-0 carry)."""
+    T, N, n = 24, L + 333, 8
+    tr = inputs.synth_traces_host(n, N, seed=77, T=T)
+    tr[0, 100] = np.float32(1e-40)            # subnormal actual
+    tr[1, L - 1] = np.float32(-0.0)           # -0.0 as the first lag (history): valid
+    tr[2, 200] = np.float32(-0.0)             # -0.0 actual: zero -> status 8
+    tr[3, 150] = np.float32(np.inf)
+    tr[4, 151] = np.float32(np.nan)
+    tr[5, L - 1] = np.float32(3e-39)          # subnormal lag from the history
+    tr[6, N - 1] = np.float32(2e-45)          # subnormal in the ragged last group
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=N)
+    f = cb.make_fcfg(history_len=L)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    mp = torch.empty((n, 2), dtype=torch.float64, device=DEV)
+    st = torch.empty(n, dtype=torch.int32, device=DEV)
+    cb.forecast_mape(t, f, mp, ws, status=st)
+    torch.cuda.synchronize()
+    om, ost, _ = oracle.evaluate_batch(tr, N=N, L=L, T=T)
+    g, gs = mp.cpu().numpy(), st.cpu().numpy()
+    assert list(gs) == list(ost) and list(gs[:5]) == [0, 0, 8, 4, 4]
+    assert np.array_equal(np.isnan(g), np.isnan(om))
+    ok = ~np.isnan(om)
+    np.testing.assert_allclose(g[ok], om[ok], rtol=1e-9, atol=0)
+
+
 # ------------------------------------------------------------------ timeline / audit rows (SURVEY §8(f) f4)
 @pytest.mark.parametrize("P", [1, 24, 7])
 def test_timeline_rows_match_oracle(P):
