@@ -255,7 +255,7 @@ chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_for
  *               plane), or NULL for the max-limit baseline;
  *   d_forecast  [n_traces][ld_f] f64 decision forecasts or NULL (rows get NaN);
  *   d_trace_ids [m] int64 trace indices, or NULL for traces 0..m-1;
- *   d_rows      [m][ceil(W/P)][8] f64 out.
+ *   d_rows      [m][ceil(W/P)][8] f64 out, 16-byte aligned (rows leave by TMA bulk stores).
  * Rows match oracle_timeline (bit-identical for the dyadic synthetic inputs). */
 chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len, int32_t period_steps,
                               const uint8_t* d_choice, int64_t ld_c, const double* d_forecast, int64_t ld_f,

@@ -446,7 +446,7 @@ chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len,
     if (period_steps < 0) return fail(CHASE_ERR_INVALID, "period_steps < 0");
     const int64_t W = traces->n_steps - history_len;
     if (m < 0 || (!d_trace_ids && m > traces->n_traces)) return fail(CHASE_ERR_INVALID, "m out of range");
-    if (m > 0 && !d_rows) return fail(CHASE_ERR_INVALID, "d_rows is NULL");
+    if (m > 0 && (!d_rows || ((uintptr_t)d_rows & 15))) return fail(CHASE_ERR_INVALID, "d_rows NULL or not 16-byte aligned");
     if (d_choice && ld_c < W) return fail(CHASE_ERR_INVALID, "ld_c < W");
     if (d_forecast && ld_f < W) return fail(CHASE_ERR_INVALID, "ld_f < W");
     const int T = 86400 / traces->interval_s;

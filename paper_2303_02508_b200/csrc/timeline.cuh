@@ -27,11 +27,16 @@ struct TimelineParams {
     double* rows;            // [m][n_per][8]
 };
 
+// Rows of a round are staged per warp in shared memory and leave as one TMA
+// bulk store (32 rows = 2 KB, contiguous in the output), not as 8 strided
+// 8-byte stores per lane.
 template <typename E>
 __global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ TimelineParams p) {
+    __shared__ __align__(128) double tl_rows[4][32 * 8];
     const int lane = threadIdx.x & 31;
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= p.m) return;
+    double* st = tl_rows[threadIdx.x >> 5];
     const int64_t i = p.ids ? p.ids[r] : r;
     const int s0 = p.L, W = p.N - p.L, Pp = p.P;
     const int n_per = (W + Pp - 1) / Pp;
@@ -90,19 +95,28 @@ __global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ T
                 C = __dadd_rn(C, __dmul_rn(ln.y, cw));
             }
         }
+        if (j0 > 0 && lane == 0) bulk_wait_read0();  // the previous round's store has read the staging rows
+        __syncwarp();
         if (valid) {
             const int k = ch ? ch[b] : pf->K - 1;
-            double* o = out + (int64_t)j * 8;
+            double* o = st + lane * 8;
             o[0] = (double)(s0 + b);
             o[1] = p.forecast ? p.forecast[i * p.ld_f + b] : CUDART_NAN;
-            o[2] = __ddiv_rn(csum, (double)n);
+            o[2] = n == 1 ? csum : __ddiv_rn(csum, (double)n);  // x/1 = x exactly
             o[3] = (double)pf->limit_w[k];
             o[4] = pf->line[k].y;
             o[5] = samples;
             o[6] = __dmul_rn(E, p.delta);
             o[7] = __ddiv_rn(__dmul_rn(C, p.delta), 3.6e6);
         }
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async();
+            bulk_s2g(out + (int64_t)j0 * 8, st, (uint32_t)(min(32, n_per - j0) * 64));
+            bulk_commit();
+        }
         done = done || hits != 0;
         S = __dadd_rn(S, __shfl_sync(kFull, incl, 31));
     }
+    if (lane == 0) bulk_wait_read0();  // the staging rows stay valid until the last store has read them
 }
