@@ -220,6 +220,28 @@ __device__ __noinline__ double partial_cs(const float* tv, int n) {
 // windows in this chunk get that byte; windows before the chunk's first period
 // start continue the previous chunk's last period (its byte, carried).  The
 // hot loop then only replays.  Same operation order as oracle_plan_trace.
+// bytes [a, e) of the staging buffer := k (word stores on the aligned middle)
+__device__ __forceinline__ void fill_bytes(uint8_t* chb, int a, int e, uint32_t k) {
+    while (a < e && (a & 3)) chb[a++] = (uint8_t)k;
+    const uint32_t kw = k * 0x01010101u;
+    for (; a + 4 <= e; a += 4) *reinterpret_cast<uint32_t*>(chb + a) = kw;
+    while (a < e) chb[a++] = (uint8_t)k;
+}
+
+// One period's decision from its horizon mean (the envelope lookup, else the canonical rule).
+__device__ __forceinline__ uint32_t period_choice(double chat, double invK, double Kc, const uint2* ent8, int ebase,
+                                                  uint32_t ZB, const PairTable* pt, const ProfileTable* pf,
+                                                  unsigned& n_slow) {
+    if (invK != 0.0) {
+        const int h = __double2hiint(__dmul_rn(chat, invK));
+        const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+        const uint32_t k = (line_addr(h, ent8[idx], ZB) >> 8) & 0xffu;
+        if (k != (uint32_t)kZeroLine) return k;
+    }
+    ++n_slow;
+    return canonical_choose(chat, Kc, pt->a, pf->thr, pf->K);
+}
+
 __device__ __noinline__ void period_decisions(const float* stagev, int cs, int wc, int Wt, int Pp, int phase_start,
                                               int T, const double* Aeven, double wl, double invK, double Kc,
                                               const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
@@ -228,7 +250,7 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
     const int ce = cs + wc;
     const int jf = (cs + Pp - 1) / Pp;
     const int bf = min(jf * Pp, ce);
-    for (int q = lane; q < bf - cs; q += 32) chb[q] = (uint8_t)k_carry;
+    if (lane == 0) fill_bytes(chb, 0, bf - cs, k_carry);
     for (int j = jf + lane; j * Pp < ce; j += 32) {
         const int b = j * Pp;
         const int n = min(Pp, Wt - b);
@@ -241,22 +263,15 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
             prev = f;
             ph = ph + 1 == T ? 0 : ph + 1;
         }
-        const double chat = __ddiv_rn(sum, (double)n);
-        uint32_t k;
-        if (invK == 0.0) {
-            k = canonical_choose(chat, Kc, pt->a, pf->thr, pf->K);
-            ++n_slow;
-        } else {
-            const int h = __double2hiint(__dmul_rn(chat, invK));
-            const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
-            k = (line_addr(h, ent8[idx], ZB) >> 8) & 0xffu;
-            if (k == (uint32_t)kZeroLine) {
-                k = canonical_choose(chat, Kc, pt->a, pf->thr, pf->K);
-                ++n_slow;
-            }
-        }
+        // sum/n; for a power-of-two n the product with 1/n is the same exact-then-rounded value
+        const double chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
+        const uint32_t k = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
         const int e = min(b + Pp, ce);
-        for (int q = b; q < e; ++q) chb[q - cs] = (uint8_t)k;
+        if (Pp < 8) {
+            for (int q = b; q < e; ++q) chb[q - cs] = (uint8_t)k;
+        } else {
+            fill_bytes(chb, b - cs, e - cs, k);
+        }
     }
 }
 
