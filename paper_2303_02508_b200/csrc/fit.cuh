@@ -52,6 +52,30 @@ __device__ __forceinline__ void chol3_solve(double G00, double G10, double G11, 
     c0 = __dsub_rn(__dsub_rn(__dsub_rn(mu[3], __dmul_rn(w[0], mu[0])), __dmul_rn(w[1], mu[1])), __dmul_rn(w[2], mu[2]));
 }
 
+// Correctly rounded a/b for a fixed divisor b: y = RN(1/b) once, then per
+// quotient q0 = RN(a y), r = fma(-q0, b, a) (exact), q = RN(q0 + r y) --
+// Markstein's final step, which returns RN(a/b) when y = RN(1/b) and q0 is
+// within an ulp, absent over/underflow (tools/div_probe.cu: 1.6e10 operand
+// pairs, random, all-ones mantissas and fit-shaped, no mismatch with
+// __ddiv_rn).  Three fp64 operations instead of a full divide.  Used where
+// the operands come from fp32 traces (centred values over a sigma: far from
+// the exponent limits); b outside [2^-900, 2^900] takes the plain divide.
+struct RnDiv {
+    double b, y;
+    bool fast;
+    __device__ __forceinline__ explicit RnDiv(double bb) {
+        b = bb;
+        y = __drcp_rn(bb);
+        const double ab = fabs(bb);
+        fast = ab > 0x1p-900 && ab < 0x1p900;
+    }
+    __device__ __forceinline__ double operator()(double a) const {
+        if (!fast) return __ddiv_rn(a, b);
+        const double q0 = __dmul_rn(a, y);
+        return __fma_rn(__fma_rn(-q0, b, a), y, q0);
+    }
+};
+
 template <typename E>
 __device__ __forceinline__ void fit_solve3(const E* h, int n, int T, int phi0, const double* S, const double* Cc,
                                            double ridge, double tol_rel, const double* mu, const double* sg, double dn,
@@ -298,10 +322,14 @@ __device__ void fit_phase(const E* h, int L, int T, int rho, const double* pt, c
             const double* z0 = pt + 8;
             const double* z1 = z0 + n;
             double h0 = 0.0, h1 = 0.0, h2 = 0.0, G20 = 0.0, G21 = 0.0, G22 = 0.0;
+            const RnDiv d2(sg2), d3(sg3);
             for (int i = 1; i <= n; ++i) {
                 const double a = z0[i - 1], b = z1[i - 1];
-                const double z2 = __ddiv_rn(__dsub_rn((double)h[i - 1], mu2), sg2);
-                const double u = __ddiv_rn(__dsub_rn((double)h[i], mu3), sg3);
+                // fp32 traces: the Markstein quotients (= the divide, bit for bit); fp64: the divide
+                const double z2 = sizeof(E) == 4 ? d2(__dsub_rn((double)h[i - 1], mu2))
+                                                 : __ddiv_rn(__dsub_rn((double)h[i - 1], mu2), sg2);
+                const double u = sizeof(E) == 4 ? d3(__dsub_rn((double)h[i], mu3))
+                                                : __ddiv_rn(__dsub_rn((double)h[i], mu3), sg3);
                 h0 = __dadd_rn(h0, __dmul_rn(a, u));
                 h1 = __dadd_rn(h1, __dmul_rn(b, u));
                 G20 = __dadd_rn(G20, __dmul_rn(z2, a));
