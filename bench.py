@@ -234,14 +234,15 @@ def svr_arg(args):
 def svr_flops(w: inputs.Workload) -> float:
     """Algorithmic fp64 operations of the SVR forecaster per launch pair
     (DESIGN §6.8), a LOWER bound, an fma counted as 2: per trace the kernel
-    matrix, n^2 RBF entries of 42 flops (squared distance 3 sub + 1 mul + 2 fma
-    = 8, gamma 1, exp 33: reduction 3 fma, 13 Horner fma, the 2^k scaling 1
-    mul -- floor is not counted), plus per window one prediction of 44n + 9
-    flops (z-scores 6, n x (RBF 42 + the coef fma 2), bias and
-    un-standardisation 3).  The SMO iterations are not counted (their number
-    depends on the data)."""
+    matrix, n^2 RBF entries of 27 flops (squared distance 3 sub + 1 mul + 2 fma
+    = 8, gamma 1; exp 18: the nearest-integer shift fma + sub 3, the two
+    reduction fma 4, 5 Horner fma 10, the table product 1 -- the 2^e scaling is
+    an integer add), plus per window one prediction of 29n + 5 flops (the lag
+    z-score 2, n x (RBF 27 + the coef fma 2), bias and un-standardisation 3;
+    the sin/cos z-scores are per phase).  The SMO iterations are not counted
+    (their number depends on the data)."""
     n = w.history_len - 1
-    return float(w.n_traces) * (42.0 * n * n + w.W * (44.0 * n + 9.0))
+    return float(w.n_traces) * (27.0 * n * n + w.W * (29.0 * n + 5.0))
 
 
 def fp64_peak():

@@ -150,14 +150,17 @@ typedef struct {
     int32_t status;                /* 0 ok, 4 bad value                */
 } oracle_svr_t;
 
-/* exp(x) for x <= 0: Cody-Waite reduction x = k ln2 + r (k the integer
- * nearest x/ln2, found by the 1.5*2^52 shift), degree-13 Taylor
- * polynomial of exp(r) in Horner form, scaled by 2^k (ldexp).  Every step is
- * one correctly rounded IEEE operation (the reduction and the Horner steps are
- * fma: a*b + c rounded once), so host and device agree bit for bit; |error|
- * <= 1 ulp of libm exp (pinned in tests).  The kernel's squared distance and
- * the prediction's sum of coef*K accumulate with fma as well. */
+/* exp(x) for x <= 0: x = (64 e + j) ln2/64 + r (kd = 64 e + j the integer
+ * nearest 64 x/ln2, found by the 1.5*2^52 shift), Cody-Waite reduction, the
+ * degree-5 Taylor polynomial of exp(r) (|r| <= ln2/128) in Horner form, times
+ * the table value 2^(j/64) (64 correctly rounded doubles), scaled by 2^e.
+ * Every step is one correctly rounded IEEE operation (the reduction and the
+ * Horner steps are fma: a*b + c rounded once), so host and device agree bit
+ * for bit; |error| <= 2 ulp of libm exp (pinned in tests).  The kernel's
+ * squared distance and the prediction's sum of coef*K accumulate with fma as
+ * well. */
 double oracle_rbf_exp(double x);
+const double* oracle_exp2_table(void);  /* the 64 values 2^(j/64) used by oracle_rbf_exp */
 
 /* Fit on the L history points hist[0..L) (rows as oracle_fit).  gamma <= 0:
  * 1/(3 * mean variance of the standardised features) (SPEC default). */

@@ -17,49 +17,83 @@ constexpr int kSvrZ = 0, kSvrCoef = 3 * kSvrMaxN, kSvrMu = kSvrCoef + kSvrMaxN, 
 constexpr int kSvrGamma = kSvrSigma + 4, kSvrRho = kSvrGamma + 1, kSvrN = kSvrRho + 1, kSvrKind = kSvrN + 1;
 constexpr int kSvrKeep = kSvrKind + 1, kSvrIters = kSvrKeep + 3, kSvrDoubles = (kSvrIters + 1 + 1) & ~1;
 
-// oracle_rbf_exp's constants in the constant bank: the fma's take them as
-// c[][] operands (no per-use uniform-register moves in the issue stream)
-__constant__ double c_svr_exp[17] = {
-    1.4426950408889634, 6.93147180369123816490e-01, 1.90821492927058770002e-10,
-    0x1.6124613a86d09p-33, 0x1.1eed8eff8d898p-29, 0x1.ae64567f544e4p-26, 0x1.27e4fb7789f5cp-22,
-    0x1.71de3a556c734p-19, 0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-13, 0x1.6c16c16c16c17p-10,
-    0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.5555555555555p-3, 0.5, 1.0, 1.0};
+// oracle_rbf_exp's scalar constants in the constant bank (the fma's take
+// them as c[][] operands): 64/ln2, (ln2/64)_hi, (ln2/64)_lo, 1/5!, 1/4!, 1/3!,
+// 1/2, 1, 1.
+__constant__ double c_svr_exp[9] = {0x1.71547652b82fep+6, 0x1.62e42feep-7, 0x1.a39ef35793c76p-39,
+                                    0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.5555555555555p-3,
+                                    0.5, 1.0, 1.0};
+// 2^(j/64), the doubles nearest the exact values (as oracle_exp2_64), in global
+// memory: indexed by data (a constant-bank read would serialise the lanes);
+// the forecast kernel stages them in shared memory.
+__device__ const double g_svr_exp2[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
 
-// q * 2^k (k <= 0 an integer, q in [0.70, 1.42]) rounded once: oracle_rbf_exp's
-// ldexp.  For k >= -1021 the product is normal and exact, so k is added to the
-// exponent field (integer pipe); below that (rare) two multiplications, the
-// first exact, the second rounding the exact value once.
+// q * 2^e (t in [0.99, 2)) rounded once: oracle_rbf_exp's ldexp.  For
+// e >= -1021 the product is normal and exact, so e is added to the exponent
+// field (integer pipe); below that (rare) two multiplications, the first
+// exact, the second rounding the exact value once.
 __device__ __forceinline__ double svr_scale2k(double q, int ki) {
     if (ki >= -1021) return __hiloint2double(__double2hiint(q) + (ki << 20), __double2loint(q));
     return __dmul_rn(__dmul_rn(q, 0x1p-600), __hiloint2double((ki + 600 + 1023) << 20, 0));
 }
 
-// oracle_rbf_exp(-y), operation for operation (fma = one rounding on both sides).
-// The oracle's guards on x = -y, !(x <= 0) -> NaN and x < -745 -> 0, are decided
-// on the bit pattern of y (integer pipe; the fp64 pipe is this kernel's bound),
-// k comes from the 1.5*2^52 shift: its low word is k, no float->int conversion.
-__device__ __forceinline__ double svr_exp_neg(double y) {
-    const unsigned long long v = (unsigned long long)__double_as_longlong(y);
-    const double m = __fma_rn(-y, c_svr_exp[0], 0x1.8p52);
-    const double k = __dsub_rn(m, 0x1.8p52);
-    double r = __fma_rn(-k, c_svr_exp[1], -y);
-    r = __fma_rn(-k, c_svr_exp[2], r);
-    double q = c_svr_exp[3];
-#pragma unroll
-    for (int j = 4; j < 17; ++j) q = __fma_rn(q, r, c_svr_exp[j]);
-    // x <= 0  <=>  y in [+0, +inf] or y == -0;  x < -745  <=>  y > 745 (not NaN)
-    if (!(v <= 0x7FF0000000000000ull || v == 0x8000000000000000ull)) return CUDART_NAN;
+// The uncommon keys of svr_exp_neg: y = -0 (x = +0), NaN or negative y
+// (x > 0 or NaN: NaN), y > 745 (0), and y in (707, 745] (a result that may be
+// subnormal: the general scaling).
+__device__ __noinline__ double svr_exp_rare(unsigned long long v, double t, int k) {
+    if (v == 0x8000000000000000ull) return svr_scale2k(t, k >> 6);
+    if (!(v <= 0x7FF0000000000000ull)) return CUDART_NAN;
     if (v > 0x4087480000000000ull) return 0.0;
-    return svr_scale2k(q, __double2loint(m));
+    return svr_scale2k(t, k >> 6);
 }
 
-__device__ __forceinline__ double svr_exp(double x) { return svr_exp_neg(-x); }
+// oracle_rbf_exp(-y), operation for operation (fma = one rounding on both
+// sides), with the 2^(j/64) table at `tab` (shared or global memory).  kd
+// comes from the 1.5*2^52 shift, whose low word is kd (no F2I), and
+// kd = 64 e + j splits with a mask and a shift.  The common keys, y in
+// [+0, 707], are one unsigned compare of the bit pattern (integer pipe; the
+// fp64 pipe is this kernel's bound) and need no further guard: x >= -707
+// gives e >= -1021, a normal result, scaled by an exponent-field add.
+__device__ __forceinline__ double svr_exp_neg(double y, const double* tab) {
+    const unsigned long long v = (unsigned long long)__double_as_longlong(y);
+    const double m = __fma_rn(-y, c_svr_exp[0], 0x1.8p52);
+    const double kd = __dsub_rn(m, 0x1.8p52);
+    double r = __fma_rn(-kd, c_svr_exp[1], -y);
+    r = __fma_rn(-kd, c_svr_exp[2], r);
+    double q = c_svr_exp[3];
+#pragma unroll
+    for (int j = 4; j < 9; ++j) q = __fma_rn(q, r, c_svr_exp[j]);
+    const int k = __double2loint(m);
+    const double t = __dmul_rn(tab[k & 63], q);
+    if (v <= 0x4086180000000000ull)  // bits(707.0)
+        return __hiloint2double(__double2hiint(t) + ((k >> 6) << 20), __double2loint(t));
+    return svr_exp_rare(v, t, k);
+}
+
+__device__ __forceinline__ double svr_exp(double x) { return svr_exp_neg(-x, g_svr_exp2); }
 
 // oracle rbf(): exp(-gamma * ((d0*d0 + d1*d1) + d2*d2)), each add fused with its product
 __device__ __forceinline__ double svr_rbf(const double* a, const double* b, double gamma) {
     const double d0 = __dsub_rn(a[0], b[0]), d1 = __dsub_rn(a[1], b[1]), d2 = __dsub_rn(a[2], b[2]);
     const double d = __fma_rn(d2, d2, __fma_rn(d1, d1, __dmul_rn(d0, d0)));
-    return svr_exp_neg(__dmul_rn(gamma, d));
+    return svr_exp_neg(__dmul_rn(gamma, d), g_svr_exp2);
 }
 
 struct SvrParams {
@@ -298,8 +332,8 @@ __global__ void __launch_bounds__(32 * kSvrWarps) svr_fit_kernel(const __grid_co
     }
 }
 
-// svr_forecast_kernel's shared memory (doubles): z[3n] | coef[n] | zs[T] | zc[T]
-__host__ __device__ inline int svr_fc_smem_doubles(int L, int T) { return 4 * (L - 1) + 2 * T; }
+// svr_forecast_kernel's shared memory (doubles): exp2[64] | z[3n] | coef[n] | zs[T] | zc[T]
+__host__ __device__ inline int svr_fc_smem_doubles(int L, int T) { return 64 + 4 * (L - 1) + 2 * T; }
 constexpr int kSvrFcThreads = 128, kSvrFcPer = 8;  // 128 threads x 8 periods per block
 
 // One block per (trace, 1024 decision periods): the trace's support vectors,
@@ -318,7 +352,8 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
     if (p.records[i * kRecDoubles + 5] != 0.0) return;  // bad history: no model (the sweep reports it)
     const double* M = p.models + i * kSvrDoubles;
     const int n = (int)M[kSvrN], T = p.T;
-    double* z = vsm;
+    double* e2 = vsm;
+    double* z = e2 + 64;
     double* cf = z + 3 * n;
     double* zs = cf + n;
     double* zc = zs + T;
@@ -328,6 +363,7 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
     const bool k0 = M[kSvrKeep] != 0.0, k1 = M[kSvrKeep + 1] != 0.0, k2 = M[kSvrKeep + 2] != 0.0;
     const double gamma = M[kSvrGamma], rho = M[kSvrRho];
     if (!constant) {
+        for (int q = threadIdx.x; q < 64; q += blockDim.x) e2[q] = g_svr_exp2[q];
         for (int q = threadIdx.x; q < 3 * n; q += blockDim.x) z[q] = M[kSvrZ + q];
         for (int q = threadIdx.x; q < n; q += blockDim.x) cf[q] = M[kSvrCoef + q];
         for (int q = threadIdx.x; q < T; q += blockDim.x) {
@@ -360,8 +396,8 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
                                  b2 = __dsub_rn(z[3 * t + 5], q2);
                     const double da = __fma_rn(a2, a2, __fma_rn(a1, a1, __dmul_rn(a0, a0)));
                     const double db = __fma_rn(b2, b2, __fma_rn(b1, b1, __dmul_rn(b0, b0)));
-                    const double Ka = svr_exp_neg(__dmul_rn(gamma, da));
-                    const double Kb = svr_exp_neg(__dmul_rn(gamma, db));
+                    const double Ka = svr_exp_neg(__dmul_rn(gamma, da), e2);
+                    const double Kb = svr_exp_neg(__dmul_rn(gamma, db), e2);
                     f = __fma_rn(cf[t], Ka, f);
                     f = __fma_rn(cf[t + 1], Kb, f);
                 }
@@ -369,7 +405,7 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
                     const double a0 = __dsub_rn(z[3 * t], q0), a1 = __dsub_rn(z[3 * t + 1], q1),
                                  a2 = __dsub_rn(z[3 * t + 2], q2);
                     const double da = __fma_rn(a2, a2, __fma_rn(a1, a1, __dmul_rn(a0, a0)));
-                    f = __fma_rn(cf[t], svr_exp_neg(__dmul_rn(gamma, da)), f);
+                    f = __fma_rn(cf[t], svr_exp_neg(__dmul_rn(gamma, da), e2), f);
                 }
                 f = __dsub_rn(f, rho);
                 pr = __dadd_rn(mu3, __dmul_rn(sg3, f));

@@ -15,15 +15,32 @@ import oracle
 
 
 def test_rbf_exp_against_libm():
-    """oracle_rbf_exp (DESIGN Q31) is within 1 ulp of libm exp on [-745, 0]."""
+    """oracle_rbf_exp (DESIGN Q31) is within 2 ulp (4.5e-16 relative) of libm
+    exp on [-745, 0]: the table value (1/2 ulp), the degree-5 polynomial on
+    |r| <= ln2/128 (truncation 3.5e-17) and the product's rounding."""
     xs = np.concatenate([-np.logspace(-14, np.log10(744.0), 40000), [-0.0, 0.0, -1e-300]])
     worst = 0.0
     for x in xs:
         ref = math.exp(x)
         if ref > 1e-300:
             worst = max(worst, abs(oracle.rbf_exp(x) - ref) / ref)
-    assert worst <= 2.3e-16
+    assert worst <= 4.5e-16
     assert oracle.rbf_exp(0.0) == 1.0 and oracle.rbf_exp(-800.0) == 0.0
+    assert math.isnan(oracle.rbf_exp(1e-300)) and oracle.rbf_exp(-math.inf) == 0.0
+    # subnormal results (the two-step scaling) within 1/2 ulp of the subnormal grid
+    for x in (-709.0, -720.5, -740.0, -744.9):
+        assert abs(oracle.rbf_exp(x) - math.exp(x)) <= 2.0 ** -1074
+
+
+def test_exp2_table_is_correctly_rounded():
+    """The 64 table values are the doubles nearest 2^(j/64) (60-digit decimal)."""
+    from decimal import Decimal, getcontext
+    getcontext().prec = 60
+    tab = oracle.exp2_table()
+    for j in range(64):
+        exact = Decimal(2) ** (Decimal(j) / Decimal(64))
+        assert tab[j] == float(exact), j          # float(Decimal) rounds to nearest
+        assert abs(Decimal(tab[j]) - exact) <= Decimal(2) ** -53 * exact
 
 
 def _history(seed, T=24, L=24, noise=20.0):
