@@ -255,13 +255,36 @@ chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_for
  *               plane), or NULL for the max-limit baseline;
  *   d_forecast  [n_traces][ld_f] f64 decision forecasts or NULL (rows get NaN);
  *   d_trace_ids [m] int64 trace indices, or NULL for traces 0..m-1;
- *   d_rows      [m][ceil(W/P)][8] f64 out, 16-byte aligned (rows leave by TMA bulk stores).
+ *   d_rows      [m][ceil(W/P)][8] f64 out, 16-byte aligned (rows leave by TMA bulk stores);
+ *   d_summary   [m][4] f64 out or NULL: Eq. 3 next to the stepwise
+ *               integration over the job's run:
+ *               {stepwise carbon g, TTA*AvgPower*AvgCI carbon g, AvgPower W,
+ *                time-weighted AvgCI g/kWh} (oracle_job_summary, <= 1e-9).
  * Rows match oracle_timeline (bit-identical for the dyadic synthetic inputs). */
 chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len, int32_t period_steps,
                               const uint8_t* d_choice, int64_t ld_c, const double* d_forecast, int64_t ld_f,
                               const chase_profile_t* profiles, int32_t n_profiles, const uint8_t* d_profile_id,
                               const double* d_job_samples, const int64_t* d_trace_ids, int64_t m, double* d_rows,
-                              void* d_ws, size_t ws_bytes, void* stream);
+                              double* d_summary, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Per-limit cost vectors behind the decisions (SPEC PeriodDecision S:296-297;
+ * Eq. 6), an audit output for m selected traces: for period j
+ * (windows s0 + jP .. , period_steps <= 1: per window) and limit k,
+ *   cost_k = ((eta*P_k)*chat + ((1-eta)*Pmax)*MaxCI) / Thr_k
+ * (the canonical rule's operations, without the 1/3.6e6 of Eq. 6, Q12) at the
+ * period's decision value chat = d_forecast[i][jP] (as chase_fit_forecast /
+ * chase_sweep write it), eta = cost->eta[0], Pmax and MaxCI as chase_sweep
+ * (d_max_ci: chase_fit_forecast's, required when cost->max_ci <= 0).  The
+ * chosen limit is the first minimum of its row.
+ *   d_costs [m][ceil(W/P)][ld_k] f64 out, ld_k >= the largest n_limits; the
+ *           entries k >= the trace's n_limits are NaN, as are all entries of a
+ *           NaN decision value (an invalid trace).
+ * Workspace: chase_workspace_bytes(traces, NULL, n_profiles, 1). */
+chase_status_t chase_period_costs(const double* d_forecast, int64_t n_traces, int64_t W, int64_t ld_f,
+                                  int32_t period_steps, const chase_profile_t* profiles, int32_t n_profiles,
+                                  const uint8_t* d_profile_id, const chase_cost_cfg_t* cost, const double* d_max_ci,
+                                  const int64_t* d_trace_ids, int64_t m, double* d_costs, int32_t ld_k, void* d_ws,
+                                  size_t ws_bytes, void* stream);
 
 /* End-to-end variant with HOST inputs (the public call a user makes when the
  * traces live in host memory; bench.py's "e2e" figure): streams chunks of

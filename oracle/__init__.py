@@ -65,6 +65,8 @@ def lib():
         L.oracle_plan_batch_f32.restype = i32
         L.oracle_timeline.argtypes = [vp, i32, i32, i32, vp, vp, i32, vp, vp, vp, f64, f64, vp]
         L.oracle_timeline.restype = i32
+        L.oracle_job_summary.argtypes = [vp, i32, i32, vp, i32, vp, vp, f64, f64, vp]
+        L.oracle_job_summary.restype = None
         L.oracle_rbf_exp.argtypes = [f64]
         L.oracle_rbf_exp.restype = f64
         L.oracle_exp2_table.argtypes = []
@@ -251,6 +253,17 @@ def timeline(c, *, L, period=1, choice=None, forecast=None, limit_w, avg_power, 
                               th.ctypes.data, delta, J, rows.ctypes.data)
     assert n == n_per
     return rows
+
+
+def job_summary(c, *, L, choice=None, avg_power, thr, delta=3600.0, J=0.0):
+    """Eq. 3 next to the stepwise carbon: [stepwise g, Eq. 3 g, AvgPower W, AvgCI g/kWh]."""
+    c = _f64(c)
+    ch = None if choice is None else np.ascontiguousarray(choice, dtype=np.uint8)
+    pw, th = _f64(avg_power), _f64(thr)
+    out = np.empty(4)
+    lib().oracle_job_summary(c.ctypes.data, len(c), L, None if ch is None else ch.ctypes.data, len(pw),
+                             pw.ctypes.data, th.ctypes.data, delta, J, out.ctypes.data)
+    return out
 
 
 def rbf_exp(x: float) -> float:

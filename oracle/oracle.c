@@ -543,6 +543,42 @@ int32_t oracle_timeline(const double* c, int32_t N, int32_t L, int32_t period, c
 }
 
 
+/* Eq. 3 next to the stepwise integration (SPEC optimizer DESIGN
+ * DECISION S:432): over the job's run (the fixed-work replay of
+ * oracle_replay, the completion window pro rata), TTA = (windows + f) Delta,
+ * AvgPower = energy / TTA, AvgCI = the time-weighted mean intensity, and
+ * CTA_eq3 = TTA * AvgPower * AvgCI = energy * AvgCI; the stepwise carbon is
+ * sum P_k c_w (pro rata).  out4 = {stepwise carbon g, Eq. 3 carbon g,
+ * AvgPower W, AvgCI g/kWh}.  choice NULL: the max-limit baseline. */
+void oracle_job_summary(const double* c, int32_t N, int32_t L, const uint8_t* choice, int32_t K,
+                        const double* avg_power, const double* thr, double delta, double J, double* out4) {
+    double S = 0.0, E = 0.0, C = 0.0, cj = 0.0, tw = 0.0;
+    for (int32_t w = L; w < N; ++w) {
+        const int k = choice ? choice[w - L] : K - 1;
+        const double sk = thr[k] * delta;
+        const double prevS = S;
+        S = S + sk;
+        if (J > 0.0 && S >= J) {
+            const double f = (J - prevS) / sk;
+            E = E + f * avg_power[k];
+            C = C + f * (avg_power[k] * c[w]);
+            cj = cj + f * c[w];
+            tw = tw + f;
+            break;
+        }
+        E = E + avg_power[k];
+        C = C + avg_power[k] * c[w];
+        cj = cj + c[w];
+        tw = tw + 1.0;
+    }
+    const double avg_ci = cj / tw;
+    out4[0] = (C * delta) / 3.6e6;
+    out4[1] = ((E * delta) * avg_ci) / 3.6e6;
+    out4[2] = E / tw;
+    out4[3] = avg_ci;
+}
+
+
 /* ---------------------------------------------------------------- epsilon-SVR (f2) */
 /* 2^(j/64), j = 0..63, each the double nearest the exact value (pinned in
  * tests/test_oracle_svr.py against a 60-digit decimal evaluation). */

@@ -184,6 +184,12 @@ int32_t oracle_timeline(const double* c, int32_t N, int32_t L, int32_t period, c
                         const double* forecast, int32_t K, const int32_t* limit_w, const double* avg_power,
                         const double* thr, double delta, double J, double* rows);
 
+/* Eq. 3 product-form carbon next to the stepwise one for one
+ * planned replay: out4 = {stepwise carbon g, TTA*AvgPower*AvgCI
+ * carbon g, AvgPower W, time-weighted AvgCI g/kWh} over the job's run. */
+void oracle_job_summary(const double* c, int32_t N, int32_t L, const uint8_t* choice, int32_t K,
+                        const double* avg_power, const double* thr, double delta, double J, double* out4);
+
 /* SPEC mape (Table 1 metric P:159-161): 100/n * sum |a_i - p_i| / |a_i|.
  * Returns NaN when n < 1 or some a_i == 0 ("errors: zero actual"). */
 double oracle_mape(const double* actual, const double* predicted, int64_t n);

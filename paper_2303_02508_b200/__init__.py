@@ -80,8 +80,11 @@ _lib.chase_sweep.restype = ctypes.c_int
 _lib.chase_forecast_mape.argtypes = [_P(Traces), _P(ForecastCfg), vp, vp, vp, sz, vp]
 _lib.chase_forecast_mape.restype = ctypes.c_int
 _lib.chase_timeline.argtypes = [_P(Traces), i32, i32, vp, i64, vp, i64, _P(Profile), i32, vp, vp, vp, i64, vp, vp,
-                                sz, vp]
+                                vp, sz, vp]
 _lib.chase_timeline.restype = ctypes.c_int
+_lib.chase_period_costs.argtypes = [vp, i64, i64, i64, i32, _P(Profile), i32, vp, _P(CostCfg), vp, vp, i64, vp, i32,
+                                    vp, sz, vp]
+_lib.chase_period_costs.restype = ctypes.c_int
 _lib.chase_diag_read.argtypes = [vp, _P(Diag), vp]
 _lib.chase_diag_read.restype = ctypes.c_int
 _lib.chase_sweep_host_staging_bytes.argtypes = [_P(Traces), i64, i32]
@@ -97,6 +100,7 @@ _lib.chase_version.restype = ctypes.c_char_p
 
 EXPORTED = ("chase_workspace_bytes", "chase_fit_forecast", "chase_plan_power_limits", "chase_replay",
             "chase_sweep", "chase_sweep_host", "chase_sweep_host_staging_bytes", "chase_forecast_mape", "chase_timeline",
+            "chase_period_costs",
             "chase_kernel_launches",
             "chase_set_kernel_events", "chase_diag_read", "chase_last_error", "chase_version")
 
@@ -232,13 +236,25 @@ def forecast_mape(traces: Traces, fcfg: ForecastCfg, mape, workspace, *, status=
 
 def timeline(traces: Traces, history_len: int, profiles, rows, m: int, workspace, *, period_steps=1, choice=None,
              ld_c: int = 0, forecast=None, ld_f: int = 0, profile_id=None, job_samples=None, trace_ids=None,
-             stream=None):
+             summary=None, stream=None):
     """chase_timeline: per-period audit rows [m][ceil(W/P)][8] of a planned replay
-    (choice None: the max-limit baseline)."""
+    (choice None: the max-limit baseline); summary [m][4]: stepwise and Eq. 3
+    carbon, AvgPower, AvgCI over the job's run."""
     Pr = _Profiles(profiles)
     _check(_lib.chase_timeline(ctypes.byref(traces), history_len, period_steps, _ptr(choice), ld_c, _ptr(forecast),
                                ld_f, Pr.arr, Pr.n, _ptr(profile_id), _ptr(job_samples), _ptr(trace_ids), m,
-                               _ptr(rows), _ptr(workspace), workspace.numel(), _stream(stream)), "chase_timeline")
+                               _ptr(rows), _ptr(summary), _ptr(workspace), workspace.numel(), _stream(stream)),
+           "chase_timeline")
+
+
+def period_costs(forecast, n_traces: int, W: int, ld_f: int, profiles, eta: float, costs, ld_k: int, m: int,
+                 workspace, *, period_steps=1, profile_id=None, max_power_w=0.0, max_ci=0.0, max_ci_per_trace=None,
+                 trace_ids=None, stream=None):
+    """chase_period_costs: Eq. 6 cost vectors [m][ceil(W/P)][ld_k] behind each decision."""
+    P, C = _Profiles(profiles), _Cost([eta], max_power_w, max_ci)
+    _check(_lib.chase_period_costs(_ptr(forecast), n_traces, W, ld_f, period_steps, P.arr, P.n, _ptr(profile_id),
+                                   ctypes.byref(C.cfg), _ptr(max_ci_per_trace), _ptr(trace_ids), m, _ptr(costs), ld_k,
+                                   _ptr(workspace), workspace.numel(), _stream(stream)), "chase_period_costs")
 
 
 def kernel_launches() -> int:

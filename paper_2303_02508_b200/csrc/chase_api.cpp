@@ -439,7 +439,7 @@ chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len,
                               const uint8_t* d_choice, int64_t ld_c, const double* d_forecast, int64_t ld_f,
                               const chase_profile_t* profiles, int32_t n_profiles, const uint8_t* d_profile_id,
                               const double* d_job_samples, const int64_t* d_trace_ids, int64_t m, double* d_rows,
-                              void* d_ws, size_t ws_bytes, void* stream) {
+                              double* d_summary, void* d_ws, size_t ws_bytes, void* stream) {
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_profiles(profiles, n_profiles))) return st;
     if (history_len < 1 || traces->n_steps <= history_len) return fail(CHASE_ERR_INVALID, "history_len");
@@ -462,9 +462,40 @@ chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len,
     cudaError_t e = launch_timeline(traces->data, traces->dtype == CHASE_F64, traces->ld, traces->n_traces,
                                     (int)traces->n_steps, history_len, period_steps > 1 ? period_steps : 1,
                                     n_profiles, (double)traces->interval_s, d_choice, ld_c, d_forecast, ld_f,
-                                    ws + WL.tables, d_profile_id, d_job_samples, d_trace_ids, m, d_rows, s);
+                                    ws + WL.tables, d_profile_id, d_job_samples, d_trace_ids, m, d_rows, d_summary, s);
     ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "timeline kernel");
+    return CHASE_OK;
+}
+
+chase_status_t chase_period_costs(const double* d_forecast, int64_t n_traces, int64_t W, int64_t ld_f,
+                                  int32_t period_steps, const chase_profile_t* profiles, int32_t n_profiles,
+                                  const uint8_t* d_profile_id, const chase_cost_cfg_t* cost, const double* d_max_ci,
+                                  const int64_t* d_trace_ids, int64_t m, double* d_costs, int32_t ld_k, void* d_ws,
+                                  size_t ws_bytes, void* stream) {
+    chase_status_t st;
+    if (n_traces < 0 || W < 1 || ld_f < W) return fail(CHASE_ERR_INVALID, "n_traces < 0, W < 1 or ld_f < W");
+    if (period_steps < 0) return fail(CHASE_ERR_INVALID, "period_steps < 0");
+    if ((st = check_profiles(profiles, n_profiles)) || (st = check_cost(cost, profiles, n_profiles))) return st;
+    int kmax = 0;
+    for (int q = 0; q < n_profiles; ++q) kmax = std::max(kmax, (int)profiles[q].n_limits);
+    if (ld_k < kmax) return fail(CHASE_ERR_INVALID, "ld_k=%d < the largest n_limits %d", ld_k, kmax);
+    if (m < 0 || (!d_trace_ids && m > n_traces)) return fail(CHASE_ERR_INVALID, "m out of range");
+    if (m > 0 && (!d_forecast || !d_costs)) return fail(CHASE_ERR_INVALID, "d_forecast / d_costs is NULL");
+    if (m > 0 && !(cost->max_ci > 0) && !d_max_ci)
+        return fail(CHASE_ERR_INVALID, "d_max_ci required when cost->max_ci <= 0 (P:184)");
+    const WsLayout WL = ws_layout(n_traces, 1, n_profiles, 1);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    chase_cost_cfg_t c1 = *cost;
+    c1.n_eta = 1;  // the cost vectors of eta[0]
+    std::vector<uint8_t> blob = build_tables(1, 1.0, profiles, n_profiles, &c1, 1);
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    const int P = period_steps > 1 ? period_steps : 1;
+    cudaError_t e = launch_period_costs(d_forecast, ld_f, n_traces, (int)W, P, ld_k, n_profiles, ws + WL.tables,
+                                        d_profile_id, d_max_ci, cost->max_ci, d_trace_ids, m, d_costs, s);
+    if (e != cudaSuccess) return cuda_fail(e, "period cost kernel");
     return CHASE_OK;
 }
 

@@ -363,7 +363,7 @@ cudaError_t launch_svr(const void* traces, bool f64, int64_t ld, int64_t n_trace
 cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int P,
                             int n_prof, double delta, const uint8_t* choice, int64_t ld_c, const double* forecast,
                             int64_t ld_f, const uint8_t* tables, const uint8_t* profile_id, const double* job,
-                            const int64_t* ids, int64_t m, double* rows, cudaStream_t s) {
+                            const int64_t* ids, int64_t m, double* rows, double* summary, cudaStream_t s) {
     if (m <= 0) return cudaSuccess;
     TimelineParams p;
     p.traces = traces;
@@ -384,9 +384,38 @@ cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_
     p.ids = ids;
     p.m = m;
     p.rows = rows;
+    p.summary = summary;
     const int64_t grid = (m + 3) / 4;
     if (f64) timeline_kernel<double><<<(unsigned)grid, 128, 0, s>>>(p);
     else timeline_kernel<float><<<(unsigned)grid, 128, 0, s>>>(p);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_period_costs(const double* forecast, int64_t ld_f, int64_t n_traces, int W, int P, int ld_k,
+                                int n_prof, const uint8_t* tables, const uint8_t* profile_id, const double* max_ci,
+                                double max_ci_fixed, const int64_t* ids, int64_t m, double* costs, cudaStream_t s) {
+    if (m <= 0) return cudaSuccess;
+    CostParams p;
+    p.forecast = forecast;
+    p.ld_f = ld_f;
+    p.n_traces = n_traces;
+    p.W = W;
+    p.P = P;
+    p.n_per = (W + P - 1) / P;
+    p.ld_k = ld_k;
+    p.n_prof = n_prof;
+    p.tables = tables;
+    p.profile_id = profile_id;
+    p.max_ci = max_ci;
+    p.max_ci_fixed = max_ci_fixed;
+    p.ids = ids;
+    p.m = m;
+    p.costs = costs;
+    const int64_t total = m * (int64_t)p.n_per * ld_k;
+    const int64_t grid = (total + 255) / 256;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    period_cost_kernel<<<(unsigned)grid, 256, 0, s>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }

@@ -136,7 +136,11 @@ cudaError_t launch_svr(const void* traces, bool f64, int64_t ld, int64_t n_trace
 cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int P,
                             int n_prof, double delta, const uint8_t* choice, int64_t ld_c, const double* forecast,
                             int64_t ld_f, const uint8_t* tables, const uint8_t* profile_id, const double* job,
-                            const int64_t* ids, int64_t m, double* rows, cudaStream_t s);
+                            const int64_t* ids, int64_t m, double* rows, double* summary, cudaStream_t s);
+// per-limit Eq. 6 cost vectors behind each period's decision (audit)
+cudaError_t launch_period_costs(const double* forecast, int64_t ld_f, int64_t n_traces, int W, int P, int ld_k,
+                                int n_prof, const uint8_t* tables, const uint8_t* profile_id, const double* max_ci,
+                                double max_ci_fixed, const int64_t* ids, int64_t m, double* costs, cudaStream_t s);
 // decision periods (period_steps > 1): one thread per (trace, period) writes the period's decision forecast
 cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
                            int P, const double* phase, const double* records, double* forecast, int64_t ld_f,

@@ -25,6 +25,7 @@ struct TimelineParams {
     const int64_t* ids;      // [m] or null: traces 0..m-1
     int64_t m;
     double* rows;            // [m][n_per][8]
+    double* summary;         // [m][4] or null: {stepwise carbon g, Eq. 3 carbon g, AvgPower W, AvgCI g/kWh}
 };
 
 // Rows of a round are staged per warp in shared memory and leave as one TMA
@@ -48,6 +49,7 @@ __global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ T
     const double J = p.job ? p.job[i] : 0.0;
     double S = 0.0;      // samples done before the current round (warp-uniform)
     bool done = false;
+    double tE = 0.0, tC = 0.0, tcj = 0.0, ttw = 0.0;  // this lane's job totals (Eq. 3 summary)
     double* out = p.rows + r * (int64_t)n_per * 8;
     for (int j0 = 0; j0 < n_per; j0 += 32) {
         const int j = j0 + lane;
@@ -71,12 +73,12 @@ __global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ T
         const bool hit = !done && valid && J > 0.0 && __dadd_rn(before, ssum) >= J;
         const unsigned hits = __ballot_sync(kFull, hit);
         const int first = hits ? __ffs(hits) - 1 : 32;
-        double samples = ssum, E = esum, C = psum;
+        double samples = ssum, E = esum, C = psum, cj = csum, tw = (double)n;
         if (done || lane > first) {
-            samples = E = C = 0.0;
+            samples = E = C = cj = tw = 0.0;
         } else if (lane == first) {  // re-walk the completion period window by window
             double Sr = before;
-            samples = E = C = 0.0;
+            samples = E = C = cj = tw = 0.0;
             for (int q = 0; q < n; ++q) {
                 const double cw = (double)row[s0 + b + q];
                 const int kw = ch ? ch[b + q] : pf->K - 1;
@@ -88,12 +90,22 @@ __global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ T
                     samples = __dadd_rn(samples, __dsub_rn(J, prevS));
                     E = __dadd_rn(E, __dmul_rn(f, ln.y));
                     C = __dadd_rn(C, __dmul_rn(f, __dmul_rn(ln.y, cw)));
+                    cj = __dadd_rn(cj, __dmul_rn(f, cw));
+                    tw = __dadd_rn(tw, f);
                     break;
                 }
                 samples = __dadd_rn(samples, ln.x);
                 E = __dadd_rn(E, ln.y);
                 C = __dadd_rn(C, __dmul_rn(ln.y, cw));
+                cj = __dadd_rn(cj, cw);
+                tw = __dadd_rn(tw, 1.0);
             }
+        }
+        if (valid) {
+            tE = __dadd_rn(tE, E);
+            tC = __dadd_rn(tC, C);
+            tcj = __dadd_rn(tcj, cj);
+            ttw = __dadd_rn(ttw, tw);
         }
         if (j0 > 0 && lane == 0) bulk_wait_read0();  // the previous round's store has read the staging rows
         __syncwarp();
@@ -118,5 +130,61 @@ __global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ T
         done = done || hits != 0;
         S = __dadd_rn(S, __shfl_sync(kFull, incl, 31));
     }
+    if (p.summary) {  // Eq. 3 next to the stepwise carbon (oracle_job_summary; sums in warp order, <= 1e-9)
+        tE = warp_sum(tE);
+        tC = warp_sum(tC);
+        tcj = warp_sum(tcj);
+        ttw = warp_sum(ttw);
+        if (lane == 0) {
+            const double avg_ci = __ddiv_rn(tcj, ttw);
+            double* o = p.summary + r * 4;
+            o[0] = __ddiv_rn(__dmul_rn(tC, p.delta), 3.6e6);
+            o[1] = __ddiv_rn(__dmul_rn(__dmul_rn(tE, p.delta), avg_ci), 3.6e6);
+            o[2] = __ddiv_rn(tE, ttw);
+            o[3] = avg_ci;
+        }
+    }
     if (lane == 0) bulk_wait_read0();  // the staging rows stay valid until the last store has read them
+}
+
+// Per-limit cost vectors behind the decisions (SPEC PeriodDecision S:296-297,
+// Eq. 6), audit output: for selected trace r and period j,
+// cost_k = ((a_k * chat) + Kc) / Thr_k with chat the period's decision value,
+// a_k = eta P_k and Kc = ((1 - eta) Pmax) MaxCI -- the canonical rule's
+// operations, so the chosen limit is the first minimum of its row.  One
+// thread per (trace, period, k); rows padded to ld_k with NaN.
+struct CostParams {
+    const double* forecast;
+    int64_t ld_f, n_traces;
+    int32_t W, P, n_per, ld_k, n_prof;
+    const uint8_t* tables;    // blob: profiles + one pair table per profile (eta[0])
+    const uint8_t* profile_id;
+    const double* max_ci;     // [n] or null (max_ci_fixed > 0)
+    double max_ci_fixed;
+    const int64_t* ids;
+    int64_t m;
+    double* costs;            // [m][n_per][ld_k]
+};
+
+__global__ void __launch_bounds__(256) period_cost_kernel(const __grid_constant__ CostParams p) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per_row = (int64_t)p.n_per * p.ld_k;
+    if (t >= p.m * per_row) return;
+    const int64_t r = t / per_row;
+    const int j = (int)((t - r * per_row) / p.ld_k);
+    const int k = (int)(t - r * per_row - (int64_t)j * p.ld_k);
+    const int64_t i = p.ids ? p.ids[r] : r;
+    int prof = p.profile_id ? (int)p.profile_id[i] : 0;
+    if (prof >= p.n_prof) prof = 0;
+    const ProfileTable* pf = blob_profiles(p.tables) + prof;
+    const TablesHeader* H = reinterpret_cast<const TablesHeader*>(p.tables);
+    const PairTable* pt = reinterpret_cast<const PairTable*>(p.tables + H->off_pair) + prof;
+    double v = CUDART_NAN;
+    if (k < pf->K) {
+        const double chat = p.forecast[i * p.ld_f + (int64_t)j * p.P];
+        const double maxci = p.max_ci_fixed > 0.0 ? p.max_ci_fixed : p.max_ci[i];
+        const double Kc = __dmul_rn(pt->kbase, maxci);
+        v = __ddiv_rn(__dadd_rn(__dmul_rn(pt->a[k], chat), Kc), pf->thr[k]);
+    }
+    p.costs[t] = v;
 }

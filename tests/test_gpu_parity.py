@@ -563,13 +563,17 @@ def test_timeline_rows_match_oracle(P):
     n_per = -(-(N - 24) // P)
     rows = torch.empty((m, n_per, 8), dtype=torch.float64, device=DEV)
     base = torch.empty_like(rows)
+    summ = torch.empty((m, 4), dtype=torch.float64, device=DEV)
+    summ_b = torch.empty_like(summ)
     t = cb.make_traces(x, n_steps=N)
     ws = cb.alloc_workspace(cb.workspace_bytes(t, cb.make_fcfg(), len(prof), 1), DEV)
     cb.timeline(t, 24, prof, rows, m, ws, period_steps=P, choice=res.choice[0], ld_c=pl.ld_c, forecast=res.forecast,
-                ld_f=pl.ld_f, profile_id=pid_t, job_samples=J_t, trace_ids=ids)
-    cb.timeline(t, 24, prof, base, m, ws, period_steps=P, profile_id=pid_t, job_samples=J_t, trace_ids=ids)
+                ld_f=pl.ld_f, profile_id=pid_t, job_samples=J_t, trace_ids=ids, summary=summ)
+    cb.timeline(t, 24, prof, base, m, ws, period_steps=P, profile_id=pid_t, job_samples=J_t, trace_ids=ids,
+                summary=summ_b)
     torch.cuda.synchronize()
     g, gb = rows.cpu().numpy(), base.cpu().numpy()
+    gs, gsb = summ.cpu().numpy(), summ_b.cpu().numpy()
     ch = res.choice.cpu().numpy()[0]
     fc = res.forecast.cpu().numpy()
     tot = res.per_trace_numpy()[0]
@@ -585,6 +589,64 @@ def test_timeline_rows_match_oracle(P):
         np.testing.assert_allclose(g[r][:, 6].sum(), tot["energy_j"][i], rtol=1e-12)
         np.testing.assert_allclose(g[r][:, 7].sum(), tot["carbon_g"][i], rtol=1e-12)
         np.testing.assert_allclose(gb[r][:, 7].sum(), tot["base_carbon_g"][i], rtol=1e-12)
+        # Eq. 3 next to the stepwise carbon (f4), aware and baseline, within 1e-9 of the oracle
+        os_ = oracle.job_summary(tr[i, :N].astype(np.float64), L=24, choice=ch[i, :N - 24], avg_power=p.avg_power_w,
+                                 thr=p.throughput_sps, J=J[i])
+        osb = oracle.job_summary(tr[i, :N].astype(np.float64), L=24, avg_power=p.avg_power_w,
+                                 thr=p.throughput_sps, J=J[i])
+        np.testing.assert_allclose(gs[r], os_, rtol=1e-9, atol=0)
+        np.testing.assert_allclose(gsb[r], osb, rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("P", [1, 24])
+def test_period_cost_vectors(P):
+    """Per-limit Eq. 6 cost vectors behind the decisions (f4; SPEC
+    PeriodDecision): each entry equals oracle_cost bit for bit at the period's
+    decision value, the chosen limit is the first minimum of its row, padding
+    and invalid traces are NaN."""
+    w = inputs.workload("C4", n_traces=40)
+    N = 24 + 700
+    prof = w.profiles
+    tr = inputs.synth_traces_host(w.n_traces, N, seed=900 + P)
+    tr[7, 300] = -1.0                                   # an invalid trace: NaN decisions and costs
+    pid = inputs.profile_ids_host(w.n_traces, seed=9, n_profiles=3)
+    x = torch.from_numpy(tr).to(DEV)
+    pid_t = torch.from_numpy(pid).to(DEV)
+    eta = 0.35
+    pl = cb.Planner(x, n_steps=N, profiles=prof, etas=[eta], profile_id=pid_t, want_choice=True,
+                    want_forecast=True, period_steps=P)
+    res = pl.run()
+    t = cb.make_traces(x, n_steps=N)
+    f = cb.make_fcfg(period_steps=P)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, len(prof), 1), DEV)
+    fc2 = torch.empty((w.n_traces, pl.ld_f), dtype=torch.float64, device=DEV)
+    maxci = torch.empty(w.n_traces, dtype=torch.float64, device=DEV)
+    cb.fit_forecast(t, f, fc2, pl.ld_f, ws, max_ci=maxci)
+    ids = torch.tensor([3, 7, 0, 39], dtype=torch.int64, device=DEV)
+    W = N - 24
+    n_per = -(-W // P)
+    ld_k = 12
+    costs = torch.empty((4, n_per, ld_k), dtype=torch.float64, device=DEV)
+    cb.period_costs(res.forecast, w.n_traces, W, pl.ld_f, prof, eta, costs, ld_k, 4, ws, period_steps=P,
+                    profile_id=pid_t, max_ci_per_trace=maxci, trace_ids=ids)
+    torch.cuda.synchronize()
+    g = costs.cpu().numpy()
+    fc = res.forecast.cpu().numpy()
+    ch = res.choice.cpu().numpy()[0]
+    mc = maxci.cpu().numpy()
+    for r, i in enumerate([3, 7, 0, 39]):
+        p = prof[pid[i]]
+        K = len(p.avg_power_w)
+        assert np.all(np.isnan(g[r][:, K:]))
+        if i == 7:
+            assert np.all(np.isnan(g[r]))
+            continue
+        pmax = float(p.limit_w[-1])
+        for j in range(n_per):
+            chat = fc[i, j * P]
+            want = [oracle.cost(eta, p.avg_power_w[k], p.throughput_sps[k], pmax, mc[i], chat) for k in range(K)]
+            assert list(g[r, j, :K]) == want
+            assert int(np.argmin(g[r, j, :K])) == ch[i, j * P]
 
 
 # ------------------------------------------------------------------ epsilon-SVR forecaster (SURVEY §8(f) f2)

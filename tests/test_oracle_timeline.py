@@ -77,3 +77,53 @@ def test_baseline_rows_are_flat_at_the_max_limit():
     one = oracle.timeline(c[:25], L=24, period=1, choice=None, limit_w=[150, 300], avg_power=[140.0, 290.0],
                           thr=[400.0, 800.0])
     assert one.shape == (1, 8)                       # S:419 one-period report -> one row
+
+
+def test_eq3_summary_covariance_identity():
+    """Eq. 3 vs the stepwise integration: over n full windows
+    stepwise - Eq.3 = n * Cov(P, c) * Delta / 3.6e6 exactly (Cov the population
+    covariance of the chosen power and the intensity); constant intensity makes
+    them equal; aligned / anti-aligned power and intensity give the sign."""
+    c = [500.0, 600.0, 200.0, 700.0, 100.0]            # L = 1: windows 600, 200, 700, 100
+    lines = dict(avg_power=[100.0, 300.0], thr=[400.0, 800.0])
+    for choice, sign in (([1, 0, 1, 0], 1), ([0, 1, 0, 1], -1)):
+        out = oracle.job_summary(np.array(c), L=1, choice=choice, **lines)
+        P = [lines["avg_power"][k] for k in choice]
+        cw = c[1:]
+        n = F(len(cw))
+        cov = sum(F(p) * F(x) for p, x in zip(P, cw)) / n - (sum(map(F, P)) / n) * (sum(map(F, cw)) / n)
+        assert out[0] - out[1] == float(n * cov * 3600 / 3600000)
+        assert (out[0] - out[1]) * sign > 0
+        assert out[2] == float(sum(map(F, P)) / n) and out[3] == float(sum(map(F, cw)) / n)
+    flat = oracle.job_summary(np.full(9, 432.0), L=1, choice=[1, 0, 0, 1, 0, 1, 1, 0], **lines)
+    assert flat[0] == flat[1] and flat[3] == 432.0
+
+
+def test_eq3_summary_matches_the_replay_and_timeline():
+    """The stepwise carbon is the replay's (and the timeline rows' sum); the
+    energy behind Eq. 3 is the replay's energy; a completing job counts its
+    last window pro rata (golden two-period scenario, exact rationals)."""
+    g = json.load(open(os.path.join(GOLDEN, "golden_2period.json")))
+    prof = g["profile"]
+    c = np.array([float(v) for v in g["trace"]])
+    out = oracle.job_summary(c, L=0, choice=g["choices"], avg_power=prof["avg_power_w"],
+                             thr=prof["throughput_sps"], delta=float(g["interval_s"]), J=float(g["job_samples"]))
+    d, J = F(g["interval_s"]), F(g["job_samples"])
+    f2 = (J - F(700) * d) / (F(850) * d)               # completion fraction of window 2 at 300 W
+    E = (F(190) + f2 * 295) * d                         # energy, J
+    tw = 1 + f2
+    avg_ci = (F(600) + f2 * 50) / tw
+    assert abs(out[0] - float(F(g["aware"]["carbon_g"]))) <= 1e-12 * out[0]
+    assert out[1] == float(E * avg_ci / 3600000) and out[3] == float(avg_ci)
+    assert out[2] == float((F(190) + f2 * 295) / tw)
+    rng = np.random.default_rng(7)
+    T, L, N = 24, 24, 24 + 300
+    tr = np.round((480 + 130 * np.sin(2 * np.pi * np.arange(N) / T) + rng.normal(0, 30, N)) * 64) / 64
+    P, Th = [140.0, 190.0, 238.0, 281.0], [400.0, 560.0, 680.0, 760.0]
+    J2 = 3600 * 250 * 420.0
+    fc, ch, tot, st = oracle.plan_trace(tr, L=L, T=T, avg_power=P, thr=Th, etas=[0.6], pmax=300.0, J=J2)
+    s = oracle.job_summary(tr, L=L, choice=ch[0], avg_power=P, thr=Th, J=J2)
+    assert abs(s[0] - tot["carbon_g"][0]) <= 1e-12 * s[0]
+    rows = oracle.timeline(tr, L=L, choice=ch[0], limit_w=[150, 200, 250, 300], avg_power=P, thr=Th, J=J2)
+    assert abs(rows[:, 7].sum() - s[0]) <= 1e-12 * s[0]
+    assert abs(s[2] * (tot["time_s"][0] / 3600) * 3600 - tot["energy_j"][0]) <= 1e-9 * tot["energy_j"][0]
