@@ -66,16 +66,21 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ clocks
-CLOCK_FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+CLOCK_FIELDS = ["timestamp", "index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
                 "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
                 "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
 
 
 class ClockSampler:
+    """nvidia-smi clocks and throttle reasons every 20 ms; the samples whose
+    timestamps fall in the timed region [begin(), end()] are reported (the one
+    nearest the region when it is shorter than the sampling interval)."""
+
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.t_begin = self.t_end = None
 
     def start(self):
         try:
@@ -83,11 +88,21 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", "--query-gpu=" + ",".join(CLOCK_FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
+            t_wait = time.time() + 3.0            # live before the timed region starts
+            while time.time() < t_wait and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
+            time.sleep(0.05)
         except (OSError, FileNotFoundError):
             self.proc = None
+
+    def begin(self):
+        self.t_begin = time.time()
+
+    def end(self):
+        self.t_end = time.time()
+        time.sleep(0.05)                          # one more sample past the region
 
     def stop(self):
         if not self.proc:
@@ -97,25 +112,31 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        import datetime
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < len(CLOCK_FIELDS):
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[2]), float(parts[3]),
+                             {n for n, v in zip(names, parts[6:10]) if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
         os.unlink(self.path)
-        if not sm:
+        if not rows:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        b = self.t_begin if self.t_begin is not None else rows[0][0]
+        e = self.t_end if self.t_end is not None else rows[-1][0]
+        sel = [r for r in rows if b <= r[0] <= e]
+        if not sel:                               # a region shorter than the interval: the nearest sample
+            mid = 0.5 * (b + e)
+            sel = [min(rows, key=lambda r: abs(r[0] - mid))]
+        reasons = set().union(*(r[3] for r in sel))
+        return {"sm_mhz": float(np.median([r[1] for r in sel])), "sm_max_mhz": float(max(r[2] for r in sel)),
+                "reasons": sorted(reasons), "samples": len(sel), "timed_region_s": round(e - b, 4)}
 
 
 def measured_peaks():
@@ -348,6 +369,7 @@ def main_chase(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = cb.kernel_launches()
+    clocks.begin()
     t0.record(stream)
     for k in range(args.steps):
         cb.set_kernel_events(*kev[k])
@@ -355,6 +377,7 @@ def main_chase(args):
     t1.record(stream)
     cb.set_kernel_events(None, None)
     torch.cuda.synchronize()
+    clocks.end()
     if world > 1:
         dist.barrier()
     launches = cb.kernel_launches() - launches0
@@ -528,6 +551,7 @@ def main_mape(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = cb.kernel_launches()
+    clocks.begin()
     t0.record(stream)
     for k in range(args.steps):
         cb.set_kernel_events(*kev[k])
@@ -535,6 +559,7 @@ def main_mape(args):
     t1.record(stream)
     cb.set_kernel_events(None, None)
     torch.cuda.synchronize()
+    clocks.end()
     if world > 1:
         dist.barrier()
     launches = cb.kernel_launches() - launches0
@@ -663,6 +688,7 @@ def main_timeline(args):
     clocks.start()
     torch.cuda.synchronize()
     launches0 = cb.kernel_launches()
+    clocks.begin()
     t0.record(stream)
     for k in range(args.steps):
         cb.set_kernel_events(*kev[k])
@@ -670,6 +696,7 @@ def main_timeline(args):
     t1.record(stream)
     cb.set_kernel_events(None, None)
     torch.cuda.synchronize()
+    clocks.end()
     launches = cb.kernel_launches() - launches0
     clk = clocks.stop()
     ms_per_step = t0.elapsed_time(t1) / args.steps
