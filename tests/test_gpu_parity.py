@@ -732,3 +732,113 @@ def test_svr_fit_forecast_and_mape():
     assert np.array_equal(np.isnan(g), np.isnan(om))
     ok = ~np.isnan(om)
     np.testing.assert_allclose(g[ok], om[ok], rtol=1e-9, atol=0)
+
+
+# ------------------------------------------------------------------ full-size sampled parity of every bench mode
+def _full_inputs(name, need_gb):
+    """The bench's inputs for a BASELINE config at full size (device-generated,
+    per-trace profile ids and budgets), or skip without the memory."""
+    w = inputs.workload(name)
+    free, _ = torch.cuda.mem_get_info()
+    if free < need_gb * 1e9:
+        pytest.skip(f"needs ~{need_gb} GB of free device memory")
+    x = torch.empty((w.n_traces, w.ld), dtype=torch.float32, device=DEV)
+    inputs.synth_traces_device(x, w.n_steps, seed=w.seed, mode=w.mode)
+    pid = None
+    if len(w.profiles) > 1:
+        pid = torch.empty(w.n_traces, dtype=torch.uint8, device=DEV)
+        inputs.profile_ids_device(pid, seed=w.seed, n_profiles=len(w.profiles))
+    per_prof = torch.tensor([w.interval_s * w.W * float(p.throughput_sps.min()) for p in w.profiles],
+                            dtype=torch.float64, device=DEV)
+    J = per_prof[pid.long()] if pid is not None else per_prof[0].expand(w.n_traces).contiguous()
+    return w, x, pid, J
+
+
+def _sample(n, k=12, seed=0):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, k)]))
+
+
+def _host_trace(w, i):
+    return inputs.synth_traces_host(1, w.n_steps, seed=w.seed, mode=w.mode, trace0=int(i))[0, :w.n_steps]
+
+
+@pytest.mark.parametrize("mode", ["svr", "roll1", "p24"])
+def test_full_size_modes_sampled(mode):
+    """The bench's launch configurations of the SVR forecaster (C4), the rolling
+    refit every window (C4) and daily decision periods (C5) at full size:
+    sampled traces against the oracle one by one (forecasts, choices, totals)."""
+    name, kw, okw = {"svr": ("C4", dict(svr={}), dict(svr={})),
+                     "roll1": ("C4", dict(refit_stride=1), dict(refit_stride=1)),
+                     "p24": ("C5", dict(period_steps=24), dict(period=24))}[mode]
+    w, x, pid, J = _full_inputs(name, 60 if name == "C5" else 20)
+    pl = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, profile_id=pid, job_samples=J,
+                    want_choice=True, want_forecast=name == "C4", want_per_trace=True, **kw)
+    res = pl.run()
+    torch.cuda.synchronize()
+    assert pl.diag().n_bad == 0 and res.sums.cpu().numpy()[0, 7] == w.n_traces
+    sample = _sample(w.n_traces, 10)
+    idx = torch.from_numpy(sample).to(DEV)
+    per = res.per_trace[:, idx].cpu().numpy().view(cb.TOTALS_DTYPE)[..., 0]
+    ch = res.choice[:, idx, :w.W].cpu().numpy()
+    fc = None if res.forecast is None else res.forecast[idx, :w.W].cpu().numpy()
+    pids = None if pid is None else pid.cpu().numpy()
+    Jh = J.cpu().numpy()
+    for q, i in enumerate(sample):
+        p = w.profiles[0 if pids is None else pids[i]]
+        ofc, och, ot, st = oracle.plan_trace(_host_trace(w, i), L=w.history_len, T=w.T, avg_power=p.avg_power_w,
+                                             thr=p.throughput_sps, etas=w.etas, pmax=float(p.limit_w[-1]),
+                                             J=float(Jh[i]), **okw)
+        assert st == 0
+        assert np.array_equal(ch[:, q], och), (mode, i)
+        if fc is not None:
+            assert np.array_equal(fc[q], ofc), (mode, i)
+        assert per[:, q].tobytes() == ot.tobytes(), (mode, i)
+    del pl, res, x
+    torch.cuda.empty_cache()
+
+
+def test_full_size_mape_and_timeline_sampled():
+    """The MAPE sweep at C5 and the timeline rows at C4, full size, in the
+    bench's launch configurations: sampled traces against the oracle."""
+    w, x, _, _ = _full_inputs("C5", 45)
+    t = cb.make_traces(x, n_steps=w.n_steps)
+    f = cb.make_fcfg(history_len=w.history_len)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    mp = torch.empty((w.n_traces, 2), dtype=torch.float64, device=DEV)
+    st = torch.empty(w.n_traces, dtype=torch.int32, device=DEV)
+    cb.forecast_mape(t, f, mp, ws, status=st)
+    torch.cuda.synchronize()
+    assert int((st != 0).sum()) == 0
+    sample = _sample(w.n_traces, 12, seed=1)
+    g = mp[torch.from_numpy(sample).to(DEV)].cpu().numpy()
+    for q, i in enumerate(sample):
+        s_, lin, per = oracle.evaluate(_host_trace(w, i), L=w.history_len, T=w.T)
+        assert s_ == 0
+        np.testing.assert_allclose(g[q], [lin, per], rtol=1e-9, atol=0)
+    del x, ws, mp, st
+    torch.cuda.empty_cache()
+
+    w, x, pid, J = _full_inputs("C4", 20)
+    pl = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, profile_id=pid, job_samples=J,
+                    want_choice=True, want_forecast=True)
+    res = pl.run()
+    sample = _sample(w.n_traces, 6, seed=2)
+    ids = torch.from_numpy(sample.astype(np.int64)).to(DEV)
+    rows = torch.empty((len(sample), w.W, 8), dtype=torch.float64, device=DEV)
+    t = cb.make_traces(x, n_steps=w.n_steps)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, cb.make_fcfg(), len(w.profiles), 1), DEV)
+    cb.timeline(t, w.history_len, w.profiles, rows, len(sample), ws, choice=res.choice[0], ld_c=pl.ld_c,
+                forecast=res.forecast, ld_f=pl.ld_f, profile_id=pid, job_samples=J, trace_ids=ids)
+    torch.cuda.synchronize()
+    g = rows.cpu().numpy()
+    ch = res.choice[0][ids, :w.W].cpu().numpy()
+    fc = res.forecast[ids, :w.W].cpu().numpy()
+    pids, Jh = pid.cpu().numpy(), J.cpu().numpy()
+    for q, i in enumerate(sample):
+        p = w.profiles[pids[i]]
+        o = oracle.timeline(_host_trace(w, i), L=w.history_len, choice=ch[q], forecast=fc[q], limit_w=p.limit_w,
+                            avg_power=p.avg_power_w, thr=p.throughput_sps, J=float(Jh[i]))
+        assert np.array_equal(g[q], o), i
+    del pl, res, x
+    torch.cuda.empty_cache()
