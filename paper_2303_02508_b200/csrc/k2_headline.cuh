@@ -27,6 +27,9 @@
 #ifndef CHASE_H_CHUNK
 #define CHASE_H_CHUNK 60
 #endif
+#ifndef CHASE_H_PAIRSUM
+#define CHASE_H_PAIRSUM 1  // 1: a group's four terms summed pairwise before the running sums
+#endif
 #ifndef CHASE_H_STG
 #define CHASE_H_STG 0   // 1: choice words stored from registers (per group) instead of a TMA store per chunk
 #endif
@@ -120,6 +123,29 @@ __device__ __forceinline__ uint32_t hot_group(const float4 v, const double2 A01,
     const float vv[4] = {v.x, v.y, v.z, v.w};
     const double AA[4] = {A01.x, A01.y, A23.x, A23.y};
     uint32_t ad[4];
+#if CHASE_H_PAIRSUM
+    // the group's four terms summed pairwise, then added to the running sums:
+    // one dependent add per group on each running sum instead of four (the
+    // totals' order changes; exact for the dyadic inputs, <= 1e-9 otherwise)
+    double2 ln4[4];
+    double cw4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const double cw = (double)vv[u];
+        const double p = __dadd_rn(AA[u], __dmul_rn(wl, lag));  // Eq. 1, unclamped for the lookup
+        const int h = __double2hiint(__dmul_rn(p, invK));
+        const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+        ad[u] = line_addr(h, ent8[idx], ZB);
+        ln4[u] = lds_line(ad[u]);  // (Thr_k * Delta, P_k)
+        cw4[u] = cw;
+        lag = cw;
+    }
+    a.S = __dadd_rn(a.S, __dadd_rn(__dadd_rn(ln4[0].x, ln4[1].x), __dadd_rn(ln4[2].x, ln4[3].x)));
+    a.E = __dadd_rn(a.E, __dadd_rn(__dadd_rn(ln4[0].y, ln4[1].y), __dadd_rn(ln4[2].y, ln4[3].y)));
+    a.C = __dadd_rn(a.C, __dadd_rn(__dadd_rn(__dmul_rn(ln4[0].y, cw4[0]), __dmul_rn(ln4[1].y, cw4[1])),
+                                   __dadd_rn(__dmul_rn(ln4[2].y, cw4[2]), __dmul_rn(ln4[3].y, cw4[3]))));
+    a.Cs = __dadd_rn(a.Cs, __dadd_rn(__dadd_rn(cw4[0], cw4[1]), __dadd_rn(cw4[2], cw4[3])));
+#else
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const double cw = (double)vv[u];
@@ -134,6 +160,7 @@ __device__ __forceinline__ uint32_t hot_group(const float4 v, const double2 A01,
         a.Cs = __dadd_rn(a.Cs, cw);
         lag = cw;
     }
+#endif
     const uint32_t word = __byte_perm(__byte_perm(ad[0], ad[1], 0x0051u), __byte_perm(ad[2], ad[3], 0x0051u), 0x5410u);
     a.slow |= word;
     return word;
