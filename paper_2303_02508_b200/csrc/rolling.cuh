@@ -55,7 +55,10 @@ __device__ int rolling_fit(const E* h, int L, int T, int rho, const RollParams& 
 }
 
 template <typename E>
-__global__ void __launch_bounds__(128) rolling_forecast_kernel(const __grid_constant__ RollParams p) {
+#ifndef CHASE_ROLL_MINB
+#define CHASE_ROLL_MINB 8  // 8 CTAs of 128 per SM (<= 64 registers): occupancy hides the fit's latency chains
+#endif
+__global__ void __launch_bounds__(128, CHASE_ROLL_MINB) rolling_forecast_kernel(const __grid_constant__ RollParams p) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= p.n_traces * (int64_t)p.n_orig) return;
     const int64_t i = idx / p.n_orig;
