@@ -75,7 +75,10 @@ __host__ __device__ inline int mape_smem_bytes(int T) { return (2 * T + 8 * (T +
 // windows per step (one 16-byte load, the lag of the first from the lane
 // below by a shuffle), 128 windows per warp step, four steps' loads in flight.
 template <typename E>
-__global__ void __launch_bounds__(256) mape_kernel(const __grid_constant__ MapeParams p) {
+#ifndef CHASE_MAPE_MINB
+#define CHASE_MAPE_MINB 1  // capping at 5-6 CTAs per SM was slower (10.4 / 10.8 vs 10.3 ms)
+#endif
+__global__ void __launch_bounds__(256, CHASE_MAPE_MINB) mape_kernel(const __grid_constant__ MapeParams p) {
     extern __shared__ double ph_sm[];
     const int T = p.T;
     for (int q = threadIdx.x; q < 2 * T; q += blockDim.x) ph_sm[q] = p.phase[q];

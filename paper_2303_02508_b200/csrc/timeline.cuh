@@ -32,7 +32,10 @@ struct TimelineParams {
 // bulk store (32 rows = 2 KB, contiguous in the output), not as 8 strided
 // 8-byte stores per lane.
 template <typename E>
-__global__ void __launch_bounds__(128) timeline_kernel(const __grid_constant__ TimelineParams p) {
+#ifndef CHASE_TL_MINB
+#define CHASE_TL_MINB 8  // <= 64 registers: 8 CTAs per SM (C4 P=1: 19.4 -> 16.0 ms on one box)
+#endif
+__global__ void __launch_bounds__(128, CHASE_TL_MINB) timeline_kernel(const __grid_constant__ TimelineParams p) {
     __shared__ __align__(128) double tl_rows[4][32 * 8];
     const int lane = threadIdx.x & 31;
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
