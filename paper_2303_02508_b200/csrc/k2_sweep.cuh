@@ -30,12 +30,18 @@ __device__ __forceinline__ void fused_full(const float* __restrict__ tv, int ngr
                                            const double2* __restrict__ lines, uint32_t* __restrict__ words,
                                            double* __restrict__ fout, Acc& a) {
     double lag = (double)tv[-1];
+    // the A terms (or, FIN, the forecasts in global memory) of group g+1 load during group g
+    double2 A01n = ngroups > 0 ? *reinterpret_cast<const double2*>(Ap) : make_double2(0.0, 0.0);
+    double2 A23n = ngroups > 0 ? *reinterpret_cast<const double2*>(Ap + 2) : make_double2(0.0, 0.0);
 #pragma unroll 1
     for (int g = 0; g < ngroups; ++g) {
         const float4 v = *reinterpret_cast<const float4*>(tv + 4 * g);
         if (FIRST) a.vmin = fminf(fminf(fminf(a.vmin, v.x), v.y), fminf(v.z, v.w));  // FMNMX3 x2
-        const double2 A01 = *reinterpret_cast<const double2*>(Ap + 4 * g);
-        const double2 A23 = *reinterpret_cast<const double2*>(Ap + 4 * g + 2);
+        const double2 A01 = A01n, A23 = A23n;
+        if (g + 1 < ngroups) {
+            A01n = *reinterpret_cast<const double2*>(Ap + 4 * g + 4);
+            A23n = *reinterpret_cast<const double2*>(Ap + 4 * g + 6);
+        }
         const float vv[4] = {v.x, v.y, v.z, v.w};
         const double AA[4] = {A01.x, A01.y, A23.x, A23.y};
         uint32_t word = 0;
