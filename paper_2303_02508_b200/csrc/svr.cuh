@@ -71,6 +71,36 @@ __device__ __noinline__ double svr_exp_rare(unsigned long long v, double t, int 
 // [+0, 707], are one unsigned compare of the bit pattern (integer pipe; the
 // fp64 pipe is this kernel's bound) and need no further guard: x >= -707
 // gives e >= -1021, a normal result, scaled by an exponent-field add.
+// The six non-trivial constants of the exp held in registers for a kernel's
+// lifetime (the moves through inline asm keep the compiler from re-reading
+// them from the constant bank inside the term loop).
+struct SvrExpK {
+    double c[6];
+    __device__ __forceinline__ SvrExpK() {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) asm volatile("mov.b64 %0, %1;" : "=d"(c[j]) : "d"(c_svr_exp[j]));
+    }
+};
+
+__device__ __forceinline__ double svr_exp_neg(double y, const double* tab, const SvrExpK& K) {
+    const unsigned long long v = (unsigned long long)__double_as_longlong(y);
+    const double m = __fma_rn(-y, K.c[0], 0x1.8p52);
+    const double kd = __dsub_rn(m, 0x1.8p52);
+    double r = __fma_rn(-kd, K.c[1], -y);
+    r = __fma_rn(-kd, K.c[2], r);
+    double q = K.c[3];
+    q = __fma_rn(q, r, K.c[4]);
+    q = __fma_rn(q, r, K.c[5]);
+    q = __fma_rn(q, r, 0.5);
+    q = __fma_rn(q, r, 1.0);
+    q = __fma_rn(q, r, 1.0);
+    const int k = __double2loint(m);
+    const double t = __dmul_rn(tab[k & 63], q);
+    if (v <= 0x4086180000000000ull)  // bits(707.0)
+        return __hiloint2double(__double2hiint(t) + ((k >> 6) << 20), __double2loint(t));
+    return svr_exp_rare(v, t, k);
+}
+
 __device__ __forceinline__ double svr_exp_neg(double y, const double* tab) {
     const unsigned long long v = (unsigned long long)__double_as_longlong(y);
     const double m = __fma_rn(-y, c_svr_exp[0], 0x1.8p52);
@@ -332,8 +362,9 @@ __global__ void __launch_bounds__(32 * kSvrWarps) svr_fit_kernel(const __grid_co
     }
 }
 
-// svr_forecast_kernel's shared memory (doubles): exp2[64] | z[3n] | coef[n] | zs[T] | zc[T]
-__host__ __device__ inline int svr_fc_smem_doubles(int L, int T) { return 64 + 4 * (L - 1) + 2 * T; }
+// svr_forecast_kernel's dynamic shared memory (doubles): z[3n] | coef[n] | zs[T] | zc[T]
+// (plus the static 2^(j/64) table)
+__host__ __device__ inline int svr_fc_smem_doubles(int L, int T) { return 4 * (L - 1) + 2 * T; }
 constexpr int kSvrFcThreads = 128, kSvrFcPer = 8;  // 128 threads x 8 periods per block
 
 // One block per (trace, 1024 decision periods): the trace's support vectors,
@@ -352,8 +383,8 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
     if (p.records[i * kRecDoubles + 5] != 0.0) return;  // bad history: no model (the sweep reports it)
     const double* M = p.models + i * kSvrDoubles;
     const int n = (int)M[kSvrN], T = p.T;
-    double* e2 = vsm;
-    double* z = e2 + 64;
+    __shared__ double e2[64];  // static: addressed as shared memory directly in the term loop
+    double* z = vsm;
     double* cf = z + 3 * n;
     double* zs = cf + n;
     double* zc = zs + T;
@@ -372,6 +403,7 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
         }
     }
     __syncthreads();
+    const SvrExpK EK;
     const int W = p.N - p.L, P = p.P;
     const E* row = reinterpret_cast<const E*>(p.traces) + i * p.ld;
     const int per_end = min(p.n_per, (int)(blockIdx.y + 1) * kSvrFcThreads * kSvrFcPer);
@@ -396,8 +428,8 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
                                  b2 = __dsub_rn(z[3 * t + 5], q2);
                     const double da = __fma_rn(a2, a2, __fma_rn(a1, a1, __dmul_rn(a0, a0)));
                     const double db = __fma_rn(b2, b2, __fma_rn(b1, b1, __dmul_rn(b0, b0)));
-                    const double Ka = svr_exp_neg(__dmul_rn(gamma, da), e2);
-                    const double Kb = svr_exp_neg(__dmul_rn(gamma, db), e2);
+                    const double Ka = svr_exp_neg(__dmul_rn(gamma, da), e2, EK);
+                    const double Kb = svr_exp_neg(__dmul_rn(gamma, db), e2, EK);
                     f = __fma_rn(cf[t], Ka, f);
                     f = __fma_rn(cf[t + 1], Kb, f);
                 }
@@ -405,7 +437,7 @@ __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __gri
                     const double a0 = __dsub_rn(z[3 * t], q0), a1 = __dsub_rn(z[3 * t + 1], q1),
                                  a2 = __dsub_rn(z[3 * t + 2], q2);
                     const double da = __fma_rn(a2, a2, __fma_rn(a1, a1, __dmul_rn(a0, a0)));
-                    f = __fma_rn(cf[t], svr_exp_neg(__dmul_rn(gamma, da), e2), f);
+                    f = __fma_rn(cf[t], svr_exp_neg(__dmul_rn(gamma, da), e2, EK), f);
                 }
                 f = __dsub_rn(f, rho);
                 pr = __dadd_rn(mu3, __dmul_rn(sg3, f));
