@@ -267,6 +267,19 @@ chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len,
                               const double* d_job_samples, const int64_t* d_trace_ids, int64_t m, double* d_rows,
                               double* d_summary, void* d_ws, size_t ws_bytes, void* stream);
 
+/* SPEC --count-profiling (DESIGN Q33): the cost of profiling the
+ * power-limit table before the job, one trace step per limit in increasing
+ * order over steps history_len-K .. history_len-1, each at that limit's
+ * average power:
+ *   d_out [n_traces][3] f64 out: {time s, energy J, carbon g}, to add to a
+ *         replay's totals (chase_sweep's per-trace totals exclude profiling).
+ * history_len >= the largest n_limits.  Workspace: chase_workspace_bytes(
+ * traces, NULL, n_profiles, 1).  Bit-identical to oracle_profiling_overhead. */
+chase_status_t chase_profiling_overhead(const chase_traces_t* traces, int32_t history_len,
+                                        const chase_profile_t* profiles, int32_t n_profiles,
+                                        const uint8_t* d_profile_id, double* d_out, void* d_ws, size_t ws_bytes,
+                                        void* stream);
+
 /* Per-limit cost vectors behind the decisions (SPEC PeriodDecision S:296-297;
  * Eq. 6), an audit output for m selected traces: for period j
  * (windows s0 + jP .. , period_steps <= 1: per window) and limit k,

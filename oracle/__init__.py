@@ -67,6 +67,8 @@ def lib():
         L.oracle_timeline.restype = i32
         L.oracle_job_summary.argtypes = [vp, i32, i32, vp, i32, vp, vp, f64, f64, vp]
         L.oracle_job_summary.restype = None
+        L.oracle_profiling_overhead.argtypes = [vp, i32, i32, vp, f64, vp]
+        L.oracle_profiling_overhead.restype = i32
         L.oracle_rbf_exp.argtypes = [f64]
         L.oracle_rbf_exp.restype = f64
         L.oracle_exp2_table.argtypes = []
@@ -264,6 +266,15 @@ def job_summary(c, *, L, choice=None, avg_power, thr, delta=3600.0, J=0.0):
     lib().oracle_job_summary(c.ctypes.data, len(c), L, None if ch is None else ch.ctypes.data, len(pw),
                              pw.ctypes.data, th.ctypes.data, delta, J, out.ctypes.data)
     return out
+
+
+def profiling_overhead(c, *, L, avg_power, delta=3600.0):
+    """SPEC --count-profiling: [time s, energy J, carbon g] of profiling the K limits before the job."""
+    c = _f64(c)
+    pw = _f64(avg_power)
+    out = np.empty(3)
+    st = lib().oracle_profiling_overhead(c.ctypes.data, L, len(pw), pw.ctypes.data, delta, out.ctypes.data)
+    return st, out
 
 
 def rbf_exp(x: float) -> float:

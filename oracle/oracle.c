@@ -579,6 +579,25 @@ void oracle_job_summary(const double* c, int32_t N, int32_t L, const uint8_t* ch
 }
 
 
+/* SPEC --count-profiling (DESIGN Q33): profiling runs one trace step
+ * per limit, in increasing limit order, over the K steps just before the job
+ * start (steps L-K .. L-1), each at that limit's average power.  out3 =
+ * {time s, energy J, carbon g} to add to a replay's totals; needs L >= K. */
+int32_t oracle_profiling_overhead(const double* c, int32_t L, int32_t K, const double* avg_power, double delta,
+                                  double* out3) {
+    if (L < K) return 2;
+    double E = 0.0, C = 0.0;
+    for (int32_t k = 0; k < K; ++k) {
+        E = E + avg_power[k];
+        C = C + avg_power[k] * c[L - K + k];
+    }
+    out3[0] = (double)K * delta;
+    out3[1] = E * delta;
+    out3[2] = (C * delta) / 3.6e6;
+    return 0;
+}
+
+
 /* ---------------------------------------------------------------- epsilon-SVR (f2) */
 /* 2^(j/64), j = 0..63, each the double nearest the exact value (pinned in
  * tests/test_oracle_svr.py against a 60-digit decimal evaluation). */

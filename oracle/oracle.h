@@ -184,6 +184,12 @@ int32_t oracle_timeline(const double* c, int32_t N, int32_t L, int32_t period, c
                         const double* forecast, int32_t K, const int32_t* limit_w, const double* avg_power,
                         const double* thr, double delta, double J, double* rows);
 
+/* SPEC --count-profiling (DESIGN Q33): one trace step per limit over
+ * steps L-K .. L-1 at each limit's average power; out3 = {time s, energy J,
+ * carbon g}.  Returns 2 when L < K. */
+int32_t oracle_profiling_overhead(const double* c, int32_t L, int32_t K, const double* avg_power, double delta,
+                                  double* out3);
+
 /* Eq. 3 product-form carbon next to the stepwise one for one
  * planned replay: out4 = {stepwise carbon g, TTA*AvgPower*AvgCI
  * carbon g, AvgPower W, time-weighted AvgCI g/kWh} over the job's run. */

@@ -85,6 +85,8 @@ _lib.chase_timeline.restype = ctypes.c_int
 _lib.chase_period_costs.argtypes = [vp, i64, i64, i64, i32, _P(Profile), i32, vp, _P(CostCfg), vp, vp, i64, vp, i32,
                                     vp, sz, vp]
 _lib.chase_period_costs.restype = ctypes.c_int
+_lib.chase_profiling_overhead.argtypes = [_P(Traces), i32, _P(Profile), i32, vp, vp, vp, sz, vp]
+_lib.chase_profiling_overhead.restype = ctypes.c_int
 _lib.chase_diag_read.argtypes = [vp, _P(Diag), vp]
 _lib.chase_diag_read.restype = ctypes.c_int
 _lib.chase_sweep_host_staging_bytes.argtypes = [_P(Traces), i64, i32]
@@ -100,7 +102,7 @@ _lib.chase_version.restype = ctypes.c_char_p
 
 EXPORTED = ("chase_workspace_bytes", "chase_fit_forecast", "chase_plan_power_limits", "chase_replay",
             "chase_sweep", "chase_sweep_host", "chase_sweep_host_staging_bytes", "chase_forecast_mape", "chase_timeline",
-            "chase_period_costs",
+            "chase_period_costs", "chase_profiling_overhead",
             "chase_kernel_launches",
             "chase_set_kernel_events", "chase_diag_read", "chase_last_error", "chase_version")
 
@@ -245,6 +247,14 @@ def timeline(traces: Traces, history_len: int, profiles, rows, m: int, workspace
                                ld_f, Pr.arr, Pr.n, _ptr(profile_id), _ptr(job_samples), _ptr(trace_ids), m,
                                _ptr(rows), _ptr(summary), _ptr(workspace), workspace.numel(), _stream(stream)),
            "chase_timeline")
+
+
+def profiling_overhead(traces: Traces, history_len: int, profiles, out, workspace, *, profile_id=None, stream=None):
+    """chase_profiling_overhead: [n][3] {time s, energy J, carbon g} of profiling the K limits before the job."""
+    P = _Profiles(profiles)
+    _check(_lib.chase_profiling_overhead(ctypes.byref(traces), history_len, P.arr, P.n, _ptr(profile_id), _ptr(out),
+                                         _ptr(workspace), workspace.numel(), _stream(stream)),
+           "chase_profiling_overhead")
 
 
 def period_costs(forecast, n_traces: int, W: int, ld_f: int, profiles, eta: float, costs, ld_k: int, m: int,

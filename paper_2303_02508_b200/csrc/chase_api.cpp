@@ -468,6 +468,34 @@ chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len,
     return CHASE_OK;
 }
 
+chase_status_t chase_profiling_overhead(const chase_traces_t* traces, int32_t history_len,
+                                        const chase_profile_t* profiles, int32_t n_profiles,
+                                        const uint8_t* d_profile_id, double* d_out, void* d_ws, size_t ws_bytes,
+                                        void* stream) {
+    chase_status_t st;
+    if ((st = check_traces(traces)) || (st = check_profiles(profiles, n_profiles))) return st;
+    int kmax = 0;
+    for (int q = 0; q < n_profiles; ++q) kmax = std::max(kmax, (int)profiles[q].n_limits);
+    if (history_len < kmax || history_len > traces->n_steps)
+        return fail(CHASE_ERR_INVALID, "history_len=%d must hold one step per limit (>= %d, DESIGN Q33)", history_len,
+                    kmax);
+    if (traces->n_traces > 0 && !d_out) return fail(CHASE_ERR_INVALID, "d_out is NULL");
+    const int T = 86400 / traces->interval_s;
+    const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, 1);
+    if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
+    std::vector<double> etas(1, 0.5);  // the tables need an eta; the overhead does not use it
+    chase_cost_cfg_t cc{etas.data(), 1, 0, 0.0, 0.0};
+    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, &cc, 1);
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    if ((st = upload_tables(blob, ws, WL, s))) return st;
+    cudaError_t e = launch_profiling(traces->data, traces->dtype == CHASE_F64, traces->ld, traces->n_traces,
+                                     history_len, (double)traces->interval_s, ws + WL.tables, n_profiles,
+                                     d_profile_id, d_out, s);
+    if (e != cudaSuccess) return cuda_fail(e, "profiling kernel");
+    return CHASE_OK;
+}
+
 chase_status_t chase_period_costs(const double* d_forecast, int64_t n_traces, int64_t W, int64_t ld_f,
                                   int32_t period_steps, const chase_profile_t* profiles, int32_t n_profiles,
                                   const uint8_t* d_profile_id, const chase_cost_cfg_t* cost, const double* d_max_ci,

@@ -392,6 +392,17 @@ cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_
     return cudaGetLastError();
 }
 
+cudaError_t launch_profiling(const void* traces, bool f64, int64_t ld, int64_t n, int L, double delta,
+                             const uint8_t* tables, int n_prof, const uint8_t* profile_id, double* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t grid = (n + 255) / 256;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (f64) profiling_kernel<double><<<(unsigned)grid, 256, 0, s>>>(traces, ld, n, L, delta, tables, n_prof, profile_id, out);
+    else profiling_kernel<float><<<(unsigned)grid, 256, 0, s>>>(traces, ld, n, L, delta, tables, n_prof, profile_id, out);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_period_costs(const double* forecast, int64_t ld_f, int64_t n_traces, int W, int P, int ld_k,
                                 int n_prof, const uint8_t* tables, const uint8_t* profile_id, const double* max_ci,
                                 double max_ci_fixed, const int64_t* ids, int64_t m, double* costs, cudaStream_t s) {

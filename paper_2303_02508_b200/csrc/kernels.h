@@ -137,6 +137,9 @@ cudaError_t launch_timeline(const void* traces, bool f64, int64_t ld, int64_t n_
                             int n_prof, double delta, const uint8_t* choice, int64_t ld_c, const double* forecast,
                             int64_t ld_f, const uint8_t* tables, const uint8_t* profile_id, const double* job,
                             const int64_t* ids, int64_t m, double* rows, double* summary, cudaStream_t s);
+// SPEC --count-profiling: the profiling run's {time, energy, carbon} per trace
+cudaError_t launch_profiling(const void* traces, bool f64, int64_t ld, int64_t n, int L, double delta,
+                             const uint8_t* tables, int n_prof, const uint8_t* profile_id, double* out, cudaStream_t s);
 // per-limit Eq. 6 cost vectors behind each period's decision (audit)
 cudaError_t launch_period_costs(const double* forecast, int64_t ld_f, int64_t n_traces, int W, int P, int ld_k,
                                 int n_prof, const uint8_t* tables, const uint8_t* profile_id, const double* max_ci,

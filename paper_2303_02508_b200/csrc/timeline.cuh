@@ -191,3 +191,29 @@ __global__ void __launch_bounds__(256) period_cost_kernel(const __grid_constant_
     }
     p.costs[t] = v;
 }
+
+// SPEC --count-profiling (DESIGN Q33): the profiling run before the job,
+// one trace step per limit in increasing order over steps L-K .. L-1, each at
+// the limit's average power.  One thread per trace: {time s, energy J,
+// carbon g} in oracle_profiling_overhead's operation order.
+template <typename E>
+__global__ void __launch_bounds__(256) profiling_kernel(const void* traces, int64_t ld, int64_t n, int L,
+                                                        double delta, const uint8_t* tables, int n_prof,
+                                                        const uint8_t* profile_id, double* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int prof = profile_id ? (int)profile_id[i] : 0;
+    if (prof >= n_prof) prof = 0;
+    const ProfileTable* pf = blob_profiles(tables) + prof;
+    const E* row = reinterpret_cast<const E*>(traces) + i * ld;
+    const int K = pf->K;
+    double Ep = 0.0, Cp = 0.0;
+    for (int k = 0; k < K; ++k) {
+        const double P = pf->line[k].y;
+        Ep = __dadd_rn(Ep, P);
+        Cp = __dadd_rn(Cp, __dmul_rn(P, (double)row[L - K + k]));
+    }
+    out[3 * i] = __dmul_rn((double)K, delta);
+    out[3 * i + 1] = __dmul_rn(Ep, delta);
+    out[3 * i + 2] = __ddiv_rn(__dmul_rn(Cp, delta), 3.6e6);
+}

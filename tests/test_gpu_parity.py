@@ -842,3 +842,25 @@ def test_full_size_mape_and_timeline_sampled():
         assert np.array_equal(g[q], o), i
     del pl, res, x
     torch.cuda.empty_cache()
+
+
+def test_profiling_overhead_matches_oracle():
+    """SPEC --count-profiling (DESIGN Q33): per-trace profiling time, energy and
+    carbon bit-identical to the oracle, per-trace profiles."""
+    w = inputs.workload("C4", n_traces=50)
+    N = 24 + 100
+    tr = inputs.synth_traces_host(w.n_traces, N, seed=31)
+    pid = inputs.profile_ids_host(w.n_traces, seed=3, n_profiles=3)
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=N)
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, None, 3, 1), DEV)
+    out = torch.empty((w.n_traces, 3), dtype=torch.float64, device=DEV)
+    cb.profiling_overhead(t, 24, w.profiles, out, ws, profile_id=torch.from_numpy(pid).to(DEV))
+    torch.cuda.synchronize()
+    g = out.cpu().numpy()
+    for i in range(w.n_traces):
+        st, o = oracle.profiling_overhead(tr[i, :N].astype(np.float64), L=24,
+                                          avg_power=w.profiles[pid[i]].avg_power_w)
+        assert st == 0 and list(g[i]) == list(o), i
+    with pytest.raises(cb.ChaseError, match="history_len"):
+        cb.profiling_overhead(t, 5, w.profiles, out, ws)

@@ -127,3 +127,14 @@ def test_eq3_summary_matches_the_replay_and_timeline():
     rows = oracle.timeline(tr, L=L, choice=ch[0], limit_w=[150, 200, 250, 300], avg_power=P, thr=Th, J=J2)
     assert abs(rows[:, 7].sum() - s[0]) <= 1e-12 * s[0]
     assert abs(s[2] * (tot["time_s"][0] / 3600) * 3600 - tot["energy_j"][0]) <= 1e-9 * tot["energy_j"][0]
+
+
+def test_profiling_overhead_by_hand():
+    """DESIGN Q33 (SPEC --count-profiling): K steps before the job, one
+    per limit in increasing order, at each limit's average power."""
+    c = np.array([100.0, 200.0, 300.0, 400.0, 500.0, 600.0])
+    st, out = oracle.profiling_overhead(c, L=5, avg_power=[150.0, 250.0, 275.0], delta=1800.0)
+    assert st == 0
+    assert out[0] == 3 * 1800.0 and out[1] == (150 + 250 + 275) * 1800.0
+    assert out[2] == float(F(150 * 300 + 250 * 400 + 275 * 500) * 1800 / 3600000)
+    assert oracle.profiling_overhead(c, L=2, avg_power=[1.0, 2.0, 3.0])[0] == 2
