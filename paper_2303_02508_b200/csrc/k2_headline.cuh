@@ -30,9 +30,6 @@
 #ifndef CHASE_H_PAIRSUM
 #define CHASE_H_PAIRSUM 1  // 1: a group's four terms summed pairwise before the running sums
 #endif
-#ifndef CHASE_H_STG
-#define CHASE_H_STG 0   // 1: choice words stored from registers (per group) instead of a TMA store per chunk
-#endif
 constexpr int kHWarps = CHASE_H_WARPS;    // independent warps per CTA
 constexpr int kHThreads = 32 * kHWarps;
 constexpr int kHStages = CHASE_H_STAGES;  // per-warp TMA ring depth
@@ -173,8 +170,7 @@ __device__ __forceinline__ uint32_t hot_group(const float4 v, const double2 A01,
 // reads at most one group past the last stay inside the stage / A buffers).
 __device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngroups, const double* __restrict__ Ap,
                                            double wl, double invK, const uint2* __restrict__ ent8, int ebase,
-                                           uint32_t ZB, uint32_t* __restrict__ words, uint32_t* __restrict__ cdst,
-                                           Acc& a) {
+                                           uint32_t ZB, uint32_t* __restrict__ words, Acc& a) {
     double lag = (double)tv[-1];
     float4 vx = *reinterpret_cast<const float4*>(tv);
     double2 Ax0 = *reinterpret_cast<const double2*>(Ap);
@@ -192,16 +188,8 @@ __device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngr
         const uint32_t w1 = hot_group(vy, Ay0, Ay1, lag, wl, invK, ent8, ebase, ZB, a);
         words[g] = w0;  // (lane blocks are 4 mod 8 bytes apart: two 4-byte stores)
         words[g + 1] = w1;
-        if (CHASE_H_STG && cdst) {
-            cdst[g] = w0;
-            cdst[g + 1] = w1;
-        }
     }
-    if (g < ngroups) {
-        const uint32_t w0 = hot_group(vx, Ax0, Ax1, lag, wl, invK, ent8, ebase, ZB, a);
-        words[g] = w0;
-        if (CHASE_H_STG && cdst) cdst[g] = w0;
-    }
+    if (g < ngroups) words[g] = hot_group(vx, Ax0, Ax1, lag, wl, invK, ent8, ebase, ZB, a);
 }
 
 // Windows [j_begin, nwin) of a lane whose count is not a multiple of 4 (the
@@ -442,7 +430,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         for (int c = 0; c < nc; ++c) {
             const bool last = c == nc - 1;
             uint8_t* stage = stage0;
-            if (!CHASE_H_STG && store_choice && lane == 0) bulk_wait_read0();  // the previous store has read chb
+            if (store_choice && lane == 0) bulk_wait_read0();  // the previous store has read chb
             mbar_wait(mbar, par);
             if (c == 0) {  // ---- per-trace setup
                 // the record: model (fit_kernel) and this trace's eta-0 scalars (record [10..15], kernels.h)
@@ -508,9 +496,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     k_carry = chb[wc - 1];
                     replay_groups(tv, nwin, chb + j0, prof_i, a);
                 }
-                uint32_t* cdst = (CHASE_H_STG && store_choice)
-                                     ? reinterpret_cast<uint32_t*>(P.choice + i * P.ld_c + c * kHWarpW + j0) : nullptr;
-                if (!PER) hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), cdst, a);
+                if (!PER) hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), a);
                 if (!PER && 4 * ngr < nwin) {  // cold: a ragged last chunk, or Kc outside [2^-900, 2^900]
                     if (invK == 0.0) {
                         a = fused_generic<true, false, float, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line, chb + j0,
@@ -580,13 +566,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                         El = __dadd_rn(El, a.E);
                         Cl = __dadd_rn(Cl, a.C);
                     }
-                    if (CHASE_H_STG && store_choice && (4 * ngr < nwin || (a.slow & 0x20202020u))) {
-                        // words not stored from registers (ragged tail, canonical or corrected windows)
-                        uint32_t* cd = reinterpret_cast<uint32_t*>(P.choice + i * P.ld_c + c * kHWarpW + j0);
-                        const uint32_t* wd = reinterpret_cast<const uint32_t*>(chb + j0);
-                        for (int g = (a.slow & 0x20202020u) || invK == 0.0 ? 0 : ngr; 4 * g < nwin; ++g) cd[g] = wd[g];
-                    }
-                    if (!CHASE_H_STG && store_choice) {  // the chunk's choices: one TMA bulk store from the staging buffer
+                    if (store_choice) {  // the chunk's choices: one TMA bulk store from the staging buffer
                         __syncwarp();
                         if (lane == 0) {
                             fence_proxy_async();
