@@ -297,12 +297,10 @@ cudaError_t launch_mape(const void* traces, bool f64, int64_t ld, int64_t n_trac
     const int64_t cap = (int64_t)num_sms() * 8;
     if (grid > cap) grid = cap;
     const int smem = mape_smem_bytes(T);
-    if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(mape_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(mape_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    }
-    if (f64) mape_kernel<double><<<(unsigned)grid, 256, smem, s>>>(p);
-    else mape_kernel<float><<<(unsigned)grid, 256, smem, s>>>(p);
+    auto kern = f64 ? (fc_in ? mape_kernel<double, true> : mape_kernel<double, false>)
+                    : (fc_in ? mape_kernel<float, true> : mape_kernel<float, false>);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<(unsigned)grid, 256, smem, s>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }

@@ -74,10 +74,10 @@ __host__ __device__ inline int mape_smem_bytes(int T) { return (2 * T + 8 * (T +
 // Fast path (fp32 traces, Eq. 1 forecasts): each lane takes 4 consecutive
 // windows per step (one 16-byte load, the lag of the first from the lane
 // below by a shuffle), 128 windows per warp step, four steps' loads in flight.
-template <typename E>
 #ifndef CHASE_MAPE_MINB
-#define CHASE_MAPE_MINB 1  // capping at 5-6 CTAs per SM was slower (10.4 / 10.8 vs 10.3 ms)
+#define CHASE_MAPE_MINB 4  // <= 64 registers (uncapped: 108-112 with the FIN variant; 9.84 vs 10.27 ms)
 #endif
+template <typename E, bool FIN>
 __global__ void __launch_bounds__(256, CHASE_MAPE_MINB) mape_kernel(const __grid_constant__ MapeParams p) {
     extern __shared__ double ph_sm[];
     const int T = p.T;
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(256, CHASE_MAPE_MINB) mape_kernel(const __grid
         const double c0 = rec[0], ws = rec[1], wc = rec[2], wl = rec[3];
         double el = 0.0, ep = 0.0;
         int bad = 0, zero = 0;
-        bool exact = sizeof(E) != 4 || p.fc_in != nullptr;
+        bool exact = sizeof(E) != 4;
+        const double* fcrow = FIN ? p.fc_in + i * p.ld_fin - s0 : nullptr;  // fcrow[w]: window w's forecast
         if (!exact) {
             for (int q = lane; q < T + 4; q += 32) {
                 const int ph = q < T ? q : q - T;
@@ -126,9 +127,14 @@ __global__ void __launch_bounds__(256, CHASE_MAPE_MINB) mape_kernel(const __grid
                     umin = min(umin, b);
                     umax = max(umax, b);
                     const double cw = f2d_normal(b);
-                    const double pr = __dadd_rn(Aw[ph + u], __dmul_rn(wl, lag));
-                    const long long pb = __double_as_longlong(pr);
-                    const double pred = __longlong_as_double(pb & ~(pb >> 63));  // max(pr, 0)
+                    double pred;
+                    if (FIN) {  // the SVR's forecast (already clamped)
+                        pred = fcrow[w];
+                    } else {
+                        const double pr = __dadd_rn(Aw[ph + u], __dmul_rn(wl, lag));
+                        const long long pb = __double_as_longlong(pr);
+                        pred = __longlong_as_double(pb & ~(pb >> 63));  // max(pr, 0)
+                    }
                     const double r = rcp_nr(cw);
                     el = __dadd_rn(el, __dmul_rn(fabs(__dsub_rn(cw, pred)), r));
                     ep = __dadd_rn(ep, __dmul_rn(fabs(__dsub_rn(cw, lag)), r));
