@@ -185,7 +185,7 @@ __host__ __device__ inline int aext_len(int T) { return T + kChunk + 4; }
 // per-lane running sums in registers and reduces only when it must)
 constexpr int kEtaState = 8;
 #ifndef CHASE_STAGES
-#define CHASE_STAGES 3
+#define CHASE_STAGES 2  // 3 before: 2 is faster on the FIN paths (C4 SVR step 46.3 -> 43.6 ms, rolling R=24 16.7 -> 14.0 ms)
 #endif
 constexpr int kStages = CHASE_STAGES;  // per-warp TMA ring depth
 
@@ -266,7 +266,10 @@ __device__ __noinline__ Completion find_completion(const E* tv_src, const uint8_
 // FIN (rolling refit): the forecasts come from P.fc_in (rolling_forecast_kernel)
 // instead of the per-trace folded table: Ap = that row, w_lag = 0, so p = fc + 0*lag = fc.
 template <int MODE, typename E, bool AL, bool MULTI, bool FIN = false>
-__global__ void __launch_bounds__(kThreads, 2) sweep_kernel(const __grid_constant__ SweepParams P) {
+#ifndef CHASE_SWEEP_MINB
+#define CHASE_SWEEP_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, CHASE_SWEEP_MINB) sweep_kernel(const __grid_constant__ SweepParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const WarpLayout WL = make_warp_layout(P.T, P.stage_bytes, P.n_eta);
