@@ -368,7 +368,7 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
     const int64_t W = traces->n_steps - fcfg->history_len;
-    if (!d_forecast || ld_f < W) return fail(CHASE_ERR_INVALID, "d_forecast NULL or ld_f < W");
+    if ((traces->n_traces > 0 && !d_forecast) || ld_f < W) return fail(CHASE_ERR_INVALID, "d_forecast NULL or ld_f < W");
     if (svr(fcfg) && d_models) return fail(CHASE_ERR_INVALID, "d_models must be NULL with the SVR forecaster");
     const int T = fcfg->steps_per_day;
     // layout sized for (1 profile, 1 eta) so one workspace serves every entry point

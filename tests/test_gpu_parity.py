@@ -864,3 +864,28 @@ def test_profiling_overhead_matches_oracle():
         assert st == 0 and list(g[i]) == list(o), i
     with pytest.raises(cb.ChaseError, match="history_len"):
         cb.profiling_overhead(t, 5, w.profiles, out, ws)
+
+
+def test_empty_batches():
+    """n_traces = 0 through every entry point: nothing launched that reads a
+    trace, sums zero, no error."""
+    N = 24 + 50
+    prof = [inputs.make_profile("resnet50", inputs.LIMITS_9)]
+    x = torch.empty((0, 80), dtype=torch.float32, device=DEV)
+    t = cb.make_traces(x, n_steps=N)
+    for kw in ({}, dict(period_steps=24), dict(refit_stride=1), dict(svr={})):
+        f = cb.make_fcfg(**kw)
+        ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+        sums = torch.full((1, 8), 7.0, dtype=torch.float64, device=DEV)
+        cb.sweep(t, f, prof, [0.5], ws, sums)
+        torch.cuda.synchronize()
+        assert np.all(sums.cpu().numpy() == 0.0), kw
+    f = cb.make_fcfg()
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    fc = torch.empty((0, 50), dtype=torch.float64, device=DEV)
+    cb.fit_forecast(t, f, fc, 50, ws)
+    mp = torch.empty((0, 2), dtype=torch.float64, device=DEV)
+    cb.forecast_mape(t, f, mp, ws)
+    rows = torch.empty((0, 50, 8), dtype=torch.float64, device=DEV)
+    cb.timeline(t, 24, prof, rows, 0, ws)
+    torch.cuda.synchronize()
