@@ -257,6 +257,22 @@ __device__ __forceinline__ uint32_t period_choice(double chat, double invK, doub
     return canonical_choose(chat, Kc, pt->a, pf->thr, pf->K);
 }
 
+// max(pr, 0) as oracle_predict writes it (pr > 0 ? pr : 0): DSETP + two SELs
+// (the compiler's fmax pattern costs twice that with its NaN fix-up)
+__device__ __forceinline__ double relu_gt(double pr) {
+    double f;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\t"
+        "selp.f64 %0, %1, 0d0000000000000000, p;\n\t}"
+        : "=d"(f) : "d"(pr));
+    return f;
+}
+
+// One recursive-forecast step (Eq. 1, oracle_predict's order): prev := max(0, A + wl*prev); sum += prev
+__device__ __forceinline__ void horizon_step(double A, double wl, double& prev, double& sum) {
+    prev = relu_gt(__dadd_rn(A, __dmul_rn(wl, prev)));
+    sum = __dadd_rn(sum, prev);
+}
+
 __device__ __noinline__ void period_decisions(const float* stagev, int cs, int wc, int Wt, int Pp, int phase_start,
                                               int T, const double* Aeven, double wl, double invK, double Kc,
                                               const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
@@ -266,27 +282,46 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
     const int jf = (cs + Pp - 1) / Pp;
     const int bf = min(jf * Pp, ce);
     if (lane == 0) fill_bytes(chb, 0, bf - cs, k_carry);
+    // Aeven holds A[phi] for phi in [0, T + ext) (the table repeats past T): a
+    // horizon runs without a wrap test for up to T + ext - phi steps
+    const int tend = haext_len(T);
+    const int ph_step = (32 * Pp) % T;  // phase advance between a lane's periods
+    const bool pow2 = (Pp & (Pp - 1)) == 0;
+    const double dP = (double)Pp, invP = 1.0 / dP;
+    int ph = (phase_start + (jf + lane) * Pp) % T;
     for (int j = jf + lane; j * Pp < ce; j += 32) {
         const int b = j * Pp;
         const int n = min(Pp, Wt - b);
-        int ph = (phase_start + b) % T;
         double prev = (double)stagev[b - cs - 1], sum = 0.0;
-        for (int k = 0; k < n; ++k) {
-            const double pr = __dadd_rn(Aeven[ph], __dmul_rn(wl, prev));  // Eq. 1, oracle_predict's order
-            const double f = pr > 0.0 ? pr : 0.0;
-            sum = __dadd_rn(sum, f);
-            prev = f;
-            ph = ph + 1 == T ? 0 : ph + 1;
+        int p = ph, k = 0;
+        while (k < n) {
+            const int seg = min(n - k, tend - p);
+            const double* Ap = Aeven + p;
+            int q = 0;
+#pragma unroll 1
+            for (; q + 2 <= seg; q += 2) {
+                const double a0 = Ap[q], a1 = Ap[q + 1];
+                horizon_step(a0, wl, prev, sum);
+                horizon_step(a1, wl, prev, sum);
+            }
+            if (q < seg) horizon_step(Ap[q], wl, prev, sum);
+            k += seg;
+            p += seg;
+            while (p >= T) p -= T;
         }
         // sum/n; for a power-of-two n the product with 1/n is the same exact-then-rounded value
-        const double chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
-        const uint32_t k = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+        double chat;
+        if (n == Pp) chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
+        else chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
+        const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
         const int e = min(b + Pp, ce);
         if (Pp < 8) {
-            for (int q = b; q < e; ++q) chb[q - cs] = (uint8_t)k;
+            for (int qq = b; qq < e; ++qq) chb[qq - cs] = (uint8_t)kk;
         } else {
-            fill_bytes(chb, b - cs, e - cs, k);
+            fill_bytes(chb, b - cs, e - cs, kk);
         }
+        ph += ph_step;
+        if (ph >= T) ph -= T;
     }
 }
 

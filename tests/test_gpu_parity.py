@@ -447,6 +447,9 @@ def test_rolling_fit_forecast_split_path_and_f64():
     (24, 24, 24 + 2000, [0.4, 0.8], 9),    # daily decisions, two etas
     (7, 23, 23 + 400, [0.6], 5),           # odd L: unaligned tile path
     (168, 24, 24 + 8760, [0.5], 3),        # weekly decisions over a year
+    (5, 24, 24 + 1001, [0.3], 7),          # headline kernel: non-power-of-two n (division), ragged
+    (64, 24, 24 + 5000, [0.7], 5),         # power-of-two P > T: horizons cross the phase table's end
+    (100, 24, 24 + 4321, [0.5], 4),        # P > T + 64: several wrap segments per horizon
 ])
 def test_decision_periods_parity(P, L, N, etas, n):
     """One decision per period on the mean of the recursive horizon forecast:
