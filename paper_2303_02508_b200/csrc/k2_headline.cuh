@@ -325,6 +325,43 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
     }
 }
 
+// Lane-local decision periods: when P divides the lane's share of a full chunk
+// (kHChunk), every period of the lane's windows starts and ends in them and its
+// start value c[b-1] is the lane's previous value (tv[-1]: the last of the
+// previous lane's windows, or the chunk's lag slot).  Each lane then decides its
+// own periods and replays them in one pass: horizon (Eq. 1, recursive), mean,
+// Eq. 6 lookup, one line load per period, the running sums in window order
+// (the same sequence replay_groups adds them in).  PC > 0: P known at compile time.
+template <int PC>
+__device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp, const double* __restrict__ Ap,
+                                            double wl, double invK, double Kc, const uint2* ent8, int ebase,
+                                            uint32_t ZB, const PairTable* pt, const ProfileTable* pf, int prof,
+                                            uint8_t* chl, Acc& a, unsigned& n_slow) {
+    const int Pn = PC > 0 ? PC : Pp;
+    const bool pow2 = (Pn & (Pn - 1)) == 0;
+    const double dP = (double)Pn, invP = 1.0 / dP;
+#pragma unroll 1
+    for (int q = 0; q < kHChunk; q += Pn) {
+        double prev = (double)tv[q - 1], sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < Pn; ++k) horizon_step(Ap[q + k], wl, prev, sum);
+        const double chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
+        const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+        const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+#pragma unroll
+        for (int k = 0; k < Pn; ++k) {
+            const float raw = tv[q + k];
+            const double cw = (double)raw;
+            a.vmin = fminf(a.vmin, raw);
+            a.S = __dadd_rn(a.S, ln.x);
+            a.E = __dadd_rn(a.E, ln.y);
+            a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+            a.Cs = __dadd_rn(a.Cs, cw);
+            chl[q + k] = (uint8_t)kk;
+        }
+    }
+}
+
 // Replay of one lane's windows from the staged choice bytes (period mode).
 __device__ __forceinline__ void replay_groups(const float* __restrict__ tv, int nwin, const uint8_t* __restrict__ bytes,
                                               int prof, Acc& a) {
@@ -522,7 +559,18 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
                 const int ngr = (PER || invK == 0.0) ? 0 : nwin >> 2;
-                if (PER) {  // decisions for the chunk's periods first, then the replay
+                if (PER && !last && kHChunk % P.period == 0) {  // lane-local periods (fused decide + replay)
+                    uint8_t* chl = chb + j0;
+                    switch (P.period) {
+                        case 2: period_lane<2>(tv, 2, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow); break;
+                        case 3: period_lane<3>(tv, 3, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow); break;
+                        case 4: period_lane<4>(tv, 4, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow); break;
+                        default:
+                            period_lane<0>(tv, P.period, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow);
+                    }
+                    __syncwarp();
+                    k_carry = chb[kHWarpW - 1];
+                } else if (PER) {  // decisions for the chunk's periods first, then the replay
                     const int wc = last ? P.W_last : kHWarpW;
                     period_decisions(reinterpret_cast<const float*>(stage) + P.off0, c * kHWarpW, wc, P.W, P.period,
                                      P.phase_start, T, A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, k_carry, chb, lane,
