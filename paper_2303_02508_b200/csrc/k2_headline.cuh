@@ -325,6 +325,40 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
     }
 }
 
+// Replay of a run of m windows at one line (the period's choice): the window
+// sums collapse to S += m s_k, E += m P_k, C += P_k * sum c, Cs += sum c.  The
+// order of the additions changes (exact for the dyadic inputs; within
+// the 1e-9 bar otherwise, as the pairwise group sums of the per-window kernel).
+__device__ __forceinline__ double run_csum(const float* __restrict__ tv, int q0, int q1, float& vmin) {
+    double cs = 0.0;
+    int q = q0;
+    for (; q < q1 && (q & 3); ++q) {
+        const float raw = tv[q];
+        vmin = fminf(vmin, raw);
+        cs = __dadd_rn(cs, (double)raw);
+    }
+#pragma unroll 1
+    for (; q + 4 <= q1; q += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(tv + q);
+        vmin = fminf(fminf(fminf(vmin, v.x), v.y), fminf(v.z, v.w));
+        cs = __dadd_rn(cs, __dadd_rn(__dadd_rn((double)v.x, (double)v.y), __dadd_rn((double)v.z, (double)v.w)));
+    }
+    for (; q < q1; ++q) {
+        const float raw = tv[q];
+        vmin = fminf(vmin, raw);
+        cs = __dadd_rn(cs, (double)raw);
+    }
+    return cs;
+}
+
+__device__ __forceinline__ void replay_run(Acc& a, double2 ln, int m, double cs) {
+    const double dm = (double)m;
+    a.S = __dadd_rn(a.S, __dmul_rn(dm, ln.x));
+    a.E = __dadd_rn(a.E, __dmul_rn(dm, ln.y));
+    a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cs));
+    a.Cs = __dadd_rn(a.Cs, cs);
+}
+
 // Lane-local decision periods: when P divides the lane's share of a full chunk
 // (kHChunk), every period of the lane's windows starts and ends in them and its
 // start value c[b-1] is the lane's previous value (tv[-1]: the last of the
@@ -348,16 +382,79 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         const double chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
         const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
         const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+        if (Pn < 16) {  // short runs: per-window sums (independent adds; the run form lengthens the chains)
 #pragma unroll
-        for (int k = 0; k < Pn; ++k) {
-            const float raw = tv[q + k];
-            const double cw = (double)raw;
-            a.vmin = fminf(a.vmin, raw);
-            a.S = __dadd_rn(a.S, ln.x);
-            a.E = __dadd_rn(a.E, ln.y);
-            a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
-            a.Cs = __dadd_rn(a.Cs, cw);
-            chl[q + k] = (uint8_t)kk;
+            for (int k = 0; k < Pn; ++k) {
+                const float raw = tv[q + k];
+                const double cw = (double)raw;
+                a.vmin = fminf(a.vmin, raw);
+                a.S = __dadd_rn(a.S, ln.x);
+                a.E = __dadd_rn(a.E, ln.y);
+                a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+                a.Cs = __dadd_rn(a.Cs, cw);
+                chl[q + k] = (uint8_t)kk;
+            }
+        } else {
+            replay_run(a, ln, Pn, run_csum(tv, q, q + Pn, a.vmin));
+            fill_bytes(chl, q, q + Pn, kk);
+        }
+    }
+}
+
+// Long decision periods (P >= kHWarpW/30: at most 31 periods meet a chunk):
+// the decisions are taken 32 periods at a time, one per lane, and kept in a
+// register (lane l holds period jb + l).  A period's start value c[b-1] is read
+// from global memory (one 4-byte load per period), so a batch spans chunks and
+// every lane has a horizon to run (P = 168: 2 batches per year-long trace, not
+// one 12-lane round per chunk).  Same per-period arithmetic as period_decisions.
+__device__ __noinline__ uint32_t period_batch(const float* __restrict__ cg, int jb, int Wt, int Pp, int phase_start,
+                                              int T, const double* Aeven, double wl, double invK, double Kc,
+                                              const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
+                                              const ProfileTable* pf, int lane, unsigned& n_slow) {
+    const int b = (jb + lane) * Pp;
+    if (b >= Wt) return 0u;
+    const int n = min(Pp, Wt - b);
+    const int tend = haext_len(T);
+    double prev = (double)__ldg(cg + b - 1), sum = 0.0;  // c[b-1]
+    int p = (int)(((int64_t)phase_start + b) % T), k = 0;
+    while (k < n) {
+        const int seg = min(n - k, tend - p);
+        const double* Ap = Aeven + p;
+        int q = 0;
+#pragma unroll 1
+        for (; q + 2 <= seg; q += 2) {
+            const double a0 = Ap[q], a1 = Ap[q + 1];
+            horizon_step(a0, wl, prev, sum);
+            horizon_step(a1, wl, prev, sum);
+        }
+        if (q < seg) horizon_step(Ap[q], wl, prev, sum);
+        k += seg;
+        p += seg;
+        while (p >= T) p -= T;
+    }
+    const double chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
+    return period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+}
+
+// Replay of one lane's windows [w0, w0 + nwin) from the batch decisions (lane l: period jb + l).
+__device__ __forceinline__ void period_replay_batch(const float* __restrict__ tv, int nwin, int w0, int Pp, int jb,
+                                                    uint32_t kb, int prof, uint8_t* chl, Acc& a) {
+    int q = 0;
+    const int jA = w0 / Pp;
+    // a lane's windows meet at most two periods (P >= kHWarpW/30 > kHChunk); the
+    // shuffles are warp-wide, so every lane fetches both
+    const uint32_t k0 = __shfl_sync(kFull, kb, min(jA - jb, 31));
+    const uint32_t k1 = __shfl_sync(kFull, kb, min(jA + 1 - jb, 31));
+    const int split = min(nwin, max(0, (jA + 1) * Pp - w0));
+#pragma unroll 1
+    for (int seg = 0; seg < 2; ++seg) {
+        const uint32_t kk = seg == 0 ? k0 : k1;
+        const int e = seg == 0 ? split : nwin;
+        if (e > q) {
+            const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+            replay_run(a, ln, e - q, run_csum(tv, q, e, a.vmin));
+            fill_bytes(chl, q, e, kk);
+            q = e;
         }
     }
 }
@@ -396,13 +493,17 @@ __device__ __forceinline__ void replay_groups(const float* __restrict__ tv, int 
     }
 }
 
-template <bool PER>
+// PM: 0 = one decision per window (the headline), 1 = decision periods decided per
+// chunk (lane-local when P | kHChunk), 2 = long periods (P >= kHWarpW/30) decided
+// in 32-period batches.  Separate instantiations keep each path's registers apart.
+template <int PM>
 #ifdef CHASE_H_MAXNREG
 __global__ void __maxnreg__(CHASE_H_MAXNREG) sweep_fast_kernel(
 #else
 __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
 #endif
     const __grid_constant__ SweepParams P) {
+    constexpr bool PER = PM != 0;
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t sbase = smem_u32(sm);
@@ -499,10 +600,24 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         const PairTable* pt = reinterpret_cast<const PairTable*>(heads);
         int prof_i = 0;
         uint32_t k_carry = 0;  // period mode: the decision of the period running into the next chunk
+        int jb = 0;            // long periods: first period of the current batch
+        uint32_t kb = 0;       // long periods: lane l's decision for period jb + l
         for (int c = 0; c < nc; ++c) {
             const bool last = c == nc - 1;
             uint8_t* stage = stage0;
             if (store_choice && lane == 0) bulk_wait_read0();  // the previous store has read chb
+            if (PM == 2 && c > 0 && status == 0) {
+                // long periods: a new batch is decided while this chunk's load is in flight
+                const int cs = c * kHWarpW, wc = last ? P.W_last : kHWarpW;
+                if ((cs + wc - 1) / P.period >= jb + 32) {
+                    const int jn = cs / P.period;
+                    unsigned ns = 0;
+                    kb = period_batch(traces + i * P.ld + P.a0 + P.off0, jn, P.W, P.period, P.phase_start, T, A_even,
+                                      wl, invK, Kc, e8, ebase, ZB, pt, pf, lane, ns);
+                    if (lane != 0 || jn > jb + 31) n_slow += ns;  // lane 0's period may be the last batch's lane 31
+                    jb = jn;
+                }
+            }
             mbar_wait(mbar, par);
             if (c == 0) {  // ---- per-trace setup
                 // the record: model (fit_kernel) and this trace's eta-0 scalars (record [10..15], kernels.h)
@@ -559,7 +674,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
                 const int ngr = (PER || invK == 0.0) ? 0 : nwin >> 2;
-                if (PER && !last && kHChunk % P.period == 0) {  // lane-local periods (fused decide + replay)
+                if (PM == 1 && !last && kHChunk % P.period == 0) {  // lane-local periods (fused decide + replay)
                     uint8_t* chl = chb + j0;
                     switch (P.period) {
                         case 2: period_lane<2>(tv, 2, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow); break;
@@ -570,6 +685,15 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     }
                     __syncwarp();
                     k_carry = chb[kHWarpW - 1];
+                } else if (PM == 2) {  // long periods: 32-period batches
+                    const int cs = c * kHWarpW;
+                    if (c == 0) {  // the trace's first batch needs its model (the record, in this stage)
+                        jb = 0;
+                        kb = period_batch(traces + i * P.ld + P.a0 + P.off0, jb, P.W, P.period, P.phase_start, T,
+                                          A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, lane, n_slow);
+                    }
+                    period_replay_batch(tv, nwin, cs + j0, P.period, jb, kb, prof_i, chb + j0, a);
+                    __syncwarp();
                 } else if (PER) {  // decisions for the chunk's periods first, then the replay
                     const int wc = last ? P.W_last : kHWarpW;
                     period_decisions(reinterpret_cast<const float*>(stage) + P.off0, c * kHWarpW, wc, P.W, P.period,

@@ -169,8 +169,9 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
             smem = t > smem ? t : smem;
         }
         q.smem_total = smem;
-        const bool per = p.period > 1;
-        auto kern = per ? sweep_fast_kernel<true> : sweep_fast_kernel<false>;
+        // decision periods: long ones (at most 31 per warp chunk) in 32-period batches
+        auto kern = p.period <= 1 ? sweep_fast_kernel<0>
+                    : (p.period * 30 >= kHWarpW ? sweep_fast_kernel<2> : sweep_fast_kernel<1>);
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
         int per_sm = 0;

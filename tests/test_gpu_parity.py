@@ -454,6 +454,9 @@ def test_rolling_fit_forecast_split_path_and_f64():
     (60, 24, 24 + 3900, [0.5], 4),         # one period per lane
     (64, 24, 24 + 5000, [0.7], 5),         # power-of-two P > T: horizons cross the phase table's end
     (100, 24, 24 + 4321, [0.5], 4),        # P > T + 64: several wrap segments per horizon
+    (1000, 24, 24 + 9000, [0.5], 3),       # periods longer than a warp chunk (32-period batches)
+    (3000, 24, 24 + 3000, [0.5], 3),       # one period for the whole job
+    (64, 24, 24 + 70000, [0.5], 2),        # several 32-period batches per trace
 ])
 def test_decision_periods_parity(P, L, N, etas, n):
     """One decision per period on the mean of the recursive horizon forecast:
