@@ -773,14 +773,17 @@ def _host_trace(w, i):
     return inputs.synth_traces_host(1, w.n_steps, seed=w.seed, mode=w.mode, trace0=int(i))[0, :w.n_steps]
 
 
-@pytest.mark.parametrize("mode", ["svr", "roll1", "p24"])
+@pytest.mark.parametrize("mode", ["svr", "roll1", "p24", "p2", "p168"])
 def test_full_size_modes_sampled(mode):
     """The bench's launch configurations of the SVR forecaster (C4), the rolling
-    refit every window (C4) and daily decision periods (C5) at full size:
+    refit every window (C4) and decision periods (C5: daily; 2-step, the
+    lane-local path; weekly, the 32-period batches) at full size:
     sampled traces against the oracle one by one (forecasts, choices, totals)."""
     name, kw, okw = {"svr": ("C4", dict(svr={}), dict(svr={})),
                      "roll1": ("C4", dict(refit_stride=1), dict(refit_stride=1)),
-                     "p24": ("C5", dict(period_steps=24), dict(period=24))}[mode]
+                     "p24": ("C5", dict(period_steps=24), dict(period=24)),
+                     "p2": ("C5", dict(period_steps=2), dict(period=2)),
+                     "p168": ("C5", dict(period_steps=168), dict(period=168))}[mode]
     w, x, pid, J = _full_inputs(name, 60 if name == "C5" else 20)
     pl = cb.Planner(x, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, profile_id=pid, job_samples=J,
                     want_choice=True, want_forecast=name == "C4", want_per_trace=True, **kw)
