@@ -273,6 +273,51 @@ __device__ __forceinline__ void horizon_step(double A, double wl, double& prev, 
     sum = __dadd_rn(sum, prev);
 }
 
+// M periods per lane decided side by side (periods j, j + 32, ..., j + 32(M-1)):
+// M independent horizon chains interleaved step by step, so the fixed fp64
+// latency of one chain is shared by M.  Chain k's phase is chain 0's plus
+// k * (32 P mod T), read from the extended A table (needs T <= 64).  Every
+// period here is a full one (n = P); lanes past the chunk's last period run
+// masked chains and store nothing.
+template <int M>
+__device__ __forceinline__ void decide_multi(const float* stagev, int cs, int ce, int Pp, int j, int ph, int dph,
+                                             int T, const double* Aeven, double wl, double invK, double Kc,
+                                             const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
+                                             const ProfileTable* pf, uint8_t* chb, unsigned& n_slow) {
+    double prev[M], sum[M];
+    int dk[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        const int b = (j + 32 * k) * Pp;
+        prev[k] = b < ce ? (double)stagev[b - cs - 1] : 0.0;
+        sum[k] = 0.0;
+        dk[k] = (k * dph) % T;
+    }
+    int p = ph, s = 0;
+    while (s < Pp) {
+        const int seg = min(Pp - s, T - p);
+        const double* Ap = Aeven + p;
+#pragma unroll 1
+        for (int q = 0; q < seg; ++q) {
+#pragma unroll
+            for (int k = 0; k < M; ++k) horizon_step(Ap[q + dk[k]], wl, prev[k], sum[k]);
+        }
+        s += seg;
+        p += seg;
+        if (p >= T) p -= T;
+    }
+    const bool pow2 = (Pp & (Pp - 1)) == 0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        const int b = (j + 32 * k) * Pp;
+        if (b < ce) {
+            const double chat = pow2 ? __dmul_rn(sum[k], 1.0 / (double)Pp) : __ddiv_rn(sum[k], (double)Pp);
+            const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            fill_bytes(chb, b - cs, min(b + Pp, ce) - cs, kk);
+        }
+    }
+}
+
 __device__ __noinline__ void period_decisions(const float* stagev, int cs, int wc, int Wt, int Pp, int phase_start,
                                               int T, const double* Aeven, double wl, double invK, double Kc,
                                               const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
@@ -282,6 +327,18 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
     const int jf = (cs + Pp - 1) / Pp;
     const int bf = min(jf * Pp, ce);
     if (lane == 0) fill_bytes(chb, 0, bf - cs, k_carry);
+    {   // 33..128 full periods start in the chunk: 2-4 side-by-side chains per lane
+        const int jl = (ce - 1) / Pp;
+        const int m = (jl - jf + 32) / 32;
+        if (T <= 64 && Pp >= 8 && m >= 2 && m <= 4 && (int64_t)jl * Pp + Pp <= Wt) {
+            const int ph0 = (phase_start + (jf + lane) * Pp) % T, dph = (32 * Pp) % T;
+            const int j = jf + lane;
+            if (m == 2) decide_multi<2>(stagev, cs, ce, Pp, j, ph0, dph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf, chb, n_slow);
+            else if (m == 3) decide_multi<3>(stagev, cs, ce, Pp, j, ph0, dph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf, chb, n_slow);
+            else decide_multi<4>(stagev, cs, ce, Pp, j, ph0, dph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf, chb, n_slow);
+            return;
+        }
+    }
     // Aeven holds A[phi] for phi in [0, T + ext) (the table repeats past T): a
     // horizon runs without a wrap test for up to T + ext - phi steps
     const int tend = haext_len(T);

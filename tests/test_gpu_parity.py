@@ -455,6 +455,9 @@ def test_rolling_fit_forecast_split_path_and_f64():
     (64, 24, 24 + 5000, [0.7], 5),         # power-of-two P > T: horizons cross the phase table's end
     (100, 24, 24 + 4321, [0.5], 4),        # P > T + 64: several wrap segments per horizon
     (1000, 24, 24 + 9000, [0.5], 3),       # periods longer than a warp chunk (32-period batches)
+    (24, 24, 24 + 5000, [0.5], 5),         # 80 periods per chunk: three side-by-side chains per lane
+    (48, 24, 24 + 4000, [0.5], 4),         # two chains per lane
+    (17, 24, 24 + 4500, [0.6], 4),         # four chains, phase offsets 32 P mod T = 16
     (3000, 24, 24 + 3000, [0.5], 3),       # one period for the whole job
     (64, 24, 24 + 70000, [0.5], 2),        # several 32-period batches per trace
 ])
