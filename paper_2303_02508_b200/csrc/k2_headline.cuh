@@ -758,7 +758,19 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                                      n_slow);
                     __syncwarp();
                     k_carry = chb[wc - 1];
-                    replay_groups(tv, nwin, chb + j0, prof_i, a);
+                    if (P.period >= 16 && (P.period & 3) == 0) {  // aligned runs of one choice: the run-form replay
+                        const uint8_t* chl = chb + j0;
+                        const int w0 = c * kHWarpW + j0;
+                        int q = 0;
+                        while (q < nwin) {
+                            const int e = min(nwin, ((w0 + q) / P.period + 1) * P.period - w0);
+                            const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof_i, (int)chl[q]));
+                            replay_run(a, ln, e - q, run_csum(tv, q, e, a.vmin));
+                            q = e;
+                        }
+                    } else {
+                        replay_groups(tv, nwin, chb + j0, prof_i, a);
+                    }
                 }
                 if (!PER) hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), a);
                 if (!PER && 4 * ngr < nwin) {  // cold: a ragged last chunk, or Kc outside [2^-900, 2^900]
