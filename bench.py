@@ -154,7 +154,7 @@ def ncu_traffic_per_window(config: str):
     if not os.path.exists(path):
         return None
     d = json.load(open(path))
-    e = d.get(config) or d.get("default")
+    e = d.get(config) or (None if "_p" in config else d.get("default"))
     return None if e is None else float(e["dram_bytes_per_window"])
 
 
@@ -284,6 +284,13 @@ def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0, svr=None) ->
         return ("svr_fit_kernel (warp per trace, SMO on the RBF dual, kernel matrix in smem) + "
                 "svr_forecast_kernel (thread per window / period)")
     if P > 1:
+        if len(w.etas) == 1 and w.history_len % 4 == 0:  # the headline kernel's period instantiations
+            if P * 30 >= 1920:
+                return ("sweep_fast_kernel<2> (decision periods in 32-period batches, one horizon per lane; "
+                        "Eq. 6 argmin + run-form replay)")
+            how = ("each lane decides and replays its own periods" if 60 % P == 0 else
+                   "per-chunk decisions, up to 4 horizon chains per lane")
+            return f"sweep_fast_kernel<1> (decision periods: {how}; Eq. 6 argmin + replay)"
         return "sweep_kernel<FUSED, FIN> (Eq. 6 argmin + replay on the period decision forecasts)"
     if R > 0:
         return "rolling_forecast_kernel (one thread per (trace, refit origin), oracle_fit's exact fp64 sequence)"
@@ -407,7 +414,7 @@ def main_chase(args):
         peak, peak_src = measured_peaks()
         alg_bytes = n * W * BYTES_PER_WINDOW
         achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-        tpw = ncu_traffic_per_window(args.config)
+        tpw = ncu_traffic_per_window(args.config if args.period_steps <= 1 else f"{args.config}_p{args.period_steps}")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": None if tpw is None else tpw * n * W,
                     "kernel": planner_kernel_name(w, 0, args.period_steps),
