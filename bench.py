@@ -288,9 +288,11 @@ def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0, svr=None) ->
             if P * 30 >= 1920:
                 return ("sweep_fast_kernel<2> (decision periods in 32-period batches, one horizon per lane; "
                         "Eq. 6 argmin + run-form replay)")
-            how = ("each lane decides and replays its own periods" if 60 % P == 0 else
-                   "per-chunk decisions, up to 4 horizon chains per lane")
-            return f"sweep_fast_kernel<1> (decision periods: {how}; Eq. 6 argmin + replay)"
+            if 60 % P == 0:
+                return (f"sweep_fast_kernel<{4 if P == 2 else 3}> (decision periods: each lane decides and replays its own periods; "
+                        "Eq. 6 argmin + replay)")
+            return ("sweep_fast_kernel<1> (decision periods: per-chunk decisions, up to 4 horizon chains per lane; "
+                    "Eq. 6 argmin + replay)")
         return "sweep_kernel<FUSED, FIN> (Eq. 6 argmin + replay on the period decision forecasts)"
     if R > 0:
         return "rolling_forecast_kernel (one thread per (trace, refit origin), oracle_fit's exact fp64 sequence)"

@@ -423,6 +423,29 @@ __device__ __forceinline__ void replay_run(Acc& a, double2 ln, int m, double cs)
 // own periods and replays them in one pass: horizon (Eq. 1, recursive), mean,
 // Eq. 6 lookup, one line load per period, the running sums in window order
 // (the same sequence replay_groups adds them in).  PC > 0: P known at compile time.
+// One period's replay at its choice kk (windows tv[q, q + Pn)).
+template <int PC>
+__device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv, int q, int Pn, uint32_t kk, int prof,
+                                                   uint8_t* chl, Acc& a) {
+    const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+    if (Pn < 16) {  // short runs: per-window sums (independent adds; the run form lengthens the chains)
+#pragma unroll
+        for (int k = 0; k < (PC > 0 ? PC : Pn); ++k) {
+            const float raw = tv[q + k];
+            const double cw = (double)raw;
+            a.vmin = fminf(a.vmin, raw);
+            a.S = __dadd_rn(a.S, ln.x);
+            a.E = __dadd_rn(a.E, ln.y);
+            a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+            a.Cs = __dadd_rn(a.Cs, cw);
+            chl[q + k] = (uint8_t)kk;
+        }
+    } else {
+        replay_run(a, ln, Pn, run_csum(tv, q, q + Pn, a.vmin));
+        fill_bytes(chl, q, q + Pn, kk);
+    }
+}
+
 template <int PC>
 __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp, const double* __restrict__ Ap,
                                             double wl, double invK, double Kc, const uint2* ent8, int ebase,
@@ -431,6 +454,25 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
     const int Pn = PC > 0 ? PC : Pp;
     const bool pow2 = (Pn & (Pn - 1)) == 0;
     const double dP = (double)Pn, invP = 1.0 / dP;
+    if (PC > 0 && (kHChunk / (PC > 0 ? PC : 1)) % 2 == 0) {
+        // two periods per iteration: their horizons are independent chains, interleaved
+#pragma unroll 1
+        for (int q = 0; q < kHChunk; q += 2 * Pn) {
+            double pa = (double)tv[q - 1], pb = (double)tv[q + Pn - 1], sa = 0.0, sb = 0.0;
+#pragma unroll
+            for (int k = 0; k < (PC > 0 ? PC : 1); ++k) {
+                horizon_step(Ap[q + k], wl, pa, sa);
+                horizon_step(Ap[q + Pn + k], wl, pb, sb);
+            }
+            const double ca = pow2 ? __dmul_rn(sa, invP) : __ddiv_rn(sa, dP);
+            const double cb = pow2 ? __dmul_rn(sb, invP) : __ddiv_rn(sb, dP);
+            const uint32_t ka = period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            const uint32_t kb = period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            lane_period_replay<PC>(tv, q, Pn, ka, prof, chl, a);
+            lane_period_replay<PC>(tv, q + Pn, Pn, kb, prof, chl, a);
+        }
+        return;
+    }
 #pragma unroll 1
     for (int q = 0; q < kHChunk; q += Pn) {
         double prev = (double)tv[q - 1], sum = 0.0;
@@ -438,23 +480,7 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         for (int k = 0; k < Pn; ++k) horizon_step(Ap[q + k], wl, prev, sum);
         const double chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
         const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
-        const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
-        if (Pn < 16) {  // short runs: per-window sums (independent adds; the run form lengthens the chains)
-#pragma unroll
-            for (int k = 0; k < Pn; ++k) {
-                const float raw = tv[q + k];
-                const double cw = (double)raw;
-                a.vmin = fminf(a.vmin, raw);
-                a.S = __dadd_rn(a.S, ln.x);
-                a.E = __dadd_rn(a.E, ln.y);
-                a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
-                a.Cs = __dadd_rn(a.Cs, cw);
-                chl[q + k] = (uint8_t)kk;
-            }
-        } else {
-            replay_run(a, ln, Pn, run_csum(tv, q, q + Pn, a.vmin));
-            fill_bytes(chl, q, q + Pn, kk);
-        }
+        lane_period_replay<PC>(tv, q, Pn, kk, prof, chl, a);
     }
 }
 
@@ -551,8 +577,9 @@ __device__ __forceinline__ void replay_groups(const float* __restrict__ tv, int 
 }
 
 // PM: 0 = one decision per window (the headline), 1 = decision periods decided per
-// chunk (lane-local when P | kHChunk), 2 = long periods (P >= kHWarpW/30) decided
-// in 32-period batches.  Separate instantiations keep each path's registers apart.
+// chunk, 2 = long periods (P >= kHWarpW/30) decided in 32-period batches, 3 =
+// lane-local periods (P | kHChunk; the last chunk as PM 1), 4 = the same for
+// P = 2 alone.  Separate instantiations keep each path's registers apart.
 template <int PM>
 #ifdef CHASE_H_MAXNREG
 __global__ void __maxnreg__(CHASE_H_MAXNREG) sweep_fast_kernel(
@@ -731,15 +758,23 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
                 const int ngr = (PER || invK == 0.0) ? 0 : nwin >> 2;
-                if (PM == 1 && !last && kHChunk % P.period == 0) {  // lane-local periods (fused decide + replay)
+                if (PM >= 3 && !last) {  // lane-local periods (P | kHChunk): fused decide + replay
                     uint8_t* chl = chb + j0;
-                    switch (P.period) {
-                        case 2: period_lane<2>(tv, 2, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow); break;
-                        case 3: period_lane<3>(tv, 3, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow); break;
-                        case 4: period_lane<4>(tv, 4, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow); break;
+#define CHASE_LANE_P(PC) period_lane<PC>(tv, PC, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow)
+                    if (PM == 4) CHASE_LANE_P(2);
+                    else switch (P.period) {
+                        case 2: CHASE_LANE_P(2); break;
+                        case 3: CHASE_LANE_P(3); break;
+                        case 4: CHASE_LANE_P(4); break;
+                        case 5: CHASE_LANE_P(5); break;
+                        case 6: CHASE_LANE_P(6); break;
+                        case 10: CHASE_LANE_P(10); break;
+                        case 12: CHASE_LANE_P(12); break;
+                        case 15: CHASE_LANE_P(15); break;
                         default:
                             period_lane<0>(tv, P.period, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow);
                     }
+#undef CHASE_LANE_P
                     __syncwarp();
                     k_carry = chb[kHWarpW - 1];
                 } else if (PM == 2) {  // long periods: 32-period batches

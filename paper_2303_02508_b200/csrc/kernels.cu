@@ -170,8 +170,11 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
         }
         q.smem_total = smem;
         // decision periods: long ones (at most 31 per warp chunk) in 32-period batches
-        auto kern = p.period <= 1 ? sweep_fast_kernel<0>
-                    : (p.period * 30 >= kHWarpW ? sweep_fast_kernel<2> : sweep_fast_kernel<1>);
+        auto kern = p.period <= 1                 ? sweep_fast_kernel<0>
+                    : p.period * 30 >= kHWarpW     ? sweep_fast_kernel<2>
+                    : p.period == 2                ? sweep_fast_kernel<4>
+                    : kHChunk % p.period == 0      ? sweep_fast_kernel<3>
+                                                   : sweep_fast_kernel<1>;
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
         int per_sm = 0;

@@ -450,7 +450,11 @@ def test_rolling_fit_forecast_split_path_and_f64():
     (5, 24, 24 + 4001, [0.3], 7),          # headline kernel: non-power-of-two n (division), ragged
     (2, 24, 24 + 4001, [0.5], 6),          # P | 60: lane-local fused periods in the full chunks
     (3, 24, 24 + 5000, [0.45], 5),
-    (12, 24, 24 + 4100, [0.5], 4),         # lane-local, P not specialised at compile time
+    (12, 24, 24 + 4100, [0.5], 4),         # lane-local, two periods per iteration
+    (6, 24, 24 + 4100, [0.5], 4),
+    (10, 24, 24 + 4100, [0.55], 4),
+    (15, 24, 24 + 4100, [0.5], 4),         # 4 periods per lane: one at a time
+    (20, 24, 24 + 4100, [0.5], 4),         # lane-local, P not specialised at compile time
     (60, 24, 24 + 3900, [0.5], 4),         # one period per lane
     (64, 24, 24 + 5000, [0.7], 5),         # power-of-two P > T: horizons cross the phase table's end
     (100, 24, 24 + 4321, [0.5], 4),        # P > T + 64: several wrap segments per horizon
