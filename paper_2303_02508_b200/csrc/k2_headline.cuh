@@ -423,10 +423,38 @@ __device__ __forceinline__ void replay_run(Acc& a, double2 ln, int m, double cs)
 // own periods and replays them in one pass: horizon (Eq. 1, recursive), mean,
 // Eq. 6 lookup, one line load per period, the running sums in window order
 // (the same sequence replay_groups adds them in).  PC > 0: P known at compile time.
+// The same replay from values already in registers (v[0, PC), PC < 16).
+template <int PC>
+__device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint32_t kk, int prof, uint8_t* chl,
+                                                     Acc& a) {
+    const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+#pragma unroll
+    for (int k = 0; k < PC; ++k) {
+        const float raw = v[k];
+        const double cw = (double)raw;
+        a.vmin = fminf(a.vmin, raw);
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        a.Cs = __dadd_rn(a.Cs, cw);
+        chl[q + k] = (uint8_t)kk;
+    }
+}
+
 // One period's replay at its choice kk (windows tv[q, q + Pn)).
 template <int PC>
 __device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv, int q, int Pn, uint32_t kk, int prof,
                                                    uint8_t* chl, Acc& a) {
+    if (PC > 0 && PC % 4 == 0 && PC < 16) {  // q % 4 == 0 too: LDS.128, conflict-free at the lane stride
+        float v[PC > 0 ? PC : 4];
+#pragma unroll
+        for (int i = 0; i < (PC > 0 ? PC : 4) / 4; ++i) {
+            const float4 f = *reinterpret_cast<const float4*>(tv + q + 4 * i);
+            v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+        }
+        lane_period_replay_v<(PC > 0 ? PC : 4)>(v, q, kk, prof, chl, a);
+        return;
+    }
     const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
     if (Pn < 16) {  // short runs: per-window sums (independent adds; the run form lengthens the chains)
 #pragma unroll
@@ -454,6 +482,36 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
     const int Pn = PC > 0 ? PC : Pp;
     const bool pow2 = (Pn & (Pn - 1)) == 0;
     const double dP = (double)Pn, invP = 1.0 / dP;
+    if (PC > 0 && PC % 2 == 0 && PC <= 6 && (kHChunk / (PC > 0 ? PC : 1)) % 2 == 0) {
+        // even P: the 2P values of an iteration start 16-B aligned (tv is, and 2P % 4 == 0),
+        // so they come in as LDS.128 (conflict-free at the 240-B lane stride; scalar loads
+        // at that stride are 4-way bank conflicts) and the start values ride in registers.
+        constexpr int P2 = PC > 0 ? 2 * PC : 4;
+        float carry = tv[-1];
+#pragma unroll 1
+        for (int q = 0; q < kHChunk; q += P2) {
+            float v[P2];
+#pragma unroll
+            for (int i = 0; i < P2 / 4; ++i) {
+                const float4 f = *reinterpret_cast<const float4*>(tv + q + 4 * i);
+                v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+            }
+            double pa = (double)carry, pb = (double)v[P2 / 2 - 1], sa = 0.0, sb = 0.0;
+            carry = v[P2 - 1];
+#pragma unroll
+            for (int k = 0; k < P2 / 2; ++k) {
+                horizon_step(Ap[q + k], wl, pa, sa);
+                horizon_step(Ap[q + P2 / 2 + k], wl, pb, sb);
+            }
+            const double ca = pow2 ? __dmul_rn(sa, invP) : __ddiv_rn(sa, dP);
+            const double cb = pow2 ? __dmul_rn(sb, invP) : __ddiv_rn(sb, dP);
+            const uint32_t ka = period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            const uint32_t kb = period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            lane_period_replay_v<P2 / 2>(v, q, ka, prof, chl, a);
+            lane_period_replay_v<P2 / 2>(v + P2 / 2, q + P2 / 2, kb, prof, chl, a);
+        }
+        return;
+    }
     if (PC > 0 && (kHChunk / (PC > 0 ? PC : 1)) % 2 == 0) {
         // two periods per iteration: their horizons are independent chains, interleaved
 #pragma unroll 1
