@@ -474,6 +474,43 @@ __device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv,
     }
 }
 
+// G consecutive periods of PN windows from tv[q] (q % 4 == 0, G*PN % 4 == 0): the
+// G*PN values as LDS.128, G independent horizon chains interleaved, then the G
+// replays in window order.  Returns the last value (the next group's start value).
+template <int PN, int G>
+__device__ __forceinline__ float period_group(const float* __restrict__ tv, int q, float carry,
+                                              const double* __restrict__ Ap, double wl, bool pow2, double dP,
+                                              double invP, double invK, double Kc, const uint2* ent8, int ebase,
+                                              uint32_t ZB, const PairTable* pt, const ProfileTable* pf, int prof,
+                                              uint8_t* chl, Acc& a, unsigned& n_slow) {
+    static_assert((G * PN) % 4 == 0, "group must be whole float4s");
+    float v[G * PN];
+#pragma unroll
+    for (int i = 0; i < G * PN / 4; ++i) {
+        const float4 f = *reinterpret_cast<const float4*>(tv + q + 4 * i);
+        v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+    }
+    double pr[G], sm[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        pr[g] = (double)(g == 0 ? carry : v[g * PN - 1]);
+        sm[g] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < PN; ++k)
+#pragma unroll
+        for (int g = 0; g < G; ++g) horizon_step(Ap[q + g * PN + k], wl, pr[g], sm[g]);
+    uint32_t kk[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const double ch = pow2 ? __dmul_rn(sm[g], invP) : __ddiv_rn(sm[g], dP);
+        kk[g] = period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) lane_period_replay_v<PN>(v + g * PN, q + g * PN, kk[g], prof, chl, a);
+    return v[G * PN - 1];
+}
+
 template <int PC>
 __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp, const double* __restrict__ Ap,
                                             double wl, double invK, double Kc, const uint2* ent8, int ebase,
@@ -486,30 +523,13 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         // even P: the 2P values of an iteration start 16-B aligned (tv is, and 2P % 4 == 0),
         // so they come in as LDS.128 (conflict-free at the 240-B lane stride; scalar loads
         // at that stride are 4-way bank conflicts) and the start values ride in registers.
-        constexpr int P2 = PC > 0 ? 2 * PC : 4;
+        constexpr int PN = (PC > 0 && PC % 2 == 0) ? PC : 2;  // (odd PC never takes this branch)
         float carry = tv[-1];
+        // (four periods per iteration at P = 2 measured slower: 17.7 -> 18.4 ms at C5, register spills)
 #pragma unroll 1
-        for (int q = 0; q < kHChunk; q += P2) {
-            float v[P2];
-#pragma unroll
-            for (int i = 0; i < P2 / 4; ++i) {
-                const float4 f = *reinterpret_cast<const float4*>(tv + q + 4 * i);
-                v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
-            }
-            double pa = (double)carry, pb = (double)v[P2 / 2 - 1], sa = 0.0, sb = 0.0;
-            carry = v[P2 - 1];
-#pragma unroll
-            for (int k = 0; k < P2 / 2; ++k) {
-                horizon_step(Ap[q + k], wl, pa, sa);
-                horizon_step(Ap[q + P2 / 2 + k], wl, pb, sb);
-            }
-            const double ca = pow2 ? __dmul_rn(sa, invP) : __ddiv_rn(sa, dP);
-            const double cb = pow2 ? __dmul_rn(sb, invP) : __ddiv_rn(sb, dP);
-            const uint32_t ka = period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
-            const uint32_t kb = period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
-            lane_period_replay_v<P2 / 2>(v, q, ka, prof, chl, a);
-            lane_period_replay_v<P2 / 2>(v + P2 / 2, q + P2 / 2, kb, prof, chl, a);
-        }
+        for (int q = 0; q < kHChunk; q += 2 * PN)
+            carry = period_group<PN, 2>(tv, q, carry, Ap, wl, pow2, dP, invP, invK, Kc, ent8, ebase, ZB, pt, pf, prof,
+                                        chl, a, n_slow);
         return;
     }
     if (PC > 0 && (kHChunk / (PC > 0 ? PC : 1)) % 2 == 0) {
@@ -821,7 +841,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
 #define CHASE_LANE_P(PC) period_lane<PC>(tv, PC, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow)
                     if (PM == 4) CHASE_LANE_P(2);
                     else switch (P.period) {
-                        case 2: CHASE_LANE_P(2); break;
+                        // P = 2 runs as PM 4 (the host picks it)
                         case 3: CHASE_LANE_P(3); break;
                         case 4: CHASE_LANE_P(4); break;
                         case 5: CHASE_LANE_P(5); break;
