@@ -289,7 +289,7 @@ def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0, svr=None) ->
                 return ("sweep_fast_kernel<2> (decision periods in 32-period batches, one horizon per lane; "
                         "Eq. 6 argmin + run-form replay)")
             if 60 % P == 0:
-                return (f"sweep_fast_kernel<{4 if P == 2 else 3}> (decision periods: each lane decides and replays its own periods; "
+                return (f"sweep_fast_kernel<{P + 2 if P in (2, 3, 4, 5, 6, 10, 12, 15) else 3}> (decision periods: each lane decides and replays its own periods; "
                         "Eq. 6 argmin + replay)")
             return ("sweep_fast_kernel<1> (decision periods: per-chunk decisions, up to 4 horizon chains per lane; "
                     "Eq. 6 argmin + replay)")

@@ -656,8 +656,10 @@ __device__ __forceinline__ void replay_groups(const float* __restrict__ tv, int 
 
 // PM: 0 = one decision per window (the headline), 1 = decision periods decided per
 // chunk, 2 = long periods (P >= kHWarpW/30) decided in 32-period batches, 3 =
-// lane-local periods (P | kHChunk; the last chunk as PM 1), 4 = the same for
-// P = 2 alone.  Separate instantiations keep each path's registers apart.
+// lane-local periods (P | kHChunk, P known at run time; the last chunk as PM 1),
+// PM >= 4 = the same with P = PM - 2 fixed at compile time (P = 2, 3, 4, 5, 6,
+// 10, 12, 15).  Separate instantiations keep each path's registers apart: one
+// kernel holding all the compile-time P spilled more (P = 12: 14.6 vs 13.6 ms).
 template <int PM>
 #ifdef CHASE_H_MAXNREG
 __global__ void __maxnreg__(CHASE_H_MAXNREG) sweep_fast_kernel(
@@ -839,19 +841,8 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 if (PM >= 3 && !last) {  // lane-local periods (P | kHChunk): fused decide + replay
                     uint8_t* chl = chb + j0;
 #define CHASE_LANE_P(PC) period_lane<PC>(tv, PC, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow)
-                    if (PM == 4) CHASE_LANE_P(2);
-                    else switch (P.period) {
-                        // P = 2 runs as PM 4 (the host picks it)
-                        case 3: CHASE_LANE_P(3); break;
-                        case 4: CHASE_LANE_P(4); break;
-                        case 5: CHASE_LANE_P(5); break;
-                        case 6: CHASE_LANE_P(6); break;
-                        case 10: CHASE_LANE_P(10); break;
-                        case 12: CHASE_LANE_P(12); break;
-                        case 15: CHASE_LANE_P(15); break;
-                        default:
-                            period_lane<0>(tv, P.period, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow);
-                    }
+                    if constexpr (PM >= 4) CHASE_LANE_P(PM - 2);
+                    else period_lane<0>(tv, P.period, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow);
 #undef CHASE_LANE_P
                     __syncwarp();
                     k_carry = chb[kHWarpW - 1];

@@ -172,9 +172,16 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
         // decision periods: long ones (at most 31 per warp chunk) in 32-period batches
         auto kern = p.period <= 1                 ? sweep_fast_kernel<0>
                     : p.period * 30 >= kHWarpW     ? sweep_fast_kernel<2>
+                    : kHChunk % p.period != 0      ? sweep_fast_kernel<1>
                     : p.period == 2                ? sweep_fast_kernel<4>
-                    : kHChunk % p.period == 0      ? sweep_fast_kernel<3>
-                                                   : sweep_fast_kernel<1>;
+                    : p.period == 3                ? sweep_fast_kernel<5>
+                    : p.period == 4                ? sweep_fast_kernel<6>
+                    : p.period == 5                ? sweep_fast_kernel<7>
+                    : p.period == 6                ? sweep_fast_kernel<8>
+                    : p.period == 10               ? sweep_fast_kernel<12>
+                    : p.period == 12               ? sweep_fast_kernel<14>
+                    : p.period == 15               ? sweep_fast_kernel<17>
+                                                   : sweep_fast_kernel<3>;
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
         int per_sm = 0;

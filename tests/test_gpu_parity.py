@@ -451,6 +451,7 @@ def test_rolling_fit_forecast_split_path_and_f64():
     (2, 24, 24 + 4001, [0.5], 6),          # P | 60: lane-local fused periods in the full chunks
     (3, 24, 24 + 5000, [0.45], 5),
     (12, 24, 24 + 4100, [0.5], 4),         # lane-local, two periods per iteration
+    (4, 24, 24 + 4100, [0.5], 4),          # lane-local, 15 periods per lane: one at a time, LDS.128
     (6, 24, 24 + 4100, [0.5], 4),
     (10, 24, 24 + 4100, [0.55], 4),
     (15, 24, 24 + 4100, [0.5], 4),         # 4 periods per lane: one at a time
