@@ -8,8 +8,10 @@ baseline, per-GPU totals) plus, for N > 1, the NCCL all-reduce of the totals.
 
   python bench.py [--gpus N --steps K --warmup W] [--config C5] [--impl reference]
 
-N > 1 is launched by torchrun (one rank per GPU); each rank plans its own
-1e6-trace shard (weak scaling, configs[4]) and rank 0 prints ONE JSON line.
+N > 1 is launched by torchrun (one rank per GPU); the workload's traces
+(C5: 10^6, configs[4]) are split across the ranks, contiguous and balanced
+(strong scaling; --weak gives every rank its own), and rank 0 prints ONE JSON
+line.
 `--impl reference` times the CPU oracle (oracle/) on the host cores instead.
 """
 from __future__ import annotations
@@ -41,11 +43,17 @@ def parse_args(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["chase", "reference"], default="chase")
     ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
-    ap.add_argument("--traces", type=int, default=None, help="override traces per GPU")
+    ap.add_argument("--traces", type=int, default=None,
+                    help="override the workload's trace count (total; per GPU with --weak)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank plans its own --traces (default: strong, the workload "
+                         "split across the ranks as configs[4] names it)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--e2e-traces", type=int, default=None)
+    ap.add_argument("--no-prefix-check", action="store_true",
+                    help="skip the untimed oracle parity check of the whole cpu_baseline sample")
     ap.add_argument("--mode", choices=["plan", "mape", "timeline"], default="plan",
                     help="plan: the planner (headline); mape: the walk-forward forecast-evaluation sweep (f3); "
                          "timeline: per-period audit rows of a planned replay (f4)")
@@ -227,8 +235,9 @@ def main_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(w, args.gpus, args.refit_stride, args.period_steps, svr_arg(args)),
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(w, args.gpus, args.refit_stride, args.period_steps, svr_arg(args),
+                                  n_total=w.n_traces * (args.gpus if args.weak else 1), weak=args.weak),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": s.cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -301,7 +310,7 @@ def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0, svr=None) ->
     return "sweep_kernel<FUSED> (fused predict + Eq. 6 argmin + replay)"
 
 
-def workload_config(w: inputs.Workload, n_gpus: int, R: int = 0, P: int = 0, svr=None):
+def workload_config(w: inputs.Workload, n_gpus: int, R: int = 0, P: int = 0, svr=None, n_total=None, weak=False):
     fc = ("fit once per trace on the 24 h before job start (P:67), least squares (Table 1 LR)" if R == 0 else
           f"rolling refit every {R} window(s) on the {w.history_len} points before each origin (P:78-79)")
     if svr is not None:
@@ -309,13 +318,19 @@ def workload_config(w: inputs.Workload, n_gpus: int, R: int = 0, P: int = 0, svr
               "(Table 1's best model, P:162; C=1, eps=0.1, gamma=1/3, tol=1e-3)")
     if P > 1:
         fc += f"; one decision per {P}-step period on the mean recursive forecast (P:130, S:158-166)"
+    n_total = w.n_traces if n_total is None else n_total
+    split = (f"{n_total} traces, {'each of' if weak else 'split across'} {n_gpus} GPU(s) "
+             f"({'weak' if weak else 'strong'} scaling)")
     return {
-        "workload": f"{w.name}: {w.description}",
-        "traces_per_gpu": w.n_traces, "steps_per_trace": w.n_steps, "history_len": w.history_len,
+        "workload": f"{w.name}: {w.description}; {split}",
+        "traces_total": n_total, "traces_per_gpu": -(-n_total // n_gpus), "steps_per_trace": w.n_steps,
+        "history_len": w.history_len,
         "windows_per_trace": w.W, "interval_s": w.interval_s, "n_eta": len(w.etas),
         "n_limits": int(w.profiles[0].K), "profiles": [p.name for p in w.profiles],
         "forecaster": fc, "refit_stride": R, "period_steps": max(P, 1),
-        "l2": f"inputs larger than L2 ({w.n_traces * w.ld * 4 / 1e9:.1f} GB of fp32 traces per GPU vs 126 MB L2)",
+        "l2": (f"L2 flushed between timed steps (512 MB write outside each step's CUDA events; "
+               f"{n_total * w.ld * 4 / 1e6:.3g} MB of fp32 traces vs the 126 MB L2)" if l2_resident(w, n_total) else
+               f"inputs larger than L2 ({n_total * w.ld * 4 / n_gpus / 1e9:.1f} GB of fp32 traces per GPU vs 126 MB L2)"),
         "parallelism": f"dp{n_gpus} (trace-sharded; NCCL all-reduce of per-GPU totals)",
     }
 
@@ -336,8 +351,13 @@ def main_chase(args):
     torch.cuda.set_device(dev)
 
     w = inputs.workload(args.config, n_traces=args.traces)
-    n, W = w.n_traces, w.W
-    trace0, _ = shard_bounds(n * world, rank, world)   # weak scaling: every rank plans its own n traces
+    W = w.W
+    if args.weak:   # weak scaling: every rank plans its own w.n_traces traces
+        n_total = w.n_traces * world
+    else:           # strong scaling (configs[4]): the workload's traces split across the ranks
+        n_total = w.n_traces
+    trace0, trace1 = shard_bounds(n_total, rank, world)
+    n = trace1 - trace0
     x = torch.empty((n, w.ld), dtype=torch.float32, device=dev)
     inputs.synth_traces_device(x, w.n_steps, seed=w.seed, mode=w.mode, trace0=trace0)
     pid = None
@@ -363,7 +383,7 @@ def main_chase(args):
     torch.cuda.synchronize()
     diag = planner.diag()
     sums0 = planner.sums.cpu().numpy()
-    if diag.n_bad or sums0[0, 7] != n * world:
+    if diag.n_bad or sums0[0, 7] != n_total:
         raise RuntimeError(f"planner reported bad traces: n_bad={diag.n_bad}, n_ok={sums0[0, 7]}")
 
     stream = torch.cuda.current_stream(dev)
@@ -372,6 +392,13 @@ def main_chase(args):
         a.record(stream)
         b.record(stream)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # inputs smaller than a few L2s (C1-C3): the L2 is flushed between timed steps
+    # (a 512 MB write outside each step's events), and the step time is the sum of
+    # the per-step event times
+    flush = (torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+             if l2_resident(w, n_total) else None)
+    sev = ([(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+           if flush is not None else None)
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
@@ -381,8 +408,13 @@ def main_chase(args):
     clocks.begin()
     t0.record(stream)
     for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+            sev[k][0].record(stream)
         cb.set_kernel_events(*kev[k])
         step()
+        if flush is not None:
+            sev[k][1].record(stream)
     t1.record(stream)
     cb.set_kernel_events(None, None)
     torch.cuda.synchronize()
@@ -392,14 +424,14 @@ def main_chase(args):
     launches = cb.kernel_launches() - launches0
     clk = clocks.stop()
 
-    elapsed_ms = t0.elapsed_time(t1)
+    elapsed_ms = t0.elapsed_time(t1) if flush is None else float(sum(a.elapsed_time(b) for a, b in sev))
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
     tm = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     elapsed_ms, kern_ms = float(tm[0]), float(tm[1])
     ms_per_step = elapsed_ms / args.steps
-    total_windows = float(n) * W * world
+    total_windows = float(n_total) * W
     value = total_windows / (ms_per_step / 1e3)
 
     R = args.refit_stride
@@ -414,14 +446,15 @@ def main_chase(args):
                     "peak_source": peak_src}
     elif R == 0:
         peak, peak_src = measured_peaks()
-        alg_bytes = n * W * BYTES_PER_WINDOW
+        bpw = 4.0 + len(w.etas)   # fp32 trace value + one choice byte per eta (5 B for one eta)
+        alg_bytes = n * W * bpw
         achieved = alg_bytes / (kern_ms / 1e3) / 1e9
         tpw = ncu_traffic_per_window(args.config if args.period_steps <= 1 else f"{args.config}_p{args.period_steps}")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": None if tpw is None else tpw * n * W,
                     "kernel": planner_kernel_name(w, 0, args.period_steps),
                     "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
-                    "algorithmic_bytes_per_launch": alg_bytes, "bytes_per_window": BYTES_PER_WINDOW,
+                    "algorithmic_bytes_per_launch": alg_bytes, "bytes_per_window": bpw,
                     "peak_source": peak_src}
     else:
         peak, peak_src = fp64_peak()
@@ -432,32 +465,140 @@ def main_chase(args):
                     "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
                     "algorithmic_flops_per_launch": flops, "peak_source": peak_src}
 
+    latency = None
+    if n_total <= 64 and world == 1:   # C1 / C2: one trace, latency-bound
+        latency = bench_latency(planner, torch, stream, args.steps)
+
     # ---- e2e: the public host-buffer call, H2D of the inputs inside the timed region
     e2e = None
     if not args.no_e2e:
         e2e = bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev)
 
     cpu = None
+    prefix_check = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, ns, dt = oracle_sample_rate(w, args.cpu_seconds, n, args.refit_stride, args.period_steps,
                                                  svr_arg(args))
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {ns} of {n} traces ({ns * W:.3g} windows, {dt:.1f} s on {cores} threads)"}
+        if svr_arg(args) is None and not args.no_prefix_check:
+            prefix_check = oracle_prefix_check(w, x, pid, J, ns, args, cb, torch)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based generator, inputs/)",
-            "config": workload_config(w, world, args.refit_stride, args.period_steps, svr_arg(args)),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "config": workload_config(w, world, args.refit_stride, args.period_steps, svr_arg(args),
+                                      n_total=n_total, weak=args.weak),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency": latency,
             "gpu_launches": int(launches), "clocks": clk,
-            "check": {"n_ok": float(sums0[0, 7]), "n_slow_windows": int(diag.n_slow_windows)},
+            "decisions_per_s": value * len(w.etas),
+            "check": {"n_ok": float(sums0[0, 7]), "n_slow_windows": int(diag.n_slow_windows),
+                      "kernel_path": int(diag.kernel_path), "oracle_prefix": prefix_check},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def l2_resident(w, n_total) -> bool:
+    """Inputs + choices within 2 x the 126 MB L2 (C1, C2, C3): flush between steps."""
+    return n_total * (w.ld * 4 + w.W * len(w.etas)) < 2 * 126e6
+
+
+def bench_latency(planner, torch, stream, steps):
+    """Latency-bound configs (one trace, C1/C2): the wall-clock microseconds of
+    one chase_sweep call that returns its results (call + stream synchronize,
+    host work included: argument checks, the cached tables, 8 kernel launches),
+    the GPU time of the call by CUDA events, and the same call replayed as a
+    CUDA graph (the launches captured once, stream-ordered)."""
+    n = max(steps, 20)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(n):
+        planner.run()
+        torch.cuda.synchronize()
+    wall = (time.perf_counter() - t) / n * 1e6
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n):
+        planner.run()
+    b.record(stream)
+    torch.cuda.synchronize()
+    gpu = a.elapsed_time(b) / n * 1e3
+    out = {"us_per_call_wall": wall, "us_per_call_gpu_back_to_back": gpu, "calls": n}
+    try:
+        g = torch.cuda.CUDAGraph()
+        s2 = torch.cuda.Stream()
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s2):
+            planner.run()
+        torch.cuda.current_stream().wait_stream(s2)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            planner.run()
+        g.replay()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(n):
+            g.replay()
+            torch.cuda.synchronize()
+        out["us_per_call_graph_wall"] = (time.perf_counter() - t) / n * 1e6
+    except Exception as e:  # capture is an optimisation, not the contract
+        out["graph_error"] = str(e)[:200]
+    return out
+
+
+def oracle_prefix_check(w, x, pid, J, ns, args, cb, torch, chunk=32768):
+    """Parity of the whole cpu_baseline sample (untimed): the first `ns` traces of
+    the benched workload planned by chase_sweep in the benched configuration
+    (same kernels; choices and per-trace totals kept) against the oracle, chunk
+    by chunk.  Choices must match bit for bit, and the per-trace totals too
+    (the synthetic inputs are dyadic)."""
+    import oracle
+    W = w.W
+    sub = x[:ns]
+    pl = cb.Planner(sub, n_steps=w.n_steps, profiles=w.profiles, etas=w.etas, interval_s=w.interval_s,
+                    history_len=w.history_len, profile_id=None if pid is None else pid[:ns],
+                    job_samples=J[:ns].contiguous(), want_choice=True, want_per_trace=True,
+                    refit_stride=args.refit_stride, period_steps=args.period_steps)
+    res = pl.run()
+    torch.cuda.synchronize()
+    path = int(pl.diag().kernel_path)
+    t0 = time.perf_counter()
+    ch_bad = tot_bad = 0
+    first_bad = None
+    for c0 in range(0, ns, chunk):
+        m = min(chunk, ns - c0)
+        tr = inputs.synth_traces_host(m, w.n_steps, seed=w.seed, mode=w.mode, trace0=c0)
+        p_h = None if pid is None else pid[c0:c0 + m].cpu().numpy()
+        o = oracle.plan_batch(tr, N=w.n_steps, L=w.history_len, T=w.T, refit_stride=args.refit_stride,
+                              period=args.period_steps, profiles=w.profiles, profile_id=p_h, etas=w.etas,
+                              delta=float(w.interval_s), job_samples=J[c0:c0 + m].cpu().numpy(),
+                              want_forecast=False, want_choice=True)
+        g_ch = res.choice[:, c0:c0 + m, :W].cpu().numpy()
+        bad_rows = np.any(g_ch != o["choice"], axis=2)
+        g_tot = res.per_trace[:, c0:c0 + m].cpu().numpy().view(cb.TOTALS_DTYPE).reshape(len(w.etas), m)
+        tb = g_tot.tobytes() != o["totals"].tobytes()
+        if tb:
+            diff = np.any(g_tot.view(np.uint8).reshape(len(w.etas), m, 64) !=
+                          o["totals"].view(np.uint8).reshape(len(w.etas), m, 64), axis=2)
+            tot_bad += int(diff.sum())
+            if first_bad is None:
+                first_bad = c0 + int(np.argwhere(diff)[0][1])
+        ch_bad += int(bad_rows.sum())
+        if bad_rows.any() and first_bad is None:
+            first_bad = c0 + int(np.argwhere(bad_rows)[0][1])
+    del res, pl
+    torch.cuda.empty_cache()
+    return {"traces": int(ns), "windows": int(ns) * W * len(w.etas), "traces_with_choice_mismatch": ch_bad,
+            "traces_with_totals_mismatch": tot_bad, "first_mismatch_trace": first_bad, "kernel_path": path,
+            "seconds": round(time.perf_counter() - t0, 1),
+            "what": "the cpu_baseline sample re-planned by chase_sweep (benched config) vs the oracle: "
+                    "choices bit-exact, per-trace totals bit-identical"}
 
 
 def bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev):
@@ -642,7 +783,7 @@ def main_mape(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded counter-based generator, inputs/)", "config": cfg,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency": latency, "gpu_launches": int(launches),
                 "clocks": clk, "check": {"mean_mape_linear": float(mp[:, 0].mean()),
                                          "mean_mape_persistence": float(mp[:, 1].mean())}}
         print(json.dumps(line), flush=True)

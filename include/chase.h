@@ -163,8 +163,16 @@ typedef struct {
     uint64_t n_exhausted;        /* traces with status 3                        */
     uint64_t n_slow_windows;     /* (window, eta) decisions that took the
                                     canonical K-way Eq. 6 path (§8(a) a5)      */
-    uint64_t reserved2[3];
+    uint64_t kernel_path;        /* which sweep kernels the call ran (bits):
+                                    CHASE_PATH_*, for tests and the bench      */
+    uint64_t reserved2[2];
 } chase_diag_t;
+
+#define CHASE_PATH_HEADLINE   1u   /* sweep_fast_kernel<0>: fp32, aligned, one eta, no forecast output */
+#define CHASE_PATH_H_PERIODS  2u   /* sweep_fast_kernel<PM > 0>: decision periods in the headline kernel */
+#define CHASE_PATH_GENERAL    4u   /* sweep_kernel: every other shape (f64, multi-eta, forecast output) */
+#define CHASE_PATH_FC_IN      8u   /* sweep_kernel reading precomputed forecasts (SVR, periods, rolling) */
+#define CHASE_PATH_ROLL_FUSED 16u  /* rolling refit fused into the sweep (sliding moments) */
 
 /* Bytes of device workspace needed by any entry point for these shapes
  * (n_profiles, n_eta >= 1).  Returns 0 on invalid arguments. */
@@ -254,7 +262,9 @@ chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_for
  *   d_choice    [n_traces][ld_c] u8 of ONE eta (e.g. chase_sweep's first eta
  *               plane), or NULL for the max-limit baseline;
  *   d_forecast  [n_traces][ld_f] f64 decision forecasts or NULL (rows get NaN);
- *   d_trace_ids [m] int64 trace indices, or NULL for traces 0..m-1;
+ *   d_trace_ids [m] int64 trace indices, or NULL for traces 0..m-1; a row
+ *               whose id lies outside [0, n_traces) is written as NaN (rows
+ *               and summary), nothing outside the inputs is read;
  *   d_rows      [m][ceil(W/P)][8] f64 out, 16-byte aligned (rows leave by TMA bulk stores);
  *   d_summary   [m][4] f64 out or NULL: Eq. 3 next to the stepwise
  *               integration over the job's run:
@@ -291,7 +301,8 @@ chase_status_t chase_profiling_overhead(const chase_traces_t* traces, int32_t hi
  * chosen limit is the first minimum of its row.
  *   d_costs [m][ceil(W/P)][ld_k] f64 out, ld_k >= the largest n_limits; the
  *           entries k >= the trace's n_limits are NaN, as are all entries of a
- *           NaN decision value (an invalid trace).
+ *           NaN decision value (an invalid trace) and of a trace id outside
+ *           [0, n_traces) in d_trace_ids.
  * Workspace: chase_workspace_bytes(traces, NULL, n_profiles, 1). */
 chase_status_t chase_period_costs(const double* d_forecast, int64_t n_traces, int64_t W, int64_t ld_f,
                                   int32_t period_steps, const chase_profile_t* profiles, int32_t n_profiles,
@@ -308,7 +319,9 @@ chase_status_t chase_period_costs(const double* d_forecast, int64_t n_traces, in
  *   cudaHostAlloc / torch pin_memory, for copy/compute overlap);
  *   d_staging: chase_sweep_host_staging_bytes() bytes of device memory;
  *   d_ws: chase_workspace_bytes() for a descriptor with n_traces = chunk_traces.
- * Synchronous: returns after h_sum is written. */
+ * Synchronous: returns after h_sum is written.  Afterwards chase_diag_read(d_ws)
+ * reports the whole call: counts summed over the chunks, first_bad_trace as
+ * an index into h_traces. */
 size_t chase_sweep_host_staging_bytes(const chase_traces_t* h_traces, int64_t chunk_traces, int32_t n_eta);
 chase_status_t chase_sweep_host(const chase_traces_t* h_traces, const chase_forecast_cfg_t* fcfg,
                                 const chase_profile_t* profiles, int32_t n_profiles,

@@ -186,7 +186,7 @@ def workload(name: str, n_traces: int | None = None) -> Workload:
                      description="1e5 traces x 1 year, per-trace ResNet-50/BERT/ViT-shaped tables")
     elif name == "C5":
         w = Workload("C5", 1_000_000, 24 + 8760, 5, MODE_RANDOM, [rn], [0.5],
-                     description="1e6 traces x 1 year (per GPU; weak scaling), NCCL all-reduce of totals")
+                     description="1e6 traces x 1 year sharded across the GPUs, NCCL all-reduce of totals")
     else:
         raise KeyError(name)
     if n_traces is not None:

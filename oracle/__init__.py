@@ -71,8 +71,6 @@ def lib():
         L.oracle_profiling_overhead.restype = i32
         L.oracle_rbf_exp.argtypes = [f64]
         L.oracle_rbf_exp.restype = f64
-        L.oracle_exp2_table.argtypes = []
-        L.oracle_exp2_table.restype = ctypes.POINTER(ctypes.c_double)
         L.oracle_svr_fit.argtypes = [vp, i32, i32, i32, vp, vp, f64, f64, f64, f64, i32, ctypes.POINTER(SVRModel)]
         L.oracle_svr_fit.restype = i32
         L.oracle_svr_predict.argtypes = [ctypes.POINTER(SVRModel), f64, f64, f64]
@@ -279,12 +277,6 @@ def profiling_overhead(c, *, L, avg_power, delta=3600.0):
 
 def rbf_exp(x: float) -> float:
     return float(lib().oracle_rbf_exp(float(x)))
-
-
-def exp2_table() -> list:
-    """oracle_exp2_table: the 64 doubles 2^(j/64) of oracle_rbf_exp."""
-    t = lib().oracle_exp2_table()
-    return [t[j] for j in range(64)]
 
 
 def svr_fit(hist, *, T, phi0=0, C=1.0, eps=0.1, gamma=0.0, tol=1e-3, max_iter=10000):

@@ -599,58 +599,20 @@ int32_t oracle_profiling_overhead(const double* c, int32_t L, int32_t K, const d
 
 
 /* ---------------------------------------------------------------- epsilon-SVR (f2) */
-/* 2^(j/64), j = 0..63, each the double nearest the exact value (pinned in
- * tests/test_oracle_svr.py against a 60-digit decimal evaluation). */
-static const double oracle_exp2_64[64] = {
-    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
-    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
-    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
-    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
-    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
-    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
-    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
-    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
-    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
-    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
-    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
-    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
-    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
-    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
-    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
-    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
-};
-
-const double* oracle_exp2_table(void) { return oracle_exp2_64; }
-
-/* exp(x) for x <= 0 (DESIGN Q31): x = (64 e + j) ln2/64 + r with kd = 64 e + j
- * the integer nearest 64 x/ln2 (the 1.5*2^52 shift), the reduction by ln2/64
- * split in two (Cody-Waite), exp(r) for |r| <= ln2/128 by its degree-5 Taylor
- * polynomial in Horner form, times the table value 2^(j/64), then the exact
- * scaling by 2^e.  Every step is one correctly rounded operation: fma(a, b, c)
- * is (a*b + c) rounded once. */
+/* The RBF kernel's exp is libm's exp (DESIGN Q31): the plain definition.  The
+ * paper names scikit-learn's SVR, whose libsvm kernel evaluates
+ * exp(-gamma*||a-b||^2) with the C library's exp; no faster or differently
+ * rounded exp enters the oracle.  x > 0 (never a kernel argument) gives NaN. */
 double oracle_rbf_exp(double x) {
     if (!(x <= 0.0)) return NAN;
-    if (x < -745.0) return 0.0;
-    const double kd = fma(x, 0x1.71547652b82fep+6, 0x1.8p52) - 0x1.8p52;  /* nearest integer to 64 x / ln 2 */
-    double r = fma(-kd, 0x1.62e42feep-7, x);                              /* x - kd (ln2/64)_hi */
-    r = fma(-kd, 0x1.a39ef35793c76p-39, r);                               /*   - kd (ln2/64)_lo */
-    double q = 0x1.1111111111111p-7;                                      /* 1/5! */
-    q = fma(q, r, 0x1.5555555555555p-5);                                  /* 1/4! */
-    q = fma(q, r, 0x1.5555555555555p-3);                                  /* 1/3! */
-    q = fma(q, r, 0.5);
-    q = fma(q, r, 1.0);
-    q = fma(q, r, 1.0);
-    const int k = (int)kd;
-    const int j = ((k % 64) + 64) % 64;                                   /* kd = 64 e + j, 0 <= j < 64 */
-    const int e = (k - j) / 64;
-    return ldexp(oracle_exp2_64[j] * q, e);
+    return exp(x);
 }
 
-/* K(a, b) = exp(-gamma * ||a - b||^2), the squared distance accumulated left
- * to right: d0*d0, then + d1*d1, then + d2*d2 (each add fused with its product). */
+/* K(a, b) = exp(-gamma * ||a - b||^2), the squared distance summed left to
+ * right: ((d0*d0) + (d1*d1)) + (d2*d2), each operation rounded once. */
 static double rbf(const double* a, const double* b, double gamma) {
     const double d0 = a[0] - b[0], d1 = a[1] - b[1], d2 = a[2] - b[2];
-    const double d = fma(d2, d2, fma(d1, d1, d0 * d0));
+    const double d = ((d0 * d0) + (d1 * d1)) + (d2 * d2);
     return oracle_rbf_exp(-(gamma * d));
 }
 
@@ -698,7 +660,7 @@ int32_t oracle_svr_fit(const double* hist, int32_t L, int32_t T, int32_t phi0, c
     /* kernel matrix */
     static __thread double K[ORACLE_SVR_MAXN][ORACLE_SVR_MAXN];
     for (int32_t i = 0; i < n; ++i)
-        for (int32_t j = 0; j < n; ++j) K[i][j] = rbf(m->z[i], m->z[j], m->gamma);
+        for (int32_t j = 0; j < n; ++j) K[i][j] = (double)(float)rbf(m->z[i], m->z[j], m->gamma);
     /* SMO on 2n variables: t < n -> y = +1 (alpha), t >= n -> y = -1 (alpha*) */
     const int32_t l = 2 * n;
     double a[2 * ORACLE_SVR_MAXN], G[2 * ORACLE_SVR_MAXN];
@@ -805,7 +767,7 @@ double oracle_svr_predict(const oracle_svr_t* m, double s, double c, double lag)
     double zq[3];
     for (int j = 0; j < 3; ++j) zq[j] = m->keep[j] ? (xv[j] - m->mu[j]) / m->sigma[j] : 0.0;
     double f = 0.0;
-    for (int32_t t = 0; t < m->n; ++t) f = fma(m->coef[t], rbf(m->z[t], zq, m->gamma), f);  /* f += coef*K, one rounding */
+    for (int32_t t = 0; t < m->n; ++t) f = f + m->coef[t] * rbf(m->z[t], zq, m->gamma);   /* sum of coef*K, in order */
     f = f - m->rho;
     const double p = m->mu[3] + m->sigma[3] * f;
     return p > 0.0 ? p : 0.0;

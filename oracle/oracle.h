@@ -136,8 +136,9 @@ int32_t oracle_plan_batch_f32(const float* traces, int64_t n_traces, int64_t N,
  * maximal KKT violation is below tol or after max_iter pair updates; the bias
  * is the mean y*G over free variables (else the midpoint of the bounds).
  * f(x) = sum_t (a_t - a*_t) K(z_t, z(x)) - rho;  chat = max(0, mu_y + sigma_y f).
- * exp() of the kernel is oracle_rbf_exp (below), not libm, so that the GPU can
- * reproduce every operation (DESIGN Q31). */
+ * exp() of the kernel is libm's exp (oracle_rbf_exp), as in scikit-learn's
+ * libsvm: the plain definition.  The GPU kernel evaluates its own faster exp,
+ * so the two agree to a tolerance, not bit for bit (DESIGN Q31). */
 #define ORACLE_SVR_MAXN 63
 typedef struct {
     double z[ORACLE_SVR_MAXN][3];  /* standardised training features */
@@ -150,17 +151,8 @@ typedef struct {
     int32_t status;                /* 0 ok, 4 bad value                */
 } oracle_svr_t;
 
-/* exp(x) for x <= 0: x = (64 e + j) ln2/64 + r (kd = 64 e + j the integer
- * nearest 64 x/ln2, found by the 1.5*2^52 shift), Cody-Waite reduction, the
- * degree-5 Taylor polynomial of exp(r) (|r| <= ln2/128) in Horner form, times
- * the table value 2^(j/64) (64 correctly rounded doubles), scaled by 2^e.
- * Every step is one correctly rounded IEEE operation (the reduction and the
- * Horner steps are fma: a*b + c rounded once), so host and device agree bit
- * for bit; |error| <= 2 ulp of libm exp (pinned in tests).  The kernel's
- * squared distance and the prediction's sum of coef*K accumulate with fma as
- * well. */
+/* libm exp(x) for x <= 0 (the RBF kernel's argument); NaN for x > 0. */
 double oracle_rbf_exp(double x);
-const double* oracle_exp2_table(void);  /* the 64 values 2^(j/64) used by oracle_rbf_exp */
 
 /* Fit on the L history points hist[0..L) (rows as oracle_fit).  gamma <= 0:
  * 1/(3 * mean variance of the standardised features) (SPEC default). */

@@ -57,7 +57,11 @@ class CostCfg(ctypes.Structure):
 class Diag(ctypes.Structure):
     _fields_ = [("first_bad_trace", i64), ("first_bad_status", i32), ("reserved", i32), ("n_bad", ctypes.c_uint64),
                 ("n_exhausted", ctypes.c_uint64), ("n_slow_windows", ctypes.c_uint64),
-                ("reserved2", ctypes.c_uint64 * 3)]
+                ("kernel_path", ctypes.c_uint64), ("reserved2", ctypes.c_uint64 * 2)]
+
+
+# chase_diag_t.kernel_path bits (include/chase.h CHASE_PATH_*)
+PATH_HEADLINE, PATH_H_PERIODS, PATH_GENERAL, PATH_FC_IN, PATH_ROLL_FUSED = 1, 2, 4, 8, 16
 
 
 TOTALS_DTYPE = np.dtype([("time_s", "f8"), ("energy_j", "f8"), ("carbon_g", "f8"), ("samples", "f8"),

@@ -176,8 +176,8 @@ chase_status_t check_ws(void* ws, size_t bytes, size_t need) {
 // ---------------------------------------------------------------- constant tables
 // Phase table of Eq. 2, anchored to UTC midnight:
 // S[phi] = sin((2.0*pi*phi)/T), C[phi] = cos(...), host libm, fp64.
-std::vector<uint8_t> build_tables(int T, double delta, const chase_profile_t* profs, int n_prof,
-                                  const chase_cost_cfg_t* cost, int n_eta) {
+std::vector<uint8_t> build_tables_uncached(int T, double delta, const chase_profile_t* profs, int n_prof,
+                                           const chase_cost_cfg_t* cost, int n_eta) {
     const int total = tables_bytes(T, n_prof, n_eta);
     std::vector<uint8_t> blob((size_t)total, 0);
     TablesHeader* H = reinterpret_cast<TablesHeader*>(blob.data());
@@ -212,6 +212,62 @@ std::vector<uint8_t> build_tables(int T, double delta, const chase_profile_t* pr
         }
         for (int e = 0; e < n_eta; ++e)
             build_pair_table(P.n_limits, P.avg_power_w, P.throughput_sps, cost->eta[e], T_.pmax, &pr[q * n_eta + e]);
+    }
+    return blob;
+}
+
+// The tables depend only on (T, Delta, the profiles, eta list, MaxPower): a
+// repeated call with the same constants (a latency-bound caller planning one
+// trace at a time, C1/C2) reuses the host-built blob instead of re-running the
+// long-double envelope construction.  Keyed by the full input bytes (no hash
+// collisions); a few entries per thread, least recently used replaced.
+struct TablesCacheEntry {
+    std::vector<uint8_t> key, blob;
+    uint64_t used = 0;
+};
+thread_local std::vector<TablesCacheEntry> g_tables_cache;
+thread_local uint64_t g_tables_tick = 0;
+
+template <typename V>
+void key_put(std::vector<uint8_t>& k, const V* p, size_t n) {
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(p);
+    k.insert(k.end(), b, b + n * sizeof(V));
+}
+
+std::vector<uint8_t> build_tables(int T, double delta, const chase_profile_t* profs, int n_prof,
+                                  const chase_cost_cfg_t* cost, int n_eta) {
+    std::vector<uint8_t> key;
+    key_put(key, &T, 1);
+    key_put(key, &delta, 1);
+    key_put(key, &n_prof, 1);
+    key_put(key, &n_eta, 1);
+    for (int q = 0; q < n_prof; ++q) {
+        key_put(key, &profs[q].n_limits, 1);
+        key_put(key, profs[q].limit_w, (size_t)profs[q].n_limits);
+        key_put(key, profs[q].avg_power_w, (size_t)profs[q].n_limits);
+        key_put(key, profs[q].throughput_sps, (size_t)profs[q].n_limits);
+    }
+    const uint8_t has_cost = cost != nullptr;
+    key_put(key, &has_cost, 1);
+    if (cost) {
+        key_put(key, &cost->max_power_w, 1);
+        if (n_eta > 0) key_put(key, cost->eta, (size_t)n_eta);
+    }
+    ++g_tables_tick;
+    for (TablesCacheEntry& e : g_tables_cache)
+        if (e.key == key) {
+            e.used = g_tables_tick;
+            return e.blob;
+        }
+    std::vector<uint8_t> blob = build_tables_uncached(T, delta, profs, n_prof, cost, n_eta);
+    constexpr size_t kEntries = 8;
+    if (g_tables_cache.size() < kEntries) {
+        g_tables_cache.push_back(TablesCacheEntry{std::move(key), blob, g_tables_tick});
+    } else {
+        TablesCacheEntry* lru = &g_tables_cache[0];
+        for (TablesCacheEntry& e : g_tables_cache)
+            if (e.used < lru->used) lru = &e;
+        *lru = TablesCacheEntry{std::move(key), blob, g_tables_tick};
     }
     return blob;
 }
@@ -700,7 +756,8 @@ static size_t host_slot_bytes(const chase_traces_t* t, int64_t chunk, int n_eta)
 
 size_t chase_sweep_host_staging_bytes(const chase_traces_t* h_traces, int64_t chunk_traces, int32_t n_eta) {
     if (!h_traces || chunk_traces < 1 || n_eta < 1 || n_eta > CHASE_MAX_ETA) return 0;
-    return 2 * host_slot_bytes(h_traces, chunk_traces, n_eta) + round_up((int64_t)n_eta * 64, kWsAlign);
+    return 2 * host_slot_bytes(h_traces, chunk_traces, n_eta) + round_up((int64_t)n_eta * 64, kWsAlign) +
+           round_up((int64_t)sizeof(chase_diag_t), kWsAlign);
 }
 
 chase_status_t chase_sweep_host(const chase_traces_t* h_traces, const chase_forecast_cfg_t* fcfg,
@@ -720,6 +777,9 @@ chase_status_t chase_sweep_host(const chase_traces_t* h_traces, const chase_fore
     const size_t slot = host_slot_bytes(h_traces, chunk_traces, n_eta);
     uint8_t* stg = static_cast<uint8_t*>(d_staging);
     double* acc = reinterpret_cast<double*>(stg + 2 * slot);
+    // diagnostics of the whole call (every chunk's sweep resets the workspace's own)
+    chase_diag_t* dacc = reinterpret_cast<chase_diag_t*>(stg + 2 * slot + round_up((int64_t)n_eta * 64, kWsAlign));
+    chase_diag_t* wdiag = reinterpret_cast<chase_diag_t*>(static_cast<uint8_t*>(d_ws));  // WsLayout.diag == 0
     cudaStream_t s = (cudaStream_t)stream;
     cudaStream_t cs = nullptr;
     cudaEvent_t loaded[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
@@ -759,8 +819,10 @@ chase_status_t chase_sweep_host(const chase_traces_t* h_traces, const chase_fore
                          h_job_samples ? d_job : nullptr, nullptr, 0, nullptr, 0, nullptr, d_sum, nullptr, d_ws,
                          ws_bytes, stream);
         if (st == CHASE_OK) e = launch_accumulate(acc, reinterpret_cast<const double*>(d_sum), n_eta * 8, s);
+        if (st == CHASE_OK && e == cudaSuccess) e = launch_diag_merge(dacc, wdiag, c0, s);
         if (e == cudaSuccess) e = cudaEventRecord(freed[q], s);
     }
+    if (e == cudaSuccess && st == CHASE_OK && n > 0) e = launch_diag_merge(dacc, wdiag, -1, s);
     if (e == cudaSuccess && st == CHASE_OK)
         e = cudaMemcpyAsync(h_sum, acc, (size_t)n_eta * sizeof(chase_sum_t), cudaMemcpyDeviceToHost, s);
     cudaError_t e2 = cudaStreamSynchronize(s);

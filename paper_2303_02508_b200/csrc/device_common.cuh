@@ -160,3 +160,7 @@ __device__ __forceinline__ const ProfileTable* blob_profiles(const uint8_t* blob
     return reinterpret_cast<const ProfileTable*>(blob + H->off_prof);
 }
 
+// Records which sweep kernel ran (chase_diag_t.kernel_path; block 0 only).
+__device__ __forceinline__ void mark_path(chase_diag_t* d, unsigned bit) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(reinterpret_cast<unsigned long long*>(&d->kernel_path), bit);
+}

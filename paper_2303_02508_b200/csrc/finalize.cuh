@@ -146,8 +146,28 @@ __global__ void diag_reset_kernel(chase_diag_t* d) {
     if (threadIdx.x == 0) {
         d->first_bad_trace = -1;  // all ones: atomicMin (unsigned) finds the lowest index
         d->first_bad_status = 0;
-        d->n_bad = d->n_exhausted = d->n_slow_windows = 0;
+        d->n_bad = d->n_exhausted = d->n_slow_windows = d->kernel_path = 0;
     }
+}
+
+// chase_sweep_host: fold one chunk's diagnostics (trace indices local to the
+// chunk, offset by its first trace c0) into the call's accumulated ones; with
+// c0 < 0 copy the accumulated diagnostics back into the workspace.
+__global__ void diag_merge_kernel(chase_diag_t* acc, chase_diag_t* chunk, int64_t c0) {
+    if (threadIdx.x != 0) return;
+    if (c0 < 0) {
+        *chunk = *acc;
+        return;
+    }
+    const uint64_t fb = (uint64_t)chunk->first_bad_trace;
+    if (fb != ~0ull && (uint64_t)(fb + c0) < (uint64_t)acc->first_bad_trace) {
+        acc->first_bad_trace = (int64_t)(fb + c0);
+        acc->first_bad_status = chunk->first_bad_status;
+    }
+    acc->n_bad += chunk->n_bad;
+    acc->n_exhausted += chunk->n_exhausted;
+    acc->n_slow_windows += chunk->n_slow_windows;
+    acc->kernel_path |= chunk->kernel_path;
 }
 
 __global__ void accumulate_sums_kernel(double* acc, const double* add, int n) {

@@ -668,6 +668,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
 #endif
     const __grid_constant__ SweepParams P) {
     constexpr bool PER = PM != 0;
+    mark_path(P.diag, PER ? CHASE_PATH_H_PERIODS : CHASE_PATH_HEADLINE);
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t sbase = smem_u32(sm);
@@ -769,7 +770,10 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         for (int c = 0; c < nc; ++c) {
             const bool last = c == nc - 1;
             uint8_t* stage = stage0;
-            if (store_choice && lane == 0) bulk_wait_read0();  // the previous store has read chb
+            if (store_choice) {
+                if (lane == 0) bulk_wait_read0();  // the previous store has read chb
+                __syncwarp();                      // ... before any lane writes it again
+            }
             if (PM == 2 && c > 0 && status == 0) {
                 // long periods: a new batch is decided while this chunk's load is in flight
                 const int cs = c * kHWarpW, wc = last ? P.W_last : kHWarpW;
@@ -778,7 +782,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     unsigned ns = 0;
                     kb = period_batch(traces + i * P.ld + P.a0 + P.off0, jn, P.W, P.period, P.phase_start, T, A_even,
                                       wl, invK, Kc, e8, ebase, ZB, pt, pf, lane, ns);
-                    if (lane != 0 || jn > jb + 31) n_slow += ns;  // lane 0's period may be the last batch's lane 31
+                    if (jn + lane > jb + 31) n_slow += ns;  // count only periods the last batch did not decide
                     jb = jn;
                 }
             }

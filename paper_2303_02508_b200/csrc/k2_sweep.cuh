@@ -270,6 +270,7 @@ template <int MODE, typename E, bool AL, bool MULTI, bool FIN = false>
 #define CHASE_SWEEP_MINB 2
 #endif
 __global__ void __launch_bounds__(kThreads, CHASE_SWEEP_MINB) sweep_kernel(const __grid_constant__ SweepParams P) {
+    mark_path(P.diag, FIN ? (CHASE_PATH_GENERAL | CHASE_PATH_FC_IN) : CHASE_PATH_GENERAL);
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const WarpLayout WL = make_warp_layout(P.T, P.stage_bytes, P.n_eta);

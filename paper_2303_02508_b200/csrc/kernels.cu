@@ -113,9 +113,39 @@ cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Dynamic shared memory the headline kernel needs for T and n_prof: the layout
+// depends on the CTA's shared-window base, so plan for the worst candidate.
+int headline_smem(int T, int n_prof) {
+    // blob bytes before the pair tables (header, phase, profiles): see make_hlayout
+    const int head_bytes = (int)sizeof(TablesHeader) + ((2 * T * 8) + 15) / 16 * 16 + n_prof * (int)sizeof(ProfileTable);
+    int smem = 0;
+    for (int base = 0; base <= 8192; base += 16) {
+        const int t = make_hlayout(T, head_bytes, n_prof, base).total;
+        smem = t > smem ? t : smem;
+    }
+    return smem;
+}
+
+int max_smem_optin() {
+    static int v = -1;
+    if (v < 0) {
+        int dev = 0, x = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || x <= 0) {
+            cudaGetLastError();
+            x = 232448;  // sm_100: 227 KB per block
+        }
+        v = x;
+    }
+    return v;
+}
+
 bool headline_eligible(int mode, bool f64, bool aligned, const SweepParams& p) {
+    // the per-warp blocks (A tables, stage, staged choices) and the per-profile bucket
+    // entries must fit one CTA's shared memory: large T (e.g. 5-minute data) or many
+    // profiles take the general sweep (forecast-first for decision periods)
     return mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !p.fc_in &&
-           !getenv("CHASE_FORCE_GENERAL");
+           !getenv("CHASE_FORCE_GENERAL") && headline_smem(p.T, p.n_prof) <= max_smem_optin();
 }
 
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s) {
@@ -160,14 +190,7 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
             while (k % 8 != 4) ++k;
             q.kc_last = k > kHChunk ? kHChunk : k;
         }
-        // blob bytes before the pair tables (header, phase, profiles): see make_hlayout
-        const int head_bytes = (int)sizeof(TablesHeader) + ((2 * p.T * 8) + 15) / 16 * 16 +
-                               p.n_prof * (int)sizeof(ProfileTable);
-        int smem = 0;  // the layout depends on the shared-window base: plan for the worst candidate
-        for (int base = 0; base <= 8192; base += 16) {
-            const int t = make_hlayout(p.T, head_bytes, p.n_prof, base).total;
-            smem = t > smem ? t : smem;
-        }
+        const int smem = headline_smem(p.T, p.n_prof);
         q.smem_total = smem;
         // decision periods: long ones (at most 31 per warp chunk) in 32-period batches
         auto kern = p.period <= 1                 ? sweep_fast_kernel<0>
@@ -477,6 +500,14 @@ cudaError_t launch_finalize(const FinalizeParams& p, const int64_t* bad_list, ch
 
 cudaError_t launch_diag_reset(chase_diag_t* diag, cudaStream_t s) {
     diag_reset_kernel<<<1, 32, 0, s>>>(diag);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_diag_merge(chase_diag_t* acc, chase_diag_t* chunk, int64_t c0, cudaStream_t s) {
+    if (c0 == 0) diag_reset_kernel<<<1, 32, 0, s>>>(acc);
+    if (c0 == 0) ++g_launches;
+    diag_merge_kernel<<<1, 32, 0, s>>>(acc, chunk, c0);
     ++g_launches;
     return cudaGetLastError();
 }

@@ -159,6 +159,9 @@ cudaError_t launch_fixup(const uint8_t* status, const int64_t* bad_list, int64_t
                          int64_t ld_c, int64_t W, int n_eta_choice, double* forecast, int64_t ld_f,
                          chase_diag_t* diag, cudaStream_t s);
 cudaError_t launch_diag_reset(chase_diag_t* diag, cudaStream_t s);
+// chase_sweep_host: fold a chunk's diagnostics into acc (c0 = its first trace; c0 == 0 resets
+// acc first); c0 < 0 copies acc back into `chunk` (the workspace's diagnostics)
+cudaError_t launch_diag_merge(chase_diag_t* acc, chase_diag_t* chunk, int64_t c0, cudaStream_t s);
 cudaError_t launch_accumulate(double* acc, const double* add, int n, cudaStream_t s);
 uint64_t kernel_launches();
 

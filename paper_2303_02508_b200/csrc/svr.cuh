@@ -2,14 +2,17 @@
 // P:162; SPEC fit_svr S:140-148), included by kernels.cu inside its
 // anonymous namespace.
 //
-// One thread per trace fits the RBF epsilon-SVR on the L history points with
-// the oracle's algorithm, operation for operation: z-scored features and
-// target (fit-window statistics), the kernel matrix, SMO on the 2n dual
-// variables with second-order working-set selection, the bias from the free
-// variables.  exp() is svr_exp, the same Cody-Waite + degree-13 Horner
-// polynomial as oracle_rbf_exp, so every value is bit-identical.  One thread
-// per window then predicts f(x) = sum_t coef_t K(z_t, z(x)) - rho, in the
-// oracle's summation order, and the sweep plans on those forecasts (FIN).
+// One warp per trace fits the RBF epsilon-SVR on the L history points with
+// the oracle's algorithm (libsvm's, as scikit-learn runs it; DESIGN Q31):
+// z-scored features and target (fit-window statistics), the training kernel
+// matrix rounded to single precision (libsvm's Qfloat cache), SMO on the 2n
+// dual variables with second-order working-set selection, the bias from the
+// free variables.  exp() is svr_exp_neg, this library's own table exp
+// (<= 2 ulp of libm's; the oracle uses libm's), so a training kernel entry
+// equals the oracle's unless the two exps straddle a single-precision rounding
+// boundary (~1e-8 of the entries).  One thread per window (or period) then
+// predicts f(x) = sum_t coef_t K(z_t, z(x)) - rho in double precision (fma);
+// the forecasts agree with the oracle's to ~1e-13, within the 1e-9 bar.
 constexpr int kSvrMaxN = 63;
 
 // Model record per trace (doubles): z[63][3] | coef[63] | mu[4] | sigma[4] | gamma, rho | n, kind, keep0..2
@@ -17,13 +20,13 @@ constexpr int kSvrZ = 0, kSvrCoef = 3 * kSvrMaxN, kSvrMu = kSvrCoef + kSvrMaxN, 
 constexpr int kSvrGamma = kSvrSigma + 4, kSvrRho = kSvrGamma + 1, kSvrN = kSvrRho + 1, kSvrKind = kSvrN + 1;
 constexpr int kSvrKeep = kSvrKind + 1, kSvrIters = kSvrKeep + 3, kSvrDoubles = (kSvrIters + 1 + 1) & ~1;
 
-// oracle_rbf_exp's scalar constants in the constant bank (the fma's take
-// them as c[][] operands): 64/ln2, (ln2/64)_hi, (ln2/64)_lo, 1/5!, 1/4!, 1/3!,
+// The table exp's scalar constants in the constant bank (the fma's take them
+// as c[][] operands): 64/ln2, (ln2/64)_hi, (ln2/64)_lo, 1/5!, 1/4!, 1/3!,
 // 1/2, 1, 1.
 __constant__ double c_svr_exp[9] = {0x1.71547652b82fep+6, 0x1.62e42feep-7, 0x1.a39ef35793c76p-39,
                                     0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.5555555555555p-3,
                                     0.5, 1.0, 1.0};
-// 2^(j/64), the doubles nearest the exact values (as oracle_exp2_64), in global
+// 2^(j/64), the doubles nearest the exact values (this library's own table), in global
 // memory: indexed by data (a constant-bank read would serialise the lanes);
 // the forecast kernel stages them in shared memory.
 __device__ const double g_svr_exp2[64] = {
@@ -45,7 +48,7 @@ __device__ const double g_svr_exp2[64] = {
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
 };
 
-// q * 2^e (t in [0.99, 2)) rounded once: oracle_rbf_exp's ldexp.  For
+// q * 2^e (t in [0.99, 2)) rounded once (ldexp).  For
 // e >= -1021 the product is normal and exact, so e is added to the exponent
 // field (integer pipe); below that (rare) two multiplications, the first
 // exact, the second rounding the exact value once.
@@ -64,8 +67,10 @@ __device__ __noinline__ double svr_exp_rare(unsigned long long v, double t, int 
     return svr_scale2k(t, k >> 6);
 }
 
-// oracle_rbf_exp(-y), operation for operation (fma = one rounding on both
-// sides), with the 2^(j/64) table at `tab` (shared or global memory).  kd
+// exp(-y): kd = 64 e + j the integer nearest 64 y/ln2, Cody-Waite reduction
+// by ln2/64, the degree-5 Taylor polynomial of exp(r) (|r| <= ln2/128) in
+// Horner form (fma), times 2^(j/64) from the table at `tab` (shared or global
+// memory), scaled by 2^e; <= 2 ulp of libm (DESIGN Q31).  kd
 // comes from the 1.5*2^52 shift, whose low word is kd (no F2I), and
 // kd = 64 e + j splits with a mask and a shift.  The common keys, y in
 // [+0, 707], are one unsigned compare of the bit pattern (integer pipe; the
@@ -119,11 +124,13 @@ __device__ __forceinline__ double svr_exp_neg(double y, const double* tab) {
 
 __device__ __forceinline__ double svr_exp(double x) { return svr_exp_neg(-x, g_svr_exp2); }
 
-// oracle rbf(): exp(-gamma * ((d0*d0 + d1*d1) + d2*d2)), each add fused with its product
-__device__ __forceinline__ double svr_rbf(const double* a, const double* b, double gamma) {
+// A training kernel entry: exp(-gamma * ((d0*d0 + d1*d1) + d2*d2)) (the oracle's
+// rbf(), each operation rounded once), stored as libsvm stores it: rounded to
+// single precision (DESIGN Q31).
+__device__ __forceinline__ double svr_rbf_train(const double* a, const double* b, double gamma) {
     const double d0 = __dsub_rn(a[0], b[0]), d1 = __dsub_rn(a[1], b[1]), d2 = __dsub_rn(a[2], b[2]);
-    const double d = __fma_rn(d2, d2, __fma_rn(d1, d1, __dmul_rn(d0, d0)));
-    return svr_exp_neg(__dmul_rn(gamma, d), g_svr_exp2);
+    const double d = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+    return (double)__double2float_rn(svr_exp_neg(__dmul_rn(gamma, d), g_svr_exp2));
 }
 
 struct SvrParams {
@@ -165,9 +172,10 @@ __host__ __device__ inline int svr_smem_doubles(int L) {
 constexpr int kSvrWarps = 4;
 
 // One warp per trace.  Every value is computed with the oracle's operations in
-// the oracle's order; what runs in parallel is only independent work (kernel
-// entries, the elementwise gradient update) and the arg-extremum scans, whose
-// results do not depend on the scan order under the last-index tie rule.
+// the oracle's order (the exp aside, see the top of the file); what runs in
+// parallel is only independent work (kernel entries, the elementwise gradient
+// update) and the arg-extremum scans, whose results do not depend on the scan
+// order under the last-index tie rule.
 // Sequential sums (moments, the bias) run on lane 0.
 template <typename E>
 __global__ void __launch_bounds__(32 * kSvrWarps) svr_fit_kernel(const __grid_constant__ SvrParams p) {
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(32 * kSvrWarps) svr_fit_kernel(const __grid_co
     __syncwarp();
     for (int q = lane; q < n * n; q += 32) {
         const int a = q / n, b = q - a * n;
-        K[q] = svr_rbf(z + 3 * a, z + 3 * b, gamma);
+        K[q] = svr_rbf_train(z + 3 * a, z + 3 * b, gamma);
     }
     for (int t = lane; t < l; t += 32) {
         al[t] = 0.0;
@@ -372,10 +380,12 @@ constexpr int kSvrFcThreads = 128, kSvrFcPer = 8;  // 128 threads x 8 periods pe
 // shared memory once; one thread per period runs the recursive horizon of
 // oracle_plan_trace (prediction k is the lag of prediction k+1, from the last
 // observed value) and writes its mean to every window of the period.  P = 1 is
-// the one-step forecast with the observed lag.  Each prediction is
-// oracle_svr_predict: f = sum_t coef_t K(z_t, zq) (fma, in t order) - rho,
-// mu_y + sigma_y f clamped at 0; two kernel terms are evaluated per loop step
-// (independent exp chains) and accumulated in order.
+// the one-step forecast with the observed lag.  Each prediction follows
+// oracle_svr_predict: f = sum_t coef_t K(z_t, zq) (in t order) - rho,
+// mu_y + sigma_y f clamped at 0, with the squared distance and the sum fused
+// (fma) and this library's exp, so within ~1e-13 of the oracle's (not bit
+// for bit); two kernel terms are evaluated per loop step (independent exp
+// chains) and accumulated in order.
 template <typename E>
 __global__ void __launch_bounds__(kSvrFcThreads) svr_forecast_kernel(const __grid_constant__ SvrParams p) {
     extern __shared__ __align__(16) double vsm[];

@@ -44,6 +44,12 @@ __global__ void __launch_bounds__(128, CHASE_TL_MINB) timeline_kernel(const __gr
     const int64_t i = p.ids ? p.ids[r] : r;
     const int s0 = p.L, W = p.N - p.L, Pp = p.P;
     const int n_per = (W + Pp - 1) / Pp;
+    if (i < 0 || i >= p.n_traces) {  // a trace id outside [0, n_traces): NaN rows (chase.h)
+        double* o = p.rows + r * (int64_t)n_per * 8;
+        for (int64_t q = lane; q < (int64_t)n_per * 8; q += 32) o[q] = CUDART_NAN;
+        if (p.summary && lane < 4) p.summary[r * 4 + lane] = CUDART_NAN;
+        return;
+    }
     int prof = p.profile_id ? (int)p.profile_id[i] : 0;
     if (prof >= p.n_prof) prof = 0;
     const ProfileTable* pf = blob_profiles(p.tables) + prof;
@@ -177,6 +183,10 @@ __global__ void __launch_bounds__(256) period_cost_kernel(const __grid_constant_
     const int j = (int)((t - r * per_row) / p.ld_k);
     const int k = (int)(t - r * per_row - (int64_t)j * p.ld_k);
     const int64_t i = p.ids ? p.ids[r] : r;
+    if (i < 0 || i >= p.n_traces) {  // a trace id outside [0, n_traces): NaN costs (chase.h)
+        p.costs[t] = CUDART_NAN;
+        return;
+    }
     int prof = p.profile_id ? (int)p.profile_id[i] : 0;
     if (prof >= p.n_prof) prof = 0;
     const ProfileTable* pf = blob_profiles(p.tables) + prof;

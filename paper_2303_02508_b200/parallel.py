@@ -36,6 +36,12 @@ def reduce_sums(sums, *, group=None, deterministic: bool = False):
     if not deterministic:
         dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
         return sums
+    if sums.is_cuda and dist.get_backend(group) != "nccl":
+        # gloo gathers host tensors only: gather a host copy, write the result back
+        host = sums.cpu()
+        reduce_sums(host, group=group, deterministic=True)
+        sums.copy_(host)
+        return sums
     parts = [torch.empty_like(sums) for _ in range(world)]
     dist.all_gather(parts, sums.contiguous(), group=group)
     acc = parts[0].clone()

@@ -66,6 +66,38 @@ def assert_parity(g, o, *, exact_totals=True):
     np.testing.assert_allclose(g["sums"], o["sums"], rtol=1e-9, atol=1e-300)
 
 
+def assert_parity_tol(g, o, profiles, etas, *, pid=None, max_ci=0.0, tr=None, L=24, rtol=1e-9):
+    """The tolerance contract (DESIGN Q31): forecasts within rtol
+    (relative; 1e-7 g/kWh absolute near a clamp at 0), choices bit-exact except
+    certified near-ties (at both the GPU's and the oracle's decision value the
+    oracle's top-2 Eq. 6 costs are within 1e-9 relative), per-trace totals of
+    traces with identical choices within 1e-9.  Returns the certified count."""
+    fo, fg = o["forecast"], g["forecast"]
+    nan = np.isnan(fo)
+    assert np.array_equal(np.isnan(fg), nan)
+    np.testing.assert_allclose(fg[~nan], fo[~nan], rtol=rtol, atol=1e-7)
+    gt, ot = g["totals"], o["totals"]
+    assert np.array_equal(gt["status"], ot["status"])
+    certified = 0
+    for e, eta in enumerate(etas):
+        bad = np.argwhere(g["choice"][e] != o["choice"][e])
+        for i, w in bad:
+            p = profiles[0 if pid is None else int(pid[i])]
+            pmax = float(p.limit_w[-1])
+            mc = max_ci if max_ci > 0 else float(np.max(tr[i, :L]))
+            for x in (fg[i, w], fo[i, w]):
+                c = sorted(oracle.cost(eta, p.avg_power_w[k], p.throughput_sps[k], pmax, mc, x) for k in range(p.K))
+                assert c[1] - c[0] <= 1e-9 * abs(c[0]), (e, i, w, x, c[:2])
+            certified += 1
+        same = ~np.any(g["choice"][e] != o["choice"][e], axis=1)
+        assert np.array_equal(gt["completion_window"][e][same], ot["completion_window"][e][same])
+        for f in ("time_s", "energy_j", "carbon_g", "samples", "base_time_s", "base_energy_j", "base_carbon_g"):
+            np.testing.assert_allclose(gt[f][e][same], ot[f][e][same], rtol=1e-9, atol=0)
+    if certified == 0:
+        np.testing.assert_allclose(g["sums"], o["sums"], rtol=1e-9, atol=1e-300)
+    return certified
+
+
 def _first_diff(a, b):
     idx = np.argwhere(a != b)
     if len(idx) == 0:
@@ -676,8 +708,10 @@ def test_period_cost_vectors(P):
     (5, 48, 48 + 504, [0.3], 7, 1800),         # T = 48 (the paper's 30-minute split)
 ])
 def test_svr_forecaster_parity(P, L, N, etas, n, interval):
-    """The SVR fit (SMO on the dual), its forecasts and the plan: forecasts
-    bit-identical to the oracle's, choices and totals exact."""
+    """The SVR fit (SMO on the dual), its forecasts and the plan against the
+    oracle (libsvm's definition: libm exp, single-precision training kernel
+    matrix; DESIGN Q31): forecasts within 1e-9, choices exact up to certified
+    near-ties, totals within 1e-9."""
     prof = [inputs.make_profile("bert", inputs.LIMITS_9)]
     T = 86400 // interval
     tr = inputs.synth_traces_host(n, N, seed=700 + L + P, T=T)
@@ -685,7 +719,7 @@ def test_svr_forecaster_parity(P, L, N, etas, n, interval):
     g = run_sweep(tr, N, prof, etas, J=J, L=L, interval_s=interval, period_steps=P, svr={})
     o = run_oracle(tr, N, prof, etas, J=J, L=L, interval_s=interval, period_steps=P, svr={})
     assert np.all(o["totals"]["status"] == 0)
-    assert_parity(g, o)
+    assert_parity_tol(g, o, prof, etas, tr=tr, L=L)
     # the SVR forecasts differ from the least-squares ones (a different model actually ran)
     lin = run_oracle(tr, N, prof, etas, J=J, L=L, interval_s=interval, period_steps=P)
     assert not np.array_equal(lin["forecast"], o["forecast"])
@@ -696,13 +730,13 @@ def test_svr_forecaster_parity(P, L, N, etas, n, interval):
                                 dict(gamma=60.0), dict(gamma=300.0)])   # RBF entries in exp's subnormal / zero ranges
 def test_svr_hyperparameters_parity(hp):
     """Box constraint, tube width, gamma, tolerance and the iteration cap all
-    reach the device solver unchanged (bit-identical forecasts)."""
+    reach the device solver unchanged (forecasts within 1e-9 of the oracle's)."""
     prof = [inputs.make_profile("resnet50", inputs.LIMITS_9)]
     N, n = 24 + 300, 12
     tr = inputs.synth_traces_host(n, N, seed=91)
     g = run_sweep(tr, N, prof, [0.5], svr=hp)
     o = run_oracle(tr, N, prof, [0.5], svr=hp)
-    assert_parity(g, o)
+    assert_parity_tol(g, o, prof, [0.5], tr=tr)
 
 
 def test_svr_degenerate_and_invalid_traces():
@@ -721,13 +755,48 @@ def test_svr_degenerate_and_invalid_traces():
         g = run_sweep(tr, N, prof, [0.5, 0.9], J=J, dtype=dt, svr={})
         o = run_oracle(tr, N, prof, [0.5, 0.9], J=J, svr={})
         assert list(o["totals"]["status"][0][:5]) == [0, 0, 4, 4, 0]
-        assert_parity(g, o)
+        assert_parity_tol(g, o, prof, [0.5, 0.9], tr=tr)
         assert np.all(g["forecast"][1] == 412.5) and np.all(g["forecast"][4] == 300.0)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_gpu_svr_matches_scikit_learn_at_tight_tolerance(seed):
+    """An external referee that no kernel change can edit: the GPU's
+    SVR forecasts (chase_fit_forecast, tol = 1e-9, one-step with the observed
+    lag) against sklearn.svm.SVR (libsvm) fitted on the same z-scored history,
+    which this test standardises itself with numpy (population sigma, P:162,
+    SPEC S:140-148): within 1e-6 sigma_y, where both sit on the unique optimum
+    of the strictly convex dual."""
+    from sklearn.svm import SVR
+    T, L, N, n = 24, 24 + 8 * seed, 24 + 8 * seed + 200, 6
+    tr = inputs.synth_traces_host(n, N, seed=300 + seed)
+    x = torch.from_numpy(tr).to(DEV)
+    t = cb.make_traces(x, n_steps=N)
+    f = cb.make_fcfg(history_len=L, svr=dict(tol=1e-9, max_iter=1000000))
+    ws = cb.alloc_workspace(cb.workspace_bytes(t, f, 1, 1), DEV)
+    fc = torch.empty((n, N - L), dtype=torch.float64, device=DEV)
+    cb.fit_forecast(t, f, fc, N - L, ws)
+    torch.cuda.synchronize()
+    g = fc.cpu().numpy()
+    ph = np.arange(N) % T
+    S, C = np.sin(2.0 * np.pi * ph / T), np.cos(2.0 * np.pi * ph / T)
+    for i in range(n):
+        c = tr[i, :N].astype(np.float64)
+        X = np.stack([S[1:L], C[1:L], c[:L - 1]], axis=1)     # rows t = 1..L-1: (sin, cos, lag), target c[t]
+        y = c[1:L]
+        mu, sd = X.mean(axis=0), X.std(axis=0)
+        my, sy = y.mean(), y.std()
+        keep = sd > 0
+        Z = (X[:, keep] - mu[keep]) / sd[keep]
+        sk = SVR(kernel="rbf", C=1.0, epsilon=0.1, gamma=1.0 / keep.sum(), tol=1e-9, shrinking=False).fit(Z, (y - my) / sy)
+        Q = np.stack([S[L:N], C[L:N], c[L - 1:N - 1]], axis=1)
+        ref = np.maximum(my + sy * sk.predict((Q[:, keep] - mu[keep]) / sd[keep]), 0.0)
+        assert np.max(np.abs(g[i] - ref)) <= 1e-6 * sy, (i, np.max(np.abs(g[i] - ref)) / sy)
 
 
 def test_svr_fit_forecast_and_mape():
     """chase_fit_forecast and chase_forecast_mape with the SVR forecaster:
-    forecasts bit-identical, MAPE within 1e-9 (Table 1's SVR column)."""
+    forecasts and MAPE within 1e-9 of the oracle's (Table 1's SVR column)."""
     T, L, N, n = 48, 48, 552, 9
     tr = inputs.synth_traces_host(n, N, seed=23, T=T)
     tr[2, 300] = 0.0                            # zero actual: MAPE undefined
@@ -743,7 +812,7 @@ def test_svr_fit_forecast_and_mape():
     torch.cuda.synchronize()
     o = oracle.plan_batch(tr, N=N, L=L, T=T, svr={}, profiles=[inputs.make_profile("bert", inputs.LIMITS_9)],
                           etas=[0.5], delta=1800.0)
-    assert np.array_equal(fc.cpu().numpy(), o["forecast"])
+    np.testing.assert_allclose(fc.cpu().numpy(), o["forecast"], rtol=1e-9, atol=1e-7)
     om, ost, _ = oracle.evaluate_batch(tr, N=N, L=L, T=T, svr={})
     g, gs = mp.cpu().numpy(), st.cpu().numpy()
     assert list(gs) == list(ost) and gs[2] == 8
@@ -811,6 +880,19 @@ def test_full_size_modes_sampled(mode):
                                              thr=p.throughput_sps, etas=w.etas, pmax=float(p.limit_w[-1]),
                                              J=float(Jh[i]), **okw)
         assert st == 0
+        if mode == "svr":   # tolerance contract (DESIGN Q31): forecasts to 1e-9, certified near-ties only
+            np.testing.assert_allclose(fc[q], ofc, rtol=1e-9, atol=1e-7)
+            if not np.array_equal(ch[:, q], och):
+                mc = float(np.max(_host_trace(w, i)[:w.history_len]))
+                for wv in np.argwhere(ch[0, q] != och[0]).ravel():
+                    for xv in (fc[q, wv], ofc[wv]):
+                        c = sorted(oracle.cost(w.etas[0], p.avg_power_w[k], p.throughput_sps[k],
+                                               float(p.limit_w[-1]), mc, xv) for k in range(p.K))
+                        assert c[1] - c[0] <= 1e-9 * c[0], (mode, i, wv)
+                continue
+            for f in ("time_s", "energy_j", "carbon_g", "samples"):
+                np.testing.assert_allclose(per[f][:, q], ot[f], rtol=1e-9, atol=0)
+            continue
         assert np.array_equal(ch[:, q], och), (mode, i)
         if fc is not None:
             assert np.array_equal(fc[q], ofc), (mode, i)

@@ -2,9 +2,11 @@
 PAPER.md:162, :171; SPEC fit_svr S:140-148).
 
 The oracle solves the RBF epsilon-SVR dual by SMO with second-order working
-set selection.  It is pinned against scikit-learn's SVR (libsvm, an
-independent implementation of the same problem), the dual constraints and
-KKT conditions, and the SPEC examples.
+set selection, as libsvm (which scikit-learn runs) defines it: libm
+exp, a single-precision training kernel matrix.  It is pinned against
+scikit-learn's SVR (an independent implementation of the same problem) to
+1e-10 in the dual coefficients, the dual constraints and KKT conditions, and
+the SPEC examples.
 """
 import math
 
@@ -14,33 +16,15 @@ import pytest
 import oracle
 
 
-def test_rbf_exp_against_libm():
-    """oracle_rbf_exp (DESIGN Q31) is within 2 ulp (4.5e-16 relative) of libm
-    exp on [-745, 0]: the table value (1/2 ulp), the degree-5 polynomial on
-    |r| <= ln2/128 (truncation 3.5e-17) and the product's rounding."""
-    xs = np.concatenate([-np.logspace(-14, np.log10(744.0), 40000), [-0.0, 0.0, -1e-300]])
-    worst = 0.0
+def test_rbf_exp_is_libm_exp():
+    """oracle_rbf_exp is the C library's exp (DESIGN Q31): Python's math.exp
+    calls the same libm, so the two agree bit for bit on [-800, 0]; NaN for a
+    positive argument (never a kernel argument)."""
+    xs = np.concatenate([-np.logspace(-14, np.log10(800.0), 20000), [-0.0, 0.0, -1e-300, -745.2, -708.4]])
     for x in xs:
-        ref = math.exp(x)
-        if ref > 1e-300:
-            worst = max(worst, abs(oracle.rbf_exp(x) - ref) / ref)
-    assert worst <= 4.5e-16
+        assert oracle.rbf_exp(float(x)) == math.exp(float(x)), x
     assert oracle.rbf_exp(0.0) == 1.0 and oracle.rbf_exp(-800.0) == 0.0
     assert math.isnan(oracle.rbf_exp(1e-300)) and oracle.rbf_exp(-math.inf) == 0.0
-    # subnormal results (the two-step scaling) within 1/2 ulp of the subnormal grid
-    for x in (-709.0, -720.5, -740.0, -744.9):
-        assert abs(oracle.rbf_exp(x) - math.exp(x)) <= 2.0 ** -1074
-
-
-def test_exp2_table_is_correctly_rounded():
-    """The 64 table values are the doubles nearest 2^(j/64) (60-digit decimal)."""
-    from decimal import Decimal, getcontext
-    getcontext().prec = 60
-    tab = oracle.exp2_table()
-    for j in range(64):
-        exact = Decimal(2) ** (Decimal(j) / Decimal(64))
-        assert tab[j] == float(exact), j          # float(Decimal) rounds to nearest
-        assert abs(Decimal(tab[j]) - exact) <= Decimal(2) ** -53 * exact
 
 
 def _history(seed, T=24, L=24, noise=20.0):
@@ -50,15 +34,16 @@ def _history(seed, T=24, L=24, noise=20.0):
 
 
 @pytest.mark.parametrize("seed", range(6))
-@pytest.mark.parametrize("tol,coef_tol,pred_tol", [(1e-3, None, 1e-2), (1e-9, 2e-5, 1e-6)])
-def test_svr_matches_scikit_learn(seed, tol, coef_tol, pred_tol):
-    """Same standardised data and hyperparameters: predictions agree with
-    sklearn.svm.SVR (libsvm) within the stopping tolerance -- loosely at the
-    default tol = 1e-3 (where the two solvers may stop at different points of
-    the tol-ball: predictions within 10 tol in z-units, dual coefficients not
-    compared), tightly at
-    1e-9, where both sit on the unique optimum of the strictly convex dual and
-    the coefficients agree too."""
+@pytest.mark.parametrize("tol", [1e-3, 1e-9])
+def test_svr_matches_scikit_learn(seed, tol):
+    """Same standardised data and hyperparameters: the dual coefficients and
+    predictions equal sklearn.svm.SVR's (libsvm, an independent implementation)
+    to 1e-10 and 1e-9 sigma_y, at the default tol = 1e-3 and at 1e-9.  The
+    oracle follows libsvm's definition of the problem (DESIGN Q31): libm exp,
+    the training kernel matrix held in single precision (libsvm's Qfloat
+    cache), WSS2 with libsvm's tie rules -- so the two solvers take the same
+    SMO path and stop at the same iterate, not merely in the same tol-ball."""
+    coef_tol, pred_tol = 1e-10, 1e-9
     from sklearn.svm import SVR
     T, L = 24, 24 + 8 * seed
     h = _history(seed, T, L)
@@ -70,8 +55,7 @@ def test_svr_matches_scikit_learn(seed, tol, coef_tol, pred_tol):
     sk = SVR(kernel="rbf", C=1.0, epsilon=0.1, gamma=m.gamma, tol=tol, shrinking=False).fit(Z, u)
     coef = np.zeros(n)
     coef[sk.support_] = sk.dual_coef_[0]
-    if coef_tol is not None:
-        assert np.max(np.abs(coef - np.array(m.coef[:n]))) < coef_tol
+    assert np.max(np.abs(coef - np.array(m.coef[:n]))) < coef_tol
     S, C = oracle.phase_table(T)
     rng = np.random.default_rng(100 + seed)
     for w in range(L, L + 12):
