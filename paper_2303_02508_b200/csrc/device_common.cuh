@@ -130,6 +130,11 @@ __device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
     return v;
 }
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+}
 __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -50,6 +50,10 @@ struct alignas(16) PairTable {
     int32_t k0;            // 1: Kc == 0 (eta == 1) -> y = x; 0: y = x * (1/Kc)
     int32_t n_test;        // entries with a threshold test (diagnostic)
     int32_t n_intervals;   // fast intervals (diagnostic)
+    double y_min;          // a lower bound on every positive finite interval endpoint (before the
+                           // shrink), +inf if none: bounds the error a key computation may make
+                           // (the headline's one-fma key)
+    double reserved;
     uint2 ent[kNB];
 };
 
@@ -60,10 +64,12 @@ struct PairHead {
     double a[kMaxK];
     double kbase;
     int32_t base, k0, n_test, n_intervals;
+    double y_min, reserved;
 };
 static_assert(offsetof(PairTable, ent) == sizeof(PairHead), "PairHead mirrors PairTable's head");
 static_assert(offsetof(PairTable, kbase) == offsetof(PairHead, kbase), "PairHead layout");
 static_assert(offsetof(PairTable, k0) == offsetof(PairHead, k0), "PairHead layout");
+static_assert(offsetof(PairTable, y_min) == offsetof(PairHead, y_min), "PairHead layout");
 
 static_assert(sizeof(TablesHeader) % 16 == 0, "header alignment");
 static_assert(sizeof(ProfileTable) % 16 == 0, "profile alignment");

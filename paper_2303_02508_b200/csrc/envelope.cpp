@@ -14,7 +14,12 @@ namespace {
 using ld = long double;
 
 constexpr ld kDelta = 0x1p-47L;        // 64u: required relative gap to every other line
-constexpr ld kShrink = 0x1p-49L;       // 16u: absorbs the 2 roundings of y = x * (1/Kc)
+// 512u: absorbs the key's error relative to x/Kc.  Two kinds of key use the
+// table: y = fl(x * fl(1/Kc)) (|error| <= 2u relative; plan_kernel, the general
+// sweep) and the headline's one-fma key y = fl(fl(w_l/Kc) c + fl(A/Kc))
+// (|error| <= 6u (|A| + |w_l c|)/Kc, which the kernel keeps below (512-2)u
+// y_min by a per-trace / per-chunk bound on |A| + |w_l c|).
+constexpr ld kShrink = 0x1p-44L;
 constexpr double kYMax = 0x1p900;      // beyond: canonical path (overflow safety)
 constexpr double kYMinK0 = 0x1p-900;   // eta == 1: below -> canonical (x == 0, underflow)
 
@@ -158,6 +163,14 @@ std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const
     }
     std::sort(iv.begin(), iv.end(), [](const FastInterval& a, const FastInterval& b) { return a.lo < b.lo; });
     out->n_intervals = (int)iv.size();
+    // y_min: every positive finite endpoint of a verified (unshrunk) interval is
+    // >= the smallest shrunk endpoint times (1 - 2^-40) (lo = lo_d/(1 + 512u),
+    // hi = hi_d/(1 - 512u))
+    double ymin = INFINITY;
+    for (const FastInterval& f : iv)
+        for (double v : {f.lo, f.hi})
+            if (v > 0 && std::isfinite(v) && v < kYMax) ymin = std::min(ymin, v);
+    out->y_min = std::isfinite(ymin) ? round_down_d((ld)ymin * (1.0L - 0x1p-40L)) : (double)INFINITY;
 
     // Bucket range: the 12-octave window [2^E0, 2^(E0+12)) holding the most
     // interval endpoints (endpoints outside it fall in the clamped end buckets,

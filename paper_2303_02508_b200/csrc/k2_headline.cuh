@@ -27,6 +27,9 @@
 #ifndef CHASE_H_CHUNK
 #define CHASE_H_CHUNK 60
 #endif
+#ifndef CHASE_H0_FAST
+#define CHASE_H0_FAST 0  // 1: the one-fma key in sweep_fast_kernel<0> (measured slower there: the lean kernel uses it)
+#endif
 #ifndef CHASE_H_PAIRSUM
 #define CHASE_H_PAIRSUM 1  // 1: a group's four terms summed pairwise before the running sums
 #endif
@@ -190,6 +193,203 @@ __device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngr
         words[g + 1] = w1;
     }
     if (g < ngroups) words[g] = hot_group(vx, Ax0, Ax1, lag, wl, invK, ent8, ebase, ZB, a);
+}
+
+// ---- the one-fma key ------------------------------------------
+// For a trace whose model and values allow it, the Eq. 6 key is computed as
+//   y = fma(wlK, c[w-1], B[phi]),  B[phi] = fl(A[phi] / Kc-ish) = fl(A[phi] * fl(1/Kc)),
+//                                  wlK = fl(w_lag * fl(1/Kc))
+// (one DFMA instead of DMUL, DADD, DMUL), and the fp32 values become fp64 on
+// the integer pipes.  |y - x/Kc| <= 6u (|A| + |w_lag c|)/Kc for the canonical
+// forecast x = fl(A + fl(w_lag c)) (Q24), which the kernel keeps below
+// (512 - 2)u y_min: the envelope intervals are shrunk by 512u (envelope.cpp),
+// so a key inside a shrunk interval puts x/Kc inside the verified one and the
+// canonical rule picks that line (the same proof as the exact key's, with a
+// wider margin).  The bound holds when |A[phi]| <= Amax and every value lies
+// in [FLT_MIN, c_lim], c_lim = (85 y_min Kc - Amax)/|w_lag|; a chunk with a
+// value outside (a zero, a subnormal, a negative, inf/NaN, or too large) is
+// redone with the exact key (lane_exact, cold).
+
+// Integer multiply-adds, written so that they issue on the FMA pipe (IMAD)
+// rather than the ALU pipe, which the lookup's compares and selects keep busy.
+__device__ __forceinline__ uint32_t imad_hi_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int imad_hi_s32(int a, int b, int c) {
+    int d;
+    asm("mad.hi.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t imad_lo_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// fp32 bits -> fp64 for a positive normal float: exponent rebias and mantissa
+// shift on the FMA pipe (hi = (b >> 3) + 896 << 20 as IMAD.HI, lo = b << 29 as
+// IMAD) instead of F2F.F64.F32, which issues at a third of the fp64 add rate.
+// Exact in that range.
+__device__ __forceinline__ double f32bits_to_f64(uint32_t b) {
+    return __hiloint2double((int)imad_hi_u32(b, 0x20000000u, 0x38000000u), (int)imad_lo_u32(b, 0x20000000u, 0u));
+}
+
+__device__ __forceinline__ uint32_t hot_group_fast(const float4 v, const double2 B01, const double2 B23, double& lag,
+                                                   double wlK, const uint2* __restrict__ ent8, int ebase, uint32_t ZB,
+                                                   double& C, uint32_t& bmax, Acc& a) {
+    const uint32_t vb[4] = {__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w)};
+    // range check of every value: b - bits(FLT_MIN) (IMAD), one unsigned max (wraps below FLT_MIN)
+    bmax = max(max(max(bmax, imad_lo_u32(vb[0], 1u, 0xff800000u)), imad_lo_u32(vb[1], 1u, 0xff800000u)),
+               max(imad_lo_u32(vb[2], 1u, 0xff800000u), imad_lo_u32(vb[3], 1u, 0xff800000u)));
+    const double BB[4] = {B01.x, B01.y, B23.x, B23.y};
+    uint32_t ad[4];
+    double2 ln4[4];
+    double cw4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const double cw = f32bits_to_f64(vb[u]);
+        const int h = __double2hiint(__fma_rn(wlK, lag, BB[u]));  // the key (unclamped forecast / Kc)
+        const int idx = max(min(imad_hi_s32(h, 1 << (32 - kSH), -ebase), kNBUsed - 1), 0);  // (h >> 14) - base
+        ad[u] = line_addr(h, ent8[idx], ZB);
+        ln4[u] = lds_line(ad[u]);  // (Thr_k * Delta, P_k)
+        cw4[u] = cw;
+        lag = cw;
+    }
+    a.S = __dadd_rn(a.S, __dadd_rn(__dadd_rn(ln4[0].x, ln4[1].x), __dadd_rn(ln4[2].x, ln4[3].x)));
+    a.E = __dadd_rn(a.E, __dadd_rn(__dadd_rn(ln4[0].y, ln4[1].y), __dadd_rn(ln4[2].y, ln4[3].y)));
+    // sum P_k c: one fma per window (the products are exact for the dyadic inputs, so
+    // the totals are unchanged there; <= 1e-9 otherwise)
+    C = __fma_rn(ln4[3].y, cw4[3], __fma_rn(ln4[2].y, cw4[2], __fma_rn(ln4[1].y, cw4[1], __fma_rn(ln4[0].y, cw4[0], C))));
+    a.Cs = __dadd_rn(a.Cs, __dadd_rn(__dadd_rn(cw4[0], cw4[1]), __dadd_rn(cw4[2], cw4[3])));
+    const uint32_t word = __byte_perm(__byte_perm(ad[0], ad[1], 0x0051u), __byte_perm(ad[2], ad[3], 0x0051u), 0x5410u);
+    a.slow |= word;
+    return word;
+}
+
+// hot_groups with the one-fma key (Bp: the B table at the lane's phase).  The two
+// register sets also carry two partial sums of P_k c, merged at the end.
+__device__ __forceinline__ void hot_groups_fast(const float* __restrict__ tv, int ngroups, const double* __restrict__ Bp,
+                                                double wlK, const uint2* __restrict__ ent8, int ebase, uint32_t ZB,
+                                                uint32_t* __restrict__ words, uint32_t& bmax, Acc& a) {
+    double lag = (double)tv[-1];
+    float4 vx = *reinterpret_cast<const float4*>(tv);
+    double2 Bx0 = *reinterpret_cast<const double2*>(Bp);
+    double2 Bx1 = *reinterpret_cast<const double2*>(Bp + 2);
+    double C0 = 0.0, C1 = 0.0;
+    int g = 0;
+#pragma unroll 1
+    for (; g + 1 < ngroups; g += 2) {
+        const float4 vy = *reinterpret_cast<const float4*>(tv + 4 * g + 4);
+        const double2 By0 = *reinterpret_cast<const double2*>(Bp + 4 * g + 4);
+        const double2 By1 = *reinterpret_cast<const double2*>(Bp + 4 * g + 6);
+        const uint32_t w0 = hot_group_fast(vx, Bx0, Bx1, lag, wlK, ent8, ebase, ZB, C0, bmax, a);
+        vx = *reinterpret_cast<const float4*>(tv + 4 * g + 8);
+        Bx0 = *reinterpret_cast<const double2*>(Bp + 4 * g + 8);
+        Bx1 = *reinterpret_cast<const double2*>(Bp + 4 * g + 10);
+        const uint32_t w1 = hot_group_fast(vy, By0, By1, lag, wlK, ent8, ebase, ZB, C1, bmax, a);
+        words[g] = w0;
+        words[g + 1] = w1;
+    }
+    if (g < ngroups) words[g] = hot_group_fast(vx, Bx0, Bx1, lag, wlK, ent8, ebase, ZB, C0, bmax, a);
+    a.C = __dadd_rn(a.C, __dadd_rn(C0, C1));
+}
+
+// The last chunk's windows past the lane's full groups, one-fma key (cold).
+__device__ __noinline__ Acc hot_tail_fast(const float* tv, int j_begin, int nwin, const double* Bp, double wlK,
+                                          const uint2* ent8, int ebase, uint32_t ZB, uint8_t* bytes, uint32_t* bmax_out) {
+    Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
+    double lag = (double)tv[j_begin - 1];
+    uint32_t bmax = 0u;
+    for (int jj = j_begin; jj < nwin; ++jj) {
+        const float raw = tv[jj];
+        const uint32_t b = __float_as_uint(raw);
+        bmax = max(bmax, b - 0x00800000u);
+        const double cw = f32bits_to_f64(b);
+        const int h = __double2hiint(__fma_rn(wlK, lag, Bp[jj]));
+        const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+        const uint32_t ad = line_addr(h, ent8[idx], ZB);
+        const uint32_t k = (ad >> 8) & 0xffu;
+        if (k == (uint32_t)kZeroLine) a.slow |= 0x20u;
+        bytes[jj] = (uint8_t)k;
+        const double2 ln = lds_line(ad);
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __fma_rn(ln.y, cw, a.C);
+        a.Cs = __dadd_rn(a.Cs, cw);
+        lag = cw;
+    }
+    *bmax_out = bmax;
+    return a;
+}
+
+// The canonical fold of Eq. 1 at phase phi, A = (c0 + w_s S[phi]) + w_c C[phi]
+// (fit_kernel's record; the same operations as the exact table).
+struct ExactModel {
+    double c0, ws, wc, wl, Kc, invK;
+    const double* phS;
+    const double* phC;
+    __device__ __forceinline__ double A(int phi) const {
+        return __dadd_rn(__dadd_rn(c0, __dmul_rn(ws, phS[phi])), __dmul_rn(wc, phC[phi]));
+    }
+};
+
+// A lane's windows of a chunk redone with the exact key (the trace's one-fma
+// bound does not hold for this chunk, see above): x = fl(A + fl(w_lag c)),
+// y = fl(x * fl(1/Kc)), the envelope lookup, the canonical rule for band
+// windows; every value validated as the generic path does (cold).
+__device__ __noinline__ Acc lane_exact(const float* tv, int nwin, int phi0, int T, const ExactModel& M,
+                                       const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
+                                       const ProfileTable* pf, uint8_t* bytes) {
+    Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
+    double lag = (double)tv[-1];
+    int phi = phi0;
+    for (int jj = 0; jj < nwin; ++jj) {
+        const float raw = tv[jj];
+        const double cw = (double)raw;
+        const double p = __dadd_rn(M.A(phi), __dmul_rn(M.wl, lag));
+        const int h = __double2hiint(__dmul_rn(p, M.invK));
+        const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+        uint32_t k = (line_addr(h, ent8[idx], ZB) >> 8) & 0xffu;
+        if (k == (uint32_t)kZeroLine) {
+            k = canonical_choose(p > 0.0 ? p : 0.0, M.Kc, pt->a, pf->thr, pf->K);
+            ++a.bad_pad;
+        }
+        bytes[jj] = (uint8_t)k;
+        const double2 ln = pf->line[k];
+        a.S = __dadd_rn(a.S, ln.x);
+        a.E = __dadd_rn(a.E, ln.y);
+        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
+        a.Cs = __dadd_rn(a.Cs, cw);
+        a.vmin = fminf(a.vmin, raw);
+        a.bad |= bad_value(raw) ? 1 : 0;
+        lag = cw;
+        phi = phi + 1 == T ? 0 : phi + 1;
+    }
+    return a;
+}
+
+// The deferred (band) windows of a one-fma-key lane: the canonical rule on the
+// exact forecast, as fix_slow does from the exact table.
+__device__ __noinline__ SlowFix fix_slow_exact(const float* tv, int nwin, int phi0, int T, const ExactModel& M,
+                                               const PairTable* pt, const ProfileTable* pf, uint8_t* bytes) {
+    SlowFix r{0.0, 0.0, 0.0, 0};
+    for (int jj = 0; jj < nwin; ++jj) {
+        if (bytes[jj] != (uint8_t)kZeroLine) continue;
+        int phi = phi0 + jj;
+        while (phi >= T) phi -= T;
+        const double x = predict(M.A(phi), M.wl, (double)tv[jj - 1]);
+        const uint32_t k = canonical_choose(x, M.Kc, pt->a, pf->thr, pf->K);
+        bytes[jj] = (uint8_t)k;
+        const double2 ln = pf->line[k];
+        const double cw = (double)tv[jj];
+        r.S = __dadd_rn(r.S, ln.x);
+        r.E = __dadd_rn(r.E, ln.y);
+        r.C = __dadd_rn(r.C, __dmul_rn(ln.y, cw));
+        ++r.n;
+    }
+    return r;
 }
 
 // Windows [j_begin, nwin) of a lane whose count is not a multiple of 4 (the
@@ -764,6 +964,9 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         const ProfileTable* pf = profs;
         const PairTable* pt = reinterpret_cast<const PairTable*>(heads);
         int prof_i = 0;
+        bool fast = false;     // the one-fma key (PM 0)
+        double wlK = 0.0;      // fl(w_lag * fl(1/Kc)) for the one-fma key
+        uint32_t clim_bits = 0u;  // fp32 bits of c_lim: values above take the exact key
         uint32_t k_carry = 0;  // period mode: the decision of the period running into the next chunk
         int jb = 0;            // long periods: first period of the current batch
         uint32_t kb = 0;       // long periods: lane l's decision for period jb + l
@@ -813,13 +1016,35 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
                     const int n_a = haext_len(T);
                     int ph = lane_mod_T;
+                    double amax = 0.0;
                     for (int j = lane; j < n_a; j += 32) {
                         // A(phi) = (c0 + w_sin*S[phi]) + w_cos*C[phi]  (canonical fold of Eq. 1)
                         const int ph1 = ph + 1 == T ? 0 : ph + 1;
                         A_even[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph])), __dmul_rn(wcs, phC[ph]));
                         A_odd[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph1])), __dmul_rn(wcs, phC[ph1]));
+                        amax = fmax(amax, fabs(A_even[j]));
                         ph += 32;
                         while (ph >= T) ph -= T;
+                    }
+                    if constexpr (PM == 0 && CHASE_H0_FAST) {
+                        // the one-fma key's bound: 6u (|A| + |w_lag| c)/Kc <= 510u y_min, i.e.
+                        // |A| + |w_lag| c <= 85 y_min Kc (envelope.cpp shrinks by 512u)
+                        amax = warp_max_d(amax);
+                        const double lam = __dmul_rn(__dmul_rn(85.0, pt->y_min), Kc);
+                        if (!pt->k0 && invK != 0.0 && amax < lam && fabs(wl) <= DBL_MAX) {
+                            const double awl = fabs(wl);
+                            const double cl = awl > 0.0 ? __ddiv_rd(__dsub_rd(lam, amax), awl) : (double)FLT_MAX;
+                            const float clf = cl >= (double)FLT_MAX ? FLT_MAX : __double2float_rd(cl);
+                            if (clf >= FLT_MIN) {
+                                fast = true;
+                                clim_bits = __float_as_uint(clf);
+                                wlK = __dmul_rn(wl, invK);
+                                for (int j = lane; j < n_a; j += 32) {  // B = fl(A * fl(1/Kc)), in place
+                                    A_even[j] = __dmul_rn(A_even[j], invK);
+                                    A_odd[j] = __dmul_rn(A_odd[j], invK);
+                                }
+                            }
+                        }
                     }
                 }
                 __syncwarp();
@@ -880,22 +1105,57 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                         replay_groups(tv, nwin, chb + j0, prof_i, a);
                     }
                 }
-                if (!PER) hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), a);
-                if (!PER && 4 * ngr < nwin) {  // cold: a ragged last chunk, or Kc outside [2^-900, 2^900]
-                    if (invK == 0.0) {
-                        a = fused_generic<true, false, float, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line, chb + j0,
-                                                                    nullptr, Kc, pf);
-                        n_slow += (unsigned)a.bad_pad;
-                    } else {
-                        acc_merge(a, hot_tail(tv, 4 * ngr, nwin, Ap, wl, invK, e8, ebase, ZB, chb + j0));
+                bool redone = false;
+                if constexpr (PM == 0 && CHASE_H0_FAST) {
+                    if (fast) {
+                        // every value's bits b, offset by bits(FLT_MIN): max(b - 0x00800000) (unsigned) <=
+                        // clim_bits - 0x00800000 iff all lie in [FLT_MIN, c_lim]; the lag of the lane's
+                        // first window is in the bound too
+                        uint32_t bmax = __float_as_uint(tv[-1]) - 0x00800000u;
+                        hot_groups_fast(tv, ngr, Ap, wlK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), bmax, a);
+                        if (4 * ngr < nwin) {  // cold: the ragged last chunk
+                            uint32_t mt;
+                            acc_merge(a, hot_tail_fast(tv, 4 * ngr, nwin, Ap, wlK, e8, ebase, ZB, chb + j0, &mt));
+                            bmax = max(bmax, mt);
+                        }
+                        // a value outside [FLT_MIN, c_lim] (zero, subnormal, negative, inf/NaN, too
+                        // large): the chunk is redone with the exact key, which also validates (cold)
+                        if (__any_sync(kFull, bmax > clim_bits - 0x00800000u)) {
+                            const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
+                            const ExactModel M{rec[0], rec[1], rec[2], wl, Kc, invK, phS, phC};
+                            a = lane_exact(tv, nwin, phi0, T, M, e8, ebase, ZB, pt, pf, chb + j0);
+                            n_slow += (unsigned)a.bad_pad;
+                            redone = true;
+                        } else if (a.slow & 0x20202020u) {  // deferred windows: canonical on the exact forecast
+                            const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
+                            const ExactModel M{rec[0], rec[1], rec[2], wl, Kc, invK, phS, phC};
+                            const SlowFix fx = fix_slow_exact(tv, nwin, phi0, T, M, pt, pf, chb + j0);
+                            a.S = __dadd_rn(a.S, fx.S);
+                            a.E = __dadd_rn(a.E, fx.E);
+                            a.C = __dadd_rn(a.C, fx.C);
+                            n_slow += (unsigned)fx.n;
+                        }
+                        redone = true;  // (every case handled)
                     }
                 }
-                if (!PER && (a.slow & 0x20202020u)) {  // deferred windows: the canonical K-way rule
-                    const SlowFix fx = fix_slow<float>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0);
-                    a.S = __dadd_rn(a.S, fx.S);
-                    a.E = __dadd_rn(a.E, fx.E);
-                    a.C = __dadd_rn(a.C, fx.C);
-                    n_slow += (unsigned)fx.n;
+                if (!PER && !redone) {
+                    hot_groups(tv, ngr, Ap, wl, invK, e8, ebase, ZB, reinterpret_cast<uint32_t*>(chb + j0), a);
+                    if (4 * ngr < nwin) {  // cold: a ragged last chunk, or Kc outside [2^-900, 2^900]
+                        if (invK == 0.0) {
+                            a = fused_generic<true, false, float, true>(tv, 0, nwin, Ap, wl, invK, pt, pf->line,
+                                                                        chb + j0, nullptr, Kc, pf);
+                            n_slow += (unsigned)a.bad_pad;
+                        } else {
+                            acc_merge(a, hot_tail(tv, 4 * ngr, nwin, Ap, wl, invK, e8, ebase, ZB, chb + j0));
+                        }
+                    }
+                    if (a.slow & 0x20202020u) {  // deferred windows: the canonical K-way rule
+                        const SlowFix fx = fix_slow<float>(tv, nwin, Ap, wl, Kc, pt, pf, chb + j0);
+                        a.S = __dadd_rn(a.S, fx.S);
+                        a.E = __dadd_rn(a.E, fx.E);
+                        a.C = __dadd_rn(a.C, fx.C);
+                        n_slow += (unsigned)fx.n;
+                    }
                 }
                 // validation: negatives via vmin, NaN/inf via the sum of c
                 const bool bad = __any_sync(kFull, !(a.vmin >= 0.0f) || !(a.Cs <= DBL_MAX) || a.bad);

@@ -335,3 +335,25 @@ def test_headline_smem_limit_falls_back_to_general_kernel():
     g = gpu_plan(tr, N, profs, 0.5, pid=pid, expect=cb.PATH_GENERAL)
     o = oracle_plan(tr, N, profs, 0.5, pid=pid)
     assert_same(g, o)
+
+
+def test_one_fma_key_falls_back_to_exact_key():
+    """The headline's one-fma key holds for values in [FLT_MIN, c_lim] (DESIGN
+    §6.2); chunks holding a zero, a subnormal or a value above c_lim (here
+    1e5-1e7 spikes, far above 85 y_min Kc / |w_lag|) are redone with the exact
+    key.  Choices, totals and statuses must still equal the oracle's."""
+    rng = np.random.default_rng(21)
+    n, N = 96, 24 + 5000
+    tr = inputs.synth_traces_host(n, N, seed=33)
+    for i in range(0, n, 3):
+        w = rng.integers(24, N, 6)
+        tr[i, w[:2]] = 0.0                                   # zeros (valid, S:29)
+        tr[i, w[2]] = np.float32(1e-40)                      # a subnormal (valid)
+        tr[i, w[3:]] = np.float32(rng.choice([1e5, 3e6, 1e7]))  # spikes above c_lim
+    tr[5, 3000] = -1.0                                       # invalid (status 4) inside a redone chunk
+    J = np.full(n, 3600.0 * (N - 24) * float(RESNET.throughput_sps.min()))
+    for eta in (0.5, 0.8):
+        g = gpu_plan(tr, N, [RESNET], eta, J=J)
+        o = oracle_plan(tr, N, [RESNET], eta, J=J)
+        assert o["totals"]["status"][5] == 4
+        assert_same(g, o, exact=False)   # the subnormal's products make the sum order visible
