@@ -256,6 +256,21 @@ def rolling_flops(w: inputs.Workload, R: int) -> float:
     return float(w.n_traces) * (origins * (42 * n + 56) + 6 * w.W)
 
 
+def rolling_fused_flops(w: inputs.Workload, R: int) -> float:
+    """Algorithmic fp64 operations of one roll_fused_kernel launch (DESIGN §6.4,
+    the sliding-moment formulation; an fma counts 2, every add/sub/mul/div 1):
+    per origin the closed-form solve, 62 (the lag moments 6, seven centred
+    moments 21, the two phase-block products 12, s_ll and r_y 8, b_l 1, b_s and
+    b_c 4, the means 4, the intercept 6), plus the moments: a slide of R rows at
+    32 per row (add one row, remove one: 2 x (1 fma + 2 mul + 6 fma)) when
+    R <= 8, else the direct sums of the n = L-1 rows at 16 per row; per window
+    the prediction 6, the Eq. 6 key 1 and the replay sums 5."""
+    n = w.history_len - 1
+    origins = -(-w.W // R)
+    mom = 32.0 * R if R <= 8 else 16.0 * n
+    return float(w.n_traces) * (origins * (62.0 + mom) + 12.0 * w.W)
+
+
 def svr_arg(args):
     """The SVR hyperparameters (the binding's defaults: C 1, eps 0.1, gamma 1/3, tol 1e-3) or None."""
     return {} if getattr(args, "forecaster", "linear") == "svr" else None
@@ -304,6 +319,9 @@ def planner_kernel_name(w: inputs.Workload, R: int = 0, P: int = 0, svr=None) ->
                     "Eq. 6 argmin + replay)")
         return "sweep_kernel<FUSED, FIN> (Eq. 6 argmin + replay on the period decision forecasts)"
     if R > 0:
+        if len(w.etas) == 1 and w.history_len % 4 == 0 and w.history_len <= 64:
+            return ("roll_fused_kernel (rolling refit fused into the sweep: sliding raw moments + closed-form "
+                    "solve per origin, Eq. 6 argmin + replay)")
         return "rolling_forecast_kernel (one thread per (trace, refit origin), oracle_fit's exact fp64 sequence)"
     if len(w.etas) == 1 and w.history_len % 4 == 0:
         return "sweep_fast_kernel (fused predict + Eq. 6 argmin + replay; fp32 traces, one eta)"
@@ -458,7 +476,8 @@ def main_chase(args):
                     "peak_source": peak_src}
     else:
         peak, peak_src = fp64_peak()
-        flops = rolling_flops(w, R)
+        fused = bool(diag.kernel_path & cb.PATH_ROLL_FUSED)
+        flops = rolling_fused_flops(w, R) if fused else rolling_flops(w, R)
         achieved = flops / (kern_ms / 1e3) / 1e12
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "traffic": None, "kernel": planner_kernel_name(w, R),
@@ -569,8 +588,13 @@ def oracle_prefix_check(w, x, pid, J, ns, args, cb, torch, chunk=32768):
     torch.cuda.synchronize()
     path = int(pl.diag().kernel_path)
     t0 = time.perf_counter()
-    ch_bad = tot_bad = 0
+    ch_bad = tot_bad = certified = 0
     first_bad = None
+    # the fused rolling refit (sliding moments) is held to the tolerance contract: a choice may
+    # differ only at a certified near-tie of the oracle's forecast
+    tol = args.refit_stride > 0 and bool(path & cb.PATH_ROLL_FUSED)
+    if tol:
+        chunk = 2048
     for c0 in range(0, ns, chunk):
         m = min(chunk, ns - c0)
         tr = inputs.synth_traces_host(m, w.n_steps, seed=w.seed, mode=w.mode, trace0=c0)
@@ -578,11 +602,28 @@ def oracle_prefix_check(w, x, pid, J, ns, args, cb, torch, chunk=32768):
         o = oracle.plan_batch(tr, N=w.n_steps, L=w.history_len, T=w.T, refit_stride=args.refit_stride,
                               period=args.period_steps, profiles=w.profiles, profile_id=p_h, etas=w.etas,
                               delta=float(w.interval_s), job_samples=J[c0:c0 + m].cpu().numpy(),
-                              want_forecast=False, want_choice=True)
+                              want_forecast=tol, want_choice=True)
         g_ch = res.choice[:, c0:c0 + m, :W].cpu().numpy()
+        if tol:
+            for e, ii, ww in np.argwhere(g_ch != o["choice"]):
+                p = w.profiles[0 if p_h is None else int(p_h[ii])]
+                mc = float(np.max(tr[ii, :w.history_len]))
+                c = sorted(oracle.cost(w.etas[e], p.avg_power_w[k], p.throughput_sps[k], float(p.limit_w[-1]), mc,
+                                       o["forecast"][ii, ww]) for k in range(p.K))
+                if c[1] - c[0] <= 1e-9 * abs(c[0]):
+                    certified += 1
+                    g_ch[e, ii, ww] = o["choice"][e, ii, ww]   # certified: counted, not a mismatch
         bad_rows = np.any(g_ch != o["choice"], axis=2)
         g_tot = res.per_trace[:, c0:c0 + m].cpu().numpy().view(cb.TOTALS_DTYPE).reshape(len(w.etas), m)
-        tb = g_tot.tobytes() != o["totals"].tobytes()
+        if tol:   # totals of the traces whose choices agree, within 1e-9 (rounding order differs)
+            ok_rows = ~np.any(res.choice[:, c0:c0 + m, :W].cpu().numpy() != o["choice"], axis=2)
+            for f in ("time_s", "energy_j", "carbon_g", "samples"):
+                a, b = g_tot[f][ok_rows], o["totals"][f][ok_rows]
+                bad = np.abs(a - b) > 1e-9 * np.maximum(np.abs(b), 1e-300)
+                tot_bad += int(bad.sum())
+            tb = False
+        else:
+            tb = g_tot.tobytes() != o["totals"].tobytes()
         if tb:
             diff = np.any(g_tot.view(np.uint8).reshape(len(w.etas), m, 64) !=
                           o["totals"].view(np.uint8).reshape(len(w.etas), m, 64), axis=2)
@@ -596,9 +637,12 @@ def oracle_prefix_check(w, x, pid, J, ns, args, cb, torch, chunk=32768):
     torch.cuda.empty_cache()
     return {"traces": int(ns), "windows": int(ns) * W * len(w.etas), "traces_with_choice_mismatch": ch_bad,
             "traces_with_totals_mismatch": tot_bad, "first_mismatch_trace": first_bad, "kernel_path": path,
+            "certified_near_ties": certified if tol else None,
             "seconds": round(time.perf_counter() - t0, 1),
-            "what": "the cpu_baseline sample re-planned by chase_sweep (benched config) vs the oracle: "
-                    "choices bit-exact, per-trace totals bit-identical"}
+            "what": ("the cpu_baseline sample re-planned by chase_sweep (benched config) vs the oracle: "
+                     + ("choices exact up to certified near-ties, per-trace totals within 1e-9 (tolerance "
+                        "contract of the fused rolling refit)" if tol else
+                        "choices bit-exact, per-trace totals bit-identical"))}
 
 
 def bench_e2e(args, w, x, pid, J, cb, torch, dist, world, local, dev):

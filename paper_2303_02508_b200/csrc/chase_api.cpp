@@ -712,6 +712,23 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     // decision periods in the headline kernel itself (decided per chunk, then replayed)
     const bool per_inplace = periods(fcfg) && !svr(fcfg) && headline_eligible(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p);
     if (per_inplace) p.period = fcfg->period_steps;
+    // rolling refit fused into the sweep (sliding moments) when no forecast output is asked for
+    if (rolling(fcfg) && !svr(fcfg) && traces->dtype == CHASE_F32 && aligned) {
+        p.refit = fcfg->refit_stride;
+        p.ridge = fcfg->ridge_lambda;
+        p.tol = fcfg->singular_tol;
+        if (roll_fused_eligible(p)) {
+            ev_start(s);
+            e = launch_roll_fused(p, s);
+            ev_stop(s);
+            if (e != cudaSuccess) return cuda_fail(e, "rolling fused kernel");
+            FinalizeParams fz = make_finalize(traces, fcfg->history_len, cost->n_eta, n_profiles, ws, WL, d_profile_id,
+                                              d_job_samples, d_per_trace);
+            e = launch_finalize(fz, p.bad_list, d_sum, d_choice, ld_c, cost->n_eta, d_forecast, ld_f, p.diag, s);
+            if (e != cudaSuccess) return cuda_fail(e, "finalize");
+            return CHASE_OK;
+        }
+    }
     if (fc_first(fcfg) && !per_inplace) {
         // rolling refit / decision periods: forecasts of every window first (into d_forecast when
         // given), then the fused argmin + replay reads them (sweep_kernel<..., FIN>)

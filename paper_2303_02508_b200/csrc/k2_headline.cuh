@@ -341,7 +341,7 @@ struct ExactModel {
 // windows; every value validated as the generic path does (cold).
 __device__ __noinline__ Acc lane_exact(const float* tv, int nwin, int phi0, int T, const ExactModel& M,
                                        const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
-                                       const ProfileTable* pf, uint8_t* bytes) {
+                                       const ProfileTable* pf, uint8_t* bytes, bool canon = false) {
     Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
     double lag = (double)tv[-1];
     int phi = phi0;
@@ -349,9 +349,12 @@ __device__ __noinline__ Acc lane_exact(const float* tv, int nwin, int phi0, int 
         const float raw = tv[jj];
         const double cw = (double)raw;
         const double p = __dadd_rn(M.A(phi), __dmul_rn(M.wl, lag));
-        const int h = __double2hiint(__dmul_rn(p, M.invK));
-        const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
-        uint32_t k = (line_addr(h, ent8[idx], ZB) >> 8) & 0xffu;
+        uint32_t k = kZeroLine;
+        if (!canon) {  // (canon: Kc outside [2^-900, 2^900], every window takes the canonical rule)
+            const int h = __double2hiint(__dmul_rn(p, M.invK));
+            const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
+            k = (line_addr(h, ent8[idx], ZB) >> 8) & 0xffu;
+        }
         if (k == (uint32_t)kZeroLine) {
             k = canonical_choose(p > 0.0 ? p : 0.0, M.Kc, pt->a, pf->thr, pf->K);
             ++a.bad_pad;
@@ -1136,6 +1139,17 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                             n_slow += (unsigned)fx.n;
                         }
                         redone = true;  // (every case handled)
+                    }
+                }
+                if constexpr (PM == 0 && CHASE_H0_FAST == 2) {
+                    // one-fma key only: a trace it does not cover (eta = 1, Kc out of range, a table
+                    // beyond the bound) takes the exact key chunk by chunk (cold)
+                    if (!redone) {
+                        const double* rec = reinterpret_cast<const double*>(stage + P.stage_bytes - kRecBytes);
+                        const ExactModel M{rec[0], rec[1], rec[2], wl, Kc, invK, phS, phC};
+                        a = lane_exact(tv, nwin, phi0, T, M, e8, ebase, ZB, pt, pf, chb + j0, invK == 0.0);
+                        n_slow += (unsigned)a.bad_pad;
+                        redone = true;
                     }
                 }
                 if (!PER && !redone) {

@@ -59,6 +59,8 @@ struct SweepParams {
     int32_t kc_last;              // headline kernel: windows per lane in the last chunk (4 mod 8)
     int32_t smem_total;           // headline kernel: dynamic shared memory planned by the host
     int32_t period;               // > 1: one decision per period of this many windows (headline kernel)
+    int32_t refit;                // roll_fused_kernel: the refit stride R >= 1
+    double ridge, tol;            // roll_fused_kernel: the fit's ridge and singular tolerance (exact fallback)
 };
 
 struct FitParams {
@@ -148,6 +150,10 @@ cudaError_t launch_period_costs(const double* forecast, int64_t ld_f, int64_t n_
 cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
                            int P, const double* phase, const double* records, double* forecast, int64_t ld_f,
                            cudaStream_t s);
+// rolling refit fused into the sweep (k2_roll.cuh): fp32, aligned, one eta, no forecast output, L <= 64,
+// T <= 2048; returns false (nothing launched) when the shape is not covered
+bool roll_fused_eligible(const SweepParams& p);
+cudaError_t launch_roll_fused(const SweepParams& p, cudaStream_t s);
 cudaError_t launch_rolling(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
                            int R, double ridge, double tol, const double* phase, double* ptab, double* records,
                            double max_ci_fixed, double* forecast, int64_t ld_f, cudaStream_t s);
