@@ -7,6 +7,18 @@ constexpr int kRecBytes = kRecDoubles * 8;
 
 thread_local uint64_t g_launches = 0;
 
+// Bounds checks of our own (compute-sanitizer is closed on this pool): a
+// build with -DCHASE_CHECKED=1 (tools/build_variant.sh checked ...) traps on
+// any shared-memory, stage or output index outside its buffer; the default
+// build compiles them away.
+#ifndef CHASE_CHECKED
+#define CHASE_CHECKED 0
+#endif
+#define CHASE_CHECK(cond)                     \
+    do {                                      \
+        if (CHASE_CHECKED && !(cond)) __trap(); \
+    } while (0)
+
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);

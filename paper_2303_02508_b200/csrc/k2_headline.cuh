@@ -136,6 +136,7 @@ __device__ __forceinline__ uint32_t hot_group(const float4 v, const double2 A01,
         const int h = __double2hiint(__dmul_rn(p, invK));
         const int idx = max(min((h >> kSH) - ebase, kNBUsed - 1), 0);
         ad[u] = line_addr(h, ent8[idx], ZB);
+        CHASE_CHECK(ad[u] >= kLineBase && ad[u] + 16 <= kLineBase + kLineRegion);
         ln4[u] = lds_line(ad[u]);  // (Thr_k * Delta, P_k)
         cw4[u] = cw;
         lag = cw;
@@ -253,6 +254,7 @@ __device__ __forceinline__ uint32_t hot_group_fast(const float4 v, const double2
         const int h = __double2hiint(__fma_rn(wlK, lag, BB[u]));  // the key (unclamped forecast / Kc)
         const int idx = max(min(imad_hi_s32(h, 1 << (32 - kSH), -ebase), kNBUsed - 1), 0);  // (h >> 14) - base
         ad[u] = line_addr(h, ent8[idx], ZB);
+        CHASE_CHECK(ad[u] >= kLineBase && ad[u] + 16 <= kLineBase + kLineRegion);
         ln4[u] = lds_line(ad[u]);  // (Thr_k * Delta, P_k)
         cw4[u] = cw;
         lag = cw;
@@ -949,6 +951,8 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         } else {
             mbar_arrive_expect_tx(mbar, bytes);
         }
+        CHASE_CHECK(bytes <= (uint32_t)(P.stage_bytes - kRecBytes) && P.a0 + (int64_t)tc * kHWarpW >= 0 &&
+                    P.a0 + (int64_t)tc * kHWarpW + bytes / 4 <= P.ld);
         bulk_g2s(stage0, traces + ti * P.ld + P.a0 + (int64_t)tc * kHWarpW, bytes, mbar, policy);
     };
     issue(gw, 0);
@@ -1059,6 +1063,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             const int j0 = kc * lane;
             const int nwin = max(0, min(kc, (last ? P.W_last : kHWarpW) - j0));
             const float* tv = reinterpret_cast<const float*>(stage) + P.off0 + j0;  // tv[jj] = c[s0 + c*kHWarpW + j0 + jj]
+            CHASE_CHECK(j0 + nwin <= kHWarpW && P.off0 + j0 + nwin + 4 <= (P.stage_bytes - kRecBytes) / 4);
             int phi0 = phase_c + (last ? lph_last : lph_full);
             if (phi0 >= T) phi0 -= T;
             const double* Ap = (phi0 & 1) ? A_odd + (phi0 - 1) : A_even + phi0;

@@ -44,8 +44,9 @@ constexpr int kRChunk = 32 * kRRun;       // 1024 windows per chunk
 constexpr int kRMaxL = 64;                // history lengths the fused kernel takes (L <= 64)
 constexpr int kRHalo = kRMaxL + 32;       // values before the chunk kept in the slot (L + R - 1 <= 96 for R <= 33)
 constexpr int kRSlotF = kRHalo + kRChunk; // floats per slot
-constexpr int kRPhase = 10;               // per-origin-phase table: Ss, Sc, i11, i12, i22, ok, S[rho], C[rho],
-                                          // S[rho - n], C[rho - n] (the window's own phase and the leaving row's)
+constexpr int kRPhase = 12;               // per-origin-phase table: Ss, Sc, i11, i12, i22, ok, S[rho], C[rho],
+                                          // S[rho - n], C[rho - n] (the window's own phase and the leaving row's),
+                                          // mu_s = Ss/n, mu_c = Sc/n
 
 struct RLayout {
     int tables, ptab, warp_bytes, total;
@@ -78,6 +79,7 @@ struct RVals {
     const float* row;    // the trace row in HBM
     int a0, a1;          // [a0, a1): absolute indices held by the slot
     __device__ __forceinline__ double operator()(int a) const {
+        CHASE_CHECK(a >= 0);
         return (double)(a >= a0 && a < a1 ? sb[a - a0] : __ldg(row + a));
     }
 };
@@ -206,16 +208,16 @@ __device__ __forceinline__ bool mom_solve_fast(const RMom& m, double cy_last, do
     const double bl = __dmul_rn(ry, rcp_nr2(sll));
     const double bs = __fma_rn(-bl, q1, u1), bc = __fma_rn(-bl, q2, u2);
     const double mu_y = __dmul_rn(m.Sy, inv_n), mu_l = __dmul_rn(Sl, inv_n);
-    md.a = __fma_rn(-bl, mu_l, __fma_rn(-bc, __dmul_rn(Sc, inv_n), __fma_rn(-bs, __dmul_rn(Ss, inv_n), mu_y)));
+    md.a = __fma_rn(-bl, mu_l, __fma_rn(-bc, pt[11], __fma_rn(-bs, pt[10], mu_y)));  // pt[10..11]: mu_s, mu_c
     md.bs = bs;
     md.bc = bc;
     md.bl = bl;
     md.exact = false;
     md.status = 0;
-    // near-degenerate (the oracle's F2 / zero-variance / ridge branches) or non-finite: the exact path
-    return Dyy > __dmul_rn(1e-10, __dmul_rn(dn, m.Syy)) && Dll > __dmul_rn(1e-10, __dmul_rn(dn, Sll)) &&
-           sll > __dmul_rn(1e-8, Dll) && fabs(md.a) <= DBL_MAX && fabs(bl) <= DBL_MAX && fabs(bs) <= DBL_MAX &&
-           fabs(bc) <= DBL_MAX;
+    // near-degenerate (the oracle's F2 / zero-variance / ridge branches): the exact path.  A
+    // non-finite value makes the trace invalid whatever its forecasts.
+    const double tn = __dmul_rn(1e-10, dn);
+    return Dyy > __dmul_rn(tn, m.Syy) && Dll > __dmul_rn(tn, Sll) && sll > __dmul_rn(1e-8, Dll);
 }
 
 // One row in and one out of the moments, values from the slot (R = 1 path):
@@ -279,6 +281,8 @@ __device__ void roll_phase_table(const double* S, const double* C, int T, int n,
         o[7] = C[rho];
         o[8] = S[pl];
         o[9] = C[pl];
+        o[10] = __dmul_rn(Ss, 1.0 / dn);
+        o[11] = __dmul_rn(Sc, 1.0 / dn);
     }
 }
 

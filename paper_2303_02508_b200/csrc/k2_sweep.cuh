@@ -328,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, CHASE_SWEEP_MINB) sweep_kernel(const
         } else {
             mbar_arrive_expect_tx(&mbar[st], bytes);
         }
+        CHASE_CHECK(bytes + (P.stage_bytes > kRecBytes ? kRecBytes : 0) <= (uint32_t)P.stage_bytes);
         bulk_g2s(dst, psrc, bytes, &mbar[st], policy);
         ctx->issued = issued + 1;
         if (pc + 1 == nc) {

@@ -37,6 +37,7 @@ namespace {
 #include "k2_headline.cuh"
 #include "k2_lean.cuh"
 #include "k2_roll.cuh"
+#include "k2_roll_lane.cuh"
 #include "finalize.cuh"
 #include "rolling.cuh"
 #include "mape.cuh"
@@ -276,6 +277,23 @@ bool roll_fused_eligible(const SweepParams& p) {
 
 cudaError_t launch_roll_fused(const SweepParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
+    if (!getenv("CHASE_ROLL_RUNS") && make_rllayout(p.T, p.L, p.tables_bytes).total <= max_smem_optin()) {
+        // lane = trace (k2_roll_lane.cuh), the default where its tiles fit
+        const int smem = make_rllayout(p.T, p.L, p.tables_bytes).total;
+        auto kern = p.refit == 1 ? roll_lane_kernel<true> : roll_lane_kernel<false>;
+        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (err != cudaSuccess) return err;
+        int per_sm = 0;
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRLThreads, smem);
+        if (err != cudaSuccess) return err;
+        if (per_sm < 1) return cudaErrorInvalidConfiguration;
+        int64_t grid = (int64_t)num_sms() * per_sm;
+        const int64_t need = ((p.n_traces + 31) / 32 + kRLWarps - 1) / kRLWarps;
+        if (grid > need) grid = need;
+        kern<<<(unsigned)grid, kRLThreads, smem, s>>>(p);
+        ++g_launches;
+        return cudaGetLastError();
+    }
     const int smem = make_rlayout(p.T, p.tables_bytes).total;
     cudaError_t err = cudaFuncSetAttribute(roll_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
