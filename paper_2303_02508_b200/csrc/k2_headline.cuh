@@ -28,7 +28,7 @@
 #define CHASE_H_CHUNK 60
 #endif
 #ifndef CHASE_H0_FAST
-#define CHASE_H0_FAST 0  // 1: the one-fma key in sweep_fast_kernel<0> (measured slower there: the lean kernel uses it)
+#define CHASE_H0_FAST 0  // 1 / 2: the one-fma key in sweep_fast_kernel<0> (measured slower: 12.5 / 11.9 vs 11.0 ms)
 #endif
 #ifndef CHASE_H_PAIRSUM
 #define CHASE_H_PAIRSUM 1  // 1: a group's four terms summed pairwise before the running sums

@@ -1,7 +1,7 @@
 // k2_roll.cuh — the rolling refit fused into the sweep (SURVEY §8(a) a3,
 // §8(c) tolerance contract): refit_stride R >= 1, fp32 traces
 // with an aligned job start, one eta, no forecast output.  Included by
-// kernels.cu inside its anonymous namespace (after k2_lean.cuh).
+// kernels.cu inside its anonymous namespace.
 //
 // Window w is forecast by the least-squares model fitted on the L points
 // before its origin r = s0 + R floor((w - s0)/R) (P:67 applied at every
@@ -29,7 +29,47 @@
 // that carries the chunk's history halo; each lane computes its run's first
 // origin's moments directly (L-1 rows), then slides.  Eq. 6 by the envelope
 // table (canonical rule in a band), replay sums per lane, completion and
-// baseline as the headline kernels (k2_lean.cuh helpers).
+// baseline as the headline kernels .
+
+// The completion walk of a run of windows in window order, 32 at a time per
+// round (lane = window), from the samples done before the run: the window
+// where the samples reach J, its fraction f and the sums before it.  Cold,
+// once per trace.
+struct LCompletion {
+    double f, Ep, Cp, Pk, cw;
+    int w;       // completion window within the slot, -1: none
+};
+__device__ __noinline__ LCompletion run_completion(const float* sv, const uint8_t* crow, int nwin, double before,
+                                                    double J, const ProfileTable* pf, int lane) {
+    LCompletion r{1.0, 0.0, 0.0, 0.0, 0.0, -1};
+    double carry = before;
+    for (int r0 = 0; r0 < nwin; r0 += 32) {
+        const int j = r0 + lane;
+        const bool valid = j < nwin;
+        const uint32_t k = valid ? crow[j] : 0u;
+        const double2 ln = valid ? pf->line[k] : make_double2(0.0, 0.0);
+        const double cw = valid ? (double)sv[j] : 0.0;
+        const double incl = __dadd_rn(carry, warp_incl_scan(ln.x, lane));
+        const double prev = __shfl_up_sync(kFull, incl, 1);
+        const double before_w = lane == 0 ? carry : prev;
+        const unsigned hits = __ballot_sync(kFull, valid && incl >= J);
+        const int wl_ = hits ? __ffs(hits) - 1 : 32;
+        const bool pre = valid && lane < wl_;
+        r.Ep = __dadd_rn(r.Ep, warp_sum(pre ? ln.y : 0.0));
+        r.Cp = __dadd_rn(r.Cp, warp_sum(pre ? __dmul_rn(ln.y, cw) : 0.0));
+        if (wl_ < 32) {
+            const double bw = __shfl_sync(kFull, before_w, wl_);
+            const double sk = __shfl_sync(kFull, ln.x, wl_);
+            r.w = r0 + wl_;
+            r.f = __ddiv_rn(__dsub_rn(J, bw), sk);  // pro-rata last window
+            r.Pk = __shfl_sync(kFull, ln.y, wl_);
+            r.cw = __shfl_sync(kFull, cw, wl_);
+            return r;
+        }
+        carry = __shfl_sync(kFull, incl, 31);
+    }
+    return r;
+}
 
 #ifndef CHASE_R_WARPS
 #define CHASE_R_WARPS 8
@@ -572,7 +612,7 @@ __global__ void __launch_bounds__(kRThreads, CHASE_R_MINB) roll_fused_kernel(con
                         const double Eb = warp_sum(full ? __dadd_rn(El, aE) : El);
                         const double Cb = warp_sum(full ? __dadd_rn(Cl, aC) : Cl);
                         const int nsrc = max(0, min(kRRun, nw - kRRun * src));
-                        const LCompletion cp = lean_completion(sb + (s0 + cs + kRRun * src - a0), chb + kRRun * src,
+                        const LCompletion cp = run_completion(sb + (s0 + cs + kRRun * src - a0), chb + kRRun * src,
                                                                nsrc, __shfl_sync(kFull, before, src), J, pf, lane);
                         if (cp.w >= 0 && lane == 0) {
                             double* o = P.raw + i * kRawDoubles;

@@ -35,7 +35,6 @@ namespace {
 #include "fit.cuh"
 #include "k2_sweep.cuh"
 #include "k2_headline.cuh"
-#include "k2_lean.cuh"
 #include "k2_roll.cuh"
 #include "k2_roll_lane.cuh"
 #include "finalize.cuh"
@@ -143,23 +142,6 @@ int max_smem_optin() {
     return v;
 }
 
-int lean_smem(int T, int n_prof) {
-    const int head_bytes = (int)sizeof(TablesHeader) + ((2 * T * 8) + 15) / 16 * 16 + n_prof * (int)sizeof(ProfileTable);
-    int smem = 0;
-    for (int base = 0; base <= 8192; base += 16) {
-        const int t = make_llayout(T, head_bytes, n_prof, base).total;
-        smem = t > smem ? t : smem;
-    }
-    return smem;
-}
-
-// The lean headline kernel (k2_lean.cuh): one decision per window, and the B
-// table's LDS.128 reads need every lane's phase even (T even, phase0 + L even).
-bool lean_eligible(const SweepParams& p) {
-    return p.period <= 1 && p.T % 2 == 0 && (p.phase0 + p.L) % 2 == 0 && getenv("CHASE_LEAN") &&
-           lean_smem(p.T, p.n_prof) <= max_smem_optin();
-}
-
 bool headline_eligible(int mode, bool f64, bool aligned, const SweepParams& p) {
     // the per-warp blocks (A tables, stage, staged choices) and the per-profile bucket
     // entries must fit one CTA's shared memory: large T (e.g. 5-minute data) or many
@@ -188,22 +170,6 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
                                   : launch_sweep_t<MODE_FUSED, float, false, true, true>(p, s);
         return aligned ? launch_sweep_t<MODE_FUSED, float, true, false, true>(p, s)
                        : launch_sweep_t<MODE_FUSED, float, false, false, true>(p, s);
-    }
-    if (headline_eligible(mode, f64, aligned, p) && lean_eligible(p)) {
-        SweepParams q = p;
-        q.smem_total = lean_smem(p.T, p.n_prof);
-        cudaError_t err = cudaFuncSetAttribute(lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, q.smem_total);
-        if (err != cudaSuccess) return err;
-        int per_sm = 0;
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lean_kernel, kLThreads, q.smem_total);
-        if (err != cudaSuccess) return err;
-        if (per_sm < 1) return cudaErrorInvalidConfiguration;
-        int64_t grid = (int64_t)num_sms() * per_sm;
-        const int64_t need = (p.n_traces + kLWarps - 1) / kLWarps;
-        if (grid > need) grid = need;
-        lean_kernel<<<(unsigned)grid, kLThreads, q.smem_total, s>>>(q);
-        ++g_launches;
-        return cudaGetLastError();
     }
     if (headline_eligible(mode, f64, aligned, p)) {
         // the headline shape: lean specialised kernel (k2_headline.cuh), with its own chunk geometry
