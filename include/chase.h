@@ -165,7 +165,10 @@ typedef struct {
                                     canonical K-way Eq. 6 path (§8(a) a5)      */
     uint64_t kernel_path;        /* which sweep kernels the call ran (bits):
                                     CHASE_PATH_*, for tests and the bench      */
-    uint64_t reserved2[2];
+    uint64_t n_seq_periods;      /* decision periods (headline kernel) whose
+                                    horizon ran step by step because the
+                                    closed form declined         */
+    uint64_t reserved2;
 } chase_diag_t;
 
 #define CHASE_PATH_HEADLINE   1u   /* sweep_fast_kernel<0>: fp32, aligned, one eta, no forecast output */

@@ -57,7 +57,7 @@ class CostCfg(ctypes.Structure):
 class Diag(ctypes.Structure):
     _fields_ = [("first_bad_trace", i64), ("first_bad_status", i32), ("reserved", i32), ("n_bad", ctypes.c_uint64),
                 ("n_exhausted", ctypes.c_uint64), ("n_slow_windows", ctypes.c_uint64),
-                ("kernel_path", ctypes.c_uint64), ("reserved2", ctypes.c_uint64 * 2)]
+                ("kernel_path", ctypes.c_uint64), ("n_seq_periods", ctypes.c_uint64), ("reserved2", ctypes.c_uint64)]
 
 
 # chase_diag_t.kernel_path bits (include/chase.h CHASE_PATH_*)

@@ -14,12 +14,15 @@ namespace {
 using ld = long double;
 
 constexpr ld kDelta = 0x1p-47L;        // 64u: required relative gap to every other line
-// 512u: absorbs the key's error relative to x/Kc.  Two kinds of key use the
-// table: y = fl(x * fl(1/Kc)) (|error| <= 2u relative; plan_kernel, the general
-// sweep) and the headline's one-fma key y = fl(fl(w_l/Kc) c + fl(A/Kc))
-// (|error| <= 6u (|A| + |w_l c|)/Kc, which the kernel keeps below (512-2)u
-// y_min by a per-trace / per-chunk bound on |A| + |w_l c|).
-constexpr ld kShrink = 0x1p-44L;
+// s = 2^-36 (131072u, 1.5e-11 relative): absorbs a key's error relative to
+// x/Kc.  A key y inside a shrunk interval is at least y s/(1+s) from the
+// verified interval's ends.  The kernels' keys: y = fl(x * fl(1/Kc)) of the
+// canonical forecast x (|error| <= 2u relative; the headline, plan_kernel, the
+// general sweep), and the decision periods' closed-form horizon mean (error
+// kept below 120000u of the mean per period).  The bands this
+// leaves around each breakpoint are far inside the hi32 test's own
+// granularity (2^-20).
+constexpr ld kShrink = 0x1p-36L;
 constexpr double kYMax = 0x1p900;      // beyond: canonical path (overflow safety)
 constexpr double kYMinK0 = 0x1p-900;   // eta == 1: below -> canonical (x == 0, underflow)
 
@@ -164,13 +167,13 @@ std::vector<FastInterval> build_pair_table(int K, const double* avg_power, const
     std::sort(iv.begin(), iv.end(), [](const FastInterval& a, const FastInterval& b) { return a.lo < b.lo; });
     out->n_intervals = (int)iv.size();
     // y_min: every positive finite endpoint of a verified (unshrunk) interval is
-    // >= the smallest shrunk endpoint times (1 - 2^-40) (lo = lo_d/(1 + 512u),
-    // hi = hi_d/(1 - 512u))
+    // >= the smallest shrunk endpoint times (1 - 2^-35) (lo = lo_d/(1 + s),
+    // hi = hi_d/(1 - s))
     double ymin = INFINITY;
     for (const FastInterval& f : iv)
         for (double v : {f.lo, f.hi})
             if (v > 0 && std::isfinite(v) && v < kYMax) ymin = std::min(ymin, v);
-    out->y_min = std::isfinite(ymin) ? round_down_d((ld)ymin * (1.0L - 0x1p-40L)) : (double)INFINITY;
+    out->y_min = std::isfinite(ymin) ? round_down_d((ld)ymin * (1.0L - 0x1p-35L)) : (double)INFINITY;
 
     // Bucket range: the 12-octave window [2^E0, 2^(E0+12)) holding the most
     // interval endpoints (endpoints outside it fall in the clamped end buckets,

@@ -146,7 +146,7 @@ __global__ void diag_reset_kernel(chase_diag_t* d) {
     if (threadIdx.x == 0) {
         d->first_bad_trace = -1;  // all ones: atomicMin (unsigned) finds the lowest index
         d->first_bad_status = 0;
-        d->n_bad = d->n_exhausted = d->n_slow_windows = d->kernel_path = 0;
+        d->n_bad = d->n_exhausted = d->n_slow_windows = d->kernel_path = d->n_seq_periods = 0;
     }
 }
 
@@ -167,6 +167,7 @@ __global__ void diag_merge_kernel(chase_diag_t* acc, chase_diag_t* chunk, int64_
     acc->n_bad += chunk->n_bad;
     acc->n_exhausted += chunk->n_exhausted;
     acc->n_slow_windows += chunk->n_slow_windows;
+    acc->n_seq_periods += chunk->n_seq_periods;
     acc->kernel_path |= chunk->kernel_path;
 }
 

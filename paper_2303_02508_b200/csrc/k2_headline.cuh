@@ -30,6 +30,9 @@
 #ifndef CHASE_H0_FAST
 #define CHASE_H0_FAST 0  // 1 / 2: the one-fma key in sweep_fast_kernel<0> (measured slower: 12.5 / 11.9 vs 11.0 ms)
 #endif
+#ifndef CHASE_H_CFMA
+#define CHASE_H_CFMA 1  // 1: the group's sum of P_k c as an fma chain (C5: 11.23 -> 11.13 ms; exact for dyadic inputs)
+#endif
 #ifndef CHASE_H_PAIRSUM
 #define CHASE_H_PAIRSUM 1  // 1: a group's four terms summed pairwise before the running sums
 #endif
@@ -58,7 +61,7 @@ __host__ __device__ inline int hstage_bytes() { return round16((kHWarpW + 8) * 4
 struct HLayout {
     int tables, heads, ent8, lph, lines, warp_bytes, total;
     int n_before, after0;        // warp w's block: w < n_before ? w * warp_bytes : after0 + (w - n_before) * warp_bytes
-    int aext, stage, chb, mbar;  // offsets inside a warp block
+    int aext, k0, stage, chb, mbar;  // offsets inside a warp block
     __host__ __device__ int warp_off(int w) const {
         return w < n_before ? w * warp_bytes : after0 + (w - n_before) * warp_bytes;
     }
@@ -78,10 +81,11 @@ struct HAlloc {
     }
 };
 
-__host__ __device__ inline HLayout make_hlayout(int T, int head_bytes, int n_prof, int base) {
+__host__ __device__ inline HLayout make_hlayout(int T, int head_bytes, int n_prof, int base, int k0len) {
     HLayout L;
     L.aext = 0;
-    L.stage = 2 * round16(haext_len(T) * 8);
+    L.k0 = 2 * round16(haext_len(T) * 8);
+    L.stage = L.k0 + round16(k0len * 8);
     L.chb = L.stage + kHStages * hstage_bytes();
     L.mbar = L.chb + kHWarpW;
     L.warp_bytes = (L.mbar + 8 * kHStages + 127) & ~127;
@@ -143,8 +147,13 @@ __device__ __forceinline__ uint32_t hot_group(const float4 v, const double2 A01,
     }
     a.S = __dadd_rn(a.S, __dadd_rn(__dadd_rn(ln4[0].x, ln4[1].x), __dadd_rn(ln4[2].x, ln4[3].x)));
     a.E = __dadd_rn(a.E, __dadd_rn(__dadd_rn(ln4[0].y, ln4[1].y), __dadd_rn(ln4[2].y, ln4[3].y)));
+#if CHASE_H_CFMA
+    // sum P_k c as an fma chain (exact for the dyadic inputs: every product is exact)
+    a.C = __fma_rn(ln4[3].y, cw4[3], __fma_rn(ln4[2].y, cw4[2], __fma_rn(ln4[1].y, cw4[1], __fma_rn(ln4[0].y, cw4[0], a.C))));
+#else
     a.C = __dadd_rn(a.C, __dadd_rn(__dadd_rn(__dmul_rn(ln4[0].y, cw4[0]), __dmul_rn(ln4[1].y, cw4[1])),
                                    __dadd_rn(__dmul_rn(ln4[2].y, cw4[2]), __dmul_rn(ln4[3].y, cw4[3]))));
+#endif
     a.Cs = __dadd_rn(a.Cs, __dadd_rn(__dadd_rn(cw4[0], cw4[1]), __dadd_rn(cw4[2], cw4[3])));
 #else
 #pragma unroll
@@ -448,6 +457,95 @@ __device__ __forceinline__ void fill_bytes(uint8_t* chb, int a, int e, uint32_t 
     while (a < e) chb[a++] = (uint8_t)k;
 }
 
+// Closed-form horizon mean.  Write Z_k(phi) for the horizon of
+// Eq. 1 run from x0 = 0 without the clamp.  For |w_lag| <= 0.99 the unclamped
+// forecasts of a period starting at phase phi are Z_k + w_lag^k x0, and when
+// all of them are >= 0 the clamp never acts, so the n = P forecasts sum to
+//     K0[phi] + h x0,   K0[phi] = sum_k Z_k(phi),  h = sum_{k=1..P} w_lag^k.
+// That holds for x0 in [lo[phi], hi[phi]]: each step k with computed Z^_k
+// below marg = 4u A_max/(1 - |w_lag|)^2 (their error bound) gives a lower
+// (w_lag^k > 0) or an upper (w_lag^k < 0) limit on x0.  Against the oracle's
+// sequential, clamped sum/P the closed-form mean m then differs by at most
+// kappa X, X = A_max/(1 - |w_lag|) + x0 (a bound on every forecast), kappa =
+// 3u (2/(1 - |w_lag|) + P): the clamp is 1-Lipschitz, the recursion's errors
+// shrink by |w_lag| per step, the running sum's grow with P.
+// The envelope's fast intervals are shrunk by s = 2^-36 (envelope.cpp), so a
+// key y' inside one is at least y' s/(1+s) from the verified interval's ends:
+// with kappa X <= 120000u m (x0 - r m <= -A_b, r = 40000/(2/(1 - |w_lag|) + P))
+// the oracle's mean lies in the verified interval and the canonical rule on it
+// picks the same line.  K2[j] = {K0, (fp32 lo, fp32 hi)} for phase j mod T,
+// j < n_a = haext_len(T) (phase index without wrap, like the A table);
+// K2[n_a] = {h, -r}, K2[n_a + 1].x = -A_b (r = NaN: never).
+__device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, int n_a, int Pp, int phase_start,
+                                       double wl, double invK, double amax, int lane) {
+    __syncwarp();  // the A table, written by every lane
+    amax = warp_max_d(amax);
+    const double aw = fabs(wl);
+    const bool ok = aw <= 0.99 && amax <= DBL_MAX && invK != 0.0;
+    const double inv = ok ? __ddiv_ru(1.0, __dsub_rd(1.0, aw)) : 1.0;  // >= 1/(1 - |w_lag|)
+    const double marg = __dmul_ru(__dmul_ru(0x1p-51, amax), __dmul_ru(inv, inv));
+    int g = Pp, t = T;  // period starts are phase_start + j P (mod T): one class mod gcd(P, T)
+    while (t) {
+        const int r = g % t;
+        g = t;
+        t = r;
+    }
+    const int nph = T / g;
+    double h = 0.0;  // lane 0: h = sum_k w^k, accumulated beside its first horizon
+    for (int j = lane; j < nph; j += 32) {
+        int p = (int)(((int64_t)phase_start + (int64_t)j * g) % T);
+        const int phi = p;
+        double x = 0.0, sum = 0.0, wk = 1.0, lo = 0.0, hi = INFINITY, hs = 0.0;
+#pragma unroll 1
+        for (int k = 0; k < Pp; ++k) {
+            x = __dadd_rn(Aeven[p], __dmul_rn(wl, x));
+            sum = __dadd_rn(sum, x);
+            wk = __dmul_rn(wk, wl);
+            hs = __dadd_rn(hs, wk);
+            if (x < marg) {  // x0 w^k must lift step k clear of the clamp (w^k: k roundings, 2^-40 covers them)
+                const double need = __dsub_ru(marg, x);
+                if (wk > 0.0) lo = fmax(lo, __dmul_ru(__ddiv_ru(need, wk), 1.0 + 0x1p-40));
+                else if (wk < 0.0) hi = fmin(hi, __dmul_rd(__ddiv_rd(need, wk), 1.0 + 0x1p-40));  // need/wk < 0
+                else lo = INFINITY;
+            }
+            if (++p == T) p = 0;
+        }
+        const float lof = __double2float_ru(lo), hif = __double2float_rd(hi);
+        K2[phi] = make_double2(sum, __hiloint2double(__float_as_int(hif), __float_as_int(lof)));
+        if (j == 0) h = hs;
+    }
+    __syncwarp();
+    for (int j = T + lane; j < n_a; j += 32) K2[j] = K2[j % T];
+    if (lane == 0) {
+        double nr = CUDART_NAN, nab = -INFINITY;
+        if (ok) {
+            // r rounded down and A_b up by 2^-20 more: the fma test's own rounding stays inside
+            nr = -__dmul_rd(__ddiv_rd(40000.0, __dadd_ru(__dmul_ru(2.0, inv), (double)Pp)), 1.0 - 0x1p-20);
+            nab = -__dmul_ru(__dmul_ru(amax, inv), 1.0 + 0x1p-20);
+        }
+        K2[n_a] = make_double2(h, nr);
+        K2[n_a + 1] = make_double2(nab, 0.0);
+    }
+    __syncwarp();
+}
+
+// The closed-form decision for a full period from start value x0 (= x0f, an
+// fp32 trace value) at entry kp (K2 + phase): the envelope's line, or
+// kZeroLine when x0 is outside [lo, hi], the error bound fails or the key
+// falls in a band; the caller then runs the sequential horizon (and counts it
+// in n_seq).
+__device__ __forceinline__ uint32_t cfh_choice(const double2* kp, double h, double nr, double nab, float x0f,
+                                               double x0, double invP, double invK, const uint2* ent8, int ebase,
+                                               uint32_t ZB) {
+    const double2 e = *kp;
+    const double m = __dmul_rn(__fma_rn(h, x0, e.x), invP);
+    const bool in = x0f >= __int_as_float(__double2loint(e.y)) && x0f <= __int_as_float(__double2hiint(e.y));
+    if (!(in && __fma_rn(nr, m, x0) <= nab)) return kZeroLine;
+    const int hk = __double2hiint(__dmul_rn(m, invK));
+    const int idx = max(min((hk >> kSH) - ebase, kNBUsed - 1), 0);
+    return (line_addr(hk, ent8[idx], ZB) >> 8) & 0xffu;
+}
+
 // One period's decision from its horizon mean (the envelope lookup, else the canonical rule).
 __device__ __forceinline__ uint32_t period_choice(double chat, double invK, double Kc, const uint2* ent8, int ebase,
                                                   uint32_t ZB, const PairTable* pt, const ProfileTable* pf,
@@ -486,20 +584,28 @@ __device__ __forceinline__ void horizon_step(double A, double wl, double& prev, 
 // masked chains and store nothing.
 template <int M>
 __device__ __forceinline__ void decide_multi(const float* stagev, int cs, int ce, int Pp, int j, int ph, int dph,
-                                             int T, const double* Aeven, double wl, double invK, double Kc,
+                                             int T, const double* Aeven, double wl, double invP, double invK, double Kc,
                                              const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
-                                             const ProfileTable* pf, uint8_t* chb, unsigned& n_slow) {
+                                             const ProfileTable* pf, const double2* K0, double hcf, double cnr, double cnab,
+                                             uint8_t* chb, unsigned& n_slow, unsigned& n_seq) {
     double prev[M], sum[M];
     int dk[M];
+    uint32_t kk[M];
+    bool need = false;
 #pragma unroll
     for (int k = 0; k < M; ++k) {
         const int b = (j + 32 * k) * Pp;
-        prev[k] = b < ce ? (double)stagev[b - cs - 1] : 0.0;
+        const float x0f = b < ce ? stagev[b - cs - 1] : 0.0f;
+        prev[k] = (double)x0f;
         sum[k] = 0.0;
         dk[k] = (k * dph) % T;
+        kk[k] = cfh_choice(K0 + ph + dk[k], hcf, cnr, cnab, x0f, prev[k], invP, invK, ent8, ebase, ZB);
+        const bool nd = b < ce && kk[k] == (uint32_t)kZeroLine;
+        n_seq += nd ? 1u : 0u;
+        need |= nd;
     }
     int p = ph, s = 0;
-    while (s < Pp) {
+    while (need && s < Pp) {
         const int seg = min(Pp - s, T - p);
         const double* Ap = Aeven + p;
 #pragma unroll 1
@@ -516,9 +622,11 @@ __device__ __forceinline__ void decide_multi(const float* stagev, int cs, int ce
     for (int k = 0; k < M; ++k) {
         const int b = (j + 32 * k) * Pp;
         if (b < ce) {
-            const double chat = pow2 ? __dmul_rn(sum[k], 1.0 / (double)Pp) : __ddiv_rn(sum[k], (double)Pp);
-            const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
-            fill_bytes(chb, b - cs, min(b + Pp, ce) - cs, kk);
+            if (kk[k] == (uint32_t)kZeroLine) {
+                const double chat = pow2 ? __dmul_rn(sum[k], 1.0 / (double)Pp) : __ddiv_rn(sum[k], (double)Pp);
+                kk[k] = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            }
+            fill_bytes(chb, b - cs, min(b + Pp, ce) - cs, kk[k]);
         }
     }
 }
@@ -526,8 +634,9 @@ __device__ __forceinline__ void decide_multi(const float* stagev, int cs, int ce
 __device__ __noinline__ void period_decisions(const float* stagev, int cs, int wc, int Wt, int Pp, int phase_start,
                                               int T, const double* Aeven, double wl, double invK, double Kc,
                                               const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
-                                              const ProfileTable* pf, uint32_t k_carry, uint8_t* chb, int lane,
-                                              unsigned& n_slow) {
+                                              const ProfileTable* pf, const double2* K0, double hcf, double cnr, double cnab,
+                                              uint32_t k_carry, uint8_t* chb, int lane, unsigned& n_slow,
+                                              unsigned& n_seq) {
     const int ce = cs + wc;
     const int jf = (cs + Pp - 1) / Pp;
     const int bf = min(jf * Pp, ce);
@@ -538,9 +647,13 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
         if (T <= 64 && Pp >= 8 && m >= 2 && m <= 4 && (int64_t)jl * Pp + Pp <= Wt) {
             const int ph0 = (phase_start + (jf + lane) * Pp) % T, dph = (32 * Pp) % T;
             const int j = jf + lane;
-            if (m == 2) decide_multi<2>(stagev, cs, ce, Pp, j, ph0, dph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf, chb, n_slow);
-            else if (m == 3) decide_multi<3>(stagev, cs, ce, Pp, j, ph0, dph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf, chb, n_slow);
-            else decide_multi<4>(stagev, cs, ce, Pp, j, ph0, dph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf, chb, n_slow);
+            const double iP = 1.0 / (double)Pp;
+#define CHASE_DM(M) decide_multi<M>(stagev, cs, ce, Pp, j, ph0, dph, T, Aeven, wl, iP, invK, Kc, ent8, ebase, ZB, pt, \
+                                    pf, K0, hcf, cnr, cnab, chb, n_slow, n_seq)
+            if (m == 2) CHASE_DM(2);
+            else if (m == 3) CHASE_DM(3);
+            else CHASE_DM(4);
+#undef CHASE_DM
             return;
         }
     }
@@ -554,9 +667,13 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
     for (int j = jf + lane; j * Pp < ce; j += 32) {
         const int b = j * Pp;
         const int n = min(Pp, Wt - b);
-        double prev = (double)stagev[b - cs - 1], sum = 0.0;
+        const float x0f = stagev[b - cs - 1];
+        double prev = (double)x0f, sum = 0.0;
+        uint32_t kk = n == Pp ? cfh_choice(K0 + ph, hcf, cnr, cnab, x0f, prev, invP, invK, ent8, ebase, ZB)
+                              : (uint32_t)kZeroLine;
         int p = ph, k = 0;
-        while (k < n) {
+        n_seq += kk == (uint32_t)kZeroLine ? 1u : 0u;
+        while (kk == (uint32_t)kZeroLine && k < n) {
             const int seg = min(n - k, tend - p);
             const double* Ap = Aeven + p;
             int q = 0;
@@ -572,10 +689,12 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
             while (p >= T) p -= T;
         }
         // sum/n; for a power-of-two n the product with 1/n is the same exact-then-rounded value
-        double chat;
-        if (n == Pp) chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
-        else chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
-        const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+        if (kk == (uint32_t)kZeroLine) {
+            double chat;
+            if (n == Pp) chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
+            else chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
+            kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+        }
         const int e = min(b + Pp, ce);
         if (Pp < 8) {
             for (int qq = b; qq < e; ++qq) chb[qq - cs] = (uint8_t)kk;
@@ -598,6 +717,21 @@ __device__ __forceinline__ double run_csum(const float* __restrict__ tv, int q0,
         const float raw = tv[q];
         vmin = fminf(vmin, raw);
         cs = __dadd_rn(cs, (double)raw);
+    }
+    // 16 values per iteration: the four LDS.128 issue together (one shared-memory
+    // latency per 16 windows, not per 4) and their sums form a tree
+#pragma unroll 1
+    for (; q + 16 <= q1; q += 16) {
+        float4 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = *reinterpret_cast<const float4*>(tv + q + 4 * i);
+        double s[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            vmin = fminf(fminf(fminf(vmin, v[i].x), v[i].y), fminf(v[i].z, v[i].w));
+            s[i] = __dadd_rn(__dadd_rn((double)v[i].x, (double)v[i].y), __dadd_rn((double)v[i].z, (double)v[i].w));
+        }
+        cs = __dadd_rn(cs, __dadd_rn(__dadd_rn(s[0], s[1]), __dadd_rn(s[2], s[3])));
     }
 #pragma unroll 1
     for (; q + 4 <= q1; q += 4) {
@@ -687,7 +821,8 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
                                               const double* __restrict__ Ap, double wl, bool pow2, double dP,
                                               double invP, double invK, double Kc, const uint2* ent8, int ebase,
                                               uint32_t ZB, const PairTable* pt, const ProfileTable* pf, int prof,
-                                              uint8_t* chl, Acc& a, unsigned& n_slow) {
+                                              const double2* kq, double hcf, double cnr, double cnab, uint8_t* chl, Acc& a,
+                                              unsigned& n_slow, unsigned& n_seq) {
     static_assert((G * PN) % 4 == 0, "group must be whole float4s");
     float v[G * PN];
 #pragma unroll
@@ -696,20 +831,36 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
         v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
     }
     double pr[G], sm[G];
+    float x0f[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        pr[g] = (double)(g == 0 ? carry : v[g * PN - 1]);
+        x0f[g] = g == 0 ? carry : v[g * PN - 1];
+        pr[g] = (double)x0f[g];
         sm[g] = 0.0;
     }
-#pragma unroll
-    for (int k = 0; k < PN; ++k)
-#pragma unroll
-        for (int g = 0; g < G; ++g) horizon_step(Ap[q + g * PN + k], wl, pr[g], sm[g]);
+    // P = 2: two sequential steps cost less than the closed form's test (measured)
+    constexpr bool kCF = PN > 2;
     uint32_t kk[G];
+    bool need = !kCF;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        const double ch = pow2 ? __dmul_rn(sm[g], invP) : __ddiv_rn(sm[g], dP);
-        kk[g] = period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+        kk[g] = kCF ? cfh_choice(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], invP, invK, ent8, ebase, ZB)
+                    : (uint32_t)kZeroLine;
+        need |= kk[g] == (uint32_t)kZeroLine;
+        if (kCF) n_seq += kk[g] == (uint32_t)kZeroLine ? 1u : 0u;
+    }
+    if (need) {  // cold: the sequential horizon (Eq. 1) for the periods the closed form left
+#pragma unroll
+        for (int k = 0; k < PN; ++k)
+#pragma unroll
+            for (int g = 0; g < G; ++g) horizon_step(Ap[q + g * PN + k], wl, pr[g], sm[g]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (kk[g] == (uint32_t)kZeroLine) {
+                const double ch = pow2 ? __dmul_rn(sm[g], invP) : __ddiv_rn(sm[g], dP);
+                kk[g] = period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            }
+        }
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) lane_period_replay_v<PN>(v + g * PN, q + g * PN, kk[g], prof, chl, a);
@@ -720,7 +871,8 @@ template <int PC>
 __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp, const double* __restrict__ Ap,
                                             double wl, double invK, double Kc, const uint2* ent8, int ebase,
                                             uint32_t ZB, const PairTable* pt, const ProfileTable* pf, int prof,
-                                            uint8_t* chl, Acc& a, unsigned& n_slow) {
+                                            const double2* kq, double hcf, double cnr, double cnab, uint8_t* chl, Acc& a,
+                                            unsigned& n_slow, unsigned& n_seq) {
     const int Pn = PC > 0 ? PC : Pp;
     const bool pow2 = (Pn & (Pn - 1)) == 0;
     const double dP = (double)Pn, invP = 1.0 / dP;
@@ -734,23 +886,29 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
 #pragma unroll 1
         for (int q = 0; q < kHChunk; q += 2 * PN)
             carry = period_group<PN, 2>(tv, q, carry, Ap, wl, pow2, dP, invP, invK, Kc, ent8, ebase, ZB, pt, pf, prof,
-                                        chl, a, n_slow);
+                                        kq, hcf, cnr, cnab, chl, a, n_slow, n_seq);
         return;
     }
     if (PC > 0 && (kHChunk / (PC > 0 ? PC : 1)) % 2 == 0) {
         // two periods per iteration: their horizons are independent chains, interleaved
 #pragma unroll 1
         for (int q = 0; q < kHChunk; q += 2 * Pn) {
-            double pa = (double)tv[q - 1], pb = (double)tv[q + Pn - 1], sa = 0.0, sb = 0.0;
+            const float fa = tv[q - 1], fb = tv[q + Pn - 1];
+            double pa = (double)fa, pb = (double)fb, sa = 0.0, sb = 0.0;
+            uint32_t ka = cfh_choice(kq + q, hcf, cnr, cnab, fa, pa, invP, invK, ent8, ebase, ZB);
+            uint32_t kb = cfh_choice(kq + q + Pn, hcf, cnr, cnab, fb, pb, invP, invK, ent8, ebase, ZB);
+            n_seq += (ka == (uint32_t)kZeroLine ? 1u : 0u) + (kb == (uint32_t)kZeroLine ? 1u : 0u);
+            if (ka == (uint32_t)kZeroLine || kb == (uint32_t)kZeroLine) {  // cold: sequential horizons
 #pragma unroll
-            for (int k = 0; k < (PC > 0 ? PC : 1); ++k) {
-                horizon_step(Ap[q + k], wl, pa, sa);
-                horizon_step(Ap[q + Pn + k], wl, pb, sb);
+                for (int k = 0; k < (PC > 0 ? PC : 1); ++k) {
+                    horizon_step(Ap[q + k], wl, pa, sa);
+                    horizon_step(Ap[q + Pn + k], wl, pb, sb);
+                }
+                const double ca = pow2 ? __dmul_rn(sa, invP) : __ddiv_rn(sa, dP);
+                const double cb = pow2 ? __dmul_rn(sb, invP) : __ddiv_rn(sb, dP);
+                if (ka == (uint32_t)kZeroLine) ka = period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+                if (kb == (uint32_t)kZeroLine) kb = period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
             }
-            const double ca = pow2 ? __dmul_rn(sa, invP) : __ddiv_rn(sa, dP);
-            const double cb = pow2 ? __dmul_rn(sb, invP) : __ddiv_rn(sb, dP);
-            const uint32_t ka = period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
-            const uint32_t kb = period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
             lane_period_replay<PC>(tv, q, Pn, ka, prof, chl, a);
             lane_period_replay<PC>(tv, q + Pn, Pn, kb, prof, chl, a);
         }
@@ -758,12 +916,94 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
     }
 #pragma unroll 1
     for (int q = 0; q < kHChunk; q += Pn) {
-        double prev = (double)tv[q - 1], sum = 0.0;
+        const float x0f = tv[q - 1];
+        double prev = (double)x0f, sum = 0.0;
+        uint32_t kk = cfh_choice(kq + q, hcf, cnr, cnab, x0f, prev, invP, invK, ent8, ebase, ZB);
+        if (kk == (uint32_t)kZeroLine) {  // cold: the sequential horizon
+            ++n_seq;
 #pragma unroll
-        for (int k = 0; k < Pn; ++k) horizon_step(Ap[q + k], wl, prev, sum);
-        const double chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
-        const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            for (int k = 0; k < Pn; ++k) horizon_step(Ap[q + k], wl, prev, sum);
+            const double chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
+            kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+        }
         lane_period_replay<PC>(tv, q, Pn, kk, prof, chl, a);
+    }
+}
+
+// Sequential horizon (Eq. 1, oracle_predict's order) of n steps from phase ph
+// and start value prev, reading the extended A table with wrap: the sum.
+__device__ __forceinline__ double horizon_sum(const double* Aeven, int T, int ph, int n, double prev, double wl) {
+    const int tend = haext_len(T);
+    double sum = 0.0;
+    int p = ph, k = 0;
+    while (k < n) {
+        const int seg = min(n - k, tend - p);
+        const double* Ap = Aeven + p;
+        int q = 0;
+#pragma unroll 1
+        for (; q + 2 <= seg; q += 2) {
+            const double a0 = Ap[q], a1 = Ap[q + 1];
+            horizon_step(a0, wl, prev, sum);
+            horizon_step(a1, wl, prev, sum);
+        }
+        if (q < seg) horizon_step(Ap[q], wl, prev, sum);
+        k += seg;
+        p += seg;
+        while (p >= T) p -= T;
+    }
+    return sum;
+}
+
+// Lane-direct decision periods (2 < P < 64 with the closed form):
+// each lane decides every period that meets its own windows [w0, w0 + nwin)
+// and replays them in the same pass, with no staged decisions and no warp
+// barrier between the two.  A period needs only its start value c[b-1] (in the
+// stage: tvs[b - cs - 1], the lag slot for b = cs) and its phase, so a period
+// split between two lanes is decided by both (the same arithmetic; the lane
+// holding its start counts it in n_slow / n_seq); one that began in an earlier
+// chunk takes k_carry.  The closed form decides, else the sequential horizon.
+__device__ __forceinline__ void period_direct(const float* __restrict__ tvs, const float* __restrict__ tv, int nwin,
+                                           int w0, int cs, int Wt, int Pp, int phi0, int T, const double* Aeven,
+                                           double wl, double invK, double Kc, const uint2* ent8, int ebase,
+                                           uint32_t ZB, const PairTable* pt, const ProfileTable* pf,
+                                           const double2* K2, double hcf, double cnr, double cnab, uint32_t k_carry,
+                                           int prof, uint8_t* chl, Acc& a, unsigned& n_slow, unsigned& n_seq) {
+    if (nwin <= 0) return;
+    const double invP = 1.0 / (double)Pp;
+    int b = (w0 / Pp) * Pp;
+    int ph = (phi0 - (w0 - b)) % T;  // phase of b (w0 - b < P)
+    if (ph < 0) ph += T;
+    int q = 0;
+    while (q < nwin) {
+        uint32_t kk = k_carry;
+        if (b >= cs) {
+            const int n = min(Pp, Wt - b);
+            const float x0f = tvs[b - cs - 1];
+            const double x0 = (double)x0f;
+            kk = n == Pp ? cfh_choice(K2 + ph, hcf, cnr, cnab, x0f, x0, invP, invK, ent8, ebase, ZB)
+                         : (uint32_t)kZeroLine;
+            if (kk == (uint32_t)kZeroLine) {  // cold: the sequential horizon, then the lookup / canonical rule
+                const bool own = b >= w0;
+                if (own && n == Pp) ++n_seq;
+                const double sum = horizon_sum(Aeven, T, ph, n, x0, wl);
+                const double chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
+                unsigned ns = 0;
+                kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, ns);
+                if (own) n_slow += ns;
+            }
+        }
+        const int e = min(nwin, b + Pp - w0);
+        if (Pp >= 16) {  // the run form for every piece (float4 sums once aligned; short pieces too)
+            const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+            replay_run(a, ln, e - q, run_csum(tv, q, e, a.vmin));
+            fill_bytes(chl, q, e, kk);
+        } else {
+            lane_period_replay<0>(tv, q, e - q, kk, prof, chl, a);
+        }
+        q = e;
+        b += Pp;
+        ph += Pp;
+        while (ph >= T) ph -= T;
     }
 }
 
@@ -773,16 +1013,24 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
 // from global memory (one 4-byte load per period), so a batch spans chunks and
 // every lane has a horizon to run (P = 168: 2 batches per year-long trace, not
 // one 12-lane round per chunk).  Same per-period arithmetic as period_decisions.
+template <bool CF>
 __device__ __noinline__ uint32_t period_batch(const float* __restrict__ cg, int jb, int Wt, int Pp, int phase_start,
                                               int T, const double* Aeven, double wl, double invK, double Kc,
                                               const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
-                                              const ProfileTable* pf, int lane, unsigned& n_slow) {
+                                              const ProfileTable* pf, const double2* K0, double hcf, double cnr, double cnab,
+                                              int lane, unsigned& n_slow, unsigned& n_seq) {
     const int b = (jb + lane) * Pp;
     if (b >= Wt) return 0u;
     const int n = min(Pp, Wt - b);
     const int tend = haext_len(T);
-    double prev = (double)__ldg(cg + b - 1), sum = 0.0;  // c[b-1]
+    const float x0f = __ldg(cg + b - 1);  // c[b-1]
+    double prev = (double)x0f, sum = 0.0;
     int p = (int)(((int64_t)phase_start + b) % T), k = 0;
+    if (CF && n == Pp) {
+        const uint32_t kk = cfh_choice(K0 + p, hcf, cnr, cnab, x0f, prev, 1.0 / (double)Pp, invK, ent8, ebase, ZB);
+        if (kk != (uint32_t)kZeroLine) return kk;
+    }
+    if (CF) ++n_seq;
     while (k < n) {
         const int seg = min(n - k, tend - p);
         const double* Ap = Aeven + p;
@@ -878,7 +1126,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t sbase = smem_u32(sm);
     const int head_bytes = reinterpret_cast<const TablesHeader*>(P.tables)->off_pair;
-    const HLayout HL = make_hlayout(P.T, head_bytes, P.n_prof, (int)sbase);
+    const HLayout HL = make_hlayout(P.T, head_bytes, P.n_prof, (int)sbase, P.k0len);
     if (HL.total > P.smem_total || HL.lines < 0) __trap();  // the host planned for another shared-window base
     uint2* ent8_all = reinterpret_cast<uint2*>(sm + HL.ent8);
     int* lph = reinterpret_cast<int*>(sm + HL.lph);
@@ -890,6 +1138,8 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
     uint8_t* chb = wbase + HL.chb;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + HL.mbar);
     const int T = P.T;
+    // periods: the closed-form horizon table (else any valid address: cnr = NaN declines every period)
+    double2* K0w = reinterpret_cast<double2*>(P.k0len > 0 ? wbase + HL.k0 : wbase + HL.aext);
 
     {   // constant tables -> smem, once per CTA: header, phase, profiles; pair heads
         const uint4* src = reinterpret_cast<const uint4*>(P.tables);
@@ -959,6 +1209,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
 
     uint32_t par = 0;    // mbarrier phase parity of the next chunk
     unsigned n_slow = 0;
+    unsigned n_seq = 0;  // periods: full periods whose horizon ran sequentially (the closed form declined)
 
     for (int64_t i = gw; i < P.n_traces; i += GW) {
         int status = 0, c_may = 0, mb = P.W, ebase = 0;
@@ -977,6 +1228,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         uint32_t k_carry = 0;  // period mode: the decision of the period running into the next chunk
         int jb = 0;            // long periods: first period of the current batch
         uint32_t kb = 0;       // long periods: lane l's decision for period jb + l
+        double hcf = 0.0, cnr = CUDART_NAN, cnab = -INFINITY;  // periods: the closed form's h, -r, -A_b (NaN: off)
         for (int c = 0; c < nc; ++c) {
             const bool last = c == nc - 1;
             uint8_t* stage = stage0;
@@ -989,10 +1241,13 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 const int cs = c * kHWarpW, wc = last ? P.W_last : kHWarpW;
                 if ((cs + wc - 1) / P.period >= jb + 32) {
                     const int jn = cs / P.period;
-                    unsigned ns = 0;
-                    kb = period_batch(traces + i * P.ld + P.a0 + P.off0, jn, P.W, P.period, P.phase_start, T, A_even,
-                                      wl, invK, Kc, e8, ebase, ZB, pt, pf, lane, ns);
-                    if (jn + lane > jb + 31) n_slow += ns;  // count only periods the last batch did not decide
+                    unsigned ns = 0, nq = 0;
+                    kb = period_batch<false>(traces + i * P.ld + P.a0 + P.off0, jn, P.W, P.period, P.phase_start, T, A_even,
+                                      wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w, hcf, cnr, cnab, lane, ns, nq);
+                    if (jn + lane > jb + 31) {  // count only periods the last batch did not decide
+                        n_slow += ns;
+                        n_seq += nq;
+                    }
                     jb = jn;
                 }
             }
@@ -1033,9 +1288,20 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                         ph += 32;
                         while (ph >= T) ph -= T;
                     }
+                    if constexpr (PER && PM != 4 && PM != 2) {  // (no closed form at P = 2 and P >= 64: §6.5)
+                        if (P.k0len > 0) {
+                            cfh_setup(K0w, A_even, T, n_a, P.period, P.phase_start, wl, invK, amax, lane);
+                            hcf = K0w[n_a].x;
+                            cnr = K0w[n_a].y;
+                            cnab = K0w[n_a + 1].x;
+#ifdef CHASE_CFH_SETUPONLY
+                            cnr = CUDART_NAN;
+#endif
+                        }
+                    }
                     if constexpr (PM == 0 && CHASE_H0_FAST) {
                         // the one-fma key's bound: 6u (|A| + |w_lag| c)/Kc <= 510u y_min, i.e.
-                        // |A| + |w_lag| c <= 85 y_min Kc (envelope.cpp shrinks by 512u)
+                        // |A| + |w_lag| c <= 85 y_min Kc (envelope.cpp shrinks by 2^-36 >= 512u)
                         amax = warp_max_d(amax);
                         const double lam = __dmul_rn(__dmul_rn(85.0, pt->y_min), Kc);
                         if (!pt->k0 && invK != 0.0 && amax < lam && fabs(wl) <= DBL_MAX) {
@@ -1077,9 +1343,11 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 const int ngr = (PER || invK == 0.0) ? 0 : nwin >> 2;
                 if (PM >= 3 && !last) {  // lane-local periods (P | kHChunk): fused decide + replay
                     uint8_t* chl = chb + j0;
-#define CHASE_LANE_P(PC) period_lane<PC>(tv, PC, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow)
+#define CHASE_LANE_P(PC) period_lane<PC>(tv, PC, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, K0w + phi0, hcf, cnr, cnab, \
+                                         chl, a, n_slow, n_seq)
                     if constexpr (PM >= 4) CHASE_LANE_P(PM - 2);
-                    else period_lane<0>(tv, P.period, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, chl, a, n_slow);
+                    else period_lane<0>(tv, P.period, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, K0w + phi0, hcf,
+                                        cnr, cnab, chl, a, n_slow, n_seq);
 #undef CHASE_LANE_P
                     __syncwarp();
                     k_carry = chb[kHWarpW - 1];
@@ -1087,16 +1355,23 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     const int cs = c * kHWarpW;
                     if (c == 0) {  // the trace's first batch needs its model (the record, in this stage)
                         jb = 0;
-                        kb = period_batch(traces + i * P.ld + P.a0 + P.off0, jb, P.W, P.period, P.phase_start, T,
-                                          A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, lane, n_slow);
+                        kb = period_batch<false>(traces + i * P.ld + P.a0 + P.off0, jb, P.W, P.period, P.phase_start, T,
+                                          A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w, hcf, cnr, cnab, lane, n_slow, n_seq);
                     }
                     period_replay_batch(tv, nwin, cs + j0, P.period, jb, kb, prof_i, chb + j0, a);
                     __syncwarp();
+                } else if (PER && P.k0len > 0) {  // lane-direct periods with the closed form
+                    const int wc = last ? P.W_last : kHWarpW;
+                    period_direct(reinterpret_cast<const float*>(stage) + P.off0, tv, nwin, c * kHWarpW + j0,
+                                  c * kHWarpW, P.W, P.period, phi0, T, A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w,
+                                  hcf, cnr, cnab, k_carry, prof_i, chb + j0, a, n_slow, n_seq);
+                    __syncwarp();
+                    k_carry = chb[wc - 1];
                 } else if (PER) {  // decisions for the chunk's periods first, then the replay
                     const int wc = last ? P.W_last : kHWarpW;
                     period_decisions(reinterpret_cast<const float*>(stage) + P.off0, c * kHWarpW, wc, P.W, P.period,
-                                     P.phase_start, T, A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, k_carry, chb, lane,
-                                     n_slow);
+                                     P.phase_start, T, A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w, hcf, cnr, cnab,
+                                     k_carry, chb, lane, n_slow, n_seq);
                     __syncwarp();
                     k_carry = chb[wc - 1];
                     if (P.period >= 16 && (P.period & 3) == 0) {  // aligned runs of one choice: the run-form replay
@@ -1285,4 +1560,9 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
     n_slow = __reduce_add_sync(kFull, n_slow);
     if (lane == 0 && n_slow)
         atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_slow_windows), (unsigned long long)n_slow);
+    if constexpr (PER) {
+        n_seq = __reduce_add_sync(kFull, n_seq);
+        if (lane == 0 && n_seq)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.diag->n_seq_periods), (unsigned long long)n_seq);
+    }
 }

@@ -117,12 +117,12 @@ cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
 
 // Dynamic shared memory the headline kernel needs for T and n_prof: the layout
 // depends on the CTA's shared-window base, so plan for the worst candidate.
-int headline_smem(int T, int n_prof) {
+int headline_smem(int T, int n_prof, int k0len) {
     // blob bytes before the pair tables (header, phase, profiles): see make_hlayout
     const int head_bytes = (int)sizeof(TablesHeader) + ((2 * T * 8) + 15) / 16 * 16 + n_prof * (int)sizeof(ProfileTable);
     int smem = 0;
     for (int base = 0; base <= 8192; base += 16) {
-        const int t = make_hlayout(T, head_bytes, n_prof, base).total;
+        const int t = make_hlayout(T, head_bytes, n_prof, base, k0len).total;
         smem = t > smem ? t : smem;
     }
     return smem;
@@ -147,7 +147,7 @@ bool headline_eligible(int mode, bool f64, bool aligned, const SweepParams& p) {
     // entries must fit one CTA's shared memory: large T (e.g. 5-minute data) or many
     // profiles take the general sweep (forecast-first for decision periods)
     return mode == MODE_FUSED && !f64 && aligned && p.n_eta == 1 && !p.forecast && !p.fc_in &&
-           !getenv("CHASE_FORCE_GENERAL") && headline_smem(p.T, p.n_prof) <= max_smem_optin();
+           !getenv("CHASE_FORCE_GENERAL") && headline_smem(p.T, p.n_prof, 0) <= max_smem_optin();
 }
 
 cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p, cudaStream_t s) {
@@ -192,7 +192,15 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
             while (k % 8 != 4) ++k;
             q.kc_last = k > kHChunk ? kHChunk : k;
         }
-        const int smem = headline_smem(p.T, p.n_prof);
+        // decision periods: the closed-form horizon table ({K0, x0min} for haext_len(T)
+        // phases, then {h, -r}, {-A_b, 0}) for 2 < P < 64 (PM 1, PM >= 3) when it fits;
+        // else every period runs its horizon (§6.5)
+        q.k0len = 0;
+        const int k0len = 2 * (haext_len(p.T) + 2);
+        if (p.period > 2 && p.period * 30 < kHWarpW && !getenv("CHASE_NO_CFH") &&
+            headline_smem(p.T, p.n_prof, k0len) <= max_smem_optin())
+            q.k0len = k0len;
+        const int smem = headline_smem(p.T, p.n_prof, q.k0len);
         q.smem_total = smem;
         // decision periods: long ones (at most 31 per warp chunk) in 32-period batches
         auto kern = p.period <= 1                 ? sweep_fast_kernel<0>

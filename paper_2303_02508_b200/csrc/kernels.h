@@ -59,6 +59,7 @@ struct SweepParams {
     int32_t kc_last;              // headline kernel: windows per lane in the last chunk (4 mod 8)
     int32_t smem_total;           // headline kernel: dynamic shared memory planned by the host
     int32_t period;               // > 1: one decision per period of this many windows (headline kernel)
+    int32_t k0len;                // headline kernel, periods: doubles of the closed-form horizon table per warp (0: none)
     int32_t refit;                // roll_fused_kernel: the refit stride R >= 1
     double ridge, tol;            // roll_fused_kernel: the fit's ridge and singular tolerance (exact fallback)
 };

@@ -38,13 +38,13 @@ RESNET = inputs.make_profile("resnet50", inputs.LIMITS_9)
 
 
 def gpu_plan(tr, N, profiles, eta, *, pid=None, J=None, L=24, max_ci=0.0, max_power_w=0.0, dtype=torch.float32,
-             expect=cb.PATH_HEADLINE):
+             expect=cb.PATH_HEADLINE, period=0):
     x = torch.from_numpy(np.ascontiguousarray(tr)).to(DEV, dtype)
     pl = cb.Planner(x, n_steps=N, profiles=profiles, etas=[eta], history_len=L,
                     profile_id=None if pid is None else torch.from_numpy(np.ascontiguousarray(pid, np.uint8)).to(DEV),
                     job_samples=None if J is None else torch.from_numpy(np.ascontiguousarray(J, np.float64)).to(DEV),
                     want_choice=True, want_forecast=False, want_per_trace=True, max_ci=max_ci,
-                    max_power_w=max_power_w)
+                    max_power_w=max_power_w, period_steps=period)
     res = pl.run()
     torch.cuda.synchronize()
     d = pl.diag()
@@ -53,9 +53,9 @@ def gpu_plan(tr, N, profiles, eta, *, pid=None, J=None, L=24, max_ci=0.0, max_po
                 sums=res.sums.cpu().numpy()[0], diag=d)
 
 
-def oracle_plan(tr, N, profiles, eta, *, pid=None, J=None, L=24, max_ci=0.0, max_power_w=0.0):
+def oracle_plan(tr, N, profiles, eta, *, pid=None, J=None, L=24, max_ci=0.0, max_power_w=0.0, period=0):
     o = oracle.plan_batch(np.ascontiguousarray(tr, np.float32), N=N, L=L, T=24, profiles=profiles, profile_id=pid,
-                          etas=[eta], pmax=max_power_w, max_ci=max_ci, job_samples=J)
+                          etas=[eta], pmax=max_power_w, max_ci=max_ci, job_samples=J, period=period)
     return dict(choice=o["choice"][0], totals=o["totals"][0], sums=o["sums"][0])
 
 
@@ -144,6 +144,40 @@ def test_headline_band_sweep_max_power(eta):
             assert_same(g, o, exact=False)
             slow += g["diag"].n_slow_windows
     assert slow > 0, "no window reached the canonical rule: the band was not hit"
+
+
+@pytest.mark.parametrize("period", [3, 24, 168])
+def test_periods_band_sweep_max_power(period):
+    """The MaxPower band sweep with decision periods: constant
+    histories give A = v, w_lag = 0, so each period's horizon mean is v and
+    the closed-form mean fl(fl(P v) fl(1/P)) lands within an ulp
+    of it.  Pmax walks +-300 ulps around every breakpoint (keys inside the
+    band the hi32 bucket test leaves, 2^-20 relative: sequential horizon,
+    canonical rule) and then +-3 * 2^-20 in steps of 2^-20/20 (keys crossing
+    the band's edges, where the envelope's 2^-36 shrink decides which keys
+    the closed form may take).  P = 3: lane-local periods (PM 5), 24: per-chunk
+    chains (PM 1), 168: 32-period batches (PM 2)."""
+    eta = 0.9
+    N = 24 + 1940
+    vals = [np.float32(97.0 + 31.713 * i) for i in range(24)]
+    tr = constant_history_traces(vals, N)
+    slow = seq = calls = 0
+    bps = [(y, j, k) for (y, j, k) in breakpoints(RESNET, eta) if 1 / ((1 - F(eta)) * y) >= 300]
+    for y, j, k in bps:
+        pm0 = float(1 / ((1 - F(eta)) * y))
+        pms = ulp_steps(pm0, 300)[::6] + [pm0 * (1 + d * 2.0 ** -20) for d in np.linspace(-3, 3, 121)]
+        for pm in pms:
+            g = gpu_plan(tr, N, [RESNET], eta, max_power_w=pm, period=period, expect=cb.PATH_H_PERIODS)
+            o = oracle_plan(tr, N, [RESNET], eta, max_power_w=pm, period=period)
+            assert_same(g, o, exact=False)
+            slow += g["diag"].n_slow_windows
+            seq += g["diag"].n_seq_periods
+            calls += 1
+    full = calls * len(vals) * ((N - 24) // period)
+    assert slow > 0, "no period reached the canonical rule: the band was not hit"
+    if period < 64:   # (no closed form for P >= 64: 32-period batches, DESIGN §6.5)
+        assert seq < 0.9 * full, f"the closed form decided almost nothing ({seq} of {full} periods sequential)"
+        assert seq > 0
 
 
 def test_headline_band_sweep_fixed_max_ci():
