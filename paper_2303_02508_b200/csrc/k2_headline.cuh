@@ -464,26 +464,30 @@ __device__ __forceinline__ void fill_bytes(uint8_t* chb, int a, int e, uint32_t 
 //     K0[phi] + h x0,   K0[phi] = sum_k Z_k(phi),  h = sum_{k=1..P} w_lag^k.
 // That holds for x0 in [lo[phi], hi[phi]]: each step k with computed Z^_k
 // below marg = 4u A_max/(1 - |w_lag|)^2 (their error bound) gives a lower
-// (w_lag^k > 0) or an upper (w_lag^k < 0) limit on x0.  Against the oracle's
-// sequential, clamped sum/P the closed-form mean m then differs by at most
-// kappa X, X = A_max/(1 - |w_lag|) + x0 (a bound on every forecast), kappa =
-// 3u (2/(1 - |w_lag|) + P): the clamp is 1-Lipschitz, the recursion's errors
-// shrink by |w_lag| per step, the running sum's grow with P.
-// The envelope's fast intervals are shrunk by s = 2^-36 (envelope.cpp), so a
-// key y' inside one is at least y' s/(1+s) from the verified interval's ends:
-// with kappa X <= 120000u m (x0 - r m <= -A_b, r = 40000/(2/(1 - |w_lag|) + P))
-// the oracle's mean lies in the verified interval and the canonical rule on it
-// picks the same line.  K2[j] = {K0, (fp32 lo, fp32 hi)} for phase j mod T,
-// j < n_a = haext_len(T) (phase index without wrap, like the A table);
-// K2[n_a] = {h, -r}, K2[n_a + 1].x = -A_b (r = NaN: never).
+// (w_lag^k > 0) or an upper (w_lag^k < 0) limit on x0.  The table holds K0
+// and h already scaled by c = fl(fl(1/P) fl(1/Kc)), so a period's Eq. 6 key
+// is one fma, y' = fl(h' x0 + K0'), against the canonical fl(fl(sum/P)/Kc).
+// Their means (y' Kc and the oracle's sequential, clamped sum/P) differ by at
+// most kappa X, X = A_max/(1 - |w_lag|) + x0 (a bound on every forecast),
+// kappa = 4u (2/(1 - |w_lag|) + P): the clamp is 1-Lipschitz, the
+// recursion's errors shrink by |w_lag| per step, the running sums' grow with
+// P, the scaling adds 5u X.  The envelope's fast intervals are
+// shrunk by s = 2^-36 (envelope.cpp), so a key y' inside one is at least
+// y' s/(1+s) from the verified interval's ends: with kappa X <= 120000u y' Kc
+// (x0 - r Kc y' <= -A_b, r = 30000/(2/(1 - |w_lag|) + P)) the oracle's mean
+// lies in the verified interval and the canonical rule on it picks the same
+// line.  K2[j] = {K0', (fp32 lo, fp32 hi)} for phase j mod T, j < n_a =
+// haext_len(T) (phase index without wrap, like the A table); K2[n_a] =
+// {h', -r Kc}, K2[n_a + 1].x = -A_b (-r Kc = NaN: never).
 __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, int n_a, int Pp, int phase_start,
-                                       double wl, double invK, double amax, int lane) {
+                                       double wl, double invK, double Kc, double amax, int lane) {
     __syncwarp();  // the A table, written by every lane
     amax = warp_max_d(amax);
     const double aw = fabs(wl);
-    const bool ok = aw <= 0.99 && amax <= DBL_MAX && invK != 0.0;
+    const bool ok = aw <= 0.99 && amax <= DBL_MAX && invK != 0.0 && Kc > 0.0 && Kc <= DBL_MAX;
     const double inv = ok ? __ddiv_ru(1.0, __dsub_rd(1.0, aw)) : 1.0;  // >= 1/(1 - |w_lag|)
     const double marg = __dmul_ru(__dmul_ru(0x1p-51, amax), __dmul_ru(inv, inv));
+    const double cs = __dmul_rn(1.0 / (double)Pp, invK);  // the key's scale c
     int g = Pp, t = T;  // period starts are phase_start + j P (mod T): one class mod gcd(P, T)
     while (t) {
         const int r = g % t;
@@ -511,7 +515,7 @@ __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, 
             if (++p == T) p = 0;
         }
         const float lof = __double2float_ru(lo), hif = __double2float_rd(hi);
-        K2[phi] = make_double2(sum, __hiloint2double(__float_as_int(hif), __float_as_int(lof)));
+        K2[phi] = make_double2(__dmul_rn(sum, cs), __hiloint2double(__float_as_int(hif), __float_as_int(lof)));
         if (j == 0) h = hs;
     }
     __syncwarp();
@@ -519,11 +523,12 @@ __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, 
     if (lane == 0) {
         double nr = CUDART_NAN, nab = -INFINITY;
         if (ok) {
-            // r rounded down and A_b up by 2^-20 more: the fma test's own rounding stays inside
-            nr = -__dmul_rd(__ddiv_rd(40000.0, __dadd_ru(__dmul_ru(2.0, inv), (double)Pp)), 1.0 - 0x1p-20);
+            // r Kc rounded down and A_b up by 2^-20 more: the fma test's own rounding stays inside
+            const double r = __ddiv_rd(30000.0, __dadd_ru(__dmul_ru(2.0, inv), (double)Pp));
+            nr = -__dmul_rd(__dmul_rd(r, Kc), 1.0 - 0x1p-20);
             nab = -__dmul_ru(__dmul_ru(amax, inv), 1.0 + 0x1p-20);
         }
-        K2[n_a] = make_double2(h, nr);
+        K2[n_a] = make_double2(__dmul_rn(h, cs), nr);
         K2[n_a + 1] = make_double2(nab, 0.0);
     }
     __syncwarp();
@@ -534,16 +539,17 @@ __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, 
 // kZeroLine when x0 is outside [lo, hi], the error bound fails or the key
 // falls in a band; the caller then runs the sequential horizon (and counts it
 // in n_seq).
-__device__ __forceinline__ uint32_t cfh_choice(const double2* kp, double h, double nr, double nab, float x0f,
-                                               double x0, double invP, double invK, const uint2* ent8, int ebase,
-                                               uint32_t ZB) {
+__device__ __forceinline__ uint32_t cfh_choice(const double2* kp, double hc, double nr, double nab, float x0f,
+                                               double x0, const uint2* ent8, int ebase, uint32_t ZB) {
     const double2 e = *kp;
-    const double m = __dmul_rn(__fma_rn(h, x0, e.x), invP);
+    const double y = __fma_rn(hc, x0, e.x);
     const bool in = x0f >= __int_as_float(__double2loint(e.y)) && x0f <= __int_as_float(__double2hiint(e.y));
-    if (!(in && __fma_rn(nr, m, x0) <= nab)) return kZeroLine;
-    const int hk = __double2hiint(__dmul_rn(m, invK));
+    // branch-free: the lookup runs either way, so the lookups of neighbouring
+    // periods overlap their shared-memory latencies
+    const int hk = __double2hiint(y);
     const int idx = max(min((hk >> kSH) - ebase, kNBUsed - 1), 0);
-    return (line_addr(hk, ent8[idx], ZB) >> 8) & 0xffu;
+    const uint32_t k = (line_addr(hk, ent8[idx], ZB) >> 8) & 0xffu;
+    return (in && __fma_rn(nr, y, x0) <= nab) ? k : (uint32_t)kZeroLine;
 }
 
 // One period's decision from its horizon mean (the envelope lookup, else the canonical rule).
@@ -599,7 +605,7 @@ __device__ __forceinline__ void decide_multi(const float* stagev, int cs, int ce
         prev[k] = (double)x0f;
         sum[k] = 0.0;
         dk[k] = (k * dph) % T;
-        kk[k] = cfh_choice(K0 + ph + dk[k], hcf, cnr, cnab, x0f, prev[k], invP, invK, ent8, ebase, ZB);
+        kk[k] = cfh_choice(K0 + ph + dk[k], hcf, cnr, cnab, x0f, prev[k], ent8, ebase, ZB);
         const bool nd = b < ce && kk[k] == (uint32_t)kZeroLine;
         n_seq += nd ? 1u : 0u;
         need |= nd;
@@ -669,7 +675,7 @@ __device__ __noinline__ void period_decisions(const float* stagev, int cs, int w
         const int n = min(Pp, Wt - b);
         const float x0f = stagev[b - cs - 1];
         double prev = (double)x0f, sum = 0.0;
-        uint32_t kk = n == Pp ? cfh_choice(K0 + ph, hcf, cnr, cnab, x0f, prev, invP, invK, ent8, ebase, ZB)
+        uint32_t kk = n == Pp ? cfh_choice(K0 + ph, hcf, cnr, cnab, x0f, prev, ent8, ebase, ZB)
                               : (uint32_t)kZeroLine;
         int p = ph, k = 0;
         n_seq += kk == (uint32_t)kZeroLine ? 1u : 0u;
@@ -844,7 +850,7 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
     bool need = !kCF;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        kk[g] = kCF ? cfh_choice(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], invP, invK, ent8, ebase, ZB)
+        kk[g] = kCF ? cfh_choice(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], ent8, ebase, ZB)
                     : (uint32_t)kZeroLine;
         need |= kk[g] == (uint32_t)kZeroLine;
         if (kCF) n_seq += kk[g] == (uint32_t)kZeroLine ? 1u : 0u;
@@ -895,8 +901,8 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         for (int q = 0; q < kHChunk; q += 2 * Pn) {
             const float fa = tv[q - 1], fb = tv[q + Pn - 1];
             double pa = (double)fa, pb = (double)fb, sa = 0.0, sb = 0.0;
-            uint32_t ka = cfh_choice(kq + q, hcf, cnr, cnab, fa, pa, invP, invK, ent8, ebase, ZB);
-            uint32_t kb = cfh_choice(kq + q + Pn, hcf, cnr, cnab, fb, pb, invP, invK, ent8, ebase, ZB);
+            uint32_t ka = cfh_choice(kq + q, hcf, cnr, cnab, fa, pa, ent8, ebase, ZB);
+            uint32_t kb = cfh_choice(kq + q + Pn, hcf, cnr, cnab, fb, pb, ent8, ebase, ZB);
             n_seq += (ka == (uint32_t)kZeroLine ? 1u : 0u) + (kb == (uint32_t)kZeroLine ? 1u : 0u);
             if (ka == (uint32_t)kZeroLine || kb == (uint32_t)kZeroLine) {  // cold: sequential horizons
 #pragma unroll
@@ -918,7 +924,7 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
     for (int q = 0; q < kHChunk; q += Pn) {
         const float x0f = tv[q - 1];
         double prev = (double)x0f, sum = 0.0;
-        uint32_t kk = cfh_choice(kq + q, hcf, cnr, cnab, x0f, prev, invP, invK, ent8, ebase, ZB);
+        uint32_t kk = cfh_choice(kq + q, hcf, cnr, cnab, x0f, prev, ent8, ebase, ZB);
         if (kk == (uint32_t)kZeroLine) {  // cold: the sequential horizon
             ++n_seq;
 #pragma unroll
@@ -969,7 +975,6 @@ __device__ __forceinline__ void period_direct(const float* __restrict__ tvs, con
                                            const double2* K2, double hcf, double cnr, double cnab, uint32_t k_carry,
                                            int prof, uint8_t* chl, Acc& a, unsigned& n_slow, unsigned& n_seq) {
     if (nwin <= 0) return;
-    const double invP = 1.0 / (double)Pp;
     int b = (w0 / Pp) * Pp;
     int ph = (phi0 - (w0 - b)) % T;  // phase of b (w0 - b < P)
     if (ph < 0) ph += T;
@@ -980,7 +985,7 @@ __device__ __forceinline__ void period_direct(const float* __restrict__ tvs, con
             const int n = min(Pp, Wt - b);
             const float x0f = tvs[b - cs - 1];
             const double x0 = (double)x0f;
-            kk = n == Pp ? cfh_choice(K2 + ph, hcf, cnr, cnab, x0f, x0, invP, invK, ent8, ebase, ZB)
+            kk = n == Pp ? cfh_choice(K2 + ph, hcf, cnr, cnab, x0f, x0, ent8, ebase, ZB)
                          : (uint32_t)kZeroLine;
             if (kk == (uint32_t)kZeroLine) {  // cold: the sequential horizon, then the lookup / canonical rule
                 const bool own = b >= w0;
@@ -1027,7 +1032,7 @@ __device__ __noinline__ uint32_t period_batch(const float* __restrict__ cg, int 
     double prev = (double)x0f, sum = 0.0;
     int p = (int)(((int64_t)phase_start + b) % T), k = 0;
     if (CF && n == Pp) {
-        const uint32_t kk = cfh_choice(K0 + p, hcf, cnr, cnab, x0f, prev, 1.0 / (double)Pp, invK, ent8, ebase, ZB);
+        const uint32_t kk = cfh_choice(K0 + p, hcf, cnr, cnab, x0f, prev, ent8, ebase, ZB);
         if (kk != (uint32_t)kZeroLine) return kk;
     }
     if (CF) ++n_seq;
@@ -1290,7 +1295,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     }
                     if constexpr (PER && PM != 4 && PM != 2) {  // (no closed form at P = 2 and P >= 64: §6.5)
                         if (P.k0len > 0) {
-                            cfh_setup(K0w, A_even, T, n_a, P.period, P.phase_start, wl, invK, amax, lane);
+                            cfh_setup(K0w, A_even, T, n_a, P.period, P.phase_start, wl, invK, Kc, amax, lane);
                             hcf = K0w[n_a].x;
                             cnr = K0w[n_a].y;
                             cnab = K0w[n_a + 1].x;
