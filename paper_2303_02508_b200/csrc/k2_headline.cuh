@@ -33,6 +33,12 @@
 #ifndef CHASE_H_CFMA
 #define CHASE_H_CFMA 1  // 1: the group's sum of P_k c as an fma chain (C5: 11.23 -> 11.13 ms; exact for dyadic inputs)
 #endif
+#ifndef CHASE_P2_CF
+#define CHASE_P2_CF 1  // 0: sequential horizons at P = 2 (sweep_fast_kernel<4>; C5 18.7 vs 16.2 ms with the closed form)
+#endif
+#ifndef CHASE_P2_G
+#define CHASE_P2_G 2   // periods per iteration at P = 2 (sweep_fast_kernel<4>; must divide 30)
+#endif
 #ifndef CHASE_H_PAIRSUM
 #define CHASE_H_PAIRSUM 1  // 1: a group's four terms summed pairwise before the running sums
 #endif
@@ -844,8 +850,8 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
         pr[g] = (double)x0f[g];
         sm[g] = 0.0;
     }
-    // P = 2: two sequential steps cost less than the closed form's test (measured)
-    constexpr bool kCF = PN > 2;
+    // (CHASE_P2_CF = 0: P = 2 keeps its two sequential steps)
+    constexpr bool kCF = PN > 2 || CHASE_P2_CF;
     uint32_t kk[G];
     bool need = !kCF;
 #pragma unroll
@@ -889,10 +895,11 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         constexpr int PN = (PC > 0 && PC % 2 == 0) ? PC : 2;  // (odd PC never takes this branch)
         float carry = tv[-1];
         // (four periods per iteration at P = 2 measured slower: 17.7 -> 18.4 ms at C5, register spills)
+        constexpr int GP = PN == 2 ? CHASE_P2_G : 2;  // periods per iteration
 #pragma unroll 1
-        for (int q = 0; q < kHChunk; q += 2 * PN)
-            carry = period_group<PN, 2>(tv, q, carry, Ap, wl, pow2, dP, invP, invK, Kc, ent8, ebase, ZB, pt, pf, prof,
-                                        kq, hcf, cnr, cnab, chl, a, n_slow, n_seq);
+        for (int q = 0; q < kHChunk; q += GP * PN)
+            carry = period_group<PN, GP>(tv, q, carry, Ap, wl, pow2, dP, invP, invK, Kc, ent8, ebase, ZB, pt, pf, prof,
+                                         kq, hcf, cnr, cnab, chl, a, n_slow, n_seq);
         return;
     }
     if (PC > 0 && (kHChunk / (PC > 0 ? PC : 1)) % 2 == 0) {
@@ -1293,7 +1300,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                         ph += 32;
                         while (ph >= T) ph -= T;
                     }
-                    if constexpr (PER && PM != 4 && PM != 2) {  // (no closed form at P = 2 and P >= 64: §6.5)
+                    if constexpr (PER && (PM != 4 || CHASE_P2_CF) && PM != 2) {  // (no closed form at P >= 64: §6.5)
                         if (P.k0len > 0) {
                             cfh_setup(K0w, A_even, T, n_a, P.period, P.phase_start, wl, invK, Kc, amax, lane);
                             hcf = K0w[n_a].x;

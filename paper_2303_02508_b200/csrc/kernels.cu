@@ -193,11 +193,11 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
             q.kc_last = k > kHChunk ? kHChunk : k;
         }
         // decision periods: the closed-form horizon table ({K0, x0min} for haext_len(T)
-        // phases, then {h, -r}, {-A_b, 0}) for 2 < P < 64 (PM 1, PM >= 3) when it fits;
+        // phases, then {h', -r Kc}, {-A_b, 0}) for 1 < P < 64 (PM 1, PM >= 3) when it fits;
         // else every period runs its horizon (§6.5)
         q.k0len = 0;
         const int k0len = 2 * (haext_len(p.T) + 2);
-        if (p.period > 2 && p.period * 30 < kHWarpW && !getenv("CHASE_NO_CFH") &&
+        if (p.period > (CHASE_P2_CF ? 1 : 2) && p.period * 30 < kHWarpW && !getenv("CHASE_NO_CFH") &&
             headline_smem(p.T, p.n_prof, k0len) <= max_smem_optin())
             q.k0len = k0len;
         const int smem = headline_smem(p.T, p.n_prof, q.k0len);
