@@ -827,7 +827,7 @@ def main_mape(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded counter-based generator, inputs/)", "config": cfg,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency": latency, "gpu_launches": int(launches),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk, "check": {"mean_mape_linear": float(mp[:, 0].mean()),
                                          "mean_mape_persistence": float(mp[:, 1].mean())}}
         print(json.dumps(line), flush=True)

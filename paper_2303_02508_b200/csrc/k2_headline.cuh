@@ -611,6 +611,7 @@ __device__ __forceinline__ void decide_multi(const float* stagev, int cs, int ce
         prev[k] = (double)x0f;
         sum[k] = 0.0;
         dk[k] = (k * dph) % T;
+        CHASE_CHECK(ph + dk[k] < haext_len(T));
         kk[k] = cfh_choice(K0 + ph + dk[k], hcf, cnr, cnab, x0f, prev[k], ent8, ebase, ZB);
         const bool nd = b < ce && kk[k] == (uint32_t)kZeroLine;
         n_seq += nd ? 1u : 0u;
@@ -987,9 +988,11 @@ __device__ __forceinline__ void period_direct(const float* __restrict__ tvs, con
     if (ph < 0) ph += T;
     int q = 0;
     while (q < nwin) {
+        CHASE_CHECK(ph >= 0 && ph < T);
         uint32_t kk = k_carry;
         if (b >= cs) {
             const int n = min(Pp, Wt - b);
+            CHASE_CHECK(b - cs < kHWarpW);
             const float x0f = tvs[b - cs - 1];
             const double x0 = (double)x0f;
             kk = n == Pp ? cfh_choice(K2 + ph, hcf, cnr, cnab, x0f, x0, ent8, ebase, ZB)
