@@ -519,6 +519,32 @@ def test_decision_periods_parity(P, L, N, etas, n):
         assert d.n_seq_periods <= 0.2 * full + d.n_slow_windows, (d.n_seq_periods, full)
 
 
+@pytest.mark.parametrize("P,interval", [(2, 3600), (3, 3600), (12, 3600), (17, 3600), (24, 3600), (48, 3600),
+                                         (24, 1800), (5, 1800)])
+def test_decision_periods_sequential_horizon_paths(P, interval, monkeypatch):
+    """The headline kernel's period paths without the closed form (DESIGN
+    §6.5): CHASE_NO_CFH=1 at T = 24, and T = 48 (half-hourly), where the
+    closed-form table does not fit in shared memory.  Every full period runs
+    its horizon step by step (n_seq_periods counts them); choices and totals
+    still match the oracle exactly."""
+    if interval == 3600:
+        monkeypatch.setenv("CHASE_NO_CFH", "1")
+    T = 86400 // interval
+    L = 24 if interval == 3600 else 48
+    prof = [inputs.make_profile("vit", inputs.LIMITS_9)]
+    N = L + 4100
+    n = 5
+    tr = inputs.synth_traces_host(n, N, seed=700 + P, T=T)
+    J = np.full(n, interval * (N - L) * prof[0].throughput_sps.min())
+    g = run_sweep(tr, N, prof, [0.5], J=J, L=L, period_steps=P, interval_s=interval, forecast=False)
+    g["forecast"] = None
+    o = run_oracle(tr, N, prof, [0.5], J=J, L=L, period_steps=P, interval_s=interval)
+    assert_parity(g, o)
+    d = g["diag"]
+    assert d.kernel_path & cb.PATH_H_PERIODS
+    assert d.n_seq_periods >= n * ((N - L) // P), (d.n_seq_periods, n * ((N - L) // P))
+
+
 def test_decision_periods_fit_forecast_split_path():
     w = inputs.workload("C4", n_traces=17)
     N = 24 + 1000
