@@ -228,7 +228,11 @@ chase_status_t chase_replay(const chase_traces_t* traces, int32_t history_len,
  * window and eta in one pass over the traces (the headline path).  Outputs
  * as above; d_choice / d_forecast / d_per_trace may be NULL.  d_sum is this
  * GPU's per-eta sum; for a multi-GPU sweep the caller all-reduces it (NCCL,
- * e.g. torch.distributed.all_reduce) — nccl_comm must be NULL. */
+ * e.g. torch.distributed.all_reduce) — nccl_comm must be NULL.
+ * A multi-eta call over at most 2368 fp32 traces with no forecast output (and
+ * neither rolling refit nor SVR) runs as n_eta concurrent one-eta sweeps on
+ * streams forked from and joined back into `stream`, each in its own slice of
+ * d_ws (chase_workspace_bytes sizes for it); results are the same. */
 chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg,
                            const chase_profile_t* profiles, int32_t n_profiles,
                            const uint8_t* d_profile_id, const chase_cost_cfg_t* cost,

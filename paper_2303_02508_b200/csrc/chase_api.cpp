@@ -405,6 +405,41 @@ cudaError_t launch_rolling_into(const chase_traces_t* t, const chase_forecast_cf
 
 }  // namespace
 
+// ---- eta-split sweep -------------------------------------------
+// A multi-eta call over few traces (C3: 64 traces x 11 eta) leaves the GPU
+// idle under the one-warp-per-trace multi-eta kernel (64 warps on 148 SMs).
+// Such a call runs as n_eta concurrent one-eta sweeps instead, each through
+// the headline kernel on its own stream and its own slice of the workspace,
+// writing its eta's planes of the outputs; the diagnostics are merged.
+constexpr int64_t kEtaSplitMaxTraces = 2368;  // one warp each: below one wave of 148 x 16 warps
+
+bool eta_split_shape(const chase_traces_t* t, const chase_forecast_cfg_t* f, int n_eta) {
+    return n_eta > 1 && t->n_traces > 0 && t->n_traces <= kEtaSplitMaxTraces && t->dtype == CHASE_F32 &&
+           !rolling(f) && !svr(f) && !getenv("CHASE_NO_ETA_SPLIT");
+}
+
+size_t eta_split_slice_bytes(const chase_traces_t* t, const chase_forecast_cfg_t* f, int n_prof) {
+    const int T = 86400 / t->interval_s;
+    return (size_t)round_up((int64_t)ws_layout(t->n_traces, T, n_prof, 1, t, f).total, 4096);
+}
+
+struct SplitStreams {
+    cudaStream_t s[CHASE_MAX_ETA] = {};
+    cudaEvent_t fork = nullptr, join[CHASE_MAX_ETA] = {};
+    bool ok = false;
+    SplitStreams() {
+        ok = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int e = 0; ok && e < CHASE_MAX_ETA; ++e)
+            ok = cudaStreamCreateWithFlags(&s[e], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&join[e], cudaEventDisableTiming) == cudaSuccess;
+    }
+};
+
+SplitStreams& split_streams() {
+    static thread_local SplitStreams ss;  // per host thread, per process (created on first use)
+    return ss;
+}
+
 extern "C" {
 
 const char* chase_last_error(void) { return g_err; }
@@ -415,7 +450,11 @@ size_t chase_workspace_bytes(const chase_traces_t* traces, const chase_forecast_
                              int32_t n_eta) {
     if (!traces || traces->interval_s <= 0 || 86400 % traces->interval_s || n_profiles < 0 || n_eta < 0) return 0;
     const int T = 86400 / traces->interval_s;
-    return ws_layout(traces->n_traces, T, n_profiles < 1 ? 1 : n_profiles, n_eta < 1 ? 1 : n_eta, traces, fcfg).total;
+    const int np = n_profiles < 1 ? 1 : n_profiles, ne = n_eta < 1 ? 1 : n_eta;
+    size_t bytes = ws_layout(traces->n_traces, T, np, ne, traces, fcfg).total;
+    if (fcfg && eta_split_shape(traces, fcfg, ne))  // room for the eta-split slices (chase_sweep)
+        bytes = std::max(bytes, (size_t)ne * eta_split_slice_bytes(traces, fcfg, np));
+    return bytes;
 }
 
 chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_forecast,
@@ -688,10 +727,45 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     const int T = fcfg->steps_per_day;
     const WsLayout WL = ws_layout(traces->n_traces, T, n_profiles, cost->n_eta, traces, fcfg);
     if ((st = check_ws(d_ws, ws_bytes, WL.total))) return st;
-    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, cost, cost->n_eta);
-    if ((st = check_smem((int)blob.size(), T, traces, cost->n_eta))) return st;
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    if (!d_forecast && eta_split_shape(traces, fcfg, cost->n_eta)) {
+        const size_t slice = eta_split_slice_bytes(traces, fcfg, n_profiles);
+        SplitStreams& ss = split_streams();
+        if (ss.ok && ws_bytes >= (size_t)cost->n_eta * slice) {
+            // n_eta concurrent one-eta sweeps (the headline kernel each), forked from and joined into s
+            chase_diag_t* slice0 = reinterpret_cast<chase_diag_t*>(ws);  // slice 0's diag == the call's (offset 0)
+            ev_start(s);
+            if (cudaEventRecord(ss.fork, s) != cudaSuccess) return cuda_fail(cudaGetLastError(), "eta split fork");
+            cudaEvent_t es = g_ev_start, eo = g_ev_stop;
+            g_ev_start = g_ev_stop = nullptr;  // the inner calls' kernel timing hooks are off; the split is timed whole
+            chase_status_t rs = CHASE_OK;
+            for (int e = 0; e < cost->n_eta && rs == CHASE_OK; ++e) {
+                chase_cost_cfg_t c1 = *cost;
+                c1.eta = cost->eta + e;
+                c1.n_eta = 1;
+                cudaStreamWaitEvent(ss.s[e], ss.fork, 0);
+                rs = chase_sweep(traces, fcfg, profiles, n_profiles, d_profile_id, &c1, d_job_samples,
+                                 d_choice ? d_choice + (int64_t)e * traces->n_traces * ld_c : nullptr, ld_c, nullptr, 0,
+                                 d_per_trace ? d_per_trace + (int64_t)e * traces->n_traces : nullptr, d_sum + e,
+                                 nullptr, ws + (size_t)e * slice, slice, ss.s[e]);
+                cudaEventRecord(ss.join[e], ss.s[e]);
+                cudaStreamWaitEvent(s, ss.join[e], 0);
+            }
+            g_ev_start = es;
+            g_ev_stop = eo;
+            if (rs != CHASE_OK) return rs;
+            // the call's diagnostics: slice 0's (in place at offset 0) plus every other slice's
+            for (int e = 1; e < cost->n_eta; ++e) {
+                cudaError_t me = launch_diag_merge(slice0, reinterpret_cast<chase_diag_t*>(ws + (size_t)e * slice), 0, s);
+                if (me != cudaSuccess) return cuda_fail(me, "eta split diag merge");
+            }
+            ev_stop(s);
+            return CHASE_OK;
+        }
+    }
+    std::vector<uint8_t> blob = build_tables(T, traces->interval_s, profiles, n_profiles, cost, cost->n_eta);
+    if ((st = check_smem((int)blob.size(), T, traces, cost->n_eta))) return st;
     if ((st = upload_tables(blob, ws, WL, s))) return st;
     FitParams fp = make_fit(traces, fcfg->history_len, fcfg, ws, WL, n_profiles, d_profile_id, d_job_samples);
     fp.n_eta = cost->n_eta;

@@ -130,6 +130,28 @@ def test_paper_configs_full_parity(name):
     assert o["totals"]["carbon_g"][0, 0] < o["totals"]["base_carbon_g"][0, 0]
 
 
+@pytest.mark.parametrize("split", [True, False])
+def test_eta_split_small_multi_eta_call(split, monkeypatch):
+    """C3's shape (64 traces, 11 eta, no forecast output): the call runs as 11
+    concurrent one-eta headline sweeps (chase.h); with
+    CHASE_NO_ETA_SPLIT=1 as one multi-eta general sweep.  Both match the
+    oracle: choices and statuses exact, totals within 1e-9."""
+    if not split:
+        monkeypatch.setenv("CHASE_NO_ETA_SPLIT", "1")
+    w = inputs.workload("C3")
+    N = 24 + 3000
+    tr = inputs.synth_traces_host(w.n_traces, N, seed=w.seed, mode=w.mode)
+    J = np.full(w.n_traces, 3600 * (N - 24) * 0.7 * w.profiles[0].throughput_sps.min())
+    g = run_sweep(tr, N, w.profiles, w.etas, J=J, forecast=False)
+    g["forecast"] = None
+    o = run_oracle(tr, N, w.profiles, w.etas, J=J)
+    assert_parity(g, o)
+    path = g["diag"].kernel_path
+    assert path & (cb.PATH_HEADLINE if split else cb.PATH_GENERAL), hex(path)
+    if split:
+        assert not path & cb.PATH_GENERAL, hex(path)
+
+
 def test_multi_profile_multi_eta():
     """C4-shaped (3 profile shapes per trace) with an eta list incl. 0 and 1."""
     w = inputs.workload("C4", n_traces=300)
