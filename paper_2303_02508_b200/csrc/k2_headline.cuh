@@ -36,6 +36,9 @@
 #ifndef CHASE_P2_CF
 #define CHASE_P2_CF 1  // 0: sequential horizons at P = 2 (sweep_fast_kernel<4>; C5 18.7 vs 16.2 ms with the closed form)
 #endif
+#ifndef CHASE_LONG_CF
+#define CHASE_LONG_CF 1  // 1: the closed form for P >= 64 too (sweep_fast_kernel<2>, cfh_setup_long)
+#endif
 #ifndef CHASE_P2_G
 #define CHASE_P2_G 2   // periods per iteration at P = 2 (sweep_fast_kernel<4>; must divide 30)
 #endif
@@ -534,6 +537,87 @@ __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, 
             nr = -__dmul_rd(__dmul_rd(r, Kc), 1.0 - 0x1p-20);
             nab = -__dmul_ru(__dmul_ru(amax, inv), 1.0 + 0x1p-20);
         }
+        K2[n_a] = make_double2(__dmul_rn(h, cs), nr);
+        K2[n_a + 1] = make_double2(nab, 0.0);
+    }
+    __syncwarp();
+}
+
+// The closed-form table for long periods (P >= 64, the 32-period batches of
+// sweep_fast_kernel<2>), built by the whole warp instead of one
+// P-step chain per phase:
+//   K0(phi) = sum_{i<P} A(phi+i) H_{P-i},  H_m = sum_{j<m} w^j = (1 - w^m)/(1 - w),
+// lane l taking the terms i = l (mod 32), then a warp sum; h = w H_P.  Each H
+// carries a relative error <= 3u/(1 - |w|) and the sums add (P + 5)u, inside
+// the same kappa.  The clamp-free start values come from one
+// warp-wide condition instead of each step: for w >= 0 every unclamped x_k >=
+// A_min > 0 once x0 >= 0; for w < 0, x_1 >= A_min - |w| x0 and x_k >= A_min -
+// |w| A_max (k >= 2), so A_min > |w| A_max and x0 < A_min/|w| suffice.
+__device__ __noinline__ void cfh_setup_long(double2* K2, const double* Aeven, int T, int n_a, int Pp, int phase_start,
+                                            double wl, double invK, double Kc, double amax, double amin, int lane) {
+    __syncwarp();  // the A table, written by every lane
+    amax = warp_max_d(amax);
+    amin = -warp_max_d(-amin);
+    const double aw = fabs(wl);
+    bool ok = aw <= 0.99 && amax <= DBL_MAX && invK != 0.0 && Kc > 0.0 && Kc <= DBL_MAX && amin > 0.0;
+    double hi = INFINITY;
+    if (wl < 0.0) {
+        ok = ok && amin > __dmul_ru(__dmul_ru(aw, amax), 1.0 + 0x1p-40);
+        hi = __dmul_rd(__ddiv_rd(amin, aw), 1.0 - 0x1p-40);
+    }
+    const double inv = ok ? __ddiv_ru(1.0, __dsub_rd(1.0, aw)) : 1.0;  // >= 1/(1 - |w|)
+    const double cs = __dmul_rn(1.0 / (double)Pp, invK);
+    const double onew = __dsub_rn(1.0, wl);
+    auto powi = [](double b, int m) {  // b^m by squaring (m >= 0)
+        double r = 1.0;
+        while (m > 0) {
+            if (m & 1) r = __dmul_rn(r, b);
+            b = __dmul_rn(b, b);
+            m >>= 1;
+        }
+        return r;
+    };
+    const double w32 = powi(wl, 32);
+    const float lof = 0.0f, hif = __double2float_rd(hi);
+    const double bounds = __hiloint2double(__float_as_int(hif), __float_as_int(lof));
+    int g = Pp, t = T;
+    while (t) {
+        const int r = g % t;
+        g = t;
+        t = r;
+    }
+    const int nph = T / g;
+    for (int j = 0; j < nph; ++j) {  // warp-uniform loop over the needed phases
+        const int phi = (int)(((int64_t)phase_start + (int64_t)j * g) % T);
+        double sum = 0.0;
+        if (lane < Pp) {
+            // terms i = lane + 32 q, q = qmax .. 0: m = P - i grows by 32 per step
+            const int qmax = (Pp - 1 - lane) / 32;
+            double wm = powi(wl, Pp - lane - 32 * qmax);
+            int p = (int)(((int64_t)phi + lane + 32 * qmax) % T);
+            const int back = 32 % T;
+#pragma unroll 1
+            for (int q = qmax; q >= 0; --q) {
+                const double H = __ddiv_rn(__dsub_rn(1.0, wm), onew);
+                sum = __fma_rn(Aeven[p], H, sum);
+                wm = __dmul_rn(wm, w32);
+                p -= back;
+                if (p < 0) p += T;
+            }
+        }
+        sum = warp_sum(sum);
+        if (lane == 0) K2[phi] = make_double2(__dmul_rn(sum, cs), bounds);
+    }
+    __syncwarp();
+    for (int j = T + lane; j < n_a; j += 32) K2[j] = K2[j % T];
+    if (lane == 0) {
+        double nr = CUDART_NAN, nab = -INFINITY;
+        if (ok) {
+            const double r = __ddiv_rd(30000.0, __dadd_ru(__dmul_ru(2.0, inv), (double)Pp));
+            nr = -__dmul_rd(__dmul_rd(r, Kc), 1.0 - 0x1p-20);
+            nab = -__dmul_ru(__dmul_ru(amax, inv), 1.0 + 0x1p-20);
+        }
+        const double h = __dmul_rn(wl, __ddiv_rn(__dsub_rn(1.0, powi(wl, Pp)), onew));
         K2[n_a] = make_double2(__dmul_rn(h, cs), nr);
         K2[n_a + 1] = make_double2(nab, 0.0);
     }
@@ -1045,7 +1129,7 @@ __device__ __noinline__ uint32_t period_batch(const float* __restrict__ cg, int 
         const uint32_t kk = cfh_choice(K0 + p, hcf, cnr, cnab, x0f, prev, ent8, ebase, ZB);
         if (kk != (uint32_t)kZeroLine) return kk;
     }
-    if (CF) ++n_seq;
+    if (CF && n == Pp) ++n_seq;
     while (k < n) {
         const int seg = min(n - k, tend - p);
         const double* Ap = Aeven + p;
@@ -1257,7 +1341,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 if ((cs + wc - 1) / P.period >= jb + 32) {
                     const int jn = cs / P.period;
                     unsigned ns = 0, nq = 0;
-                    kb = period_batch<false>(traces + i * P.ld + P.a0 + P.off0, jn, P.W, P.period, P.phase_start, T, A_even,
+                    kb = period_batch<CHASE_LONG_CF>(traces + i * P.ld + P.a0 + P.off0, jn, P.W, P.period, P.phase_start, T, A_even,
                                       wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w, hcf, cnr, cnab, lane, ns, nq);
                     if (jn + lane > jb + 31) {  // count only periods the last batch did not decide
                         n_slow += ns;
@@ -1293,19 +1377,24 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     const double c0 = rec[0], wsn = rec[1], wcs = rec[2];
                     const int n_a = haext_len(T);
                     int ph = lane_mod_T;
-                    double amax = 0.0;
+                    double amax = 0.0, amin = DBL_MAX;
                     for (int j = lane; j < n_a; j += 32) {
                         // A(phi) = (c0 + w_sin*S[phi]) + w_cos*C[phi]  (canonical fold of Eq. 1)
                         const int ph1 = ph + 1 == T ? 0 : ph + 1;
                         A_even[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph])), __dmul_rn(wcs, phC[ph]));
                         A_odd[j] = __dadd_rn(__dadd_rn(c0, __dmul_rn(wsn, phS[ph1])), __dmul_rn(wcs, phC[ph1]));
                         amax = fmax(amax, fabs(A_even[j]));
+                        amin = fmin(amin, A_even[j]);
                         ph += 32;
                         while (ph >= T) ph -= T;
                     }
-                    if constexpr (PER && (PM != 4 || CHASE_P2_CF) && PM != 2) {  // (no closed form at P >= 64: §6.5)
+                    if constexpr (PER && (PM != 4 || CHASE_P2_CF)) {
                         if (P.k0len > 0) {
-                            cfh_setup(K0w, A_even, T, n_a, P.period, P.phase_start, wl, invK, Kc, amax, lane);
+                            if constexpr (PM == 2)  // (long P: the warp-wide table)
+                                cfh_setup_long(K0w, A_even, T, n_a, P.period, P.phase_start, wl, invK, Kc, amax, amin,
+                                               lane);
+                            else
+                                cfh_setup(K0w, A_even, T, n_a, P.period, P.phase_start, wl, invK, Kc, amax, lane);
                             hcf = K0w[n_a].x;
                             cnr = K0w[n_a].y;
                             cnab = K0w[n_a + 1].x;
@@ -1370,7 +1459,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     const int cs = c * kHWarpW;
                     if (c == 0) {  // the trace's first batch needs its model (the record, in this stage)
                         jb = 0;
-                        kb = period_batch<false>(traces + i * P.ld + P.a0 + P.off0, jb, P.W, P.period, P.phase_start, T,
+                        kb = period_batch<CHASE_LONG_CF>(traces + i * P.ld + P.a0 + P.off0, jb, P.W, P.period, P.phase_start, T,
                                           A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w, hcf, cnr, cnab, lane, n_slow, n_seq);
                     }
                     period_replay_batch(tv, nwin, cs + j0, P.period, jb, kb, prof_i, chb + j0, a);

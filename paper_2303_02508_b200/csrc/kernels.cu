@@ -193,16 +193,17 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
             q.kc_last = k > kHChunk ? kHChunk : k;
         }
         // decision periods: the closed-form horizon table ({K0, x0min} for haext_len(T)
-        // phases, then {h', -r Kc}, {-A_b, 0}) for 1 < P < 64 (PM 1, PM >= 3) when it fits;
+        // phases, then {h', -r Kc}, {-A_b, 0}) for every P > 1 when it fits;
         // else every period runs its horizon (§6.5)
         q.k0len = 0;
         const int k0len = 2 * (haext_len(p.T) + 2);
-        if (p.period > (CHASE_P2_CF ? 1 : 2) && p.period * 30 < kHWarpW && !getenv("CHASE_NO_CFH") &&
+        if (p.period > (CHASE_P2_CF ? 1 : 2) && (CHASE_LONG_CF || p.period * 30 < kHWarpW) && !getenv("CHASE_NO_CFH") &&
             headline_smem(p.T, p.n_prof, k0len) <= max_smem_optin())
             q.k0len = k0len;
         const int smem = headline_smem(p.T, p.n_prof, q.k0len);
         q.smem_total = smem;
         // decision periods: long ones (at most 31 per warp chunk) in 32-period batches
+        // (lane-direct for them measured slower: P = 168 14.3 vs 12.9 ms, P = 720 16.2 vs 11.6)
         auto kern = p.period <= 1                 ? sweep_fast_kernel<0>
                     : p.period * 30 >= kHWarpW     ? sweep_fast_kernel<2>
                     : kHChunk % p.period != 0      ? sweep_fast_kernel<1>

@@ -175,9 +175,8 @@ def test_periods_band_sweep_max_power(period):
             calls += 1
     full = calls * len(vals) * ((N - 24) // period)
     assert slow > 0, "no period reached the canonical rule: the band was not hit"
-    if period < 64:   # (no closed form for P >= 64: 32-period batches)
-        assert seq < 0.9 * full, f"the closed form decided almost nothing ({seq} of {full} periods sequential)"
-        assert seq > 0
+    assert seq < 0.9 * full, f"the closed form decided almost nothing ({seq} of {full} periods sequential)"
+    assert seq > 0
 
 
 def test_headline_band_sweep_fixed_max_ci():
