@@ -1060,13 +1060,15 @@ __device__ __forceinline__ double horizon_sum(const double* Aeven, int T, int ph
 // split between two lanes is decided by both (the same arithmetic; the lane
 // holding its start counts it in n_slow / n_seq); one that began in an earlier
 // chunk takes k_carry.  The closed form decides, else the sequential horizon.
+template <int PC>
 __device__ __forceinline__ void period_direct(const float* __restrict__ tvs, const float* __restrict__ tv, int nwin,
-                                           int w0, int cs, int Wt, int Pp, int phi0, int T, const double* Aeven,
+                                           int w0, int cs, int Wt, int Pr, int phi0, int T, const double* Aeven,
                                            double wl, double invK, double Kc, const uint2* ent8, int ebase,
                                            uint32_t ZB, const PairTable* pt, const ProfileTable* pf,
                                            const double2* K2, double hcf, double cnr, double cnab, uint32_t k_carry,
                                            int prof, uint8_t* chl, Acc& a, unsigned& n_slow, unsigned& n_seq) {
     if (nwin <= 0) return;
+    const int Pp = PC > 0 ? PC : Pr;  // (PC > 0: P fixed at compile time)
     int b = (w0 / Pp) * Pp;
     int ph = (phi0 - (w0 - b)) % T;  // phase of b (w0 - b < P)
     if (ph < 0) ph += T;
@@ -1210,8 +1212,10 @@ __device__ __forceinline__ void replay_groups(const float* __restrict__ tv, int 
 // chunk, 2 = long periods (P >= kHWarpW/30) decided in 32-period batches, 3 =
 // lane-local periods (P | kHChunk, P known at run time; the last chunk as PM 1),
 // PM >= 4 = the same with P = PM - 2 fixed at compile time (P = 2, 3, 4, 5, 6,
-// 10, 12, 15).  Separate instantiations keep each path's registers apart: one
-// kernel holding all the compile-time P spilled more (P = 12: 14.6 vs 13.6 ms).
+// 10, 12, 15), or lane-direct with P fixed when P does not divide a lane's
+// chunk (PM 26: P = 24, with the closed-form table).  Separate instantiations
+// keep each path's registers apart: one kernel holding all the compile-time P
+// spilled more (P = 12: 14.6 vs 13.6 ms).
 template <int PM>
 #ifdef CHASE_H_MAXNREG
 __global__ void __maxnreg__(CHASE_H_MAXNREG) sweep_fast_kernel(
@@ -1220,6 +1224,10 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
 #endif
     const __grid_constant__ SweepParams P) {
     constexpr bool PER = PM != 0;
+    // PM >= 4: P = PM - 2 fixed at compile time, lane-local when it divides a lane's
+    // chunk, else lane-direct (period_direct<P>, e.g. P = 24)
+    constexpr bool kLaneLocal = PM == 3 || (PM >= 4 && kHChunk % (PM >= 4 ? PM - 2 : 1) == 0);
+    constexpr int kDirectP = (PM >= 4 && !kLaneLocal) ? PM - 2 : 0;
     mark_path(P.diag, PER ? CHASE_PATH_H_PERIODS : CHASE_PATH_HEADLINE);
     extern __shared__ __align__(128) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1445,7 +1453,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
             if (status == 0) {
                 Acc a{0.0, 0.0, 0.0, 0.0, FLT_MAX, 0u, 0, 0};
                 const int ngr = (PER || invK == 0.0) ? 0 : nwin >> 2;
-                if (PM >= 3 && !last) {  // lane-local periods (P | kHChunk): fused decide + replay
+                if (kLaneLocal && !last) {  // lane-local periods (P | kHChunk): fused decide + replay
                     uint8_t* chl = chb + j0;
 #define CHASE_LANE_P(PC) period_lane<PC>(tv, PC, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, K0w + phi0, hcf, cnr, cnab, \
                                          chl, a, n_slow, n_seq)
@@ -1466,7 +1474,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     __syncwarp();
                 } else if (PER && P.k0len > 0) {  // lane-direct periods with the closed form
                     const int wc = last ? P.W_last : kHWarpW;
-                    period_direct(reinterpret_cast<const float*>(stage) + P.off0, tv, nwin, c * kHWarpW + j0,
+                    period_direct<kDirectP>(reinterpret_cast<const float*>(stage) + P.off0, tv, nwin, c * kHWarpW + j0,
                                   c * kHWarpW, P.W, P.period, phi0, T, A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w,
                                   hcf, cnr, cnab, k_carry, prof_i, chb + j0, a, n_slow, n_seq);
                     __syncwarp();

@@ -206,6 +206,7 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
         // (lane-direct for them measured slower: P = 168 14.3 vs 12.9 ms, P = 720 16.2 vs 11.6)
         auto kern = p.period <= 1                 ? sweep_fast_kernel<0>
                     : p.period * 30 >= kHWarpW     ? sweep_fast_kernel<2>
+                    : p.period == 24 && q.k0len > 0 ? sweep_fast_kernel<26>  // daily: lane-direct, P fixed
                     : kHChunk % p.period != 0      ? sweep_fast_kernel<1>
                     : p.period == 2                ? sweep_fast_kernel<4>
                     : p.period == 3                ? sweep_fast_kernel<5>
