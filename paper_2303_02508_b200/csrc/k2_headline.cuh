@@ -642,6 +642,21 @@ __device__ __forceinline__ uint32_t cfh_choice(const double2* kp, double hc, dou
     return (in && __fma_rn(nr, y, x0) <= nab) ? k : (uint32_t)kZeroLine;
 }
 
+// The same decision as its line's shared address (the fused replay loads the
+// line from it directly; the choice byte is its byte 1), ZB on decline.
+__device__ __forceinline__ uint32_t cfh_line(const double2* kp, double hc, double nr, double nab, float x0f, double x0,
+                                             const uint2* ent8, int ebase, uint32_t ZB) {
+    const double2 e = *kp;
+    const double y = __fma_rn(hc, x0, e.x);
+    const bool in = x0f >= __int_as_float(__double2loint(e.y)) && x0f <= __int_as_float(__double2hiint(e.y));
+    const int hk = __double2hiint(y);
+    const int idx = max(min((hk >> kSH) - ebase, kNBUsed - 1), 0);
+    const uint32_t la = line_addr(hk, ent8[idx], ZB);
+    return (in && __fma_rn(nr, y, x0) <= nab) ? la : ZB;
+}
+
+__device__ __forceinline__ uint32_t line_of(int prof, uint32_t k) { return kLineBase + (uint32_t)line_off(prof, (int)k); }
+
 // One period's decision from its horizon mean (the envelope lookup, else the canonical rule).
 __device__ __forceinline__ uint32_t period_choice(double chat, double invK, double Kc, const uint2* ent8, int ebase,
                                                   uint32_t ZB, const PairTable* pt, const ProfileTable* pf,
@@ -861,9 +876,9 @@ __device__ __forceinline__ void replay_run(Acc& a, double2 ln, int m, double cs)
 // (the same sequence replay_groups adds them in).  PC > 0: P known at compile time.
 // The same replay from values already in registers (v[0, PC), PC < 16).
 template <int PC>
-__device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint32_t kk, int prof, uint8_t* chl,
-                                                     Acc& a) {
-    const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+__device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint32_t la, uint8_t* chl, Acc& a) {
+    const double2 ln = lds_line(la);
+    const uint8_t kk = (uint8_t)(la >> 8);  // the choice: byte 1 of the line address
 #pragma unroll
     for (int k = 0; k < PC; ++k) {
         const float raw = v[k];
@@ -873,13 +888,13 @@ __device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint
         a.E = __dadd_rn(a.E, ln.y);
         a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
         a.Cs = __dadd_rn(a.Cs, cw);
-        chl[q + k] = (uint8_t)kk;
+        chl[q + k] = kk;
     }
 }
 
-// One period's replay at its choice kk (windows tv[q, q + Pn)).
+// One period's replay at the line at shared address la (windows tv[q, q + Pn)).
 template <int PC>
-__device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv, int q, int Pn, uint32_t kk, int prof,
+__device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv, int q, int Pn, uint32_t la,
                                                    uint8_t* chl, Acc& a) {
     if (PC > 0 && PC % 4 == 0 && PC < 16) {  // q % 4 == 0 too: LDS.128, conflict-free at the lane stride
         float v[PC > 0 ? PC : 4];
@@ -888,10 +903,11 @@ __device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv,
             const float4 f = *reinterpret_cast<const float4*>(tv + q + 4 * i);
             v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
         }
-        lane_period_replay_v<(PC > 0 ? PC : 4)>(v, q, kk, prof, chl, a);
+        lane_period_replay_v<(PC > 0 ? PC : 4)>(v, q, la, chl, a);
         return;
     }
-    const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+    const double2 ln = lds_line(la);
+    const uint32_t kk = (la >> 8) & 0xffu;
     if (Pn < 16) {  // short runs: per-window sums (independent adds; the run form lengthens the chains)
 #pragma unroll
         for (int k = 0; k < (PC > 0 ? PC : Pn); ++k) {
@@ -937,14 +953,13 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
     }
     // (CHASE_P2_CF = 0: P = 2 keeps its two sequential steps)
     constexpr bool kCF = PN > 2 || CHASE_P2_CF;
-    uint32_t kk[G];
+    uint32_t la[G];  // the periods' line addresses (ZB: not decided yet)
     bool need = !kCF;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        kk[g] = kCF ? cfh_choice(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], ent8, ebase, ZB)
-                    : (uint32_t)kZeroLine;
-        need |= kk[g] == (uint32_t)kZeroLine;
-        if (kCF) n_seq += kk[g] == (uint32_t)kZeroLine ? 1u : 0u;
+        la[g] = kCF ? cfh_line(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], ent8, ebase, ZB) : ZB;
+        need |= la[g] == ZB;
+        if (kCF) n_seq += la[g] == ZB ? 1u : 0u;
     }
     if (need) {  // cold: the sequential horizon (Eq. 1) for the periods the closed form left
 #pragma unroll
@@ -953,14 +968,14 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
             for (int g = 0; g < G; ++g) horizon_step(Ap[q + g * PN + k], wl, pr[g], sm[g]);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            if (kk[g] == (uint32_t)kZeroLine) {
+            if (la[g] == ZB) {
                 const double ch = pow2 ? __dmul_rn(sm[g], invP) : __ddiv_rn(sm[g], dP);
-                kk[g] = period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+                la[g] = line_of(prof, period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
             }
         }
     }
 #pragma unroll
-    for (int g = 0; g < G; ++g) lane_period_replay_v<PN>(v + g * PN, q + g * PN, kk[g], prof, chl, a);
+    for (int g = 0; g < G; ++g) lane_period_replay_v<PN>(v + g * PN, q + g * PN, la[g], chl, a);
     return v[G * PN - 1];
 }
 
@@ -993,10 +1008,10 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         for (int q = 0; q < kHChunk; q += 2 * Pn) {
             const float fa = tv[q - 1], fb = tv[q + Pn - 1];
             double pa = (double)fa, pb = (double)fb, sa = 0.0, sb = 0.0;
-            uint32_t ka = cfh_choice(kq + q, hcf, cnr, cnab, fa, pa, ent8, ebase, ZB);
-            uint32_t kb = cfh_choice(kq + q + Pn, hcf, cnr, cnab, fb, pb, ent8, ebase, ZB);
-            n_seq += (ka == (uint32_t)kZeroLine ? 1u : 0u) + (kb == (uint32_t)kZeroLine ? 1u : 0u);
-            if (ka == (uint32_t)kZeroLine || kb == (uint32_t)kZeroLine) {  // cold: sequential horizons
+            uint32_t ka = cfh_line(kq + q, hcf, cnr, cnab, fa, pa, ent8, ebase, ZB);
+            uint32_t kb = cfh_line(kq + q + Pn, hcf, cnr, cnab, fb, pb, ent8, ebase, ZB);
+            n_seq += (ka == ZB ? 1u : 0u) + (kb == ZB ? 1u : 0u);
+            if (ka == ZB || kb == ZB) {  // cold: sequential horizons
 #pragma unroll
                 for (int k = 0; k < (PC > 0 ? PC : 1); ++k) {
                     horizon_step(Ap[q + k], wl, pa, sa);
@@ -1004,11 +1019,11 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
                 }
                 const double ca = pow2 ? __dmul_rn(sa, invP) : __ddiv_rn(sa, dP);
                 const double cb = pow2 ? __dmul_rn(sb, invP) : __ddiv_rn(sb, dP);
-                if (ka == (uint32_t)kZeroLine) ka = period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
-                if (kb == (uint32_t)kZeroLine) kb = period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+                if (ka == ZB) ka = line_of(prof, period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
+                if (kb == ZB) kb = line_of(prof, period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
             }
-            lane_period_replay<PC>(tv, q, Pn, ka, prof, chl, a);
-            lane_period_replay<PC>(tv, q + Pn, Pn, kb, prof, chl, a);
+            lane_period_replay<PC>(tv, q, Pn, ka, chl, a);
+            lane_period_replay<PC>(tv, q + Pn, Pn, kb, chl, a);
         }
         return;
     }
@@ -1016,15 +1031,15 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
     for (int q = 0; q < kHChunk; q += Pn) {
         const float x0f = tv[q - 1];
         double prev = (double)x0f, sum = 0.0;
-        uint32_t kk = cfh_choice(kq + q, hcf, cnr, cnab, x0f, prev, ent8, ebase, ZB);
-        if (kk == (uint32_t)kZeroLine) {  // cold: the sequential horizon
+        uint32_t la = cfh_line(kq + q, hcf, cnr, cnab, x0f, prev, ent8, ebase, ZB);
+        if (la == ZB) {  // cold: the sequential horizon
             ++n_seq;
 #pragma unroll
             for (int k = 0; k < Pn; ++k) horizon_step(Ap[q + k], wl, prev, sum);
             const double chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
-            kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            la = line_of(prof, period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
         }
-        lane_period_replay<PC>(tv, q, Pn, kk, prof, chl, a);
+        lane_period_replay<PC>(tv, q, Pn, la, chl, a);
     }
 }
 
@@ -1095,11 +1110,11 @@ __device__ __forceinline__ void period_direct(const float* __restrict__ tvs, con
         }
         const int e = min(nwin, b + Pp - w0);
         if (Pp >= 16) {  // the run form for every piece (float4 sums once aligned; short pieces too)
-            const double2 ln = lds_line(kLineBase + (uint32_t)line_off(prof, (int)kk));
+            const double2 ln = lds_line(line_of(prof, kk));
             replay_run(a, ln, e - q, run_csum(tv, q, e, a.vmin));
             fill_bytes(chl, q, e, kk);
         } else {
-            lane_period_replay<0>(tv, q, e - q, kk, prof, chl, a);
+            lane_period_replay<0>(tv, q, e - q, line_of(prof, kk), chl, a);
         }
         q = e;
         b += Pp;

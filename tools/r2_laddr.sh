@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+OUT=gpurun_out/laddr; rm -rf $OUT; mkdir -p $OUT
+timeout 1500 python -m pytest tests -m gpu -q -x -k "period or headline" > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/ab.txt
+for P in 24 12 3 2 7; do
+  bash tools/ab_mode.sh "--steps 10 --warmup 3 --period-steps $P" p24d laddr laddr2 | sed "s/^/P$P /" >> $OUT/ab.txt 2>&1
+done
