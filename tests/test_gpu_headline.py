@@ -302,6 +302,51 @@ def test_nondyadic_headline_fp32():
     assert np.all(o["totals"]["completion_window"] > 0)
 
 
+def shaped_traces(n, N, seed=0):
+    """Non-dyadic fp32 traces of varied shape for the closed-form period
+    horizons: deep diurnal swings (some phases' A(phi) < 0),
+    near-persistent random walks (w_lag near 1), anti-persistent noise
+    (w_lag < 0), near-constant traces and intensities close to zero."""
+    rng = np.random.default_rng(seed)
+    t = np.arange(N)
+    out = np.empty((n, N))
+    for i in range(n):
+        kind = i % 5
+        mean = rng.uniform(50.0, 600.0)
+        if kind == 0:     # persistent (AR(1)) with a deep diurnal forcing: A(phi) < 0 at some phases
+            ph, phi = rng.integers(0, 24), rng.uniform(0.6, 0.9)
+            force = mean * (1.0 + 0.9 * np.sin(2 * np.pi * (t + ph) / 24)) + rng.normal(0, 0.01 * mean, N)
+            v = np.empty(N)
+            v[0] = mean
+            for k in range(1, N):
+                v[k] = phi * v[k - 1] + (1.0 - phi) * force[k]
+        elif kind == 1:   # random walk around the mean
+            v = mean + np.cumsum(rng.normal(0, 0.02 * mean, N))
+        elif kind == 2:   # alternating noise (negative lag coefficient)
+            v = mean + 0.2 * mean * (-1.0) ** t * rng.uniform(0.5, 1.0, N)
+        elif kind == 3:   # near-constant
+            v = mean + rng.normal(0, 1e-3, N)
+        else:             # small intensities
+            v = rng.uniform(0.5, 3.0) * (1.0 + 0.5 * np.sin(2 * np.pi * t / 24)) + rng.normal(0, 0.05, N)
+        out[i] = v
+    return np.maximum(out, 0.01) * (1.0 + 1e-7 * rng.random((n, N)))
+
+
+@pytest.mark.parametrize("P", [2, 3, 5, 12, 24, 48, 168, 720])
+def test_periods_shaped_nondyadic_traces(P):
+    """Decision periods on non-dyadic traces of every shape the closed-form
+    horizon has to handle or decline (clamped horizons, |w_lag| near 1,
+    w_lag < 0, tiny means): choices bit-exact, totals within 1e-9 of the
+    oracle, through the headline kernel's period paths."""
+    n, N = 200, 24 + 3000
+    prof = nondyadic_profile(3)
+    tr = shaped_traces(n, inputs.round_up(N, 4), seed=P).astype(np.float32)
+    J = np.full(n, 3600.0 * (N - 24) * float(prof.throughput_sps.min()) * 0.9)
+    g = gpu_plan(tr, N, [prof], 0.5, J=J, period=P, expect=cb.PATH_H_PERIODS)
+    o = oracle_plan(tr, N, [prof], 0.5, J=J, period=P)
+    assert_same(g, o, exact=False)
+
+
 def _oracle_running_samples(choice, thr, delta):
     """S after each window in the oracle's sequential order (R1: S += Thr_k*Delta)."""
     s, out = 0.0, []
