@@ -755,11 +755,11 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
             g_ev_start = es;
             g_ev_stop = eo;
             if (rs != CHASE_OK) return rs;
-            // the call's diagnostics: slice 0's (in place at offset 0) plus every other slice's
-            for (int e = 1; e < cost->n_eta; ++e) {
-                cudaError_t me = launch_diag_merge(slice0, reinterpret_cast<chase_diag_t*>(ws + (size_t)e * slice), 0, s);
-                if (me != cudaSuccess) return cuda_fail(me, "eta split diag merge");
-            }
+            // the call's diagnostics: slice 0's (in place at offset 0) with the other slices folded in
+            const WsLayout WS1 = ws_layout(traces->n_traces, T, n_profiles, 1, traces, fcfg);
+            cudaError_t me = launch_diag_merge_eta(slice0, ws, slice, WS1.diag, WS1.status, cost->n_eta,
+                                                   traces->n_traces, s);
+            if (me != cudaSuccess) return cuda_fail(me, "eta split diag merge");
             ev_stop(s);
             return CHASE_OK;
         }

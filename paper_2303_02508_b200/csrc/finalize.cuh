@@ -171,6 +171,35 @@ __global__ void diag_merge_kernel(chase_diag_t* acc, chase_diag_t* chunk, int64_
     acc->kernel_path |= chunk->kernel_path;
 }
 
+// chase_sweep's eta split: fold the one-eta slices' diagnostics
+// into slice 0's (in place).  Every slice validates the same traces, so n_bad
+// and first_bad stay slice 0's; n_exhausted is recounted per trace from the
+// slices' status bytes (a trace counts once, at its worst status over the
+// eta, as finalize_kernel counts it); the rest add up.
+__global__ void diag_merge_eta_kernel(chase_diag_t* acc, const uint8_t* ws, size_t slice, size_t diag_off,
+                                      size_t status_off, int n_eta, int64_t n) {
+    __shared__ unsigned long long ex;
+    if (threadIdx.x == 0) ex = 0;
+    __syncthreads();
+    unsigned long long mine = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        uint8_t worst = 0;
+        for (int e = 0; e < n_eta; ++e) worst = max(worst, ws[(size_t)e * slice + status_off + i]);
+        mine += worst == CHASE_ERR_TRACE_EXHAUSTED ? 1ull : 0ull;
+    }
+    atomicAdd(&ex, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        acc->n_exhausted = ex;
+        for (int e = 1; e < n_eta; ++e) {
+            const chase_diag_t* d = reinterpret_cast<const chase_diag_t*>(ws + (size_t)e * slice + diag_off);
+            acc->n_slow_windows += d->n_slow_windows;
+            acc->n_seq_periods += d->n_seq_periods;
+            acc->kernel_path |= d->kernel_path;
+        }
+    }
+}
+
 __global__ void accumulate_sums_kernel(double* acc, const double* add, int n) {
     const int q = threadIdx.x;
     if (q < n) acc[q] = __dadd_rn(acc[q], add[q]);

@@ -564,6 +564,13 @@ cudaError_t launch_diag_merge(chase_diag_t* acc, chase_diag_t* chunk, int64_t c0
     return cudaGetLastError();
 }
 
+cudaError_t launch_diag_merge_eta(chase_diag_t* acc, const uint8_t* ws, size_t slice, size_t diag_off,
+                                  size_t status_off, int n_eta, int64_t n, cudaStream_t s) {
+    diag_merge_eta_kernel<<<1, 256, 0, s>>>(acc, ws, slice, diag_off, status_off, n_eta, n);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_accumulate(double* acc, const double* add, int n, cudaStream_t s) {
     accumulate_sums_kernel<<<1, 128, 0, s>>>(acc, add, n);
     ++g_launches;

@@ -169,6 +169,8 @@ cudaError_t launch_diag_reset(chase_diag_t* diag, cudaStream_t s);
 // chase_sweep_host: fold a chunk's diagnostics into acc (c0 = its first trace; c0 == 0 resets
 // acc first); c0 < 0 copies acc back into `chunk` (the workspace's diagnostics)
 cudaError_t launch_diag_merge(chase_diag_t* acc, chase_diag_t* chunk, int64_t c0, cudaStream_t s);
+cudaError_t launch_diag_merge_eta(chase_diag_t* acc, const uint8_t* ws, size_t slice, size_t diag_off,
+                                  size_t status_off, int n_eta, int64_t n, cudaStream_t s);
 cudaError_t launch_accumulate(double* acc, const double* add, int n, cudaStream_t s);
 uint64_t kernel_launches();
 

@@ -130,26 +130,34 @@ def test_paper_configs_full_parity(name):
     assert o["totals"]["carbon_g"][0, 0] < o["totals"]["base_carbon_g"][0, 0]
 
 
-@pytest.mark.parametrize("split", [True, False])
-def test_eta_split_small_multi_eta_call(split, monkeypatch):
+def test_eta_split_small_multi_eta_call(monkeypatch):
     """C3's shape (64 traces, 11 eta, no forecast output): the call runs as 11
     concurrent one-eta headline sweeps (chase.h); with
     CHASE_NO_ETA_SPLIT=1 as one multi-eta general sweep.  Both match the
-    oracle: choices and statuses exact, totals within 1e-9."""
-    if not split:
-        monkeypatch.setenv("CHASE_NO_ETA_SPLIT", "1")
+    oracle (choices and statuses exact, totals within 1e-9), including an
+    invalid trace and a trace whose job cannot finish, and report the same
+    diagnostics (n_bad, first bad trace, n_exhausted counted per trace)."""
     w = inputs.workload("C3")
     N = 24 + 3000
     tr = inputs.synth_traces_host(w.n_traces, N, seed=w.seed, mode=w.mode)
+    tr[5, 900] = -1.0                       # status 4 (S:29)
     J = np.full(w.n_traces, 3600 * (N - 24) * 0.7 * w.profiles[0].throughput_sps.min())
-    g = run_sweep(tr, N, w.profiles, w.etas, J=J, forecast=False)
-    g["forecast"] = None
+    J[9] = 1e30                             # never completes: status 3 for every eta
     o = run_oracle(tr, N, w.profiles, w.etas, J=J)
-    assert_parity(g, o)
-    path = g["diag"].kernel_path
-    assert path & (cb.PATH_HEADLINE if split else cb.PATH_GENERAL), hex(path)
-    if split:
-        assert not path & cb.PATH_GENERAL, hex(path)
+    diags = {}
+    for split in (True, False):
+        if not split:
+            monkeypatch.setenv("CHASE_NO_ETA_SPLIT", "1")
+        g = run_sweep(tr, N, w.profiles, w.etas, J=J, forecast=False)
+        g["forecast"] = None
+        assert_parity(g, o)
+        d = g["diag"]
+        assert d.kernel_path & (cb.PATH_HEADLINE if split else cb.PATH_GENERAL), hex(d.kernel_path)
+        if split:
+            assert not d.kernel_path & cb.PATH_GENERAL, hex(d.kernel_path)
+        diags[split] = (d.n_bad, d.first_bad_trace, d.first_bad_status, d.n_exhausted)
+    assert diags[True] == diags[False], diags
+    assert diags[True][0] == 1 and diags[True][1] == 5 and diags[True][3] == 1, diags
 
 
 def test_multi_profile_multi_eta():
