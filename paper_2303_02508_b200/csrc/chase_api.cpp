@@ -278,10 +278,14 @@ struct Prepared {
 };
 
 chase_status_t upload_tables(const std::vector<uint8_t>& blob, uint8_t* ws, const WsLayout& L, cudaStream_t s) {
-    cudaError_t e = launch_upload(blob.data(), blob.size(), ws + L.tables, s);
+    // the first upload launch also resets the diagnostics (one launch fewer per call)
+    chase_diag_t* diag = reinterpret_cast<chase_diag_t*>(ws + L.diag);
+    cudaError_t e = launch_upload(blob.data(), blob.size(), ws + L.tables, s, diag);
     if (e != cudaSuccess) return cuda_fail(e, "upload tables");
-    e = launch_diag_reset(reinterpret_cast<chase_diag_t*>(ws + L.diag), s);
-    if (e != cudaSuccess) return cuda_fail(e, "diag reset");
+    if (blob.empty()) {
+        e = launch_diag_reset(diag, s);
+        if (e != cudaSuccess) return cuda_fail(e, "diag reset");
+    }
     return CHASE_OK;
 }
 

@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const __grid_cons
             double acc = 0.0;
             for (int t = 0; t < kFinThreads; ++t) acc = __dadd_rn(acc, red[t][threadIdx.x]);
             p.block_sums[((int64_t)blockIdx.x * p.n_eta + e) * 8 + threadIdx.x] = acc;
+            // one block: finalize_sums_kernel would fold exactly this value (0 + acc, + 0s)
+            if (p.sum_direct) reinterpret_cast<double*>(p.sum_direct + e)[threadIdx.x] = acc;
         }
         __syncthreads();
     }
@@ -121,8 +123,13 @@ __global__ void __launch_bounds__(256) finalize_sums_kernel(const double* block_
 
 // Invalid traces (status 4..7; listed by the sweep kernels as they finish a
 // trace): choices 0xFF, forecasts NaN.
-__global__ void fixup_kernel(const int64_t* bad_list, const chase_diag_t* diag, int64_t n, uint8_t* choice,
-                             int64_t ld_c, int64_t W, int n_eta, double* forecast, int64_t ld_f) {
+__global__ void fixup_kernel(const int64_t* bad_list, chase_diag_t* diag, int64_t n, uint8_t* choice,
+                             int64_t ld_c, int64_t W, int n_eta, double* forecast, int64_t ld_f,
+                             const uint8_t* status) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // (diag_status_kernel's work, one launch fewer)
+        const uint64_t fb = (uint64_t)diag->first_bad_trace;
+        if (fb < (uint64_t)n) diag->first_bad_status = status[fb];
+    }
     const int64_t n_bad = (int64_t)diag->n_bad;
     for (int64_t b = blockIdx.x; b < n_bad; b += gridDim.x) {
         const int64_t i = bad_list[b];
@@ -255,7 +262,12 @@ __global__ void __launch_bounds__(256) plan_kernel(const __grid_constant__ PlanP
 struct UploadChunk {
     uint8_t bytes[30720];
 };
-__global__ void upload_kernel(const __grid_constant__ UploadChunk c, int n, uint8_t* dst) {
+__global__ void upload_kernel(const __grid_constant__ UploadChunk c, int n, uint8_t* dst, chase_diag_t* reset) {
+    if (reset && threadIdx.x == 0) {  // (diag_reset_kernel's work, one launch fewer)
+        reset->first_bad_trace = -1;
+        reset->first_bad_status = 0;
+        reset->n_bad = reset->n_exhausted = reset->n_slow_windows = reset->kernel_path = reset->n_seq_periods = 0;
+    }
     for (int q = threadIdx.x; q < n; q += blockDim.x) dst[q] = c.bytes[q];
 }
 

@@ -389,8 +389,12 @@ __global__ void __launch_bounds__(128) fit_kernel(const __grid_constant__ FitPar
         }
     }
     __syncthreads();
-    if (staged) {  // the job-start phase record (fit_phase_kernel, once per call)
-        for (int q = threadIdx.x; q < phase_stride(L); q += blockDim.x) prec[q] = p.prec[q];
+    if (staged) {  // the job-start phase record (fit_phase_kernel, once per call; one CTA: here)
+        if (gridDim.x == 1) {
+            if (threadIdx.x == 0) phase_record(tab, tab + T, T, L, p.phase0 % T, prec);
+        } else {
+            for (int q = threadIdx.x; q < phase_stride(L); q += blockDim.x) prec[q] = p.prec[q];
+        }
     }
     __syncthreads();
     const int64_t i = first + threadIdx.x;

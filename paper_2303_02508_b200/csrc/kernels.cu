@@ -81,13 +81,13 @@ size_t sweep_smem_bytes(int tables_bytes, int T, int elem_size, int mode) {  // 
 
 int64_t finalize_grid(int64_t n_traces) { return (n_traces + kFinThreads - 1) / kFinThreads; }
 
-cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_t s) {
+cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_t s, chase_diag_t* reset) {
     const uint8_t* h = static_cast<const uint8_t*>(host);
     for (size_t off = 0; off < bytes; off += sizeof(UploadChunk)) {
         UploadChunk c;
         const size_t n = bytes - off < sizeof(UploadChunk) ? bytes - off : sizeof(UploadChunk);
         memcpy(c.bytes, h + off, n);
-        upload_kernel<<<1, 256, 0, s>>>(c, (int)n, static_cast<uint8_t*>(dst) + off);
+        upload_kernel<<<1, 256, 0, s>>>(c, (int)n, static_cast<uint8_t*>(dst) + off, off == 0 ? reset : nullptr);
         ++g_launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -97,13 +97,13 @@ cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_
 
 cudaError_t launch_fit(const FitParams& p, cudaStream_t s) {
     if (p.n_traces <= 0) return cudaSuccess;
-    if (!p.baseline_only && p.L <= 64) {
+    const unsigned grid = (unsigned)((p.n_traces + 127) / 128);
+    if (!p.baseline_only && p.L <= 64 && grid > 1) {  // (one CTA computes the record itself)
         fit_phase_kernel<<<1, 1, 0, s>>>(p.tables, p.T, p.L, p.phase0, p.prec);
         ++g_launches;
     }
     const int esz = p.is_f64 ? 8 : 4;
     const int smem = round16(128 * 65 * esz) + 2 * p.T * 8 + (p.L <= 64 ? phase_stride(p.L) * 8 : 0);
-    const unsigned grid = (unsigned)((p.n_traces + 127) / 128);
     if (p.is_f64) {
         cudaFuncSetAttribute(fit_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         fit_kernel<double><<<grid, 128, smem, s>>>(p);
@@ -519,12 +519,12 @@ cudaError_t launch_fixup(const uint8_t* status, const int64_t* bad_list, int64_t
                          int64_t ld_c, int64_t W, int n_eta_choice, double* forecast, int64_t ld_f,
                          chase_diag_t* diag, cudaStream_t s) {
     if (n_traces <= 0) return cudaSuccess;
-    if (choice || forecast) {
+    if (choice || forecast) {  // (with the first-bad status)
         fixup_kernel<<<(unsigned)(2 * num_sms()), 256, 0, s>>>(bad_list, diag, n_traces, choice, ld_c, W, n_eta_choice,
-                                                                forecast, ld_f);
-        ++g_launches;
+                                                                forecast, ld_f, status);
+    } else {
+        diag_status_kernel<<<1, 32, 0, s>>>(status, n_traces, diag);
     }
-    diag_status_kernel<<<1, 32, 0, s>>>(status, n_traces, diag);
     ++g_launches;
     return cudaGetLastError();
 }
@@ -534,12 +534,14 @@ cudaError_t launch_finalize(const FinalizeParams& p, const int64_t* bad_list, ch
                             cudaStream_t s) {
     if (p.n_traces > 0) {
         const int64_t grid = finalize_grid(p.n_traces);
-        if (p.is_f64) finalize_kernel<double><<<(unsigned)grid, kFinThreads, 0, s>>>(p);
-        else finalize_kernel<float><<<(unsigned)grid, kFinThreads, 0, s>>>(p);
+        FinalizeParams q = p;
+        q.sum_direct = grid == 1 ? sum : nullptr;  // one block writes the sums itself
+        if (p.is_f64) finalize_kernel<double><<<(unsigned)grid, kFinThreads, 0, s>>>(q);
+        else finalize_kernel<float><<<(unsigned)grid, kFinThreads, 0, s>>>(q);
         ++g_launches;
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        if (sum) {
+        if (sum && grid > 1) {
             finalize_sums_kernel<<<p.n_eta, 256, 0, s>>>(p.block_sums, grid, p.n_eta, sum);
             ++g_launches;
         }

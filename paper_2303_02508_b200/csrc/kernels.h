@@ -96,6 +96,7 @@ struct FinalizeParams {
     chase_totals_t* per_trace;    // may be null
     double* block_sums;           // [grid][n_eta][8]
     chase_diag_t* diag;
+    chase_sum_t* sum_direct;      // one-block launch: the block writes the per-eta sums itself
 };
 
 struct PlanParams {
@@ -115,7 +116,7 @@ size_t sweep_smem_bytes(int tables_bytes, int T, int elem_size, int mode);
 int sweep_stage_bytes(int elem_size);
 int64_t finalize_grid(int64_t n_traces);
 
-cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_t s);
+cudaError_t launch_upload(const void* host, size_t bytes, void* dst, cudaStream_t s, chase_diag_t* reset = nullptr);
 cudaError_t launch_fit(const FitParams& p, cudaStream_t s);
 // the specialised headline kernel applies (fp32, aligned, one eta, no forecast in/out); it also
 // runs decision periods in place (p.period > 1), every other period path is forecast-first
