@@ -162,7 +162,7 @@ def ncu_traffic_per_window(config: str):
     if not os.path.exists(path):
         return None
     d = json.load(open(path))
-    e = d.get(config) or (None if "_p" in config else d.get("default"))
+    e = d.get(config) or (None if "_" in config else d.get("default"))
     return None if e is None else float(e["dram_bytes_per_window"])
 
 
@@ -479,10 +479,12 @@ def main_chase(args):
         fused = bool(diag.kernel_path & cb.PATH_ROLL_FUSED)
         flops = rolling_fused_flops(w, R) if fused else rolling_flops(w, R)
         achieved = flops / (kern_ms / 1e3) / 1e12
+        tpw = ncu_traffic_per_window(f"{args.config}_roll{R}") if fused else None
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": planner_kernel_name(w, R),
+                    "traffic": None if tpw is None else tpw * n * W, "kernel": planner_kernel_name(w, R),
                     "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
-                    "algorithmic_flops_per_launch": flops, "peak_source": peak_src}
+                    "algorithmic_flops_per_launch": flops, "peak_source": peak_src,
+                    "dram_bytes_per_window": tpw}
 
     latency = None
     if n_total <= 64 and world == 1:   # C1 / C2: one trace, latency-bound

@@ -27,6 +27,12 @@ constexpr int kRLThreads = 32 * kRLWarps;
 #ifndef CHASE_RL_TILE
 #define CHASE_RL_TILE 64
 #endif
+#ifndef CHASE_RL_ALIGN
+#define CHASE_RL_ALIGN 1  // 1: tiles after the first start on 128-B boundaries
+#endif
+#ifndef CHASE_RL_HALO_COPY
+#define CHASE_RL_HALO_COPY 1  // 1: tiles after a trace's first load only their own windows (4 B/window)
+#endif
 #ifndef CHASE_RL_MINB
 #define CHASE_RL_MINB 1
 #endif
@@ -183,7 +189,13 @@ __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(co
     const float* traces = reinterpret_cast<const float*>(P.traces);
     const int64_t n_groups = (P.n_traces + 31) / 32;
     const int64_t GW = (int64_t)gridDim.x * kRLWarps;
-    const int n_tiles = (W + kRLTile - 1) / kRLTile;
+    // tiles: the first runs from the job start s0 to the next 128-B boundary past it plus
+    // one tile, the rest start on 128-B boundaries (whole L2 lines: the per-lane loads
+    // of 256 B then touch 2 lines, not 3)
+    const int tbase = CHASE_RL_ALIGN ? (s0 & ~31) : s0;
+    const int n_tiles = (P.N - tbase + kRLTile - 1) / kRLTile;
+    auto tile_ab = [&](int t) { return t == 0 ? s0 : tbase + t * kRLTile; };
+    auto tile_end = [&](int t) { return min(tbase + (t + 1) * kRLTile, P.N); };
     const bool store_choice = P.choice != nullptr;
 
     // producer: every lane loads its own trace's row of the tile (a unit = (group, tile))
@@ -194,13 +206,17 @@ __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(co
         if (pg >= n_groups) return;
         const int slot = produced & 1;
         const int64_t i = pg * 32 + lane;
-        const int c0 = s0 + pt_ * kRLTile - L;               // first column of the tile's row
-        const int c1 = min(s0 + (pt_ + 1) * kRLTile, P.N);
+        // a trace's first tile brings its L-value history; later tiles only their own
+        // windows (their halo c[ab - L, ab) is copied from the previous tile's row)
+        const int skip = pt_ == 0 || !CHASE_RL_HALO_COPY ? 0 : L;
+        const int c0 = tile_ab(pt_) - L + skip;               // first column loaded
+        const int c1 = tile_end(pt_);
         const uint32_t bytes = i < P.n_traces ? (uint32_t)(((c1 - c0) * 4 + 15) & ~15) : 0u;
-        CHASE_CHECK(c1 - c0 <= stride);
+        CHASE_CHECK(c1 - c0 + skip <= stride);
         uint64_t* bar = mbar + slot;
         mbar_arrive_expect_tx(bar, bytes);
-        if (bytes) bulk_g2s(ring + (slot * 32 + lane) * stride, traces + i * P.ld + c0, bytes, bar, evict_first_policy());
+        if (bytes)
+            bulk_g2s(ring + (slot * 32 + lane) * stride + skip, traces + i * P.ld + c0, bytes, bar, evict_first_policy());
         ++produced;
         if (++pt_ == n_tiles) {
             pt_ = 0;
@@ -257,8 +273,8 @@ __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(co
             const int slot = consumed & 1;
             mbar_wait(mbar + slot, (consumed >> 1) & 1u);
             k.row = ring + (slot * 32 + lane) * stride;  // row[q] = c[ab - L + q]
-            k.ab = s0 + tl * kRLTile;                     // absolute index of the tile's window 0
-            k.nw = min(kRLTile, W - tl * kRLTile);
+            k.ab = tile_ab(tl);                           // absolute index of the tile's window 0
+            k.nw = tile_end(tl) - k.ab;
             const float* cv = k.row + L - k.ab;           // cv[a] = c[a] for a in [ab - L, ab + 64)
             CHASE_CHECK(L + k.nw <= stride);
             if (tl == 0) {
@@ -294,9 +310,15 @@ __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(co
             }
             __syncwarp();
             if (store_choice && k.live) {  // this lane's choice bytes of the tile
-                uint8_t* dst = P.choice + i * P.ld_c + tl * kRLTile;
-                const int nb = (k.nw + 15) & ~15;
-                for (int q = 0; q < nb / 4; ++q) reinterpret_cast<uint32_t*>(dst)[q] = chw[q];
+                uint8_t* dst = P.choice + i * P.ld_c + (k.ab - s0);  // (4-byte aligned: L % 4 == 0)
+                for (int q = 0; q < (k.nw + 3) / 4; ++q) reinterpret_cast<uint32_t*>(dst)[q] = chw[q];
+            }
+            if (CHASE_RL_HALO_COPY && tl + 1 < n_tiles) {
+                // the next tile's halo c[ab + 64 - L, ab + 64): this row's last L values, into
+                // the head of the next slot's row (its TMA load writes only past the head)
+                float* nrow = ring + (((consumed + 1) & 1) * 32 + lane) * stride;
+                for (int q = 0; q < L; q += 4)
+                    *reinterpret_cast<float4*>(nrow + q) = *reinterpret_cast<const float4*>(k.row + k.nw + q);
             }
             __syncwarp();
             issue();  // this slot is free again (every lane has read its row)
