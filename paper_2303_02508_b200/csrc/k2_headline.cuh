@@ -221,11 +221,11 @@ __device__ __forceinline__ void hot_groups(const float* __restrict__ tv, int ngr
 // (one DFMA instead of DMUL, DADD, DMUL), and the fp32 values become fp64 on
 // the integer pipes.  |y - x/Kc| <= 6u (|A| + |w_lag c|)/Kc for the canonical
 // forecast x = fl(A + fl(w_lag c)) (Q24), which the kernel keeps below
-// (512 - 2)u y_min: the envelope intervals are shrunk by 512u (envelope.cpp),
-// so a key inside a shrunk interval puts x/Kc inside the verified one and the
-// canonical rule picks that line (the same proof as the exact key's, with a
-// wider margin).  The bound holds when |A[phi]| <= Amax and every value lies
-// in [FLT_MIN, c_lim], c_lim = (85 y_min Kc - Amax)/|w_lag|; a chunk with a
+// 126000u y_min: the envelope intervals are shrunk by s = 2^-36 = 131072u
+// (envelope.cpp), so a key inside a shrunk interval puts x/Kc inside the
+// verified one and the canonical rule picks that line (the same proof as the
+// exact key's, with a wider margin).  The bound holds when |A[phi]| <= Amax and
+// every value lies in [FLT_MIN, c_lim], c_lim = (21000 y_min Kc - Amax)/|w_lag|; a chunk with a
 // value outside (a zero, a subnormal, a negative, inf/NaN, or too large) is
 // redone with the exact key (lane_exact, cold).
 
@@ -1427,10 +1427,10 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                         }
                     }
                     if constexpr (PM == 0 && CHASE_H0_FAST) {
-                        // the one-fma key's bound: 6u (|A| + |w_lag| c)/Kc <= 510u y_min, i.e.
-                        // |A| + |w_lag| c <= 85 y_min Kc (envelope.cpp shrinks by 2^-36 >= 512u)
+                        // the one-fma key's bound: 6u (|A| + |w_lag| c)/Kc <= 126000u y_min, i.e.
+                        // |A| + |w_lag| c <= 21000 y_min Kc (envelope.cpp shrinks by 2^-36)
                         amax = warp_max_d(amax);
-                        const double lam = __dmul_rn(__dmul_rn(85.0, pt->y_min), Kc);
+                        const double lam = __dmul_rd(__dmul_rd(21000.0, pt->y_min), Kc);
                         if (!pt->k0 && invK != 0.0 && amax < lam && fabs(wl) <= DBL_MAX) {
                             const double awl = fabs(wl);
                             const double cl = awl > 0.0 ? __ddiv_rd(__dsub_rd(lam, amax), awl) : (double)FLT_MAX;
