@@ -77,7 +77,7 @@ def build_chase(force=False):
             _run([NVCC, *ARCH, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", *common,
                   "-c", s, "-o", o])
         objs.append(o)
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-ldl"])
     return out
 
 

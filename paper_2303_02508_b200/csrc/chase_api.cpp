@@ -2,6 +2,7 @@
 // validation, the per-call constant tables (phase table, profiles, Eq. 6
 // envelope buckets), workspace layout and kernel launch planning.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost a null check unless a tool attaches
 
 #include <cmath>
 #include <cstdarg>
@@ -17,6 +18,14 @@
 using namespace chase;
 
 namespace {
+
+// NVTX range over a C-ABI call or one of its stages (nsys / ncu --nvtx timelines)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 thread_local char g_err[512] = "";
 thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;
@@ -464,6 +473,7 @@ size_t chase_workspace_bytes(const chase_traces_t* traces, const chase_forecast_
 chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_forecast,
                                   int64_t ld_f, double* d_max_ci, double* d_models, void* d_ws, size_t ws_bytes,
                                   void* stream) {
+    const Nvtx nvtx_call("chase_fit_forecast");
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
     const int64_t W = traces->n_steps - fcfg->history_len;
@@ -502,6 +512,7 @@ chase_status_t chase_fit_forecast(const chase_traces_t* traces, const chase_fore
 
 chase_status_t chase_forecast_mape(const chase_traces_t* traces, const chase_forecast_cfg_t* fcfg, double* d_mape,
                                    int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+    const Nvtx nvtx_call("chase_forecast_mape");
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
     if (rolling(fcfg) || periods(fcfg))
@@ -539,6 +550,7 @@ chase_status_t chase_timeline(const chase_traces_t* traces, int32_t history_len,
                               const chase_profile_t* profiles, int32_t n_profiles, const uint8_t* d_profile_id,
                               const double* d_job_samples, const int64_t* d_trace_ids, int64_t m, double* d_rows,
                               double* d_summary, void* d_ws, size_t ws_bytes, void* stream) {
+    const Nvtx nvtx_call("chase_timeline");
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_profiles(profiles, n_profiles))) return st;
     if (history_len < 1 || traces->n_steps <= history_len) return fail(CHASE_ERR_INVALID, "history_len");
@@ -571,6 +583,7 @@ chase_status_t chase_profiling_overhead(const chase_traces_t* traces, int32_t hi
                                         const chase_profile_t* profiles, int32_t n_profiles,
                                         const uint8_t* d_profile_id, double* d_out, void* d_ws, size_t ws_bytes,
                                         void* stream) {
+    const Nvtx nvtx_call("chase_profiling_overhead");
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_profiles(profiles, n_profiles))) return st;
     int kmax = 0;
@@ -600,6 +613,7 @@ chase_status_t chase_period_costs(const double* d_forecast, int64_t n_traces, in
                                   const uint8_t* d_profile_id, const chase_cost_cfg_t* cost, const double* d_max_ci,
                                   const int64_t* d_trace_ids, int64_t m, double* d_costs, int32_t ld_k, void* d_ws,
                                   size_t ws_bytes, void* stream) {
+    const Nvtx nvtx_call("chase_period_costs");
     chase_status_t st;
     if (n_traces < 0 || W < 1 || ld_f < W) return fail(CHASE_ERR_INVALID, "n_traces < 0, W < 1 or ld_f < W");
     if (period_steps < 0) return fail(CHASE_ERR_INVALID, "period_steps < 0");
@@ -631,6 +645,7 @@ chase_status_t chase_plan_power_limits(const double* d_forecast, int64_t n_trace
                                        const uint8_t* d_profile_id, const chase_cost_cfg_t* cost,
                                        const double* d_max_ci, uint8_t* d_choice, int64_t ld_c, void* d_ws,
                                        size_t ws_bytes, void* stream) {
+    const Nvtx nvtx_call("chase_plan_power_limits");
     chase_status_t st;
     if (n_traces < 0 || W < 1 || ld_f < W) return fail(CHASE_ERR_INVALID, "n_traces < 0, W < 1 or ld_f < W");
     if ((st = check_profiles(profiles, n_profiles)) || (st = check_cost(cost, profiles, n_profiles))) return st;
@@ -674,6 +689,7 @@ chase_status_t chase_replay(const chase_traces_t* traces, int32_t history_len, c
                             int32_t n_eta, const chase_profile_t* profiles, int32_t n_profiles,
                             const uint8_t* d_profile_id, const double* d_job_samples, chase_totals_t* d_per_trace,
                             chase_sum_t* d_sum, void* d_ws, size_t ws_bytes, void* stream) {
+    const Nvtx nvtx_call("chase_replay");
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_profiles(profiles, n_profiles))) return st;
     if (history_len < 1 || traces->n_steps <= history_len) return fail(CHASE_ERR_INVALID, "history_len");
@@ -719,6 +735,7 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
                            const chase_cost_cfg_t* cost, const double* d_job_samples, uint8_t* d_choice, int64_t ld_c,
                            double* d_forecast, int64_t ld_f, chase_totals_t* d_per_trace, chase_sum_t* d_sum,
                            void* nccl_comm, void* d_ws, size_t ws_bytes, void* stream) {
+    const Nvtx nvtx_call("chase_sweep");
     chase_status_t st;
     if ((st = check_traces(traces)) || (st = check_fcfg(traces, fcfg))) return st;
     if ((st = check_profiles(profiles, n_profiles)) || (st = check_cost(cost, profiles, n_profiles))) return st;
@@ -774,7 +791,11 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     FitParams fp = make_fit(traces, fcfg->history_len, fcfg, ws, WL, n_profiles, d_profile_id, d_job_samples);
     fp.n_eta = cost->n_eta;
     fp.max_ci_fixed = cost->max_ci;
-    cudaError_t e = launch_fit(fp, s);
+    cudaError_t e;
+    {
+        const Nvtx r("chase_sweep/fit");
+        e = launch_fit(fp, s);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
     SweepParams p = base_sweep(traces, fcfg->history_len, WL, ws, (int)blob.size());
     p.n_eta = cost->n_eta;
@@ -823,7 +844,10 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
         aligned = aligned && ldf % 2 == 0 && ((uintptr_t)fc & 15) == 0;
     }
     if (!rolling(fcfg) && !svr(fcfg)) ev_start(s);
-    e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p, s);
+    {
+        const Nvtx r("chase_sweep/predict+argmin+replay");
+        e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p, s);
+    }
     if (!rolling(fcfg) && !svr(fcfg)) ev_stop(s);
     if (e != cudaSuccess) return cuda_fail(e, "sweep kernel");
     FinalizeParams fz = make_finalize(traces, fcfg->history_len, cost->n_eta, n_profiles, ws, WL, d_profile_id,
@@ -860,6 +884,7 @@ chase_status_t chase_sweep_host(const chase_traces_t* h_traces, const chase_fore
                                 const chase_cost_cfg_t* cost, const double* h_job_samples, int64_t chunk_traces,
                                 chase_sum_t* h_sum, void* d_staging, size_t staging_bytes, void* d_ws,
                                 size_t ws_bytes, void* stream) {
+    const Nvtx nvtx_call("chase_sweep_host");
     chase_status_t st;
     if ((st = check_traces(h_traces)) || (st = check_fcfg(h_traces, fcfg))) return st;
     if ((st = check_profiles(profiles, n_profiles)) || (st = check_cost(cost, profiles, n_profiles))) return st;

@@ -13,6 +13,6 @@ nvcc $ARCH -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v -Xcompiler -fPIC -I $
     -c $C/kernels.cu -o $O/kernels.o 2>&1 | grep -A3 "entry function.*sweep_fast" | grep -E "spill|Used" || true
 nvcc $ARCH -O2 -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -I ${CINC:-$ROOT/include} -I $C "$@" -c $C/chase_api.cpp -o $O/api.o
 nvcc $ARCH -O2 -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -I ${CINC:-$ROOT/include} -I $C -c $C/envelope.cpp -o $O/env.o
-nvcc $ARCH -shared -cudart static -o $ROOT/build/variants/libchase_$name.so $O/kernels.o $O/api.o $O/env.o
+nvcc $ARCH -shared -cudart static -o $ROOT/build/variants/libchase_$name.so $O/kernels.o $O/api.o $O/env.o -ldl
 rm -rf "$O"
 echo built $ROOT/build/variants/libchase_$name.so
