@@ -793,7 +793,7 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     fp.max_ci_fixed = cost->max_ci;
     cudaError_t e;
     {
-        const Nvtx r("chase_sweep/fit");
+        const Nvtx r("fit");
         e = launch_fit(fp, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "fit kernel");
@@ -845,7 +845,7 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     }
     if (!rolling(fcfg) && !svr(fcfg)) ev_start(s);
     {
-        const Nvtx r("chase_sweep/predict+argmin+replay");
+        const Nvtx r("predict_argmin_replay");
         e = launch_sweep(MODE_FUSED, traces->dtype == CHASE_F64, aligned, p, s);
     }
     if (!rolling(fcfg) && !svr(fcfg)) ev_stop(s);
