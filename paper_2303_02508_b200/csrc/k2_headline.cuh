@@ -39,6 +39,12 @@
 #ifndef CHASE_LONG_CF
 #define CHASE_LONG_CF 1  // 1: the closed form for P >= 64 too (sweep_fast_kernel<2>, cfh_setup_long)
 #endif
+#ifndef CHASE_LANE_RUNS
+#define CHASE_LANE_RUNS 1  // 1: lane-local periods with P % 4 == 0 (P = 4, 12) replay each period as one run
+#endif
+#ifndef CHASE_DAY_BLOCKS
+#define CHASE_DAY_BLOCKS 1  // 1: P = 24 full chunks as five 12-window runs per lane (period_day)
+#endif
 #ifndef CHASE_P2_G
 #define CHASE_P2_G 2   // periods per iteration at P = 2 (sweep_fast_kernel<4>; must divide 30)
 #endif
@@ -896,6 +902,27 @@ __device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint
 template <int PC>
 __device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv, int q, int Pn, uint32_t la,
                                                    uint8_t* chl, Acc& a) {
+    if constexpr (PC > 0 && PC % 4 == 0 && PC <= 16 && CHASE_LANE_RUNS) {
+        // the period as one run (S += P s_k, E += P P_k, C += P_k sum c, Cs += sum c), its
+        // values as LDS.128 summed in a tree: fewer dependent adds than per-window sums
+        constexpr int NV = PC > 0 ? PC / 4 : 1;
+        double s4[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const float4 f = *reinterpret_cast<const float4*>(tv + q + 4 * i);
+            a.vmin = fminf(fminf(fminf(a.vmin, f.x), f.y), fminf(f.z, f.w));
+            s4[i] = __dadd_rn(__dadd_rn((double)f.x, (double)f.y), __dadd_rn((double)f.z, (double)f.w));
+        }
+#pragma unroll
+        for (int w = 1; w < NV; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w < NV; i += 2 * w) s4[i] = __dadd_rn(s4[i], s4[i + w]);
+        replay_run(a, lds_line(la), PC > 0 ? PC : 4, s4[0]);
+        const uint32_t kw = ((la >> 8) & 0xffu) * 0x01010101u;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) *reinterpret_cast<uint32_t*>(chl + q + 4 * i) = kw;
+        return;
+    }
     if (PC > 0 && PC % 4 == 0 && PC < 16) {  // q % 4 == 0 too: LDS.128, conflict-free at the lane stride
         float v[PC > 0 ? PC : 4];
 #pragma unroll
@@ -1121,6 +1148,77 @@ __device__ __forceinline__ void period_direct(const float* __restrict__ tvs, con
         ph += Pp;
         while (ph >= T) ph -= T;
     }
+}
+
+// Daily periods (P = 24, PM 26) in a full chunk: a lane's 60 windows are five
+// 12-window blocks, and with 1920 = 80 P and 60 = 2.5 P every period boundary
+// is a block boundary (even lanes start on one, odd lanes 12 windows past one).
+// The lane decides the three periods meeting its blocks (the first of an odd
+// lane began in the previous lane's windows: decided by both, counted by the
+// one holding its start) and replays each block as one run: S += 12 s_k,
+// E += 12 P_k, C += P_k sum c, Cs += sum c (the run form's contract).
+__device__ __forceinline__ uint32_t day_decide(const float* __restrict__ tv, int s, int b, int Wt, int ph, int T,
+                                               const double* Aeven, double wl, double invK, double Kc,
+                                               const uint2* ent8, int ebase, uint32_t ZB, const PairTable* pt,
+                                               const ProfileTable* pf, const double2* K2, double hcf, double cnr,
+                                               double cnab, int prof, bool own, unsigned& n_slow, unsigned& n_seq) {
+    constexpr int Pp = 24;
+    const int n = min(Pp, Wt - b);
+    const float x0f = tv[s - 1];
+    const double x0 = (double)x0f;
+    uint32_t la = n == Pp ? cfh_line(K2 + ph, hcf, cnr, cnab, x0f, x0, ent8, ebase, ZB) : ZB;
+    if (la == ZB) {  // cold: the sequential horizon, then the lookup / canonical rule
+        if (own && n == Pp) ++n_seq;
+        const double sum = horizon_sum(Aeven, T, ph, n, x0, wl);
+        const double chat = (n & (n - 1)) ? __ddiv_rn(sum, (double)n) : __dmul_rn(sum, 1.0 / (double)n);
+        unsigned ns = 0;
+        la = line_of(prof, period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, ns));
+        if (own) n_slow += ns;
+    }
+    return la;
+}
+
+__device__ __forceinline__ void day_block(const float* __restrict__ tv, int q, uint32_t la, uint8_t* chl, Acc& a) {
+    float4 v[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) v[i] = *reinterpret_cast<const float4*>(tv + q + 4 * i);
+    double s4[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        a.vmin = fminf(fminf(fminf(a.vmin, v[i].x), v[i].y), fminf(v[i].z, v[i].w));
+        s4[i] = __dadd_rn(__dadd_rn((double)v[i].x, (double)v[i].y), __dadd_rn((double)v[i].z, (double)v[i].w));
+    }
+    const double cs = __dadd_rn(__dadd_rn(s4[0], s4[1]), s4[2]);
+    replay_run(a, lds_line(la), 12, cs);
+    const uint32_t kb = (la >> 8) & 0xffu;
+    const uint32_t kw = kb * 0x01010101u;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) *reinterpret_cast<uint32_t*>(chl + q + 4 * i) = kw;
+}
+
+__device__ __forceinline__ void period_day(const float* __restrict__ tv, int w0, int Wt, int phi0, int T,
+                                           const double* Aeven, double wl, double invK, double Kc, const uint2* ent8,
+                                           int ebase, uint32_t ZB, const PairTable* pt, const ProfileTable* pf,
+                                           const double2* K2, double hcf, double cnr, double cnab, int prof,
+                                           uint8_t* chl, Acc& a, unsigned& n_slow, unsigned& n_seq) {
+    const int odd = (w0 % 24) != 0;       // 12 windows past a period start
+    const int sA = odd ? -12 : 0;         // the three periods' starts relative to the lane's first window
+    int ph = phi0 + sA;
+    if (ph < 0) ph += T;
+    const uint32_t lA = day_decide(tv, sA, w0 + sA, Wt, ph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf, K2,
+                                   hcf, cnr, cnab, prof, !odd, n_slow, n_seq);
+    ph = (ph + 24) % T;
+    const uint32_t lB = day_decide(tv, sA + 24, w0 + sA + 24, Wt, ph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf,
+                                   K2, hcf, cnr, cnab, prof, true, n_slow, n_seq);
+    ph = (ph + 24) % T;
+    const uint32_t lC = day_decide(tv, sA + 48, w0 + sA + 48, Wt, ph, T, Aeven, wl, invK, Kc, ent8, ebase, ZB, pt, pf,
+                                   K2, hcf, cnr, cnab, prof, true, n_slow, n_seq);
+    // blocks 0..4: even lanes A A B B C, odd lanes A B B C C
+    day_block(tv, 0, lA, chl, a);
+    day_block(tv, 12, odd ? lB : lA, chl, a);
+    day_block(tv, 24, lB, chl, a);
+    day_block(tv, 36, odd ? lC : lB, chl, a);
+    day_block(tv, 48, lC, chl, a);
 }
 
 // Long decision periods (P >= kHWarpW/30: at most 31 periods meet a chunk):
@@ -1487,6 +1585,11 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                     }
                     period_replay_batch(tv, nwin, cs + j0, P.period, jb, kb, prof_i, chb + j0, a);
                     __syncwarp();
+                } else if (PM == 26 && CHASE_DAY_BLOCKS && !last) {  // daily periods, full chunk: 12-window blocks
+                    period_day(tv, c * kHWarpW + j0, P.W, phi0, T, A_even, wl, invK, Kc, e8, ebase, ZB, pt, pf, K0w, hcf,
+                               cnr, cnab, prof_i, chb + j0, a, n_slow, n_seq);
+                    __syncwarp();
+                    k_carry = chb[kHWarpW - 1];
                 } else if (PER && P.k0len > 0) {  // lane-direct periods with the closed form
                     const int wc = last ? P.W_last : kHWarpW;
                     period_direct<kDirectP>(reinterpret_cast<const float*>(stage) + P.off0, tv, nwin, c * kHWarpW + j0,
