@@ -40,7 +40,10 @@
 #define CHASE_LONG_CF 1  // 1: the closed form for P >= 64 too (sweep_fast_kernel<2>, cfh_setup_long)
 #endif
 #ifndef CHASE_LANE_RUNS
-#define CHASE_LANE_RUNS 1  // 1: lane-local periods with P % 4 == 0 (P = 4, 12) replay each period as one run
+#define CHASE_LANE_RUNS 2  // lane-local periods replayed as runs: 1: P % 4 == 0 (LDS.128 tree), 2: every P >= CHASE_RUN_MIN_P
+#endif
+#ifndef CHASE_RUN_MIN_P
+#define CHASE_RUN_MIN_P 2  // CHASE_LANE_RUNS >= 2: the shortest period replayed as a run
 #endif
 #ifndef CHASE_DAY_BLOCKS
 #define CHASE_DAY_BLOCKS 1  // 1: P = 24 full chunks as five 12-window runs per lane (period_day)
@@ -898,6 +901,26 @@ __device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint
     }
 }
 
+// The same period as one run (the run form's contract): its PC values summed in
+// a pairwise tree, then S += PC s_k, E += PC P_k, C += P_k sum c, Cs += sum c.
+template <int PC>
+__device__ __forceinline__ void lane_period_run_v(const float* v, int q, uint32_t la, uint8_t* chl, Acc& a) {
+    double t[PC];
+#pragma unroll
+    for (int k = 0; k < PC; ++k) {
+        a.vmin = fminf(a.vmin, v[k]);
+        t[k] = (double)v[k];
+    }
+#pragma unroll
+    for (int w = 1; w < PC; w *= 2)
+#pragma unroll
+        for (int i = 0; i + w < PC; i += 2 * w) t[i] = __dadd_rn(t[i], t[i + w]);
+    replay_run(a, lds_line(la), PC, t[0]);
+    const uint8_t kk = (uint8_t)(la >> 8);
+#pragma unroll
+    for (int k = 0; k < PC; ++k) chl[q + k] = kk;
+}
+
 // One period's replay at the line at shared address la (windows tv[q, q + Pn)).
 template <int PC>
 __device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv, int q, int Pn, uint32_t la,
@@ -1002,7 +1025,12 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
         }
     }
 #pragma unroll
-    for (int g = 0; g < G; ++g) lane_period_replay_v<PN>(v + g * PN, q + g * PN, la[g], chl, a);
+    for (int g = 0; g < G; ++g) {
+        if constexpr (CHASE_LANE_RUNS >= 2 && PN > CHASE_RUN_MIN_P - 1)
+            lane_period_run_v<PN>(v + g * PN, q + g * PN, la[g], chl, a);
+        else
+            lane_period_replay_v<PN>(v + g * PN, q + g * PN, la[g], chl, a);
+    }
     return v[G * PN - 1];
 }
 
@@ -1049,8 +1077,19 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
                 if (ka == ZB) ka = line_of(prof, period_choice(ca, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
                 if (kb == ZB) kb = line_of(prof, period_choice(cb, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
             }
-            lane_period_replay<PC>(tv, q, Pn, ka, chl, a);
-            lane_period_replay<PC>(tv, q + Pn, Pn, kb, chl, a);
+            if constexpr (CHASE_LANE_RUNS >= 2 && PC > CHASE_RUN_MIN_P - 1 && PC % 4 != 0) {
+                float va[PC > 0 ? PC : 1], vb[PC > 0 ? PC : 1];
+#pragma unroll
+                for (int k = 0; k < (PC > 0 ? PC : 1); ++k) {
+                    va[k] = tv[q + k];
+                    vb[k] = tv[q + Pn + k];
+                }
+                lane_period_run_v<(PC > 0 ? PC : 1)>(va, q, ka, chl, a);
+                lane_period_run_v<(PC > 0 ? PC : 1)>(vb, q + Pn, kb, chl, a);
+            } else {
+                lane_period_replay<PC>(tv, q, Pn, ka, chl, a);
+                lane_period_replay<PC>(tv, q + Pn, Pn, kb, chl, a);
+            }
         }
         return;
     }
