@@ -45,6 +45,9 @@
 #ifndef CHASE_RUN_MIN_P
 #define CHASE_RUN_MIN_P 2  // CHASE_LANE_RUNS >= 2: the shortest period replayed as a run
 #endif
+#ifndef CHASE_BATCH_BLOCKS
+#define CHASE_BATCH_BLOCKS 1  // 1: long periods' full lanes replay as two runs over 4-window blocks
+#endif
 #ifndef CHASE_DAY_BLOCKS
 #define CHASE_DAY_BLOCKS 1  // 1: P = 24 full chunks as five 12-window runs per lane (period_day)
 #endif
@@ -1313,6 +1316,25 @@ __device__ __forceinline__ void period_replay_batch(const float* __restrict__ tv
     const uint32_t k0 = __shfl_sync(kFull, kb, min(jA - jb, 31));
     const uint32_t k1 = __shfl_sync(kFull, kb, min(jA + 1 - jb, 31));
     const int split = min(nwin, max(0, (jA + 1) * Pp - w0));
+    if (CHASE_BATCH_BLOCKS && nwin == kHChunk && (split & 3) == 0) {
+        // a full lane, the period boundary on a 4-window block: 15 LDS.128 blocks summed
+        // in trees into the two runs' value sums, one choice word per block
+        double c0 = 0.0, c1 = 0.0;
+        const uint32_t kw0 = k0 * 0x01010101u, kw1 = k1 * 0x01010101u;
+#pragma unroll
+        for (int i = 0; i < kHChunk / 4; ++i) {
+            const float4 f = *reinterpret_cast<const float4*>(tv + 4 * i);
+            a.vmin = fminf(fminf(fminf(a.vmin, f.x), f.y), fminf(f.z, f.w));
+            const double sb = __dadd_rn(__dadd_rn((double)f.x, (double)f.y), __dadd_rn((double)f.z, (double)f.w));
+            const bool first = 4 * i < split;
+            if (first) c0 = __dadd_rn(c0, sb);
+            else c1 = __dadd_rn(c1, sb);
+            *reinterpret_cast<uint32_t*>(chl + 4 * i) = first ? kw0 : kw1;
+        }
+        if (split > 0) replay_run(a, lds_line(kLineBase + (uint32_t)line_off(prof, (int)k0)), split, c0);
+        if (split < kHChunk) replay_run(a, lds_line(kLineBase + (uint32_t)line_off(prof, (int)k1)), kHChunk - split, c1);
+        return;
+    }
 #pragma unroll 1
     for (int seg = 0; seg < 2; ++seg) {
         const uint32_t kk = seg == 0 ? k0 : k1;
