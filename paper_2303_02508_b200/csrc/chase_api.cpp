@@ -85,8 +85,15 @@ WsLayout ws_layout(int64_t n_traces, int T, int n_prof, int n_eta, const chase_t
     w.ld_roll = 0;
     if (fc_first(f) && t && f->history_len >= 2 && t->n_steps > f->history_len) {
         if (rolling(f)) { w.roll_ptab = o; o += round_up((int64_t)roll_phase_doubles(T, f->history_len) * 8, kWsAlign); }
-        w.ld_roll = round_up(t->n_steps - f->history_len, 2);
-        w.roll_fc = o; o += round_up(n_traces * w.ld_roll * 8, kWsAlign);
+        // the forecast scratch, unless every call of this shape runs in place (headline
+        // periods, fused rolling refit) or writes the caller's d_forecast
+        const int L = f->history_len, vec = t->dtype == CHASE_F64 ? 2 : 4;
+        const bool in_place = !svr(f) && sweep_in_place(t->dtype == CHASE_F64, L % vec == 0 && L >= vec, L, T, n_prof,
+                                                        n_eta, rolling(f), periods(f), tables_bytes(T, n_prof, n_eta));
+        if (!in_place) {
+            w.ld_roll = round_up(t->n_steps - f->history_len, 2);
+            w.roll_fc = o; o += round_up(n_traces * w.ld_roll * 8, kWsAlign);
+        }
         if (svr(f)) { w.svr_models = o; o += round_up(n_traces * kSvrModelDoubles * 8, kWsAlign); }
     }
     w.total = o;
@@ -831,6 +838,8 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     if (fc_first(fcfg) && !per_inplace) {
         // rolling refit / decision periods: forecasts of every window first (into d_forecast when
         // given), then the fused argmin + replay reads them (sweep_kernel<..., FIN>)
+        if (!d_forecast && WL.ld_roll == 0)  // (the layout planned an in-place run: e.g. an env override)
+            return fail(CHASE_ERR_WORKSPACE, "this call needs the forecast scratch its workspace layout omits");
         double* fc = d_forecast ? d_forecast : reinterpret_cast<double*>(ws + WL.roll_fc);
         const int64_t ldf = d_forecast ? ld_f : WL.ld_roll;
         // rolling refit / SVR: the forecaster dominates (timing hook)

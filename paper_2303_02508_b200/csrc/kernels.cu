@@ -245,6 +245,26 @@ cudaError_t launch_sweep(int mode, bool f64, bool aligned, const SweepParams& p,
     return cudaErrorInvalidValue;
 }
 
+// Does a one-eta sweep of this shape without forecast output run in place (periods in
+// the headline kernel, or the fused rolling refit), i.e. need no forecast scratch?
+bool sweep_in_place(bool f64, bool aligned, int L, int T, int n_prof, int n_eta, bool rolling, bool periods,
+                    int tables_bytes) {
+    if (f64 || !aligned || n_eta != 1) return false;
+    SweepParams p;
+    memset(&p, 0, sizeof(p));
+    p.L = L;
+    p.T = T;
+    p.n_eta = 1;
+    p.n_prof = n_prof;
+    p.tables_bytes = tables_bytes;
+    if (periods) return headline_eligible(MODE_FUSED, false, true, p);
+    if (rolling) {
+        p.refit = 1;
+        return roll_fused_eligible(p);
+    }
+    return false;
+}
+
 bool roll_fused_eligible(const SweepParams& p) {
     return p.refit >= 1 && p.n_eta == 1 && !p.forecast && !p.fc_in && p.L <= kRMaxL && p.L % 4 == 0 &&
            p.T <= 2048 && !getenv("CHASE_ROLL_EXACT") &&

@@ -155,6 +155,8 @@ cudaError_t launch_periods(const void* traces, bool f64, int64_t ld, int64_t n_t
 // rolling refit fused into the sweep (k2_roll.cuh): fp32, aligned, one eta, no forecast output, L <= 64,
 // T <= 2048; returns false (nothing launched) when the shape is not covered
 bool roll_fused_eligible(const SweepParams& p);
+bool sweep_in_place(bool f64, bool aligned, int L, int T, int n_prof, int n_eta, bool rolling, bool periods,
+                    int tables_bytes);
 cudaError_t launch_roll_fused(const SweepParams& p, cudaStream_t s);
 cudaError_t launch_rolling(const void* traces, bool f64, int64_t ld, int64_t n_traces, int N, int L, int T, int phase0,
                            int R, double ridge, double tol, const double* phase, double* ptab, double* records,
