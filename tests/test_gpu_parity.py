@@ -575,6 +575,24 @@ def test_decision_periods_sequential_horizon_paths(P, interval, monkeypatch):
     assert d.n_seq_periods >= n * ((N - L) // P), (d.n_seq_periods, n * ((N - L) // P))
 
 
+@pytest.mark.parametrize("interval,L,phase0", [(7200, 12, 0), (3600, 24, 5), (3600, 48, 17)])
+def test_daily_periods_block_path_other_shapes(interval, L, phase0):
+    """P = 24 runs as five 12-window blocks per lane (period_day)
+    whatever the phase table: 2-hourly data (T = 12), a job start off phase 0,
+    a 48-point history.  Choices and totals match the oracle exactly."""
+    T = 86400 // interval
+    prof = [inputs.make_profile("bert", inputs.LIMITS_9)]
+    N = L + 3 * 1920 + 700
+    n = 6
+    tr = inputs.synth_traces_host(n, N, seed=900 + L, T=T, phase0=phase0)
+    J = np.full(n, interval * (N - L) * prof[0].throughput_sps.min())
+    g = run_sweep(tr, N, prof, [0.5], J=J, L=L, period_steps=24, interval_s=interval, phase0=phase0, forecast=False)
+    g["forecast"] = None
+    o = run_oracle(tr, N, prof, [0.5], J=J, L=L, period_steps=24, interval_s=interval, phase0=phase0)
+    assert_parity(g, o)
+    assert g["diag"].kernel_path & cb.PATH_H_PERIODS
+
+
 def test_decision_periods_fit_forecast_split_path():
     w = inputs.workload("C4", n_traces=17)
     N = 24 + 1000
