@@ -455,9 +455,17 @@ struct SplitStreams {
     }
 };
 
-SplitStreams& split_streams() {
-    static thread_local SplitStreams ss;  // per host thread, per process (created on first use)
-    return ss;
+SplitStreams* split_streams() {
+    // per host thread and device (created on first use on that device)
+    constexpr int kMaxDev = 64;
+    static thread_local SplitStreams* ss[kMaxDev] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (!ss[dev]) ss[dev] = new SplitStreams();
+    return ss[dev];
 }
 
 extern "C" {
@@ -759,8 +767,9 @@ chase_status_t chase_sweep(const chase_traces_t* traces, const chase_forecast_cf
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     if (!d_forecast && eta_split_shape(traces, fcfg, cost->n_eta)) {
         const size_t slice = eta_split_slice_bytes(traces, fcfg, n_profiles);
-        SplitStreams& ss = split_streams();
-        if (ss.ok && ws_bytes >= (size_t)cost->n_eta * slice) {
+        SplitStreams* sp = split_streams();
+        if (sp && sp->ok && ws_bytes >= (size_t)cost->n_eta * slice) {
+            SplitStreams& ss = *sp;
             // n_eta concurrent one-eta sweeps (the headline kernel each), forked from and joined into s
             chase_diag_t* slice0 = reinterpret_cast<chase_diag_t*>(ws);  // slice 0's diag == the call's (offset 0)
             ev_start(s);
