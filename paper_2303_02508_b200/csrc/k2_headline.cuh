@@ -1238,7 +1238,7 @@ __device__ __forceinline__ void day_block(const float* __restrict__ tv, int q, u
     for (int i = 0; i < 3; ++i) *reinterpret_cast<uint32_t*>(chl + q + 4 * i) = kw;
 }
 
-static_assert(kHChunk == 60 && kHWarpW % 24 == 0, "period_day's five 12-window blocks assume 60-window lanes");
+static_assert(!CHASE_DAY_BLOCKS || (kHChunk == 60 && kHWarpW % 24 == 0), "period_day: five 12-window blocks per 60-window lane");
 __device__ __forceinline__ void period_day(const float* __restrict__ tv, int w0, int Wt, int phi0, int T,
                                            const double* Aeven, double wl, double invK, double Kc, const uint2* ent8,
                                            int ebase, uint32_t ZB, const PairTable* pt, const ProfileTable* pf,
