@@ -1581,9 +1581,6 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                             hcf = K0w[n_a].x;
                             cnr = K0w[n_a].y;
                             cnab = K0w[n_a + 1].x;
-#ifdef CHASE_CFH_SETUPONLY
-                            cnr = CUDART_NAN;
-#endif
                         }
                     }
                     if constexpr (PM == 0 && CHASE_H0_FAST) {
