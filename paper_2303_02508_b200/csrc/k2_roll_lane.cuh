@@ -72,6 +72,7 @@ struct RLState {
     double Sr, Er, Cr, Cb, Cs_all;     // replay sums, baseline c sum, validation sum
     double rE, rC, rf, rPk, rcw;       // the completion window's record
     int ph, rw, fit_bad;
+    int to_origin;                     // R > 1: windows until the next refit origin (0: this one)
     unsigned n_slow;
     float vmin;
     bool done;
@@ -94,15 +95,20 @@ struct RLConst {
 // Window a of a lane (cw = c[a], ov = c[a - n]): for R = 1 the closed-form fit of
 // the current moments and their slide to a + 1, else (at an origin) the fit of
 // the origin's rows; then the forecast, Eq. 6 and the replay in window order.
-template <bool R1>
+// MODE 0: R = 1 (a fit every window); 1: R > 1 with the moments slid every window
+// and a fit at each origin; 2: R > 1 with each origin's moments from its rows.
+template <int MODE>
 __device__ __forceinline__ uint32_t rl_window(RLState& st, const RLConst& k, int a, double cw, double ov) {
+    constexpr bool R1 = MODE == 0;
     const int w = a - k.s0;
     const double* rp = k.ptab + st.ph * kRPhase;
-    if (R1) {
-        if (!mom_solve_fast(st.m, st.c_prev, st.o_prev, k.dn, k.inv_n, rp, st.md)) {
-            const RVals V{k.row, k.grow, k.ab - k.L, k.ab + k.nw};
-            st.md = exact_model(V, a, k.L, k.T, k.phase0, k.S, k.C, k.ridge, k.tol);
-            st.fit_bad |= st.md.status;
+    if (MODE != 2) {
+        if (MODE == 0 || st.to_origin == 0) {  // (MODE 1: an origin, w % R == 0; warp-uniform)
+            if (!mom_solve_fast(st.m, st.c_prev, st.o_prev, k.dn, k.inv_n, rp, st.md)) {
+                const RVals V{k.row, k.grow, k.ab - k.L, k.ab + k.nw};
+                st.md = exact_model(V, a, k.L, k.T, k.phase0, k.S, k.C, k.ridge, k.tol);
+                st.fit_bad |= st.md.status;
+            }
         }
         // slide to a + 1: row a in, row a - n out (phase columns: the window's and the leaving row's)
         RMom& m = st.m;
@@ -113,7 +119,7 @@ __device__ __forceinline__ uint32_t rl_window(RLState& st, const RLConst& k, int
         m.Sky = __fma_rn(-rp[9], ov, __fma_rn(rp[7], cw, m.Sky));
         m.Ssl = __fma_rn(-rp[8], st.o_prev, __fma_rn(rp[6], st.c_prev, m.Ssl));
         m.Skl = __fma_rn(-rp[9], st.o_prev, __fma_rn(rp[7], st.c_prev, m.Skl));
-    } else if (w % k.R == 0) {  // an origin (warp-uniform)
+    } else if (st.to_origin == 0) {  // an origin (w % R == 0; warp-uniform)
         const RVals V{k.row, k.grow, k.ab - k.L, k.ab + k.nw};
         const RMom mo = mom_direct(V, a, k.n, k.phase0, k.T, k.S, k.C);
         if (!mom_solve_fast(mo, st.c_prev, V(a - k.n - 1), k.dn, k.inv_n, rp, st.md)) {
@@ -127,6 +133,7 @@ __device__ __forceinline__ uint32_t rl_window(RLState& st, const RLConst& k, int
     st.c_prev = cw;
     st.o_prev = ov;
     st.ph = st.ph + 1 == k.T ? 0 : st.ph + 1;
+    if (!R1) st.to_origin = st.to_origin == 0 ? k.R - 1 : st.to_origin - 1;
     // Eq. 6: the envelope lookup, the canonical rule in a band
     uint32_t kk = plan_lookup(__dmul_rn(p, k.invK), k.pt);
     if (kk == (uint32_t)kZeroLine || k.invK == 0.0) {
@@ -153,7 +160,7 @@ __device__ __forceinline__ uint32_t rl_window(RLState& st, const RLConst& k, int
     return kk;
 }
 
-template <bool R1>
+template <int MODE>
 __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(const __grid_constant__ SweepParams P) {
     mark_path(P.diag, CHASE_PATH_ROLL_FUSED);
     extern __shared__ __align__(128) uint8_t sm[];
@@ -265,6 +272,7 @@ __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(co
         st.rE = st.rC = st.rf = st.rPk = st.rcw = 0.0;
         st.ph = (int)(((int64_t)P.phase0 + s0) % T);  // phase of window 0 (= its origin's for R = 1)
         st.rw = -1;
+        st.to_origin = 0;
         st.fit_bad = 0;
         st.n_slow = 0;
         st.vmin = FLT_MAX;
@@ -293,10 +301,10 @@ __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(co
                 const float o5 = cv[k.ab + j - L + 4];
                 st.vmin = fminf(fminf(fminf(st.vmin, v4.x), v4.y), fminf(v4.z, v4.w));
                 const int a = k.ab + j;
-                uint32_t word = rl_window<R1>(st, k, a, (double)v4.x, (double)o4.y);
-                word |= rl_window<R1>(st, k, a + 1, (double)v4.y, (double)o4.z) << 8;
-                word |= rl_window<R1>(st, k, a + 2, (double)v4.z, (double)o4.w) << 16;
-                word |= rl_window<R1>(st, k, a + 3, (double)v4.w, (double)o5) << 24;
+                uint32_t word = rl_window<MODE>(st, k, a, (double)v4.x, (double)o4.y);
+                word |= rl_window<MODE>(st, k, a + 1, (double)v4.y, (double)o4.z) << 8;
+                word |= rl_window<MODE>(st, k, a + 2, (double)v4.z, (double)o4.w) << 16;
+                word |= rl_window<MODE>(st, k, a + 3, (double)v4.w, (double)o5) << 24;
                 chw[j >> 2] = word;
             }
             if (nfull < k.nw) {  // the trace's last windows (W % 4 != 0)
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(kRLThreads, CHASE_RL_MINB) roll_lane_kernel(co
                 for (int j = nfull; j < k.nw; ++j) {
                     const float v = cv[k.ab + j];
                     st.vmin = fminf(st.vmin, v);
-                    word |= rl_window<R1>(st, k, k.ab + j, (double)v, (double)cv[k.ab + j - n]) << (8 * (j - nfull));
+                    word |= rl_window<MODE>(st, k, k.ab + j, (double)v, (double)cv[k.ab + j - n]) << (8 * (j - nfull));
                 }
                 chw[nfull >> 2] = word;
             }

@@ -276,7 +276,9 @@ cudaError_t launch_roll_fused(const SweepParams& p, cudaStream_t s) {
     if (!getenv("CHASE_ROLL_RUNS") && make_rllayout(p.T, p.L, p.tables_bytes).total <= max_smem_optin()) {
         // lane = trace (k2_roll_lane.cuh), the default where its tiles fit
         const int smem = make_rllayout(p.T, p.L, p.tables_bytes).total;
-        auto kern = p.refit == 1 ? roll_lane_kernel<true> : roll_lane_kernel<false>;
+        // R > 1: the moments slide every window and each origin fits them (mode 1), or each
+        // origin's moments come from its rows (mode 2, CHASE_RL_DIRECT)
+        auto kern = p.refit == 1 ? roll_lane_kernel<0> : getenv("CHASE_RL_DIRECT") ? roll_lane_kernel<2> : roll_lane_kernel<1>;
         cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return err;
         int per_sm = 0;
