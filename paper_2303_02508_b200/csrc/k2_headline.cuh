@@ -54,6 +54,12 @@
 #ifndef CHASE_P2_G
 #define CHASE_P2_G 2   // periods per iteration at P = 2 (sweep_fast_kernel<4>; must divide 30)
 #endif
+#ifndef CHASE_P_FULL
+#define CHASE_P_FULL 1  // 1: P = 2 skips the per-period range test when every range is [0, inf)
+#endif
+#ifndef CHASE_P_WORDS
+#define CHASE_P_WORDS 1  // 1: lane-local even periods store a group's choices as 4-byte words
+#endif
 #ifndef CHASE_H_PAIRSUM
 #define CHASE_H_PAIRSUM 1  // 1: a group's four terms summed pairwise before the running sums
 #endif
@@ -517,6 +523,7 @@ __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, 
     }
     const int nph = T / g;
     double h = 0.0;  // lane 0: h = sum_k w^k, accumulated beside its first horizon
+    bool full = true;  // every phase's start-value range is [0, inf)
     for (int j = lane; j < nph; j += 32) {
         int p = (int)(((int64_t)phase_start + (int64_t)j * g) % T);
         const int phi = p;
@@ -537,9 +544,10 @@ __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, 
         }
         const float lof = __double2float_ru(lo), hif = __double2float_rd(hi);
         K2[phi] = make_double2(__dmul_rn(sum, cs), __hiloint2double(__float_as_int(hif), __float_as_int(lof)));
+        full = full && lof == 0.0f && hif == INFINITY;
         if (j == 0) h = hs;
     }
-    __syncwarp();
+    full = __all_sync(kFull, full);
     for (int j = T + lane; j < n_a; j += 32) K2[j] = K2[j % T];
     if (lane == 0) {
         double nr = CUDART_NAN, nab = -INFINITY;
@@ -550,7 +558,7 @@ __device__ __noinline__ void cfh_setup(double2* K2, const double* Aeven, int T, 
             nab = -__dmul_ru(__dmul_ru(amax, inv), 1.0 + 0x1p-20);
         }
         K2[n_a] = make_double2(__dmul_rn(h, cs), nr);
-        K2[n_a + 1] = make_double2(nab, 0.0);
+        K2[n_a + 1] = make_double2(nab, full ? 1.0 : 0.0);  // .y = 1: every range is [0, inf) (period_lane)
     }
     __syncwarp();
 }
@@ -656,11 +664,15 @@ __device__ __forceinline__ uint32_t cfh_choice(const double2* kp, double hc, dou
 
 // The same decision as its line's shared address (the fused replay loads the
 // line from it directly; the choice byte is its byte 1), ZB on decline.
+// RANGE = false: every phase's range is [0, inf) (cfh_setup's flag), which every
+// valid value is in; a chunk with an invalid value makes its trace status 4, whose
+// choices and totals are replaced (Q25), so its decisions need no range test.
+template <bool RANGE = true>
 __device__ __forceinline__ uint32_t cfh_line(const double2* kp, double hc, double nr, double nab, float x0f, double x0,
                                              const uint2* ent8, int ebase, uint32_t ZB) {
-    const double2 e = *kp;
+    const double2 e = RANGE ? *kp : make_double2(kp->x, 0.0);
     const double y = __fma_rn(hc, x0, e.x);
-    const bool in = x0f >= __int_as_float(__double2loint(e.y)) && x0f <= __int_as_float(__double2hiint(e.y));
+    const bool in = !RANGE || (x0f >= __int_as_float(__double2loint(e.y)) && x0f <= __int_as_float(__double2hiint(e.y)));
     const int hk = __double2hiint(y);
     const int idx = max(min((hk >> kSH) - ebase, kNBUsed - 1), 0);
     const uint32_t la = line_addr(hk, ent8[idx], ZB);
@@ -887,7 +899,7 @@ __device__ __forceinline__ void replay_run(Acc& a, double2 ln, int m, double cs)
 // Eq. 6 lookup, one line load per period, the running sums in window order
 // (the same sequence replay_groups adds them in).  PC > 0: P known at compile time.
 // The same replay from values already in registers (v[0, PC), PC < 16).
-template <int PC>
+template <int PC, bool STORE = true>
 __device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint32_t la, uint8_t* chl, Acc& a) {
     const double2 ln = lds_line(la);
     const uint8_t kk = (uint8_t)(la >> 8);  // the choice: byte 1 of the line address
@@ -900,13 +912,13 @@ __device__ __forceinline__ void lane_period_replay_v(const float* v, int q, uint
         a.E = __dadd_rn(a.E, ln.y);
         a.C = __dadd_rn(a.C, __dmul_rn(ln.y, cw));
         a.Cs = __dadd_rn(a.Cs, cw);
-        chl[q + k] = kk;
+        if (STORE) chl[q + k] = kk;
     }
 }
 
 // The same period as one run (the run form's contract): its PC values summed in
 // a pairwise tree, then S += PC s_k, E += PC P_k, C += P_k sum c, Cs += sum c.
-template <int PC>
+template <int PC, bool STORE = true>
 __device__ __forceinline__ void lane_period_run_v(const float* v, int q, uint32_t la, uint8_t* chl, Acc& a) {
     double t[PC];
 #pragma unroll
@@ -919,9 +931,11 @@ __device__ __forceinline__ void lane_period_run_v(const float* v, int q, uint32_
 #pragma unroll
         for (int i = 0; i + w < PC; i += 2 * w) t[i] = __dadd_rn(t[i], t[i + w]);
     replay_run(a, lds_line(la), PC, t[0]);
-    const uint8_t kk = (uint8_t)(la >> 8);
+    if (STORE) {
+        const uint8_t kk = (uint8_t)(la >> 8);
 #pragma unroll
-    for (int k = 0; k < PC; ++k) chl[q + k] = kk;
+        for (int k = 0; k < PC; ++k) chl[q + k] = kk;
+    }
 }
 
 // One period's replay at the line at shared address la (windows tv[q, q + Pn)).
@@ -982,7 +996,7 @@ __device__ __forceinline__ void lane_period_replay(const float* __restrict__ tv,
 // G consecutive periods of PN windows from tv[q] (q % 4 == 0, G*PN % 4 == 0): the
 // G*PN values as LDS.128, G independent horizon chains interleaved, then the G
 // replays in window order.  Returns the last value (the next group's start value).
-template <int PN, int G>
+template <int PN, int G, bool RANGE = true>
 __device__ __forceinline__ float period_group(const float* __restrict__ tv, int q, float carry,
                                               const double* __restrict__ Ap, double wl, bool pow2, double dP,
                                               double invP, double invK, double Kc, const uint2* ent8, int ebase,
@@ -1010,9 +1024,8 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
     bool need = !kCF;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        la[g] = kCF ? cfh_line(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], ent8, ebase, ZB) : ZB;
+        la[g] = kCF ? cfh_line<RANGE>(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], ent8, ebase, ZB) : ZB;
         need |= la[g] == ZB;
-        if (kCF) n_seq += la[g] == ZB ? 1u : 0u;
     }
     if (need) {  // cold: the sequential horizon (Eq. 1) for the periods the closed form left
 #pragma unroll
@@ -1022,6 +1035,7 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             if (la[g] == ZB) {
+                if (kCF) ++n_seq;
                 const double ch = pow2 ? __dmul_rn(sm[g], invP) : __ddiv_rn(sm[g], dP);
                 la[g] = line_of(prof, period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
             }
@@ -1030,10 +1044,22 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         if constexpr (CHASE_LANE_RUNS >= 2 && PN > CHASE_RUN_MIN_P - 1)
-            lane_period_run_v<PN>(v + g * PN, q + g * PN, la[g], chl, a);
+            lane_period_run_v<PN, !CHASE_P_WORDS>(v + g * PN, q + g * PN, la[g], chl, a);
         else
-            lane_period_replay_v<PN>(v + g * PN, q + g * PN, la[g], chl, a);
+            lane_period_replay_v<PN, !CHASE_P_WORDS>(v + g * PN, q + g * PN, la[g], chl, a);
     }
+#if CHASE_P_WORDS
+    // the group's choice bytes as 4-byte words (q % 4 == 0, chl 4-B aligned): byte 1 of
+    // each period's line address; a word spans at most two periods (PN even)
+#pragma unroll
+    for (int w = 0; w < G * PN / 4; ++w) {
+        const int pa = 4 * w / PN, pb = (4 * w + 3) / PN;
+        uint32_t sel = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sel |= (uint32_t)(((4 * w + i) / PN == pa) ? 1 : 5) << (4 * i);
+        *reinterpret_cast<uint32_t*>(chl + q + 4 * w) = __byte_perm(la[pa], la[pb], sel);
+    }
+#endif
     return v[G * PN - 1];
 }
 
@@ -1042,7 +1068,7 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
                                             double wl, double invK, double Kc, const uint2* ent8, int ebase,
                                             uint32_t ZB, const PairTable* pt, const ProfileTable* pf, int prof,
                                             const double2* kq, double hcf, double cnr, double cnab, uint8_t* chl, Acc& a,
-                                            unsigned& n_slow, unsigned& n_seq) {
+                                            unsigned& n_slow, unsigned& n_seq, bool full = false) {
     const int Pn = PC > 0 ? PC : Pp;
     const bool pow2 = (Pn & (Pn - 1)) == 0;
     const double dP = (double)Pn, invP = 1.0 / dP;
@@ -1054,6 +1080,15 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         float carry = tv[-1];
         // (four periods per iteration at P = 2 measured slower: 17.7 -> 18.4 ms at C5, register spills)
         constexpr int GP = PN == 2 ? CHASE_P2_G : 2;  // periods per iteration
+#if CHASE_P_FULL
+        if (PN == 2 && full) {  // every start-value range is [0, inf): no range test per period (P = 6: slower)
+#pragma unroll 1
+            for (int q = 0; q < kHChunk; q += GP * PN)
+                carry = period_group<PN, GP, false>(tv, q, carry, Ap, wl, pow2, dP, invP, invK, Kc, ent8, ebase, ZB, pt,
+                                                    pf, prof, kq, hcf, cnr, cnab, chl, a, n_slow, n_seq);
+            return;
+        }
+#endif
 #pragma unroll 1
         for (int q = 0; q < kHChunk; q += GP * PN)
             carry = period_group<PN, GP>(tv, q, carry, Ap, wl, pow2, dP, invP, invK, Kc, ent8, ebase, ZB, pt, pf, prof,
@@ -1511,6 +1546,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
         int jb = 0;            // long periods: first period of the current batch
         uint32_t kb = 0;       // long periods: lane l's decision for period jb + l
         double hcf = 0.0, cnr = CUDART_NAN, cnab = -INFINITY;  // periods: the closed form's h, -r, -A_b (NaN: off)
+        bool cfull = false;    // periods: every closed-form start-value range is [0, inf)
         for (int c = 0; c < nc; ++c) {
             const bool last = c == nc - 1;
             uint8_t* stage = stage0;
@@ -1581,6 +1617,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                             hcf = K0w[n_a].x;
                             cnr = K0w[n_a].y;
                             cnab = K0w[n_a + 1].x;
+                            cfull = K0w[n_a + 1].y == 1.0;
                         }
                     }
                     if constexpr (PM == 0 && CHASE_H0_FAST) {
@@ -1628,7 +1665,7 @@ __global__ void __launch_bounds__(kHThreads, CHASE_H_MINB) sweep_fast_kernel(
                 if (kLaneLocal && !last) {  // lane-local periods (P | kHChunk): fused decide + replay
                     uint8_t* chl = chb + j0;
 #define CHASE_LANE_P(PC) period_lane<PC>(tv, PC, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, K0w + phi0, hcf, cnr, cnab, \
-                                         chl, a, n_slow, n_seq)
+                                         chl, a, n_slow, n_seq, cfull)
                     if constexpr (PM >= 4) CHASE_LANE_P(PM - 2);
                     else period_lane<0>(tv, P.period, Ap, wl, invK, Kc, e8, ebase, ZB, pt, pf, prof_i, K0w + phi0, hcf,
                                         cnr, cnab, chl, a, n_slow, n_seq);
