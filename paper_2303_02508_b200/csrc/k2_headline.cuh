@@ -57,6 +57,9 @@
 #ifndef CHASE_P_FULL
 #define CHASE_P_FULL 1  // 1: P = 2 skips the per-period range test when every range is [0, inf)
 #endif
+#ifndef CHASE_P_DEFER
+#define CHASE_P_DEFER 1  // 1: even lane-local periods replay first and fix declined closed-form periods after
+#endif
 #ifndef CHASE_P_WORDS
 #define CHASE_P_WORDS 1  // 1: lane-local even periods store a group's choices as 4-byte words
 #endif
@@ -1027,7 +1030,11 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
         la[g] = kCF ? cfh_line<RANGE>(kq + q + g * PN, hcf, cnr, cnab, x0f[g], pr[g], ent8, ebase, ZB) : ZB;
         need |= la[g] == ZB;
     }
-    if (need) {  // cold: the sequential horizon (Eq. 1) for the periods the closed form left
+    // Deferred: the group replays first, a declined period on the zero line (no S, E,
+    // C; its sum of c counts), and the cold block below adds its line's run afterwards
+    // (S += PN s_k, E += PN P_k, C += P_k sum c) and rewrites its choice bytes.
+    constexpr bool kDefer = CHASE_P_DEFER && kCF && CHASE_P_WORDS && CHASE_LANE_RUNS >= 2 && PN > CHASE_RUN_MIN_P - 1;
+    if (!kDefer && need) {  // cold: the sequential horizon (Eq. 1) for the periods the closed form left
 #pragma unroll
         for (int k = 0; k < PN; ++k)
 #pragma unroll
@@ -1060,6 +1067,33 @@ __device__ __forceinline__ float period_group(const float* __restrict__ tv, int 
         *reinterpret_cast<uint32_t*>(chl + q + 4 * w) = __byte_perm(la[pa], la[pb], sel);
     }
 #endif
+    if (kDefer && need) {  // cold: the declined periods' horizons, choices and runs
+#pragma unroll
+        for (int k = 0; k < PN; ++k)
+#pragma unroll
+            for (int g = 0; g < G; ++g) horizon_step(Ap[q + g * PN + k], wl, pr[g], sm[g]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (la[g] == ZB) {
+                ++n_seq;
+                const double ch = pow2 ? __dmul_rn(sm[g], invP) : __ddiv_rn(sm[g], dP);
+                const uint32_t kk = period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+                double t[PN];
+#pragma unroll
+                for (int k = 0; k < PN; ++k) t[k] = (double)v[g * PN + k];
+#pragma unroll
+                for (int w = 1; w < PN; w *= 2)
+#pragma unroll
+                    for (int i = 0; i + w < PN; i += 2 * w) t[i] = __dadd_rn(t[i], t[i + w]);
+                const double2 ln = lds_line(line_of(prof, kk));
+                a.S = __dadd_rn(a.S, __dmul_rn((double)PN, ln.x));
+                a.E = __dadd_rn(a.E, __dmul_rn((double)PN, ln.y));
+                a.C = __dadd_rn(a.C, __dmul_rn(ln.y, t[0]));
+#pragma unroll
+                for (int k = 0; k < PN; ++k) chl[q + g * PN + k] = (uint8_t)kk;
+            }
+        }
+    }
     return v[G * PN - 1];
 }
 
@@ -1103,6 +1137,48 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
             double pa = (double)fa, pb = (double)fb, sa = 0.0, sb = 0.0;
             uint32_t ka = cfh_line(kq + q, hcf, cnr, cnab, fa, pa, ent8, ebase, ZB);
             uint32_t kb = cfh_line(kq + q + Pn, hcf, cnr, cnab, fb, pb, ent8, ebase, ZB);
+            // deferred (period_group's contract): both runs replay first, a declined one on
+            // the zero line, and the cold block adds its line's run afterwards
+            constexpr bool kDefer = CHASE_P_DEFER && CHASE_LANE_RUNS >= 2 && PC > CHASE_RUN_MIN_P - 1 && PC % 4 != 0;
+            if constexpr (kDefer) {
+                constexpr int PR = PC > 0 ? PC : 1;
+                float va[PR], vb[PR];
+#pragma unroll
+                for (int k = 0; k < PR; ++k) {
+                    va[k] = tv[q + k];
+                    vb[k] = tv[q + Pn + k];
+                }
+                lane_period_run_v<PR>(va, q, ka, chl, a);
+                lane_period_run_v<PR>(vb, q + Pn, kb, chl, a);
+                if (ka == ZB || kb == ZB) {  // cold: sequential horizons, then the declined runs
+#pragma unroll
+                    for (int k = 0; k < PR; ++k) {
+                        horizon_step(Ap[q + k], wl, pa, sa);
+                        horizon_step(Ap[q + Pn + k], wl, pb, sb);
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if ((h ? kb : ka) != ZB) continue;
+                        ++n_seq;
+                        const double sh = h ? sb : sa;
+                        const double ch = pow2 ? __dmul_rn(sh, invP) : __ddiv_rn(sh, dP);
+                        const uint32_t kk = period_choice(ch, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+                        double t[PR];
+#pragma unroll
+                        for (int k = 0; k < PR; ++k) t[k] = (double)(h ? vb[k] : va[k]);
+#pragma unroll
+                        for (int w = 1; w < PR; w *= 2)
+#pragma unroll
+                            for (int i = 0; i + w < PR; i += 2 * w) t[i] = __dadd_rn(t[i], t[i + w]);
+                        const double2 ln = lds_line(line_of(prof, kk));
+                        a.S = __dadd_rn(a.S, __dmul_rn((double)PR, ln.x));
+                        a.E = __dadd_rn(a.E, __dmul_rn((double)PR, ln.y));
+                        a.C = __dadd_rn(a.C, __dmul_rn(ln.y, t[0]));
+                        fill_bytes(chl, q + h * Pn, q + h * Pn + PR, kk);
+                    }
+                }
+                continue;
+            }
             n_seq += (ka == ZB ? 1u : 0u) + (kb == ZB ? 1u : 0u);
             if (ka == ZB || kb == ZB) {  // cold: sequential horizons
 #pragma unroll
