@@ -1212,14 +1212,37 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         const float x0f = tv[q - 1];
         double prev = (double)x0f, sum = 0.0;
         uint32_t la = cfh_line(kq + q, hcf, cnr, cnab, x0f, prev, ent8, ebase, ZB);
+        // deferred (period_group's contract) for the LDS.128 run form: replay first, a
+        // declined period on the zero line, its line's run added in the cold block
+        constexpr bool kDefer = CHASE_P_DEFER && PC > 0 && PC % 4 == 0 && PC <= 16 && CHASE_LANE_RUNS;
+        if (kDefer) lane_period_replay<PC>(tv, q, Pn, la, chl, a);
         if (la == ZB) {  // cold: the sequential horizon
             ++n_seq;
 #pragma unroll
             for (int k = 0; k < Pn; ++k) horizon_step(Ap[q + k], wl, prev, sum);
             const double chat = pow2 ? __dmul_rn(sum, invP) : __ddiv_rn(sum, dP);
-            la = line_of(prof, period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow));
+            const uint32_t kk = period_choice(chat, invK, Kc, ent8, ebase, ZB, pt, pf, n_slow);
+            la = line_of(prof, kk);
+            if constexpr (kDefer) {
+                constexpr int NV = PC >= 4 ? PC / 4 : 1;
+                double s4[NV];  // the run's sum of c, as lane_period_replay forms it
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    const float4 f = *reinterpret_cast<const float4*>(tv + q + 4 * i);
+                    s4[i] = __dadd_rn(__dadd_rn((double)f.x, (double)f.y), __dadd_rn((double)f.z, (double)f.w));
+                }
+#pragma unroll
+                for (int w = 1; w < NV; w *= 2)
+#pragma unroll
+                    for (int i = 0; i + w < NV; i += 2 * w) s4[i] = __dadd_rn(s4[i], s4[i + w]);
+                const double2 ln = lds_line(la);
+                a.S = __dadd_rn(a.S, __dmul_rn((double)(PC > 0 ? PC : 4), ln.x));
+                a.E = __dadd_rn(a.E, __dmul_rn((double)(PC > 0 ? PC : 4), ln.y));
+                a.C = __dadd_rn(a.C, __dmul_rn(ln.y, s4[0]));
+                fill_bytes(chl, q, q + Pn, kk);
+            }
         }
-        lane_period_replay<PC>(tv, q, Pn, la, chl, a);
+        if (!kDefer) lane_period_replay<PC>(tv, q, Pn, la, chl, a);
     }
 }
 
