@@ -57,6 +57,9 @@
 #ifndef CHASE_P_FULL
 #define CHASE_P_FULL 1  // 1: P = 2 skips the per-period range test when every range is [0, inf)
 #endif
+#ifndef CHASE_P_LD2
+#define CHASE_P_LD2 1  // 1: P = 3, 5 load their values as LDS.64 pairs
+#endif
 #ifndef CHASE_P_DEFER
 #define CHASE_P_DEFER 1  // 1: even lane-local periods replay first and fix declined closed-form periods after
 #endif
@@ -1131,9 +1134,25 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
     }
     if (PC > 0 && (kHChunk / (PC > 0 ? PC : 1)) % 2 == 0) {
         // two periods per iteration: their horizons are independent chains, interleaved
+        // (odd P <= 5: the 2P values come in as LDS.64 pairs, 8-B aligned since 2P | q,
+        // two-way bank conflicts at the 240-B lane stride instead of the scalar loads'
+        // four-way; the start values ride in registers)
+        constexpr int PR2 = PC > 0 ? PC : 1;
+        constexpr bool kLd2 = CHASE_P_LD2 && PC > 0 && PC % 2 == 1 && PC <= 5;
+        float carry2 = tv[-1];
 #pragma unroll 1
         for (int q = 0; q < kHChunk; q += 2 * Pn) {
-            const float fa = tv[q - 1], fb = tv[q + Pn - 1];
+            float w2[2 * PR2];
+            if constexpr (kLd2) {
+#pragma unroll
+                for (int i = 0; i < PR2; ++i) {
+                    const float2 f = *reinterpret_cast<const float2*>(tv + q + 2 * i);
+                    w2[2 * i] = f.x;
+                    w2[2 * i + 1] = f.y;
+                }
+            }
+            const float fa = kLd2 ? carry2 : tv[q - 1], fb = kLd2 ? w2[PR2 - 1] : tv[q + Pn - 1];
+            if constexpr (kLd2) carry2 = w2[2 * PR2 - 1];
             double pa = (double)fa, pb = (double)fb, sa = 0.0, sb = 0.0;
             uint32_t ka = cfh_line(kq + q, hcf, cnr, cnab, fa, pa, ent8, ebase, ZB);
             uint32_t kb = cfh_line(kq + q + Pn, hcf, cnr, cnab, fb, pb, ent8, ebase, ZB);
@@ -1145,8 +1164,8 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
                 float va[PR], vb[PR];
 #pragma unroll
                 for (int k = 0; k < PR; ++k) {
-                    va[k] = tv[q + k];
-                    vb[k] = tv[q + Pn + k];
+                    va[k] = kLd2 ? w2[k] : tv[q + k];
+                    vb[k] = kLd2 ? w2[PR + k] : tv[q + Pn + k];
                 }
                 lane_period_run_v<PR>(va, q, ka, chl, a);
                 lane_period_run_v<PR>(vb, q + Pn, kb, chl, a);
