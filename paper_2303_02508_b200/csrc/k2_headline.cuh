@@ -58,7 +58,10 @@
 #define CHASE_P_FULL 1  // 1: P = 2 skips the per-period range test when every range is [0, inf)
 #endif
 #ifndef CHASE_P_LD2
-#define CHASE_P_LD2 1  // 1: P = 3, 5 load their values as LDS.64 pairs
+#define CHASE_P_LD2 1  // 1: odd lane-local P up to CHASE_P_LD2_MAXP load their values as LDS.64 pairs
+#endif
+#ifndef CHASE_P_LD2_MAXP
+#define CHASE_P_LD2_MAXP 15
 #endif
 #ifndef CHASE_P_DEFER
 #define CHASE_P_DEFER 1  // 1: even lane-local periods replay first and fix declined closed-form periods after
@@ -1138,7 +1141,7 @@ __device__ __forceinline__ void period_lane(const float* __restrict__ tv, int Pp
         // two-way bank conflicts at the 240-B lane stride instead of the scalar loads'
         // four-way; the start values ride in registers)
         constexpr int PR2 = PC > 0 ? PC : 1;
-        constexpr bool kLd2 = CHASE_P_LD2 && PC > 0 && PC % 2 == 1 && PC <= 5;
+        constexpr bool kLd2 = CHASE_P_LD2 && PC > 0 && PC % 2 == 1 && PC <= CHASE_P_LD2_MAXP;
         float carry2 = tv[-1];
 #pragma unroll 1
         for (int q = 0; q < kHChunk; q += 2 * Pn) {
